@@ -1,0 +1,13 @@
+"""paper_2602_22575_b200 -- B200-native S2O sparse prefill attention (arxiv 2602.22575).
+
+The product is libs2o_cuda.so (hand-written sm_100a kernels behind the C-ABI in
+include/s2o_cuda.h). This package holds its sources (csrc/), the in-tree build
+(build.py) and a Python mirror of the reference's entry points (s2o.py).
+"""
+from .s2o import (  # noqa: F401
+    KernelConfig, TileSpec, SegmentConfig, PermutationPlan, PassBuffers, KernelTrace,
+    RankingCost, Representatives, S2oResult, build_plan, segment_representatives,
+    pass1_dense_init, pass2_sparse, fused_single_pass, s2o_attention, early_stop_check,
+    dense_causal_attention, generate_synthetic, attention_host, select_path, lib,
+    PATH_AUTO, PATH_GENERIC, PATH_TCGEN05, SCORE_EXACT, SCORE_FAST, S2O_F32, S2O_BF16,
+)

@@ -1,0 +1,521 @@
+// capi.cu -- the extern "C" boundary (include/s2o_cuda.h): argument checks with the
+// reference's exception messages, workspace layout, kernel dispatch, host-buffer entry.
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "internal.h"
+
+namespace s2o {
+namespace {
+
+thread_local std::string g_err;
+
+s2o_status fail(s2o_status st, const std::string& msg) {
+    g_err = msg;
+    return st;
+}
+
+s2o_status cuda_fail(cudaError_t e, const char* where) {
+    return fail(S2O_ERR_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+#define S2O_CUDA_TRY(expr, where)                    \
+    do {                                             \
+        cudaError_t e_ = (expr);                     \
+        if (e_ != cudaSuccess) return cuda_fail(e_, where); \
+    } while (0)
+
+size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+// Geometry + generic argument checks shared by every entry point.
+s2o_status make_geo(const s2o_problem* p, int64_t seg_len, Geo* g) {
+    if (!p) return fail(S2O_ERR_INVALID_ARG, "null problem");
+    if (p->z < 1 || p->hq < 1 || p->hkv < 1 || p->l < 1 || p->d < 1)
+        return fail(S2O_ERR_INVALID_ARG, "tensor dims must all be >= 1");
+    if (p->hq % p->hkv != 0) return fail(S2O_ERR_QKV_DIMS, "Q/K/V dims must match");
+    if ((p->in_dtype != S2O_F32 && p->in_dtype != S2O_BF16) ||
+        (p->out_dtype != S2O_F32 && p->out_dtype != S2O_BF16))
+        return fail(S2O_ERR_INVALID_ARG, "unknown dtype");
+    if (seg_len < 1 || seg_len > p->l)
+        return fail(S2O_ERR_SEG_LEN, "segment length must satisfy 1 <= S <= L");
+    if (p->d > 512) return fail(S2O_ERR_UNSUPPORTED, "head dim D > 512 is not supported");
+    if (p->l > (int64_t(1) << 31) - 1) return fail(S2O_ERR_UNSUPPORTED, "L must fit int32");
+    Geo& o = *g;
+    o.z = p->z; o.hq = p->hq; o.hkv = p->hkv; o.l = p->l; o.d = p->d;
+    o.group = p->hq / p->hkv;
+    o.S = seg_len;
+    o.N = (p->l + seg_len - 1) / seg_len;
+    o.last_len = p->l - (o.N - 1) * seg_len;
+    for (int i = 0; i < 3; ++i) {
+        o.qs[i] = p->q_stride[i]; o.ks[i] = p->k_stride[i];
+        o.vs[i] = p->v_stride[i]; o.os[i] = p->o_stride[i];
+    }
+    o.in_bf16 = p->in_dtype == S2O_BF16;
+    o.out_bf16 = p->out_dtype == S2O_BF16;
+    return S2O_OK;
+}
+
+s2o_status validate_cfg(const s2o_kernel_config* c, int64_t l) {
+    if (!c) return fail(S2O_ERR_INVALID_ARG, "null config");
+    if (c->seg_len < 1 || c->seg_len > l)
+        return fail(S2O_ERR_SEG_LEN, "segment length must satisfy 1 <= S <= L");
+    if (!(c->tau >= 0.0)) return fail(S2O_ERR_TAU, "tau must be >= 0");
+    if (c->b_m < 1 || c->b_n < 1) return fail(S2O_ERR_TILES, "tile sizes must be >= 1");
+    if (c->local_window > c->seg_len)
+        return fail(S2O_ERR_LOCAL_WINDOW, "local window must satisfy W <= S");
+    if (c->fused && c->q_reorder)
+        return fail(S2O_ERR_FUSED_REORDER, "fused variant requires q_reorder = false");
+    return S2O_OK;
+}
+
+PassArgs base_args(const Geo& g, const s2o_kernel_config* c) {
+    PassArgs a;
+    std::memset(&a, 0, sizeof a);
+    a.g = g;
+    a.bm = c->b_m;
+    a.bn = c->b_n;
+    a.tau = c->tau;
+    a.scale = 1.0 / std::sqrt((double)g.d);
+    a.q_reorder = c->q_reorder;
+    a.T = (g.S + c->b_m - 1) / c->b_m;
+    a.tiles_per_head = (g.N - 1) * a.T + (g.last_len + c->b_m - 1) / c->b_m;
+    return a;
+}
+
+bool path_is_tc(const PassArgs& a, int32_t path) {
+    if (path == S2O_PATH_GENERIC) return false;
+    return tc_supported(a);
+}
+
+// Pass scratch: generic path scratch + error flag.
+size_t pass_ws_bytes(const PassArgs& a) { return align256(generic_scratch_bytes(a)) + 256; }
+
+s2o_status run_pass(PassArgs a, int32_t path, void* ws, size_t ws_bytes, cudaStream_t st) {
+    char* base = reinterpret_cast<char*>(ws);
+    if (!ws || ws_bytes < pass_ws_bytes(a)) return fail(S2O_ERR_WORKSPACE, "workspace too small");
+    a.err_flag = reinterpret_cast<int32_t*>(base + align256(generic_scratch_bytes(a)));
+    if (path == S2O_PATH_TCGEN05 && !tc_supported(a))
+        return fail(S2O_ERR_UNSUPPORTED,
+                    "tcgen05 path needs bf16 inputs, D=128, b_m=128, b_n in {64,128}");
+    if (path_is_tc(a, path)) {
+        S2O_CUDA_TRY(launch_tc_pass(a, st), "tcgen05 pass launch");
+    } else {
+        S2O_CUDA_TRY(launch_generic_pass(a, base, st), "generic pass launch");
+    }
+    return S2O_OK;
+}
+
+// Stream/arena for the host-buffer entry point.
+struct HostArena {
+    std::mutex mu;
+    cudaStream_t stream = nullptr;
+    void* dev = nullptr;
+    size_t bytes = 0;
+} g_host;
+
+}  // namespace
+}  // namespace s2o
+
+using namespace s2o;
+
+extern "C" {
+
+int s2o_abi_version(void) { return S2O_ABI_VERSION; }
+
+const char* s2o_last_error(void) { return g_err.c_str(); }
+
+const char* s2o_status_string(int status) {
+    switch (status) {
+        case S2O_OK: return "ok";
+        case S2O_ERR_SEG_LEN: return "segment length must satisfy 1 <= S <= L";
+        case S2O_ERR_TAU: return "tau must be >= 0";
+        case S2O_ERR_TILES: return "tile sizes must be >= 1";
+        case S2O_ERR_LOCAL_WINDOW: return "local window must satisfy W <= S";
+        case S2O_ERR_FUSED_REORDER: return "fused variant requires q_reorder = false";
+        case S2O_ERR_FUSED_FLAGS: return "fused variant requires fused = true, q_reorder = false";
+        case S2O_ERR_PLAN_MISMATCH: return "plan/config mismatch: segment layout differs";
+        case S2O_ERR_BUFS_MISMATCH: return "pass buffers do not match tensor dims";
+        case S2O_ERR_QKV_DIMS: return "Q/K/V dims must match";
+        case S2O_ERR_UNINIT_STATE: return "uninitialized state";
+        case S2O_ERR_EMPTY_SCORES: return "empty score vector";
+        case S2O_ERR_UNCOVERED_ROW: return "uncovered query row";
+        case S2O_ERR_NORMALIZER_ALIGN: return "normalizer vectors must align";
+        case S2O_ERR_INVALID_ARG: return "invalid argument";
+        case S2O_ERR_UNSUPPORTED: return "unsupported shape";
+        case S2O_ERR_WORKSPACE: return "workspace too small";
+        case S2O_ERR_CUDA: return "CUDA error";
+        case S2O_ERR_NO_DEVICE: return "no usable sm_100 device";
+        default: return "unknown status";
+    }
+}
+
+void s2o_problem_init(s2o_problem* p, int64_t z, int64_t hq, int64_t hkv, int64_t l, int64_t d,
+                      int32_t in_dtype, int32_t out_dtype) {
+    std::memset(p, 0, sizeof *p);
+    p->z = z; p->hq = hq; p->hkv = hkv; p->l = l; p->d = d;
+    p->in_dtype = in_dtype;
+    p->out_dtype = out_dtype;
+    const int64_t qs[3] = {hq * l * d, l * d, d};
+    const int64_t ks[3] = {hkv * l * d, l * d, d};
+    for (int i = 0; i < 3; ++i) {
+        p->q_stride[i] = qs[i]; p->o_stride[i] = qs[i];
+        p->k_stride[i] = ks[i]; p->v_stride[i] = ks[i];
+    }
+}
+
+void s2o_kernel_config_init(s2o_kernel_config* c) {
+    std::memset(c, 0, sizeof *c);
+    c->seg_len = 128;
+    c->tau = 0.005;
+    c->b_m = 128;
+    c->b_n = 128;
+    c->q_reorder = 1;
+    c->fused = 0;
+    c->local_window = -1;
+    c->path = S2O_PATH_AUTO;
+    c->score_mode = S2O_SCORE_EXACT;
+}
+
+s2o_status s2o_kernel_config_validate(const s2o_kernel_config* c, int64_t l) {
+    s2o_status st = validate_cfg(c, l);
+    if (st == S2O_OK) g_err.clear();
+    return st;
+}
+
+s2o_status s2o_early_stop_check(const double* prev, const double* nw, int64_t n, double tau,
+                                int32_t* stop) {
+    if (!prev || !nw || !stop || n <= 0)
+        return fail(S2O_ERR_NORMALIZER_ALIGN, "normalizer vectors must align");
+    double max_gain = -INFINITY;
+    for (int64_t r = 0; r < n; ++r) {
+        if (prev[r] <= 0.0) return fail(S2O_ERR_UNINIT_STATE, "uninitialized state");
+        const double g = (nw[r] - prev[r]) / prev[r];
+        max_gain = (max_gain < g) ? g : max_gain;
+    }
+    *stop = max_gain < tau;
+    return S2O_OK;
+}
+
+s2o_status s2o_select_path(const s2o_problem* p, const s2o_kernel_config* c, int32_t* path) {
+    Geo g;
+    s2o_status st = make_geo(p, c ? c->seg_len : 0, &g);
+    if (st) return st;
+    if ((st = validate_cfg(c, p->l))) return st;
+    PassArgs a = base_args(g, c);
+    *path = path_is_tc(a, c->path) ? S2O_PATH_TCGEN05 : S2O_PATH_GENERIC;
+    return S2O_OK;
+}
+
+s2o_status s2o_plan_workspace_size(const s2o_problem* p, int64_t seg_len, size_t* bytes) {
+    Geo g;
+    s2o_status st = make_geo(p, seg_len, &g);
+    if (st) return st;
+    *bytes = plan_workspace_bytes(g);
+    return S2O_OK;
+}
+
+s2o_status s2o_segment_representatives(const s2o_problem* p, const void* q, const void* k,
+                                       int64_t seg_len, float* q_mean, float* k_mean,
+                                       void* stream) {
+    Geo g;
+    s2o_status st = make_geo(p, seg_len, &g);
+    if (st) return st;
+    if (!q || !k) return fail(S2O_ERR_INVALID_ARG, "null tensor");
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    if (q_mean) S2O_CUDA_TRY(launch_segment_means(g, q, 0, g.N, q_mean, s), "segment means");
+    if (k_mean) S2O_CUDA_TRY(launch_segment_means(g, k, 1, g.N, k_mean, s), "segment means");
+    return S2O_OK;
+}
+
+s2o_status s2o_plan_build(const s2o_problem* p, const void* q, const void* k,
+                          const s2o_kernel_config* cfg, int32_t* q_perm, int32_t* kv_perm,
+                          int64_t* cost2, void* workspace, size_t workspace_bytes, void* stream) {
+    if (!cfg) return fail(S2O_ERR_INVALID_ARG, "null config");
+    Geo g;
+    s2o_status st = make_geo(p, cfg->seg_len, &g);
+    if (st) return st;
+    if (!q || !k || !q_perm || (g.N > 1 && !kv_perm)) return fail(S2O_ERR_INVALID_ARG, "null pointer");
+    if (!workspace || workspace_bytes < plan_workspace_bytes(g))
+        return fail(S2O_ERR_WORKSPACE, "workspace too small");
+    if (cfg->score_mode != S2O_SCORE_EXACT && cfg->score_mode != S2O_SCORE_FAST)
+        return fail(S2O_ERR_INVALID_ARG, "unknown score mode");
+    void* ws = reinterpret_cast<void*>((reinterpret_cast<uintptr_t>(workspace) + 255) & ~uintptr_t(255));
+    S2O_CUDA_TRY(launch_plan_build(g, q, k, q_perm, kv_perm, ws, reinterpret_cast<cudaStream_t>(stream)),
+                 "plan build");
+    if (cost2) {
+        // RankingCost per slice: L query dots + sum of prefixes (plan.cpp:93-94, 130-131)
+        const int64_t dots = g.l + g.S * g.N * (g.N - 1) / 2;
+        cost2[0] = dots;
+        cost2[1] = dots;
+    }
+    g_err.clear();
+    return S2O_OK;
+}
+
+s2o_status s2o_pass_workspace_size(const s2o_problem* p, const s2o_kernel_config* cfg,
+                                   size_t* bytes) {
+    Geo g;
+    s2o_status st = make_geo(p, cfg ? cfg->seg_len : 0, &g);
+    if (st) return st;
+    if ((st = validate_cfg(cfg, p->l))) return st;
+    *bytes = pass_ws_bytes(base_args(g, cfg));
+    return S2O_OK;
+}
+
+s2o_status s2o_pass1(const s2o_problem* p, const void* q, const void* k, const void* v,
+                     const s2o_kernel_config* cfg, float* acc, float* ell, float* m,
+                     void* workspace, size_t workspace_bytes, void* stream) {
+    Geo g;
+    s2o_status st = make_geo(p, cfg ? cfg->seg_len : 0, &g);
+    if (st) return st;
+    if ((st = validate_cfg(cfg, p->l))) return st;
+    if (!q || !k || !v || !acc || !ell || !m) return fail(S2O_ERR_INVALID_ARG, "null pointer");
+    PassArgs a = base_args(g, cfg);
+    a.mode = kDiag | kStateOut;
+    a.q = q; a.k = k; a.v = v;
+    a.acc_out = acc; a.ell_out = ell; a.m_out = m;
+    a.q_reorder = 0;
+    st = run_pass(a, cfg->path, workspace, workspace_bytes, reinterpret_cast<cudaStream_t>(stream));
+    if (st == S2O_OK) g_err.clear();
+    return st;
+}
+
+s2o_status s2o_pass2(const s2o_problem* p, const void* q, const void* k, const void* v,
+                     const s2o_kernel_config* cfg, const float* acc, const float* ell,
+                     const float* m, const int32_t* q_perm, const int32_t* kv_perm, void* o,
+                     int32_t* processed, int64_t* pass1_pairs, int64_t* pass2_pairs,
+                     void* workspace, size_t workspace_bytes, void* stream) {
+    Geo g;
+    s2o_status st = make_geo(p, cfg ? cfg->seg_len : 0, &g);
+    if (st) return st;
+    if ((st = validate_cfg(cfg, p->l))) return st;
+    if (!q || !k || !v || !acc || !ell || !m || !o || !processed || !pass2_pairs ||
+        (cfg->q_reorder && !q_perm) || (g.N > 1 && !kv_perm))
+        return fail(S2O_ERR_INVALID_ARG, "null pointer");
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    PassArgs a = base_args(g, cfg);
+    a.mode = kStateIn | kPrefix | kFinal;
+    a.q = q; a.k = k; a.v = v; a.o = o;
+    a.acc_in = acc; a.ell_in = ell; a.m_in = m;
+    a.q_perm = q_perm; a.kv_perm = kv_perm;
+    a.processed = processed; a.pass2_pairs = pass2_pairs;
+    S2O_CUDA_TRY(launch_trace_init(a, pass1_pairs, s), "trace init");
+    st = run_pass(a, cfg->path, workspace, workspace_bytes, s);
+    if (st == S2O_OK) g_err.clear();
+    return st;
+}
+
+s2o_status s2o_fused(const s2o_problem* p, const void* q, const void* k, const void* v,
+                     const s2o_kernel_config* cfg, const int32_t* kv_perm, void* o,
+                     int32_t* processed, int64_t* pass1_pairs, int64_t* pass2_pairs,
+                     void* workspace, size_t workspace_bytes, void* stream) {
+    if (cfg && (!cfg->fused || cfg->q_reorder))
+        return fail(S2O_ERR_FUSED_FLAGS, "fused variant requires fused = true, q_reorder = false");
+    Geo g;
+    s2o_status st = make_geo(p, cfg ? cfg->seg_len : 0, &g);
+    if (st) return st;
+    if ((st = validate_cfg(cfg, p->l))) return st;
+    if (!q || !k || !v || !o || !processed || !pass2_pairs || (g.N > 1 && !kv_perm))
+        return fail(S2O_ERR_INVALID_ARG, "null pointer");
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    PassArgs a = base_args(g, cfg);
+    a.mode = kDiag | kPrefix | kFinal;
+    a.q = q; a.k = k; a.v = v; a.o = o;
+    a.kv_perm = kv_perm;
+    a.processed = processed; a.pass2_pairs = pass2_pairs;
+    a.q_reorder = 0;
+    S2O_CUDA_TRY(launch_trace_init(a, pass1_pairs, s), "trace init");
+    st = run_pass(a, cfg->path, workspace, workspace_bytes, s);
+    if (st == S2O_OK) g_err.clear();
+    return st;
+}
+
+// Workspace of the whole operator:
+//   [plan ws][pass ws][q_perm][kv_perm][acc][ell][m][processed][pass1][pass2]
+struct OpLayout {
+    size_t plan, pass, qperm, kvperm, acc, ell, m, proc, p1, p2, total;
+};
+
+static OpLayout op_layout(const Geo& g, const PassArgs& a, int fused) {
+    OpLayout L;
+    size_t off = 0;
+    auto take = [&](size_t b) { size_t o = off; off += align256(b); return o; };
+    const int64_t zh = g.z * g.hq;
+    L.plan = take(plan_workspace_bytes(g));
+    L.pass = take(pass_ws_bytes(a));
+    L.qperm = take(sizeof(int32_t) * zh * g.N * g.S);
+    L.kvperm = take(sizeof(int32_t) * std::max<int64_t>(1, zh * g.kv_per_head()));
+    L.acc = take(fused ? 0 : sizeof(float) * zh * g.l * g.d);
+    L.ell = take(fused ? 0 : sizeof(float) * zh * g.l);
+    L.m = take(fused ? 0 : sizeof(float) * zh * g.l);
+    L.proc = take(sizeof(int32_t) * zh * g.N * a.T);
+    L.p1 = take(sizeof(int64_t) * zh);
+    L.p2 = take(sizeof(int64_t) * zh);
+    L.total = off + 256;
+    return L;
+}
+
+s2o_status s2o_attention_workspace_size(const s2o_problem* p, const s2o_kernel_config* cfg,
+                                        size_t* bytes) {
+    Geo g;
+    s2o_status st = make_geo(p, cfg ? cfg->seg_len : 0, &g);
+    if (st) return st;
+    if ((st = validate_cfg(cfg, p->l))) return st;
+    *bytes = op_layout(g, base_args(g, cfg), cfg->fused).total;
+    return S2O_OK;
+}
+
+s2o_status s2o_attention_fwd(const s2o_problem* p, const void* q, const void* k, const void* v,
+                             const s2o_kernel_config* cfg, void* o, int32_t* q_perm,
+                             int32_t* kv_perm, int32_t* processed, int64_t* pass1_pairs,
+                             int64_t* pass2_pairs, void* workspace, size_t workspace_bytes,
+                             void* stream) {
+    Geo g;
+    s2o_status st = make_geo(p, cfg ? cfg->seg_len : 0, &g);
+    if (st) return st;
+    if ((st = validate_cfg(cfg, p->l))) return st;
+    if (!q || !k || !v || !o) return fail(S2O_ERR_INVALID_ARG, "null pointer");
+    PassArgs a = base_args(g, cfg);
+    const OpLayout L = op_layout(g, a, cfg->fused);
+    if (!workspace || workspace_bytes < L.total) return fail(S2O_ERR_WORKSPACE, "workspace too small");
+    char* base = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(workspace) + 255) & ~uintptr_t(255));
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    int32_t* qp = q_perm ? q_perm : reinterpret_cast<int32_t*>(base + L.qperm);
+    int32_t* kvp = kv_perm ? kv_perm : reinterpret_cast<int32_t*>(base + L.kvperm);
+    int32_t* proc = processed ? processed : reinterpret_cast<int32_t*>(base + L.proc);
+    int64_t* p1 = pass1_pairs ? pass1_pairs : reinterpret_cast<int64_t*>(base + L.p1);
+    int64_t* p2 = pass2_pairs ? pass2_pairs : reinterpret_cast<int64_t*>(base + L.p2);
+    S2O_CUDA_TRY(launch_plan_build(g, q, k, qp, kvp, base + L.plan, s), "plan build");
+    a.q = q; a.k = k; a.v = v; a.o = o;
+    a.kv_perm = kvp;
+    a.processed = proc;
+    a.pass2_pairs = p2;
+    S2O_CUDA_TRY(launch_trace_init(a, p1, s), "trace init");
+    if (cfg->fused) {
+        a.mode = kDiag | kPrefix | kFinal;
+        a.q_reorder = 0;
+        st = run_pass(a, cfg->path, base + L.pass, pass_ws_bytes(a), s);
+        if (st) return st;
+    } else {
+        float* acc = reinterpret_cast<float*>(base + L.acc);
+        float* ell = reinterpret_cast<float*>(base + L.ell);
+        float* m = reinterpret_cast<float*>(base + L.m);
+        PassArgs a1 = a;
+        a1.mode = kDiag | kStateOut;
+        a1.q_reorder = 0;
+        a1.acc_out = acc; a1.ell_out = ell; a1.m_out = m;
+        if ((st = run_pass(a1, cfg->path, base + L.pass, pass_ws_bytes(a), s))) return st;
+        PassArgs a2 = a;
+        a2.mode = kStateIn | kPrefix | kFinal;
+        a2.q_perm = qp;
+        a2.acc_in = acc; a2.ell_in = ell; a2.m_in = m;
+        if ((st = run_pass(a2, cfg->path, base + L.pass, pass_ws_bytes(a), s))) return st;
+    }
+    g_err.clear();
+    return S2O_OK;
+}
+
+s2o_status s2o_dense_causal_fwd(const s2o_problem* p, const void* q, const void* k,
+                                const void* v, int32_t path, void* o, void* workspace,
+                                size_t workspace_bytes, void* stream) {
+    Geo g;
+    s2o_status st = make_geo(p, p ? p->l : 0, &g);  // one segment: S = L
+    if (st) return st;
+    if (!q || !k || !v || !o) return fail(S2O_ERR_INVALID_ARG, "null pointer");
+    s2o_kernel_config c;
+    s2o_kernel_config_init(&c);
+    c.seg_len = p->l;
+    c.q_reorder = 0;
+    c.path = path;
+    if (path == S2O_PATH_GENERIC) { c.b_m = 64; c.b_n = 64; }
+    PassArgs a = base_args(g, &c);
+    a.mode = kDiag | kFinal;
+    a.q = q; a.k = k; a.v = v; a.o = o;
+    st = run_pass(a, path, workspace, workspace_bytes, reinterpret_cast<cudaStream_t>(stream));
+    if (st == S2O_OK) g_err.clear();
+    return st;
+}
+
+s2o_status s2o_attention_host(const s2o_problem* p, const void* q, const void* k, const void* v,
+                              const s2o_kernel_config* cfg, void* o, int32_t* q_perm,
+                              int32_t* kv_perm, int32_t* processed, int64_t* pass1_pairs,
+                              int64_t* pass2_pairs) {
+    Geo g;
+    s2o_status st = make_geo(p, cfg ? cfg->seg_len : 0, &g);
+    if (st) return st;
+    if ((st = validate_cfg(cfg, p->l))) return st;
+    if (!q || !k || !v || !o) return fail(S2O_ERR_INVALID_ARG, "null pointer");
+    // host buffers are dense [Z,H,L,D]
+    s2o_problem dp;
+    s2o_problem_init(&dp, p->z, p->hq, p->hkv, p->l, p->d, p->in_dtype, p->out_dtype);
+    PassArgs a = base_args(g, cfg);
+    const OpLayout L = op_layout(g, a, cfg->fused);
+    const size_t esz_in = p->in_dtype == S2O_BF16 ? 2 : 4;
+    const size_t esz_out = p->out_dtype == S2O_BF16 ? 2 : 4;
+    const size_t qb = esz_in * p->z * p->hq * p->l * p->d;
+    const size_t kb = esz_in * p->z * p->hkv * p->l * p->d;
+    const size_t ob = esz_out * p->z * p->hq * p->l * p->d;
+    const size_t need = align256(qb) + 2 * align256(kb) + align256(ob) + L.total;
+    std::lock_guard<std::mutex> lock(g_host.mu);
+    if (!g_host.stream) S2O_CUDA_TRY(cudaStreamCreateWithFlags(&g_host.stream, cudaStreamNonBlocking), "stream");
+    if (g_host.bytes < need) {
+        if (g_host.dev) cudaFree(g_host.dev);
+        g_host.dev = nullptr;
+        g_host.bytes = 0;
+        S2O_CUDA_TRY(cudaMalloc(&g_host.dev, need), "arena alloc");
+        g_host.bytes = need;
+    }
+    char* d = reinterpret_cast<char*>(g_host.dev);
+    char* dq = d;
+    char* dk = dq + align256(qb);
+    char* dv = dk + align256(kb);
+    char* dout = dv + align256(kb);
+    char* ws = dout + align256(ob);
+    cudaStream_t s = g_host.stream;
+    S2O_CUDA_TRY(cudaMemcpyAsync(dq, q, qb, cudaMemcpyHostToDevice, s), "h2d q");
+    S2O_CUDA_TRY(cudaMemcpyAsync(dk, k, kb, cudaMemcpyHostToDevice, s), "h2d k");
+    S2O_CUDA_TRY(cudaMemcpyAsync(dv, v, kb, cudaMemcpyHostToDevice, s), "h2d v");
+    char* wbase = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(ws) + 255) & ~uintptr_t(255));
+    st = s2o_attention_fwd(&dp, dq, dk, dv, cfg, dout, nullptr, nullptr, nullptr, nullptr, nullptr,
+                           ws, L.total, s);
+    if (st) return st;
+    S2O_CUDA_TRY(cudaMemcpyAsync(o, dout, ob, cudaMemcpyDeviceToHost, s), "d2h o");
+    const int64_t zh = g.z * g.hq;
+    if (q_perm)
+        S2O_CUDA_TRY(cudaMemcpyAsync(q_perm, wbase + L.qperm, sizeof(int32_t) * zh * g.N * g.S,
+                                     cudaMemcpyDeviceToHost, s), "d2h q_perm");
+    if (kv_perm && g.N > 1)
+        S2O_CUDA_TRY(cudaMemcpyAsync(kv_perm, wbase + L.kvperm, sizeof(int32_t) * zh * g.kv_per_head(),
+                                     cudaMemcpyDeviceToHost, s), "d2h kv_perm");
+    if (processed)
+        S2O_CUDA_TRY(cudaMemcpyAsync(processed, wbase + L.proc, sizeof(int32_t) * zh * g.N * a.T,
+                                     cudaMemcpyDeviceToHost, s), "d2h trace");
+    if (pass1_pairs)
+        S2O_CUDA_TRY(cudaMemcpyAsync(pass1_pairs, wbase + L.p1, sizeof(int64_t) * zh,
+                                     cudaMemcpyDeviceToHost, s), "d2h pairs");
+    if (pass2_pairs)
+        S2O_CUDA_TRY(cudaMemcpyAsync(pass2_pairs, wbase + L.p2, sizeof(int64_t) * zh,
+                                     cudaMemcpyDeviceToHost, s), "d2h pairs");
+    int32_t flag = 0;
+    S2O_CUDA_TRY(cudaMemcpyAsync(&flag, wbase + L.pass + align256(generic_scratch_bytes(a)),
+                                 sizeof(int32_t), cudaMemcpyDeviceToHost, s), "d2h flag");
+    S2O_CUDA_TRY(cudaStreamSynchronize(s), "sync");
+    if (flag == 1) return fail(S2O_ERR_UNINIT_STATE, "uninitialized state");
+    if (flag == 2) return fail(S2O_ERR_UNCOVERED_ROW, "uncovered query row");
+    g_err.clear();
+    return S2O_OK;
+}
+
+void s2o_host_release(void) {
+    std::lock_guard<std::mutex> lock(g_host.mu);
+    if (g_host.dev) cudaFree(g_host.dev);
+    g_host.dev = nullptr;
+    g_host.bytes = 0;
+    if (g_host.stream) cudaStreamDestroy(g_host.stream);
+    g_host.stream = nullptr;
+}
+
+}  // extern "C"

@@ -1,0 +1,65 @@
+// internal.h -- declarations shared between the translation units of libs2o_cuda.so.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <algorithm>
+
+#include "common.cuh"
+
+namespace s2o {
+
+// Pass modes (bit set).
+enum PassMode : int {
+    kDiag = 1,      // intra-segment causal scan (segment_causal_tile kernel.cpp:36-71)
+    kPrefix = 2,    // ranked prefix traversal with stop (traverse_prefix kernel.cpp:86-122)
+    kStateIn = 4,   // resume PassBuffers (kernel.cpp:275-286)
+    kStateOut = 8,  // persist PassBuffers (kernel.cpp:206-213)
+    kFinal = 16,    // finalize acc/ell and scatter (finalize_rows kernel.cpp:149-162)
+};
+
+struct PassArgs {
+    Geo g;
+    int64_t bm, bn;
+    double tau;
+    double scale;  // 1/sqrt(D) in fp64 (attention.cpp:47)
+    int mode;
+    int q_reorder;
+    const void* q;
+    const void* k;
+    const void* v;
+    void* o;
+    const float* acc_in;
+    const float* ell_in;
+    const float* m_in;
+    float* acc_out;
+    float* ell_out;
+    float* m_out;
+    const int32_t* q_perm;
+    const int32_t* kv_perm;
+    int32_t* processed;     // [Z*Hq][N][T]
+    int64_t* pass2_pairs;   // [Z*Hq]
+    int64_t T;              // query tiles per full segment = ceil(S/bm)
+    int64_t tiles_per_head; // sum over segments
+    int32_t* err_flag;      // device: 1 uninitialized state, 2 uncovered row
+};
+
+size_t plan_workspace_bytes(const Geo& g);
+cudaError_t launch_plan_build(const Geo& g, const void* q, const void* k, int32_t* q_perm,
+                              int32_t* kv_perm, void* workspace, cudaStream_t st);
+cudaError_t launch_segment_means(const Geo& g, const void* x, int which_kv, int64_t nseg_out,
+                                 float* out, cudaStream_t st);
+
+// generic SIMT fp64 path
+size_t generic_scratch_bytes(const PassArgs& a);
+cudaError_t launch_generic_pass(const PassArgs& a, void* scratch, cudaStream_t st);
+
+// tcgen05 path (bf16, D = 128, b_m = 128, b_n in {64, 128})
+bool tc_supported(const PassArgs& a);
+cudaError_t launch_tc_pass(const PassArgs& a, cudaStream_t st);
+
+// trace helpers
+cudaError_t launch_trace_init(const PassArgs& a, int64_t* pass1_pairs, cudaStream_t st);
+
+}  // namespace s2o

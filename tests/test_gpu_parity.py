@@ -1,0 +1,259 @@
+"""Parity of the CUDA path (through the C-ABI) with the CPU oracle. Needs a B200.
+
+Bars:
+  * plans (q_perm, kv_perm): bit-identical to the oracle (exact fp64 scoring mode);
+  * traces (processed tiles, pair counts): identical;
+  * outputs: generic SIMT path within rtol 2e-6 / atol 2e-6 of the oracle (fp64 math, fp32
+    pass buffers); tcgen05 path within the bf16 tolerance stated in tests/test_gpu_tc.py.
+"""
+from __future__ import annotations
+
+import os
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN, Cfg, bf16_round, t4
+
+pytestmark = pytest.mark.gpu
+
+GEN = 1  # s2o.PATH_GENERIC
+
+
+def dev(torch, x, dtype=None):
+    t = torch.from_numpy(np.ascontiguousarray(x)).cuda()
+    return t.to(dtype) if dtype is not None else t
+
+
+def kcfg(s2o, c: Cfg, path=GEN):
+    return s2o.KernelConfig(seg_len=c.seg_len, tau=c.tau, tiles=s2o.TileSpec(c.b_m, c.b_n),
+                            q_reorder=c.q_reorder, fused=c.fused, local_window=c.local_window,
+                            path=path)
+
+
+def expand(x, hq):
+    return np.repeat(x, hq // x.shape[1], axis=1)
+
+
+def run_gpu(torch, s2o, q, k, v, c: Cfg, path=GEN, dtype=None):
+    res = s2o.s2o_attention(dev(torch, q, dtype), dev(torch, k, dtype), dev(torch, v, dtype),
+                            kcfg(s2o, c, path))
+    torch.cuda.synchronize()
+    return res
+
+
+def test_plan_bit_identical_random(cuda, port):
+    import paper_2602_22575_b200 as s2o
+    torch = cuda
+    rng = np.random.default_rng(11)
+    shapes = [(37, 6, 8), (64, 5, 1), (300, 16, 7), (5000, 4, 1000), (9000, 3, 7), (4500, 8, 4500)]
+    for (l, d, s) in shapes:
+        q = rng.standard_normal((2, 2, l, d)).astype(np.float32)
+        k = rng.standard_normal((2, 2, l, d)).astype(np.float32)
+        if l == 64:  # identical keys / zero guide -> stable ties
+            k[:] = 0.5
+        plan, cost = s2o.build_plan(dev(torch, q), dev(torch, k), s)
+        want = port.build_plan(q, k, s)
+        mask = _last_seg_mask(l, s)
+        got_q = plan.q_perm.reshape(4, -1, s).cpu().numpy()
+        np.testing.assert_array_equal(got_q[:, mask], want.q_perm[:, mask], err_msg=f"q_perm {l},{d},{s}")
+        np.testing.assert_array_equal(plan.kv_perm.reshape(4, -1).cpu().numpy(), want.kv_perm,
+                                      err_msg=f"kv_perm {l},{d},{s}")
+        assert cost.dot_products == want.cost[0]
+
+
+def _last_seg_mask(l, s):
+    n = -(-l // s)
+    last = l - (n - 1) * s
+    m = np.ones((n, s), bool)
+    m[-1, last:] = False
+    return m
+
+
+def test_plan_q_perm_ragged_tail(cuda, port):
+    """Short last segment: only len(n) slots are meaningful (plan.hpp:24-26)."""
+    import paper_2602_22575_b200 as s2o
+    torch = cuda
+    rng = np.random.default_rng(3)
+    l, d, s = 50, 4, 8
+    q = rng.standard_normal((1, 1, l, d)).astype(np.float32)
+    k = rng.standard_normal((1, 1, l, d)).astype(np.float32)
+    plan, _ = s2o.build_plan(dev(torch, q), dev(torch, k), s)
+    want = port.build_plan(q, k, s)
+    mask = _last_seg_mask(l, s)
+    got = plan.q_perm[0, 0].cpu().numpy()
+    np.testing.assert_array_equal(got[mask], want.q_perm[0][mask])
+
+
+def test_generic_path_matches_oracle_random(cuda, port):
+    import paper_2602_22575_b200 as s2o
+    torch = cuda
+    rng = np.random.default_rng(2024)
+    for trial in range(40):
+        l = int(rng.integers(8, 70))
+        d = int(rng.integers(2, 9))
+        s = int(rng.integers(1, l + 1))
+        bm, bn = int(rng.integers(1, 9)), int(rng.integers(1, 9))
+        tau = [0.0, 0.002, 0.01, 0.08, 1e9][trial % 5]
+        reorder = trial % 2 == 0
+        fused = (not reorder) and trial % 4 == 1
+        q, k, v = (rng.standard_normal((1, 2, l, d)).astype(np.float32) for _ in range(3))
+        c = Cfg(s, tau, bm, bn, reorder, fused)
+        want_o, want_t, want_p = port.attention(q, k, v, c)
+        res = run_gpu(torch, s2o, q, k, v, c)
+        np.testing.assert_array_equal(res.trace.processed.reshape(2, -1).cpu().numpy(),
+                                      want_t.processed.reshape(2, -1), err_msg=f"trial {trial}")
+        np.testing.assert_array_equal(res.trace.pass1_pairs.reshape(-1).cpu().numpy(), want_t.pass1_pairs)
+        np.testing.assert_array_equal(res.trace.pass2_pairs.reshape(-1).cpu().numpy(), want_t.pass2_pairs)
+        np.testing.assert_allclose(res.out.cpu().numpy(), want_o, rtol=2e-6, atol=2e-6,
+                                   err_msg=f"trial {trial}")
+
+
+def test_reference_fixtures_through_gpu(cuda, fixtures):
+    import paper_2602_22575_b200 as s2o
+    from test_oracle import early_stop_inputs
+    torch = cuda
+    # pass-1 frozen states (test_kernel.cpp:121-132); fp32 pass buffers
+    f, p = fixtures["pass1_l8"], fixtures["plan_l8"]
+    for bn in (2, 4):
+        bufs = s2o.pass1_dense_init(dev(torch, t4(p["q"])), dev(torch, t4(p["k"])), dev(torch, t4(f["v"])),
+                                    kcfg(s2o, Cfg(4, 0.0, 2, bn)))
+        st = np.stack([bufs.m[0, 0].cpu().numpy(), bufs.ell[0, 0].cpu().numpy(),
+                       bufs.acc[0, 0, :, 0].cpu().numpy(), bufs.acc[0, 0, :, 1].cpu().numpy()], axis=1)
+        np.testing.assert_allclose(st, np.asarray(f["states"]), rtol=1e-6)
+    # plan fixture (test_plan.cpp:100-108)
+    plan, cost = s2o.build_plan(dev(torch, t4(p["q"])), dev(torch, t4(p["k"])), 4)
+    assert plan.q_perm[0, 0].cpu().tolist() == p["q_perm"]
+    assert plan.kv_perm[0, 0].cpu().tolist() == p["kv_perm_1"]
+    assert cost.dot_products == p["dot_products"]
+    reps = s2o.segment_representatives(dev(torch, t4(p["q"])), dev(torch, t4(p["k"])),
+                                       s2o.SegmentConfig.for_sequence(8, 4))
+    np.testing.assert_array_equal(reps.q_mean[0, 0].cpu().numpy(), np.asarray(p["q_mean"], np.float32))
+    np.testing.assert_array_equal(reps.k_mean[0, 0].cpu().numpy(), np.asarray(p["k_mean"], np.float32))
+    # early-stop fixture (test_kernel.cpp:200-233)
+    e = fixtures["early_stop_fixture"]
+    q, k, v = early_stop_inputs(fixtures)
+    c = kcfg(s2o, Cfg(e["seg_len"], e["tau"], e["b_m"], e["b_n"], e["q_reorder"]))
+    qd, kd, vd = dev(torch, q), dev(torch, k), dev(torch, v)
+    plan, _ = s2o.build_plan(qd, kd, e["seg_len"])
+    assert plan.kv_perm_at(0, 0, 1).cpu().tolist() == e["kv_perm_1"]
+    bufs = s2o.pass1_dense_init(qd, kd, vd, c)
+    out, tr = s2o.pass2_sparse(qd, kd, vd, bufs, plan, c)
+    assert tr.processed_tiles()[0] == e["processed"]
+    assert int(tr.pass1_pairs[0, 0]) == e["pass1_pairs"]
+    assert int(tr.pass2_pairs[0, 0]) == e["pass2_pairs"]
+    np.testing.assert_allclose(out[0, 0].cpu().numpy(), np.asarray(e["o"]), rtol=e["rel_eps"])
+    # dense golden (test_attention.cpp:61-69) via the S = L path
+    g = fixtures["dense_l4"]
+    o = s2o.dense_causal_attention(dev(torch, t4(g["q"])), dev(torch, t4(g["k"])), dev(torch, t4(g["v"])),
+                                   path=GEN)
+    np.testing.assert_allclose(o[0, 0].cpu().numpy(), np.asarray(g["o"]), rtol=g["rel_eps"])
+
+
+def test_tau0_is_dense_and_fused_equals_two_pass(cuda, port):
+    import paper_2602_22575_b200 as s2o
+    torch = cuda
+    rng = np.random.default_rng(109)
+    for trial in range(8):
+        l = int(rng.integers(10, 60))
+        d = int(rng.integers(2, 7))
+        s = int(rng.integers(1, l + 1))
+        bm, bn = int(rng.integers(1, 7)), int(rng.integers(1, 7))
+        tau = [0.0, 0.002, 0.01, 0.08, 1e9][trial % 5]
+        q, k, v = (rng.standard_normal((1, 2, l, d)).astype(np.float32) for _ in range(3))
+        two = run_gpu(torch, s2o, q, k, v, Cfg(s, tau, bm, bn, False, False))
+        one = run_gpu(torch, s2o, q, k, v, Cfg(s, tau, bm, bn, False, True))
+        assert torch.equal(two.trace.processed, one.trace.processed)
+        assert torch.equal(two.trace.pass2_pairs, one.trace.pass2_pairs)
+        np.testing.assert_allclose(two.out.cpu().numpy(), one.out.cpu().numpy(), rtol=1e-5, atol=1e-6)
+        if tau == 0.0:
+            dense = port.dense_causal(q, k, v)
+            np.testing.assert_allclose(two.out.cpu().numpy(), dense, atol=1e-4)
+
+
+def test_nan_poisoned_future_keys(cuda):
+    """Acceptance C4 / test_kernel.cpp:383-409 on the exact path."""
+    import paper_2602_22575_b200 as s2o
+    torch = cuda
+    rng = np.random.default_rng(149)
+    l = 32
+    q = rng.standard_normal((1, 1, l, 4)).astype(np.float32)
+    kc = rng.standard_normal((1, 1, l, 4)).astype(np.float32)
+    vc = rng.standard_normal((1, 1, l, 4)).astype(np.float32)
+    for tau in (0.0, 0.005, 0.05):
+        clean = run_gpu(torch, s2o, q, kc, vc, Cfg(8, tau, 4, 4)).out.cpu().numpy()
+        for cut in (5, 15, 23):
+            k, v = kc.copy(), vc.copy()
+            k[0, 0, cut + 1:] = np.nan
+            v[0, 0, cut + 1:] = np.nan
+            got = run_gpu(torch, s2o, q, k, v, Cfg(8, tau, 4, 4)).out.cpu().numpy()
+            assert np.isfinite(got[0, 0, cut]).all()
+            np.testing.assert_array_equal(got[0, 0, cut], clean[0, 0, cut])
+
+
+def test_c1_golden_on_gpu(cuda):
+    """BASELINE.json configs[0] (C1) through the C-ABI vs the committed reference golden."""
+    import paper_2602_22575_b200 as s2o
+    torch = cuda
+    g = np.load(os.path.join(GOLDEN, "c1_golden.npz"))
+    q, k, v = s2o.generate_synthetic("mixed", 64, 8.0, 0, 1, 1, 4096, 128)
+    res = run_gpu(torch, s2o, q, k, v, Cfg(512, 0.005, 64, 64))
+    np.testing.assert_array_equal(res.plan.q_perm.reshape(1, 8, 512).cpu().numpy(), g["q_perm"])
+    np.testing.assert_array_equal(res.plan.kv_perm.reshape(1, -1).cpu().numpy(), g["kv_perm"])
+    np.testing.assert_array_equal(res.trace.processed.reshape(1, 8, -1).cpu().numpy(), g["processed"])
+    np.testing.assert_array_equal(res.trace.pass2_pairs.reshape(-1).cpu().numpy(), g["pass2_pairs"])
+    np.testing.assert_allclose(res.out.cpu().numpy()[:, :, ::8], g["out_rows"], rtol=2e-6, atol=2e-6)
+
+
+def test_gqa_golden_generic(cuda):
+    """GQA (Hq=4, Hkv=2) bf16 inputs: the reference ran on K/V expanded h -> h/2."""
+    import paper_2602_22575_b200 as s2o
+    torch = cuda
+    g = np.load(os.path.join(GOLDEN, "gqa_golden.npz"))
+    q, k, v = s2o.generate_synthetic("mixed", 64, 8.0, 7, 1, 4, 4096, 128)
+    q, k, v = bf16_round(q), bf16_round(k[:, :2]), bf16_round(v[:, :2])
+    res = run_gpu(torch, s2o, q, k, v, Cfg(512, 0.005, 128, 128), dtype=torch.bfloat16)
+    np.testing.assert_array_equal(res.plan.q_perm.reshape(4, 8, 512).cpu().numpy(), g["q_perm"])
+    np.testing.assert_array_equal(res.plan.kv_perm.reshape(4, -1).cpu().numpy(), g["kv_perm"])
+    np.testing.assert_array_equal(res.trace.processed.reshape(4, 8, -1).cpu().numpy(), g["processed"])
+    out = res.out.float().cpu().numpy()[:, :, ::8]
+    np.testing.assert_allclose(out, g["out_rows"], rtol=8e-3, atol=8e-3)  # bf16 output rounding
+
+
+def test_strided_layout_and_host_api(cuda, port):
+    """[Z,L,H,D] views give the same result as [Z,H,L,D]; the host-buffer entry point matches."""
+    import paper_2602_22575_b200 as s2o
+    torch = cuda
+    rng = np.random.default_rng(5)
+    l, d = 96, 8
+    q = rng.standard_normal((1, 4, l, d)).astype(np.float32)
+    k = rng.standard_normal((1, 2, l, d)).astype(np.float32)
+    v = rng.standard_normal((1, 2, l, d)).astype(np.float32)
+    c = Cfg(32, 0.01, 8, 8)
+    base = run_gpu(torch, s2o, q, k, v, c)
+    qs = dev(torch, q.transpose(0, 2, 1, 3)).transpose(1, 2)
+    ks = dev(torch, k.transpose(0, 2, 1, 3)).transpose(1, 2)
+    vs = dev(torch, v.transpose(0, 2, 1, 3)).transpose(1, 2)
+    res = s2o.s2o_attention(qs, ks, vs, kcfg(s2o, c))
+    assert torch.equal(res.out, base.out)
+    assert torch.equal(res.trace.processed, base.trace.processed)
+    out, proc, p1, p2 = s2o.attention_host(q, k, v, kcfg(s2o, c))
+    np.testing.assert_array_equal(out, base.out.cpu().numpy())
+    np.testing.assert_array_equal(proc, base.trace.processed.cpu().numpy())
+    # GQA semantics == reference on expanded K/V
+    want_o, want_t, _ = port.attention(q, expand(k, 4), expand(v, 4), c)
+    np.testing.assert_array_equal(proc.reshape(4, -1), want_t.processed.reshape(4, -1))
+    np.testing.assert_allclose(out, want_o, rtol=2e-6, atol=2e-6)
+
+
+@pytest.mark.slow
+def test_plan_32k_bf16_bit_identical(cuda, port):
+    """One Llama head at 32K (C2 shape, S=2048): exact plan == oracle build_plan."""
+    import paper_2602_22575_b200 as s2o
+    torch = cuda
+    q, k, _ = s2o.generate_synthetic("mixed", 512, 8.0, 0, 1, 1, 32768, 128)
+    q, k = bf16_round(q), bf16_round(k)
+    plan, _ = s2o.build_plan(dev(torch, q, torch.bfloat16), dev(torch, k, torch.bfloat16), 2048)
+    want = port.build_plan(q, k, 2048)
+    np.testing.assert_array_equal(plan.q_perm.reshape(1, 16, 2048).cpu().numpy(), want.q_perm)
+    np.testing.assert_array_equal(plan.kv_perm.reshape(1, -1).cpu().numpy(), want.kv_perm)
