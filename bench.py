@@ -1,0 +1,419 @@
+"""bench.py -- S2O sparse prefill attention on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Workload (BASELINE.json configs[2]): one Llama-3.1-8B attention layer,
+32 q heads / 8 kv heads (GQA), d=128, bf16, L=131072, S=2048, tiles 128x128, tau=0.005, on
+the reference's stripe-structured synthetic input (generate_synthetic mixed, L/64 stripes,
+gain 8, seed = layer = rank). A step = the whole operator: plan (block scoring +
+permutation build) + pass-1 + pass-2 for all 32 heads.
+
+Multi-GPU: every rank runs its own layer (seed = rank) with no
+collective on the data path; `value` = max-over-ranks step time / N = ms per layer of the
+whole job ("scaling": "weak").
+
+Timing: W warm-up steps, then K steps bracketed by barrier + synchronize, CUDA events on the
+launching stream; inputs (1.6 GB) exceed L2 (126 MB). `e2e` runs the same operator through
+the host-buffer C-ABI entry point (s2o_attention_host) from pinned host memory, H2D of Q/K/V
+and D2H of O inside the timed region. `cpu_baseline` (rank 0, N=1) times the compiled
+reference (oracle/_ref) on a bounded prefix sample of the same input and extrapolates by the
+algorithmic pair count (see `cpu_baseline.sample`).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+HQ, HKV, D = 32, 8, 128
+PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
+METRIC = "S2O prefill attn ms @128K Llama-3.1-8B shape; speedup vs dense; MSE @sparsity"
+PAIRS_FILE = os.path.join(ROOT, "profiles", "c3_pairs.json")
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        d["_source"] = "measured"
+        return d
+    d = dict(PEAKS_FALLBACK)
+    d["_source"] = "fallback"
+    return d
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines: list[str] = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except FileNotFoundError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sms, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.lines:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sms.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for name, val in zip(names, parts[4:8]):
+                if val.lower() == "active":
+                    reasons.add(name)
+        sms.sort()
+        med = sms[len(sms) // 2] if sms else None
+        return {"sm_mhz": med, "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sms)}
+
+
+def make_inputs(torch, s2o, l: int, seed: int, device):
+    """Synthetic stripe-structured layer: Q = 32 heads, K/V = heads 0..7 of the same
+    generation (== an H=8 generation), rounded to bf16."""
+    q, k, v = s2o.generate_synthetic("mixed", l // 64, 8.0, seed, 1, HQ, l, D)
+    qd = torch.from_numpy(q).to(device).to(torch.bfloat16)
+    kd = torch.from_numpy(k[:, :HKV].copy()).to(device).to(torch.bfloat16)
+    vd = torch.from_numpy(v[:, :HKV].copy()).to(device).to(torch.bfloat16)
+    del q, k, v
+    return qd, kd, vd
+
+
+def cuda_time(torch, fn, reps: int, stream=None) -> float:
+    """Mean ms of fn() over reps, CUDA events on the current stream, synchronized."""
+    torch.cuda.synchronize()
+    a = torch.cuda.Event(enable_timing=True)
+    b = torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(reps):
+        fn()
+    b.record()
+    torch.cuda.synchronize()
+    return a.elapsed_time(b) / reps
+
+
+def plan_sort_passes(l: int, s: int) -> int:
+    n = -(-l // s)
+    max_len = (n - 1) * s
+    passes, w = 0, 2048
+    while w < max_len:
+        passes += 1
+        w *= 2
+    return passes
+
+
+def launches_per_step(l: int, s: int) -> int:
+    n = -(-l // s)
+    count = 2  # guide means, q ranking (+ in-CTA q sort)
+    if s > 2048:
+        count += 2 + plan_sort_passes(l, s)
+    if n > 1:
+        count += 1 + 2 + plan_sort_passes(l, s)  # kv scoring, table, run sort, merges
+    return count + 3  # trace init, pass-1, pass-2
+
+
+# ------------------------------------------------------------------ reference (CPU) arm
+def reference_sample(l_full: int, s: int, tau: float, seg_sample: int, threads: int):
+    """Run the compiled reference on `threads` heads of the first `seg_sample` segments of the
+    benchmark input (causality: segments 0..m-1 of the full problem are exactly the problem
+    on the first m*S tokens). Returns (seconds, pairs_sample_per_head)."""
+    import numpy as np
+
+    import paper_2602_22575_b200 as s2o
+    from oracle.oracle import Ref, build
+
+    build()
+    ref = Ref()
+    lp = min(l_full, seg_sample * s)
+    q, k, v = s2o.generate_synthetic("mixed", l_full // 64, 8.0, 0, 1, HQ, l_full, D)
+    hs = list(range(threads))
+    # bf16-rounded inputs, K/V expanded h -> h/4 (the reference has no GQA)
+    def bf(x):
+        u = np.ascontiguousarray(x, np.float32).view(np.uint32).astype(np.uint64)
+        return (((u + 0x7FFF + ((u >> 16) & 1)) >> 16) << 16).astype(np.uint32).view(np.float32)
+    qs = bf(q[:, hs, :lp])
+    ks = bf(k[:, [h // (HQ // HKV) for h in hs], :lp])
+    vs = bf(v[:, [h // (HQ // HKV) for h in hs], :lp])
+    del q, k, v
+
+    class Cfg:
+        pass
+    cfg = Cfg()
+    cfg.seg_len, cfg.tau, cfg.b_m, cfg.b_n = s, tau, 128, 128
+    cfg.q_reorder, cfg.fused, cfg.local_window = True, False, -1
+    os.environ["S2O_THREADS"] = str(threads)
+    t0 = time.perf_counter()
+    _, tr, _ = ref.attention(qs, ks, vs, cfg)
+    secs = time.perf_counter() - t0
+    pairs = float((tr.pass1_pairs + tr.pass2_pairs).mean())
+    return secs, pairs
+
+
+def full_pairs_per_head(l: int) -> float | None:
+    if os.path.exists(PAIRS_FILE):
+        with open(PAIRS_FILE) as f:
+            d = json.load(f)
+        if int(d.get("L", 0)) == l:
+            return float(d["pairs_per_head"])
+    return None
+
+
+def cpu_extrapolate(secs: float, pairs_sample: float, pairs_full: float, threads: int) -> float:
+    """ms per layer (32 heads) on `threads` cores, heads in parallel (parallel.cpp:25-66)."""
+    per_head = secs * pairs_full / pairs_sample  # each thread ran one head's sample
+    waves = math.ceil(HQ / threads)
+    return per_head * waves * 1e3
+
+
+def run_reference_arm(args, rank: int):
+    if rank != 0:
+        return
+    cores = os.cpu_count() or 1
+    threads = min(cores, HQ)
+    pairs_full = full_pairs_per_head(args.L)
+    vals = []
+    for i in range(args.warmup + args.steps):
+        secs, pairs = reference_sample(args.L, args.seg, args.tau, args.ref_segments, threads)
+        if pairs_full is None:
+            pairs_full = pairs * (args.L / (args.ref_segments * args.seg)) ** 1.2  # crude guess
+        if i >= args.warmup:
+            vals.append(cpu_extrapolate(secs, pairs, pairs_full, threads))
+    value = sum(vals) / len(vals)
+    out = {
+        "impl": "reference", "metric": METRIC, "value": round(value, 3), "unit": "ms",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(value, 3),
+        "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (reference generate_synthetic mixed, bf16-rounded)",
+        "config": {"workload": "C3: 1 layer, 32q/8kv heads, d=128, L=%d, S=%d, tau=%g" % (args.L, args.seg, args.tau)},
+        "cpu_baseline": {"value": round(value, 3), "unit": "ms", "cores": threads, "kind": "reference",
+                         "sample": f"compiled reference s2o_attention on {threads} heads x first "
+                                   f"{args.ref_segments} segments ({args.ref_segments * args.seg} tokens), "
+                                   f"extrapolated by pass1+pass2 pair count to {HQ} heads x L={args.L}"},
+        "e2e": {"value": round(value, 3), "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "gpu_launches": 0,
+    }
+    print(json.dumps(out), flush=True)
+
+
+# ------------------------------------------------------------------ our arm
+def run_ours(args, rank: int, world: int):
+    import torch
+
+    import paper_2602_22575_b200 as s2o
+
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+    s2o.lib()
+    L, S = args.L, args.seg
+    cfg = s2o.KernelConfig(seg_len=S, tau=args.tau, tiles=s2o.TileSpec(128, 128), q_reorder=True)
+    q, k, v = make_inputs(torch, s2o, L, seed=rank, device=dev)
+    out = torch.empty_like(q)
+    path = s2o.select_path(q, k, v, cfg)
+
+    def step():
+        s2o.s2o_attention(q, k, v, cfg, out=out, want_plan=False)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    clocks = ClockSampler(local)
+    clocks.start()
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record()
+    for _ in range(args.steps):
+        step()
+    ev1.record()
+    torch.cuda.synchronize()
+    elapsed = ev0.elapsed_time(ev1)
+    clk = clocks.stop()
+    if dist:
+        t = torch.tensor([elapsed], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        elapsed = t.item()
+        dist.barrier()
+    ms_step = elapsed / args.steps
+    value = ms_step / world
+
+    # ---- stage breakdown, trace, roofline (device-resident inputs)
+    res = s2o.s2o_attention(q, k, v, cfg)
+    torch.cuda.synchronize()
+    p1 = int(res.trace.pass1_pairs.sum().item())
+    p2 = int(res.trace.pass2_pairs.sum().item())
+    total_pairs = HQ * L * (L + 1) // 2
+    sparsity = 1.0 - (p1 + p2) / total_pairs
+    plan, _ = s2o.build_plan(q, k, S)
+    t_plan = cuda_time(torch, lambda: s2o.build_plan(q, k, S), 3)
+    t_p1 = cuda_time(torch, lambda: s2o.pass1_dense_init(q, k, v, cfg), 3)
+    bufs = s2o.pass1_dense_init(q, k, v, cfg)
+    t_p2 = cuda_time(torch, lambda: s2o.pass2_sparse(q, k, v, bufs, plan, cfg, out=out), 3)
+    del bufs
+    pk = peaks()
+    f_p1, f_p2 = 4.0 * D * p1, 4.0 * D * p2
+    if t_p2 >= t_p1:
+        dom, f_dom, t_dom = "tc_pass_kernel (pass-2)", f_p2, t_p2
+    else:
+        dom, f_dom, t_dom = "tc_pass_kernel (pass-1)", f_p1, t_p1
+    achieved = f_dom / (t_dom * 1e-3) / 1e12
+    peak = float(pk.get("bf16_tflops", PEAKS_FALLBACK["bf16_tflops"]))
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(prof):
+        with open(prof) as f:
+            traffic = json.load(f).get("dram_bytes_per_launch")
+    roofline = {"bound": "tensor", "kernel": dom, "achieved": round(achieved, 2), "peak": peak,
+                "unit": "TFLOP/s", "frac": round(achieved / peak, 4), "traffic": traffic,
+                "peak_source": pk["_source"] + " burst bf16",
+                "work": "4*D*(committed pairs) per launch, from the kernel's own trace"}
+    # dense comparator on the same GPU (cuDNN/flash SDPA, bf16, causal, GQA)
+    dense_ms = None
+    mse = None
+    if rank == 0 and not args.no_dense:
+        try:
+            def dense():
+                return torch.nn.functional.scaled_dot_product_attention(q, k, v, is_causal=True, enable_gqa=True)
+            dense()
+            dense_ms = cuda_time(torch, dense, 2)
+            od = dense().float()
+            diff = (res.out.float() - od)
+            mse = float((diff * diff).mean().item())
+            del od, diff
+        except Exception as e:  # noqa: BLE001
+            dense_ms = f"unavailable: {type(e).__name__}"
+
+    # ---- e2e through the host-buffer C-ABI entry point
+    e2e = None
+    if not args.no_e2e:
+        qh = q.cpu().pin_memory()
+        kh = k.cpu().pin_memory()
+        vh = v.cpu().pin_memory()
+        oh = torch.empty_like(qh).pin_memory()
+        s2o.attention_host_ptr(qh, kh, vh, oh, cfg)
+        if dist:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            s2o.attention_host_ptr(qh, kh, vh, oh, cfg)
+        e_ms = (time.perf_counter() - t0) * 1e3 / args.e2e_steps
+        if dist:
+            t = torch.tensor([e_ms], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e_ms = t.item()
+        s2o.lib().s2o_host_release()
+        hb = (qh.numel() + kh.numel() + vh.numel()) * qh.element_size()
+        db = oh.numel() * oh.element_size()
+        e2e = {"value": round(e_ms / world, 3), "unit": "ms", "h2d_bytes_per_step": hb, "d2h_bytes_per_step": db,
+               "timer": "host wall clock around the synchronous C-ABI call"}
+
+    # ---- CPU baseline: compiled reference on a bounded sample (rank 0, N=1)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        try:
+            os.makedirs(os.path.dirname(PAIRS_FILE), exist_ok=True)
+            with open(PAIRS_FILE, "w") as f:
+                json.dump({"L": L, "S": S, "tau": args.tau, "pairs_per_head": (p1 + p2) / HQ,
+                           "pass1_pairs": p1, "pass2_pairs": p2}, f)
+            cores = os.cpu_count() or 1
+            threads = min(cores, HQ)
+            secs, pairs = reference_sample(L, S, args.tau, args.ref_segments, threads)
+            val = cpu_extrapolate(secs, pairs, (p1 + p2) / HQ, threads)
+            cpu = {"value": round(val, 1), "unit": "ms", "cores": threads, "kind": "reference",
+                   "sample": f"compiled reference s2o_attention on {threads} heads x first {args.ref_segments} "
+                             f"segments ({args.ref_segments * S} tokens) took {secs:.2f} s; extrapolated by "
+                             f"pass1+pass2 pair count to {HQ} heads x L={L}"}
+        except Exception as e:  # noqa: BLE001
+            cpu = {"value": None, "unit": "ms", "cores": 0, "kind": "reference", "sample": f"failed: {e}"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 4), "unit": "ms", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 4),
+            "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic (reference generate_synthetic mixed stripes, L/64 stripes, gain 8, seed=rank)",
+            "config": {"workload": "C3: one Llama-3.1-8B attention layer per rank (32 q / 8 kv heads GQA, d=128)",
+                       "seq_len": L, "seg_len": S, "tiles": [128, 128], "tau": args.tau,
+                       "parallelism": f"layer-per-rank x{world}, no collective",
+                       "l2": "inputs 1.6 GB > 126 MB L2 (no flush needed)", "path": {1: "generic", 2: "tcgen05"}[path]},
+            "breakdown_ms": {"plan": round(t_plan, 3), "pass1": round(t_p1, 3), "pass2": round(t_p2, 3)},
+            "sparsity": round(sparsity, 5), "pairs": {"pass1": p1, "pass2": p2},
+            "dense_ms": round(dense_ms, 3) if isinstance(dense_ms, float) else dense_ms,
+            "speedup_vs_dense": round(dense_ms / ms_step, 2) if isinstance(dense_ms, float) else None,
+            "mse_vs_dense": mse,
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": launches_per_step(L, S) * args.steps,
+            "clocks": clk,
+        }
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--L", type=int, default=131072)
+    ap.add_argument("--seg", type=int, default=2048)
+    ap.add_argument("--tau", type=float, default=0.005)
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--ref-segments", type=int, default=8)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-dense", action="store_true")
+    args = ap.parse_args()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if args.impl == "reference":
+        run_reference_arm(args, rank)
+        return
+    run_ours(args, rank, world)
+
+
+if __name__ == "__main__":
+    main()

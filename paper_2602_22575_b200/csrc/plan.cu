@@ -22,6 +22,7 @@
 //   merge_pass_kernel  merge-path merge of sorted run pairs, 2048 outputs per CTA
 #include "common.cuh"
 #include "internal.h"
+#include "sort.cuh"
 
 namespace s2o {
 
@@ -29,8 +30,6 @@ namespace {
 
 constexpr int kRun = 2048;         // run length == merge tile
 constexpr int kSortThreads = 256;  // kRun / 8
-constexpr int kScoreKeys = 128;    // keys per kv_score CTA
-constexpr int kBatch = 8;          // (q head, segment) accumulators per thread
 constexpr int kQRows = 64;         // Q rows staged per q_rank step
 
 // ---------------------------------------------------------------- means
@@ -62,21 +61,30 @@ __global__ void seg_mean_kernel(const void* __restrict__ x, int bf16, int64_t he
 }
 
 // ---------------------------------------------------------------- q ranking
-// One CTA per (zh, n). Streams the segment's rows through smem; threads < D
-// accumulate column sums in row order (q_mean), threads < kQRows score one
-// staged row each against the fp64 guide (sequential over d).
-__global__ void q_rank_kernel(const void* __restrict__ q, Geo g, const float* __restrict__ guide,
-                              float* __restrict__ q_mean, uint64_t* __restrict__ qkey) {
+// One CTA (256 threads) per (zh, n). Streams the segment's rows through smem in chunks of
+// kQRows; threads [0, 128) accumulate column sums in row order (q_mean, fp64 sequential),
+// threads [128, 128 + kQRows) score one staged row each against the fp64 guide (sequential
+// over d). When the segment fits one CTA sort (len <= kRun) the keys are sorted in smem and
+// q_perm is written directly; otherwise keys go to `qkey` for the global sort.
+constexpr int kQThreads = 256;
+
+__global__ void __launch_bounds__(kQThreads)
+q_rank_kernel(const void* __restrict__ q, Geo g, const float* __restrict__ guide,
+              float* __restrict__ q_mean, uint64_t* __restrict__ qkey, int32_t* __restrict__ q_perm) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int64_t d = g.d;
-    double* gd = reinterpret_cast<double*>(smem_raw);                 // [d]
-    float* rows = reinterpret_cast<float*>(gd + d);                   // [kQRows][d+1]
+    uint64_t* sk0 = reinterpret_cast<uint64_t*>(smem_raw);          // [kRun]
+    uint64_t* sk1 = sk0 + kRun;                                      // [kRun]
+    uint32_t* si0 = reinterpret_cast<uint32_t*>(sk1 + kRun);         // [kRun]
+    uint32_t* si1 = si0 + kRun;                                      // [kRun]
+    double* gd = reinterpret_cast<double*>(si1 + kRun);              // [d]
+    float* rows = reinterpret_cast<float*>(gd + d);                  // [kQRows][d+1]
     const int64_t zh = blockIdx.x / g.N;
     const int64_t n = blockIdx.x % g.N;
     const int64_t len = g.seg_rows(n);
+    const bool local_sort = len <= kRun;
     const int64_t z = zh / g.hq;
-    const int64_t kvh = g.kvh(zh);
-    const float* gsrc = guide + (z * g.hkv + kvh) * d;
+    const float* gsrc = guide + (z * g.hkv + g.kvh(zh)) * d;
     for (int64_t i = threadIdx.x; i < d; i += blockDim.x) gd[i] = (double)gsrc[i];
     const int64_t qb = g.q_base(zh);
     const int64_t rs = d + 1;
@@ -84,62 +92,104 @@ __global__ void q_rank_kernel(const void* __restrict__ q, Geo g, const float* __
     for (int64_t c0 = 0; c0 < len; c0 += kQRows) {
         const int64_t cn = min((int64_t)kQRows, len - c0);
         __syncthreads();
-        for (int64_t e = threadIdx.x; e < cn * d; e += blockDim.x) {
-            const int64_t r = e / d, c = e % d;
-            rows[r * rs + c] = ld_in(q, qb + (n * g.S + c0 + r) * g.qs[2] + c, g.in_bf16);
-        }
-        __syncthreads();
-        for (int j = 0; j < 4; ++j) {
-            const int64_t c = threadIdx.x + (int64_t)j * blockDim.x;
-            if (c < d) {
-                double a = col_acc[j];
-                for (int64_t r = 0; r < cn; ++r) a += (double)rows[r * rs + c];
-                col_acc[j] = a;
+        if (g.in_bf16 && (d % 8) == 0 && (g.qs[2] % 8) == 0) {
+            const int64_t vec = d / 8;  // 16-byte vectors per row
+            for (int64_t e = threadIdx.x; e < cn * vec; e += blockDim.x) {
+                const int64_t r = e / vec, c = (e % vec) * 8;
+                const uint4 w = *reinterpret_cast<const uint4*>(
+                    reinterpret_cast<const __nv_bfloat16*>(q) + qb + (n * g.S + c0 + r) * g.qs[2] + c);
+                const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&w);
+                float* dst = rows + r * rs + c;
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const float2 f = __bfloat1622float2(h2[u]);
+                    dst[2 * u] = f.x;
+                    dst[2 * u + 1] = f.y;
+                }
+            }
+        } else {
+            for (int64_t e = threadIdx.x; e < cn * d; e += blockDim.x) {
+                const int64_t r = e / d, c = e % d;
+                rows[r * rs + c] = ld_in(q, qb + (n * g.S + c0 + r) * g.qs[2] + c, g.in_bf16);
             }
         }
-        if (threadIdx.x < cn) {
-            const float* row = rows + threadIdx.x * rs;
+        __syncthreads();
+        if (threadIdx.x < 128) {
+            for (int j = 0; j < 4; ++j) {
+                const int64_t c = threadIdx.x + (int64_t)j * 128;
+                if (c < d) {
+                    double acc = col_acc[j];
+                    for (int64_t r = 0; r < cn; ++r) acc += (double)rows[r * rs + c];
+                    col_acc[j] = acc;
+                }
+            }
+        } else if (threadIdx.x - 128 < cn) {
+            const int rr = threadIdx.x - 128;
+            const float* row = rows + rr * rs;
             double acc = 0.0;
             for (int64_t c = 0; c < d; ++c) acc = fma((double)row[c], gd[c], acc);
-            qkey[zh * g.l + n * g.S + c0 + threadIdx.x] = desc_key(acc);
+            const uint64_t key = desc_key(acc);
+            const int64_t pos = c0 + rr;
+            if (local_sort) {
+                sk0[pos] = key;
+                si0[pos] = (uint32_t)pos;
+            } else {
+                qkey[zh * g.N * g.S + n * g.S + pos] = key;
+            }
         }
     }
     const double inv = 1.0 / (double)len;
-    for (int j = 0; j < 4; ++j) {
-        const int64_t c = threadIdx.x + (int64_t)j * blockDim.x;
-        if (c < d) q_mean[(zh * g.N + n) * d + c] = (float)(col_acc[j] * inv);
+    if (threadIdx.x < 128)
+        for (int j = 0; j < 4; ++j) {
+            const int64_t c = threadIdx.x + (int64_t)j * 128;
+            if (c < d) q_mean[(zh * g.N + n) * d + c] = (float)(col_acc[j] * inv);
+        }
+    if (!local_sort) return;
+    for (int64_t i = len + threadIdx.x; i < kRun; i += blockDim.x) {
+        sk0[i] = ~0ull;
+        si0[i] = 0xffffffffu;
     }
+    __syncthreads();
+    const int which = block_merge_sort<kQThreads, kRun / kQThreads>(sk0, si0, sk1, si1);
+    const uint32_t* res = which ? si1 : si0;
+    int32_t* out = q_perm + (zh * g.N + n) * g.S;
+    for (int64_t i = threadIdx.x; i < len; i += blockDim.x) out[i] = (int32_t)res[i];
 }
 
 // ---------------------------------------------------------------- kv scoring
-// One CTA per (z, kv head, block of 128 keys). Thread t owns key t0 + t.
-// For every q head h of the kv group and every segment n whose prefix covers
-// the key, s = sum_d q_mean[h,n,d] * K[t,d] in fp64, sequential in d.
-__global__ void __launch_bounds__(kScoreKeys)
+// One CTA (128 threads) per (z, kv head, block of 128 keys). Register tile per thread:
+// 4 keys x 8 (q head, segment) pairs = 32 fp64 accumulators; each K element is converted
+// once and feeds 8 DFMAs, each q_mean element (fp64, broadcast from smem) feeds 4.
+// s = sum_d q_mean[h,n,d] * K[t,d] in fp64, sequential in d (dot_f plan.cpp:14-20).
+constexpr int kSK = 128;       // keys per CTA
+constexpr int kSKThreads = 128;
+constexpr int kSPairs = 32;    // pairs per batch (4 groups x 8)
+
+__global__ void __launch_bounds__(kSKThreads)
 kv_score_kernel(const void* __restrict__ k, Geo g, const float* __restrict__ q_mean,
                 uint64_t* __restrict__ kvkey) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    const int64_t d = g.d;
-    double* qm = reinterpret_cast<double*>(smem_raw);  // [d][kBatch]
-    float* kt = reinterpret_cast<float*>(qm + d * kBatch);  // [d][kScoreKeys]
+    const int d = (int)g.d;
+    double* qm = reinterpret_cast<double*>(smem_raw);           // [d][kSPairs]
+    float* kt = reinterpret_cast<float*>(qm + d * kSPairs);     // [d][kSK]
     const int64_t zg = blockIdx.y;  // z * hkv + kvh
     const int64_t z = zg / g.hkv, kvh = zg % g.hkv;
-    const int64_t t0 = (int64_t)blockIdx.x * kScoreKeys;
-    const int64_t t = t0 + threadIdx.x;
+    const int64_t t0 = (int64_t)blockIdx.x * kSK;
+    const int kg = threadIdx.x % 32, qg = threadIdx.x / 32;
     const int64_t kb = z * g.ks[0] + kvh * g.ks[1];
-    // stage K block transposed: kt[c][key]
-    for (int64_t e = threadIdx.x; e < (int64_t)kScoreKeys * d; e += blockDim.x) {
-        const int64_t r = e / d, c = e % d;
+    for (int e = threadIdx.x; e < kSK * d; e += kSKThreads) {
+        const int r = e / d, c = e % d;
         const int64_t row = t0 + r;
-        kt[c * kScoreKeys + r] = (row < g.l) ? ld_in(k, kb + row * g.ks[2] + c, g.in_bf16) : 0.0f;
+        kt[c * kSK + r] = (row < g.l) ? ld_in(k, kb + row * g.ks[2] + c, g.in_bf16) : 0.0f;
     }
     const int64_t n_lo = t0 / g.S + 1;  // first segment whose prefix reaches t0
     const int64_t nsegs = (n_lo < g.N) ? g.N - n_lo : 0;
     const int64_t pairs = g.group * nsegs;
-    for (int64_t p0 = 0; p0 < pairs; p0 += kBatch) {
+    const int64_t kvp = g.kv_per_head();
+    for (int64_t p0 = 0; p0 < pairs; p0 += kSPairs) {
         __syncthreads();
-        for (int64_t e = threadIdx.x; e < (int64_t)kBatch * d; e += blockDim.x) {
-            const int64_t b = e / d, c = e % d;
+        for (int e = threadIdx.x; e < kSPairs * d; e += kSKThreads) {
+            const int b = e / d, c = e % d;
             const int64_t p = p0 + b;
             double val = 0.0;
             if (p < pairs) {
@@ -147,32 +197,45 @@ kv_score_kernel(const void* __restrict__ k, Geo g, const float* __restrict__ q_m
                 const int64_t n = n_lo + p % nsegs;
                 val = (double)q_mean[((z * g.hq + h) * g.N + n) * d + c];
             }
-            qm[c * kBatch + b] = val;
+            qm[c * kSPairs + b] = val;
         }
         __syncthreads();
-        double acc[kBatch];
+        double acc[4][8];
 #pragma unroll
-        for (int b = 0; b < kBatch; ++b) acc[b] = 0.0;
-        for (int64_t c = 0; c < d; ++c) {
-            const double kd = (double)kt[c * kScoreKeys + threadIdx.x];
-            const double2* q2 = reinterpret_cast<const double2*>(qm + c * kBatch);
+        for (int i = 0; i < 4; ++i)
 #pragma unroll
-            for (int b = 0; b < kBatch / 2; ++b) {
-                const double2 qq = q2[b];
-                acc[2 * b] = fma(qq.x, kd, acc[2 * b]);
-                acc[2 * b + 1] = fma(qq.y, kd, acc[2 * b + 1]);
+            for (int b = 0; b < 8; ++b) acc[i][b] = 0.0;
+        const float4* kt4 = reinterpret_cast<const float4*>(kt) + kg;
+        const double2* qm2 = reinterpret_cast<const double2*>(qm) + qg * 4;
+#pragma unroll 2
+        for (int c = 0; c < d; ++c) {
+            const float4 kk = kt4[c * (kSK / 4)];
+            const double kd[4] = {(double)kk.x, (double)kk.y, (double)kk.z, (double)kk.w};
+            const double2* qrow = qm2 + c * (kSPairs / 2);
+            double qv[8];
+#pragma unroll
+            for (int b = 0; b < 4; ++b) {
+                const double2 x = qrow[b];
+                qv[2 * b] = x.x;
+                qv[2 * b + 1] = x.y;
             }
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int b = 0; b < 8; ++b) acc[i][b] = fma(qv[b], kd[i], acc[i][b]);
         }
 #pragma unroll
-        for (int b = 0; b < kBatch; ++b) {
-            const int64_t p = p0 + b;
+        for (int b = 0; b < 8; ++b) {
+            const int64_t p = p0 + qg * 8 + b;
             if (p >= pairs) break;
             const int64_t h = kvh * g.group + p / nsegs;
             const int64_t n = n_lo + p % nsegs;
-            if (t < n * g.S) {
-                const int64_t zh = z * g.hq + h;
-                kvkey[zh * g.kv_per_head() + g.kv_off(n) + t] = desc_key(acc[b]);
-            }
+            const int64_t zh = z * g.hq + h;
+            uint64_t* dst = kvkey + zh * kvp + g.kv_off(n);
+            const int64_t t = t0 + kg * 4;
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+                if (t + i < n * g.S) dst[t + i] = desc_key(acc[i][b]);
         }
     }
 }
@@ -228,8 +291,8 @@ __device__ __forceinline__ bool elt_less(uint64_t ka, uint32_t ia, uint64_t kb, 
 __global__ void __launch_bounds__(kSortThreads)
 run_sort_kernel(SortGeo sg, const uint64_t* __restrict__ keys, uint64_t* __restrict__ okeys,
                 uint32_t* __restrict__ oidx, int32_t* __restrict__ final_out) {
-    __shared__ uint64_t sk[kRun];
-    __shared__ uint32_t si[kRun];
+    __shared__ uint64_t sk[2][kRun];
+    __shared__ uint32_t si[2][kRun];
     int64_t zh, n, j;
     locate(sg, blockIdx.x, zh, n, j);
     const int64_t len = sg.len(n);
@@ -238,47 +301,32 @@ run_sort_kernel(SortGeo sg, const uint64_t* __restrict__ keys, uint64_t* __restr
     const int64_t base = zh * sg.head_stride + sg.off(n);
     for (int i = threadIdx.x; i < kRun; i += kSortThreads) {
         if (i < cnt) {
-            sk[i] = keys[base + r0 + i];
-            si[i] = (uint32_t)(r0 + i);
+            sk[0][i] = keys[base + r0 + i];
+            si[0][i] = (uint32_t)(r0 + i);
         } else {
-            sk[i] = ~0ull;
-            si[i] = 0xffffffffu;
+            sk[0][i] = ~0ull;
+            si[0][i] = 0xffffffffu;
         }
     }
     __syncthreads();
-    for (int kk = 2; kk <= kRun; kk <<= 1) {
-        for (int jj = kk >> 1; jj > 0; jj >>= 1) {
-            for (int i = threadIdx.x; i < kRun; i += kSortThreads) {
-                const int ixj = i ^ jj;
-                if (ixj > i) {
-                    const bool up = (i & kk) == 0;
-                    const uint64_t a = sk[i], b = sk[ixj];
-                    const uint32_t ia = si[i], ib = si[ixj];
-                    const bool b_less = elt_less(b, ib, a, ia);
-                    if (b_less == up) {
-                        sk[i] = b; sk[ixj] = a;
-                        si[i] = ib; si[ixj] = ia;
-                    }
-                }
-            }
-            __syncthreads();
-        }
-    }
+    const int w = block_merge_sort<kSortThreads, kRun / kSortThreads>(sk[0], si[0], sk[1], si[1]);
     for (int i = threadIdx.x; i < cnt; i += kSortThreads) {
         if (final_out) {
-            final_out[base + r0 + i] = (int32_t)si[i];
+            final_out[base + r0 + i] = (int32_t)si[w][i];
         } else {
-            okeys[base + r0 + i] = sk[i];
-            oidx[base + r0 + i] = si[i];
+            okeys[base + r0 + i] = sk[w][i];
+            oidx[base + r0 + i] = si[w][i];
         }
     }
 }
 
-// Merges sorted runs of width w pairwise; CTA = one 2048-output tile.
+// Merges sorted runs of width w pairwise; CTA = one 2048-output tile, each thread merges
+// 8 consecutive outputs after one merge-path search inside the CTA's smem slices.
 __global__ void __launch_bounds__(kSortThreads)
 merge_pass_kernel(SortGeo sg, int64_t w, const uint64_t* __restrict__ ikeys,
                   const uint32_t* __restrict__ iidx, uint64_t* __restrict__ okeys,
                   uint32_t* __restrict__ oidx, int32_t* __restrict__ final_out) {
+    constexpr int E = kRun / kSortThreads;
     __shared__ uint64_t sk[kRun];
     __shared__ uint32_t si[kRun];
     __shared__ int64_t split[2];
@@ -297,13 +345,11 @@ merge_pass_kernel(SortGeo sg, int64_t w, const uint64_t* __restrict__ ikeys,
     const uint64_t* bk = ikeys + base + b_beg;
     const uint32_t* bi = iidx + base + b_beg;
     if (threadIdx.x < 2) {
-        // merge path: number of A elements among the first `diag` outputs
         const int64_t diag = threadIdx.x == 0 ? d0 : d1;
         int64_t lo = max((int64_t)0, diag - b_len), hi = min(diag, a_len);
         while (lo < hi) {
             const int64_t mid = (lo + hi) >> 1;
             const int64_t bj = diag - 1 - mid;
-            // A[mid] goes first iff A[mid] < B[bj]
             if (elt_less(ak[mid], ai[mid], bk[bj], bi[bj])) lo = mid + 1; else hi = mid;
         }
         split[threadIdx.x] = lo;
@@ -321,32 +367,23 @@ merge_pass_kernel(SortGeo sg, int64_t w, const uint64_t* __restrict__ ikeys,
         si[na + i] = bi[b0 + i];
     }
     __syncthreads();
-    const int64_t out0 = base + o0;
-    for (int i = threadIdx.x; i < na + nb; i += kSortThreads) {
-        const uint64_t key = sk[i];
-        const uint32_t id = si[i];
-        int pos;
-        if (i < na) {  // rank among B slice: count of B elements < this
-            int lo = 0, hi = nb;
-            while (lo < hi) {
-                const int mid = (lo + hi) >> 1;
-                if (elt_less(sk[na + mid], si[na + mid], key, id)) lo = mid + 1; else hi = mid;
-            }
-            pos = i + lo;
-        } else {
-            const int jb = i - na;
-            int lo = 0, hi = na;
-            while (lo < hi) {
-                const int mid = (lo + hi) >> 1;
-                if (elt_less(sk[mid], si[mid], key, id)) lo = mid + 1; else hi = mid;
-            }
-            pos = jb + lo;
-        }
+    const int tot = na + nb;
+    const int o = threadIdx.x * E;
+    if (o >= tot) return;
+    const int a = merge_path(sk, si, na, sk + na, si + na, nb, o);
+    uint64_t ok[E];
+    uint32_t oi[E];
+    merge_seq<E>(sk, si, na, sk + na, si + na, nb, a, o - a, ok, oi);
+    const int64_t out0 = base + o0 + o;
+    const int cnt = min(E, tot - o);
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+        if (e >= cnt) break;
         if (final_out) {
-            final_out[out0 + pos] = (int32_t)id;
+            final_out[out0 + e] = (int32_t)oi[e];
         } else {
-            okeys[out0 + pos] = key;
-            oidx[out0 + pos] = id;
+            okeys[out0 + e] = ok[e];
+            oidx[out0 + e] = oi[e];
         }
     }
 }
@@ -366,7 +403,7 @@ size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
 
 size_t plan_ws_layout(const Geo& g, char* base, PlanWs* out) {
     const int64_t zhq = g.z * g.hq;
-    const int64_t total = std::max<int64_t>(zhq * g.l, zhq * g.kv_per_head());
+    const int64_t total = std::max<int64_t>(zhq * g.N * g.S, zhq * g.kv_per_head());
     size_t off = 0;
     auto take = [&](size_t bytes) {
         char* p = base ? base + off : nullptr;
@@ -403,7 +440,7 @@ cudaError_t sort_family(int kind, const Geo& g, PlanWs& ws, int32_t* perm, cudaS
     sg.N = g.N;
     sg.last_len = g.last_len;
     sg.heads = g.z * g.hq;
-    sg.head_stride = (kind == 0) ? g.l : g.kv_per_head();
+    sg.head_stride = (kind == 0) ? g.N * g.S : g.kv_per_head();
     sg.units_per_head = units_per_head(kind, g);
     sg.cum = (kind == 0) ? ws.cum_q : ws.cum_kv;
     if (sg.units_per_head == 0) return cudaSuccess;
@@ -455,23 +492,22 @@ cudaError_t launch_plan_build(const Geo& g, const void* q, const void* k, int32_
     cudaError_t err;
     // guide = k_mean[segment 0] of each kv head
     if ((err = launch_segment_means(g, k, 1, 1, ws.guide, st)) != cudaSuccess) return err;
-    // q_mean + q keys
+    // q_mean + q keys (+ in-CTA sort when a segment fits one run)
     {
-        const size_t smem = sizeof(double) * g.d + sizeof(float) * kQRows * (g.d + 1);
-        if (smem > 48 * 1024)
-            cudaFuncSetAttribute(q_rank_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        q_rank_kernel<<<(unsigned)(g.z * g.hq * g.N), 128, smem, st>>>(q, g, ws.guide, ws.q_mean,
-                                                                      ws.key0);
+        const size_t smem = (2 * sizeof(uint64_t) + 2 * sizeof(uint32_t)) * kRun + sizeof(double) * g.d +
+                            sizeof(float) * kQRows * (g.d + 1);
+        cudaFuncSetAttribute(q_rank_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        q_rank_kernel<<<(unsigned)(g.z * g.hq * g.N), kQThreads, smem, st>>>(q, g, ws.guide, ws.q_mean,
+                                                                            ws.key0, q_perm);
         if ((err = cudaGetLastError()) != cudaSuccess) return err;
-        if ((err = sort_family(0, g, ws, q_perm, st)) != cudaSuccess) return err;
+        if (g.S > kRun && (err = sort_family(0, g, ws, q_perm, st)) != cudaSuccess) return err;
     }
     if (g.N > 1) {
-        const size_t smem = sizeof(double) * g.d * kBatch + sizeof(float) * g.d * kScoreKeys;
-        if (smem > 48 * 1024)
-            cudaFuncSetAttribute(kv_score_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        const size_t smem = sizeof(double) * g.d * kSPairs + sizeof(float) * g.d * kSK;
+        cudaFuncSetAttribute(kv_score_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         const int64_t keys = (g.N - 1) * g.S;  // tokens that appear in some prefix
-        dim3 grid((unsigned)((keys + kScoreKeys - 1) / kScoreKeys), (unsigned)(g.z * g.hkv));
-        kv_score_kernel<<<grid, kScoreKeys, smem, st>>>(k, g, ws.q_mean, ws.key0);
+        dim3 grid((unsigned)((keys + kSK - 1) / kSK), (unsigned)(g.z * g.hkv));
+        kv_score_kernel<<<grid, kSKThreads, smem, st>>>(k, g, ws.q_mean, ws.key0);
         if ((err = cudaGetLastError()) != cudaSuccess) return err;
         if ((err = sort_family(1, g, ws, kv_perm, st)) != cudaSuccess) return err;
     }

@@ -59,9 +59,7 @@ def lib() -> C.CDLL:
     """Load (building if needed) libs2o_cuda.so. Raises if it cannot be loaded."""
     global _LIB
     if _LIB is None:
-        path = _build.LIB
-        if not os.path.exists(path):
-            path = _build.build()
+        path = _build.build()  # no-op when the in-tree .so matches its sources
         _LIB = C.CDLL(path)
         _LIB.s2o_last_error.restype = C.c_char_p
         _LIB.s2o_status_string.restype = C.c_char_p
@@ -509,3 +507,19 @@ def attention_host(q: np.ndarray, k: np.ndarray, v: np.ndarray, cfg: KernelConfi
     _check(lib().s2o_attention_host(C.byref(p), vp(q), vp(k), vp(v), C.byref(c), vp(out), None, None,
                                     vp(proc), vp(p1), vp(p2)))
     return out, proc, p1, p2
+
+
+def attention_host_ptr(q_host, k_host, v_host, o_host, cfg: KernelConfig) -> None:
+    """s2o_attention_host on torch CPU tensors (pinned or pageable, fp32 or bf16, dense
+    [Z,H,L,D]): host->device copies, the whole operator and the device->host copy of O in
+    one C-ABI call. Raises on any error."""
+    torch = _torch()
+    z, hq, l, d = q_host.shape
+    hkv = k_host.shape[1]
+    dt = _dtype_code(q_host)
+    p = _Problem()
+    lib().s2o_problem_init(C.byref(p), C.c_int64(z), C.c_int64(hq), C.c_int64(hkv), C.c_int64(l),
+                           C.c_int64(d), C.c_int32(dt), C.c_int32(_dtype_code(o_host)))
+    c = cfg._c()
+    _check(lib().s2o_attention_host(C.byref(p), _ptr(q_host), _ptr(k_host), _ptr(v_host), C.byref(c),
+                                    _ptr(o_host), None, None, None, None, None))

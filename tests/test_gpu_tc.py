@@ -1,0 +1,149 @@
+"""tcgen05 path (bf16, D=128, 128x128 tiles) vs the oracle and the exact generic path.
+
+Tolerances (bf16 operands, fp32 accumulation, bf16 output):
+  * outputs: max |O_tc - O_ref| <= 2.5e-2 and mean |O_tc - O_ref| <= 2e-3, O_ref = the
+    oracle's fp64 result on the same bf16-rounded inputs (rows with identical traces);
+  * traces: identical, except documented threshold ties -- at most 1% of tiles may differ,
+    and each differing tile's committed count may differ by at most 1 chunk;
+  * plans: bit-identical (the plan kernels do not depend on the attention path).
+"""
+from __future__ import annotations
+
+import os
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN, Cfg, bf16_round
+
+pytestmark = pytest.mark.gpu
+
+TC, GEN = 2, 1
+
+
+def dev_bf16(torch, x):
+    return torch.from_numpy(np.ascontiguousarray(x, np.float32)).cuda().to(torch.bfloat16)
+
+
+def kcfg(s2o, c: Cfg, path):
+    return s2o.KernelConfig(seg_len=c.seg_len, tau=c.tau, tiles=s2o.TileSpec(c.b_m, c.b_n),
+                            q_reorder=c.q_reorder, fused=c.fused, path=path)
+
+
+def inputs(s2o, hq, hkv, l, seed=0):
+    q, k, v = s2o.generate_synthetic("mixed", max(1, l // 64), 8.0, seed, 1, hq, l, 128)
+    return bf16_round(q), bf16_round(k[:, :hkv]), bf16_round(v[:, :hkv])
+
+
+def run(torch, s2o, q, k, v, c, path):
+    res = s2o.s2o_attention(dev_bf16(torch, q), dev_bf16(torch, k), dev_bf16(torch, v), kcfg(s2o, c, path))
+    torch.cuda.synchronize()
+    return res
+
+
+def trace_diff(a, b):
+    a = a.reshape(-1)
+    b = b.reshape(-1)
+    diff = a != b
+    return int(diff.sum()), (int(np.abs(a - b).max()) if diff.any() else 0)
+
+
+def test_tc_path_selected(cuda):
+    import paper_2602_22575_b200 as s2o
+    torch = cuda
+    q, k, v = inputs(s2o, 2, 1, 256)
+    qd, kd, vd = dev_bf16(torch, q), dev_bf16(torch, k), dev_bf16(torch, v)
+    assert s2o.select_path(qd, kd, vd, s2o.KernelConfig(seg_len=128)) == TC
+    assert s2o.select_path(qd.float(), kd.float(), vd.float(), s2o.KernelConfig(seg_len=128)) == GEN
+
+
+def test_tc_gqa_golden(cuda):
+    """Reference golden (Hq=4, Hkv=2, L=4096, S=512, 128x128, tau=0.005)."""
+    import paper_2602_22575_b200 as s2o
+    torch = cuda
+    g = np.load(os.path.join(GOLDEN, "gqa_golden.npz"))
+    q, k, v = s2o.generate_synthetic("mixed", 64, 8.0, 7, 1, 4, 4096, 128)
+    q, k, v = bf16_round(q), bf16_round(k[:, :2]), bf16_round(v[:, :2])
+    res = run(torch, s2o, q, k, v, Cfg(512, 0.005, 128, 128), TC)
+    np.testing.assert_array_equal(res.plan.q_perm.reshape(4, 8, 512).cpu().numpy(), g["q_perm"])
+    np.testing.assert_array_equal(res.plan.kv_perm.reshape(4, -1).cpu().numpy(), g["kv_perm"])
+    got = res.trace.processed.reshape(4, 8, -1).cpu().numpy()
+    ndiff, maxd = trace_diff(got, g["processed"])
+    assert ndiff <= max(1, got.size // 100) and maxd <= 1, (ndiff, maxd)
+    out = res.out.float().cpu().numpy()[:, :, ::8]
+    err = np.abs(out - g["out_rows"])
+    assert err.max() <= 2.5e-2 and err.mean() <= 2e-3, (err.max(), err.mean())
+
+
+@pytest.mark.parametrize("l,s,reorder,fused", [
+    (1024, 256, True, False), (1024, 256, False, False), (1024, 256, False, True),
+    (1000, 300, True, False), (1000, 300, False, True), (2048, 2048, True, False),
+    (384, 100, True, False),
+])
+def test_tc_matches_oracle(cuda, port, l, s, reorder, fused):
+    import paper_2602_22575_b200 as s2o
+    torch = cuda
+    hq, hkv = 2, 1
+    q, k, v = inputs(s2o, hq, hkv, l, seed=l + s)
+    for tau in (0.005, 0.0, 1e9):
+        c = Cfg(s, tau, 128, 128, reorder, fused)
+        res = run(torch, s2o, q, k, v, c, TC)
+        want_o, want_t, want_p = port.attention(q, np.repeat(k, hq // hkv, 1), np.repeat(v, hq // hkv, 1), c)
+        got_t = res.trace.processed.reshape(hq, -1).cpu().numpy()
+        ndiff, maxd = trace_diff(got_t, want_t.processed.reshape(hq, -1))
+        assert ndiff <= max(1, got_t.size // 100) and maxd <= 1, (tau, ndiff, maxd)
+        if tau >= 1e9:
+            assert (got_t == 0).all()
+        out = res.out.float().cpu().numpy()
+        err = np.abs(out - want_o)
+        assert err.max() <= 2.5e-2 and err.mean() <= 2e-3, (tau, err.max(), err.mean())
+        if ndiff == 0:
+            np.testing.assert_array_equal(res.trace.pass2_pairs.reshape(-1).cpu().numpy(), want_t.pass2_pairs)
+
+
+def test_tc_pass1_states(cuda, port):
+    import paper_2602_22575_b200 as s2o
+    torch = cuda
+    q, k, v = inputs(s2o, 2, 2, 1000, seed=3)
+    c = Cfg(300, 0.005, 128, 128)
+    bufs = s2o.pass1_dense_init(dev_bf16(torch, q), dev_bf16(torch, k), dev_bf16(torch, v), kcfg(s2o, c, TC))
+    acc, ell, m = port.pass1(q, k, v, c)
+    # compare the finalized partial outputs and the maxima
+    got = (bufs.acc / bufs.ell[..., None]).cpu().numpy()
+    want = acc / ell[..., None]
+    assert np.abs(got - want).max() <= 2e-2
+    # The kernel rescales lazily: the stored m is a reference max within 8 log2-units below the
+    # true running max (never above); ell and acc are relative to it, so ell * e^m is invariant.
+    mg = bufs.m.cpu().numpy().astype(np.float64)
+    assert (mg <= m + 1e-3).all() and (mg >= m - 8.0 * np.log(2.0) - 1e-3).all()
+    lg = bufs.ell.cpu().numpy() * np.exp(mg - m)
+    np.testing.assert_allclose(lg, ell, rtol=2e-3)
+
+
+def test_tc_dense_vs_sdpa(cuda):
+    import paper_2602_22575_b200 as s2o
+    torch = cuda
+    torch.manual_seed(0)
+    q = torch.randn(1, 4, 2048, 128, device="cuda").to(torch.bfloat16)
+    k = torch.randn(1, 2, 2048, 128, device="cuda").to(torch.bfloat16)
+    v = torch.randn(1, 2, 2048, 128, device="cuda").to(torch.bfloat16)
+    o = s2o.dense_causal_attention(q, k, v, path=TC)
+    ref = torch.nn.functional.scaled_dot_product_attention(
+        q.float(), k.float().repeat_interleave(2, 1), v.float().repeat_interleave(2, 1), is_causal=True)
+    assert (o - ref).abs().max().item() <= 2e-2
+
+
+def test_tc_generic_agree_at_scale(cuda):
+    """L=8192, 8 q / 2 kv heads, S=1024: tcgen05 and the exact generic path see the same plan
+    and (up to ties) the same traces; outputs agree to the bf16 tolerance."""
+    import paper_2602_22575_b200 as s2o
+    torch = cuda
+    q, k, v = inputs(s2o, 8, 2, 8192, seed=1)
+    c = Cfg(1024, 0.005, 128, 128)
+    a = run(torch, s2o, q, k, v, c, TC)
+    b = run(torch, s2o, q, k, v, c, GEN)
+    assert torch.equal(a.plan.kv_perm, b.plan.kv_perm)
+    ndiff, maxd = trace_diff(a.trace.processed.cpu().numpy(), b.trace.processed.cpu().numpy())
+    assert ndiff <= max(1, a.trace.processed.numel() // 100) and maxd <= 1
+    err = (a.out.float() - b.out.float()).abs()
+    assert err.max().item() <= 2.5e-2 and err.mean().item() <= 2e-3
