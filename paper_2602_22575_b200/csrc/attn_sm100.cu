@@ -7,10 +7,13 @@
 // a list of 128-key blocks: first the causal blocks of its own segment (masked on original
 // token positions), then the chunks of kv_perm in rank order (non-contiguous rows).
 //
-// Warp roles (192 threads, 1 CTA per SM):
+// Warp roles (256 threads, 1 CTA per SM):
 //   warps 0-3  softmax/correction/epilogue: thread r owns query row r = TMEM lane r
-//   warp 4     loader: TMA tile::gather4 of Q rows (q_perm order) and K/V rows (block order)
-//   warp 5     MMA issuer (one lane): S = Q K^T into TMEM (double-buffered), O += P V
+//   warp 4     MMA issuer (one lane): S = Q K^T into TMEM (double-buffered), O += P V
+//   warps 5-7  loaders: contiguous blocks (the causal blocks of pass-1, Q in token order) by
+//              2-D tile TMA (4 ops per block); permuted rows (Q by q_perm, prefix chunks by
+//              kv_perm) by TMA tile::gather4 spread over the three warps (the gather issue
+//              rate, ~1 op per 22 cycles per SM, is the limit; see scripts/load_bench.cu)
 //
 // Early stop (reference semantics): for a prefix chunk the softmax warps
 // compute each row's relative normaliser gain sum_j exp(s_j - m) / ell from the chunk's
@@ -20,9 +23,11 @@
 //
 // Data layout in shared memory (all SWIZZLE_128B, 1024-B aligned):
 //   sQ   [2][128 rows][128 B]        Q tile, K-major (two 64-column halves)
-//   sK   [2 stages][2][128][128 B]   K block, K-major (B operand of Q K^T)
-//   sV   [2 stages][2][128][128 B]   V block, used MN-major (B operand of P V)
-//   sP   [2][128 rows][128 B]        P = exp2(s - m) in bf16, K-major (A operand of P V)
+//   sK   [3 stages][2][128][128 B]   K block, K-major (B operand of Q K^T)
+//   sV   [3 stages][2][128][128 B]   V block, used MN-major (B operand of P V)
+//   P    = exp2(s - m) in bf16, K-major (A operand of P V), written into the K buffer of the
+//          block's own stage: K(j) is dead once Q K^T(j) completed (the softmax only writes P
+//          after reading S(j)), and the stage is released only after P V(j) completes.
 // TMEM (512 columns): S buffers at columns [0,128) and [128,256), O at [256,384).
 #include <cudaTypedefs.h>
 
@@ -42,15 +47,15 @@ namespace {
 constexpr int kD = 128;
 constexpr int kBM = 128;
 constexpr int kBN = 128;
-constexpr int kStages = 2;
-constexpr int kThreads = 192;
+constexpr int kStages = 3;
+constexpr int kThreads = 256;
+constexpr int kLoaderWarps = 3;  // warps 5..7 issue TMA (gather4 issue rate scales with warps)
 constexpr uint32_t kHalf = 128u * 128u;            // bytes of one 64-column half tile
 constexpr uint32_t kTileBytes = 2 * kHalf;         // 32 KB
 constexpr uint32_t kOffQ = 0;
 constexpr uint32_t kOffK = kOffQ + kTileBytes;
 constexpr uint32_t kOffV = kOffK + kStages * kTileBytes;
-constexpr uint32_t kOffP = kOffV + kStages * kTileBytes;
-constexpr uint32_t kOffCtrl = kOffP + kTileBytes;
+constexpr uint32_t kOffCtrl = kOffV + kStages * kTileBytes;
 constexpr uint32_t kSmemBytes = kOffCtrl + 2048 + 1024;  // + control block + alignment slack
 constexpr uint32_t kTmemCols = 512;
 constexpr uint32_t kColO = 256;
@@ -58,7 +63,7 @@ constexpr float kRescaleThresh = 8.0f;  // lazy max update, log2 units (factor 2
 
 struct Ctrl {
     uint64_t q_full, q_empty;
-    uint64_t kv_full[kStages], kv_empty[kStages];
+    uint64_t k_full[kStages], v_full[kStages], kv_empty[kStages];
     uint64_t s_full[2], s_empty[2];
     uint64_t p_full, o_done;
     uint32_t tmem_base;
@@ -69,6 +74,7 @@ struct Ctrl {
 struct TcParams {
     PassArgs a;
     float scale_log2;  // (1/sqrt(D)) * log2(e)
+    int q_contig, kv_contig;  // token stride == one row (tile TMA usable)
 };
 
 struct TileInfo {
@@ -118,7 +124,9 @@ __device__ __forceinline__ int64_t key_token(const PassArgs& a, const TileInfo& 
 
 __global__ void __launch_bounds__(kThreads, 1)
 tc_pass_kernel(const TcParams p, const __grid_constant__ CUtensorMap qmap,
-               const __grid_constant__ CUtensorMap kmap, const __grid_constant__ CUtensorMap vmap) {
+               const __grid_constant__ CUtensorMap kmap, const __grid_constant__ CUtensorMap vmap,
+               const __grid_constant__ CUtensorMap qtile, const __grid_constant__ CUtensorMap ktile,
+               const __grid_constant__ CUtensorMap vtile) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char* smem = reinterpret_cast<unsigned char*>(
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -130,13 +138,13 @@ tc_pass_kernel(const TcParams p, const __grid_constant__ CUtensorMap qmap,
     const uint32_t sQ = smem_u32(smem + kOffQ);
     const uint32_t sK = smem_u32(smem + kOffK);
     const uint32_t sV = smem_u32(smem + kOffV);
-    const uint32_t sP = smem_u32(smem + kOffP);
 
     if (threadIdx.x == 0) {
         mbar_init(smem_u32(&c.q_full), 1);
         mbar_init(smem_u32(&c.q_empty), 1);
         for (int s = 0; s < kStages; ++s) {
-            mbar_init(smem_u32(&c.kv_full[s]), 1);
+            mbar_init(smem_u32(&c.k_full[s]), 1);
+            mbar_init(smem_u32(&c.v_full[s]), 1);
             mbar_init(smem_u32(&c.kv_empty[s]), 1);
         }
         for (int s = 0; s < 2; ++s) {
@@ -159,57 +167,104 @@ tc_pass_kernel(const TcParams p, const __grid_constant__ CUtensorMap qmap,
     const int64_t total_tiles = g.z * g.hq * a.tiles_per_head;
     const int64_t kv_div = g.d;  // row unit of the tensor maps = D elements
 
-    if (warp == 4) {
-        // ============================== loader ==============================
+    if (warp >= 5) {
+        // ============================== loaders ==============================
+        const int lw = warp - 5;             // loader warp 0..2
+        const int lt = lw * 32 + lane;       // loader thread 0..95
+        const uint32_t lbar = 5 * 32;        // named barrier 2 over the 96 loader threads
         uint32_t gblk = 0, qcount = 0;
         for (int64_t tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
             const TileInfo t = tile_info(a, tile);
             if (t.nb == 0) continue;
             const int32_t* kv = (t.np > 0) ? a.kv_perm + t.zh * g.kv_per_head() + g.kv_off(t.n) : nullptr;
-            // Q rows (gather by q_perm); wait until the previous tile's Q K^T are done
+            // Q rows; wait until the previous tile's Q K^T are done
             mbar_wait(smem_u32(&c.q_empty), (qcount & 1) ^ 1, 1001);
-            if (lane == 0) mbar_expect_tx(smem_u32(&c.q_full), kTileBytes);
-            __syncwarp();
-            {
-                const int64_t qb = g.q_base(t.zh) / kv_div;
-                int32_t rows[4];
-                for (int i = 0; i < 4; ++i) rows[i] = (int32_t)(qb + q_local_row(a, t, lane * 4 + i) * (g.qs[2] / kv_div));
-                for (int h = 0; h < 2; ++h)
-                    tma_gather4(sQ + h * kHalf + lane * 512, &qmap, h * 64, rows[0], rows[1], rows[2], rows[3],
+            const int64_t qb = g.q_base(t.zh) / kv_div;
+            const bool q_tile = p.q_contig && !((a.mode & kStateIn) && a.q_reorder) && t.tn == kBM;
+            if (lt == 0) mbar_expect_tx(smem_u32(&c.q_full), kTileBytes);
+            named_bar_sync(2, 96);
+            if (q_tile) {
+                if (lt == 0)
+                    for (int h = 0; h < 2; ++h)
+                        tma_load2d(sQ + h * kHalf, &qtile, h * 64, (int32_t)(qb + t.sb + t.t0), smem_u32(&c.q_full));
+            } else {
+                for (int op = lt; op < 64; op += 96) {  // 32 row groups x 2 halves
+                    const int grp = op >> 1, h = op & 1;
+                    int32_t rows[4];
+                    for (int i = 0; i < 4; ++i)
+                        rows[i] = (int32_t)(qb + q_local_row(a, t, grp * 4 + i) * (g.qs[2] / kv_div));
+                    tma_gather4(sQ + h * kHalf + grp * 512, &qmap, h * 64, rows[0], rows[1], rows[2], rows[3],
                                 smem_u32(&c.q_full));
+                }
             }
             ++qcount;
             const int64_t kb = g.k_base(t.zh) / kv_div, vb = g.v_base(t.zh) / kv_div;
             const int64_t ks = g.ks[2] / kv_div, vs = g.vs[2] / kv_div;
             int loaded = 0;
+            // gather indices for block j live in registers; block j+1's are prefetched while
+            // block j is issued (kv_perm reads are L2 round trips)
+            auto fetch_rows = [&](int j, int32_t (&rk)[2][4], int32_t (&rv)[2][4]) {
+                for (int u = 0; u < 2; ++u) {
+                    const int op = lt + u * 96;
+                    const int grp = (op >> 1) & 31;
+                    for (int i = 0; i < 4; ++i) {
+                        const int64_t tok = (j < t.nb) ? key_token(a, t, kv, j, grp * 4 + i) : 0;
+                        rk[u][i] = (int32_t)(kb + tok * ks);
+                        rv[u][i] = (int32_t)(vb + tok * vs);
+                    }
+                }
+            };
+            int32_t ck[2][4], cv[2][4], nk[2][4], nv[2][4];
+            fetch_rows(0, ck, cv);
             for (int j = 0; j < t.nb; ++j) {
                 const uint32_t gi = gblk + j;
                 const int st = gi % kStages;
+                if (j + 1 < t.nb && !(j + 1 < t.nd && p.kv_contig)) fetch_rows(j + 1, nk, nv);
                 mbar_wait(smem_u32(&c.kv_empty[st]), ((gi / kStages) & 1) ^ 1, 1002);
-                if (j >= 2 && c.dec[(j - 2) & 3] == 2) break;  // tile stopped at block j-2
-                if (lane == 0) mbar_expect_tx(smem_u32(&c.kv_full[st]), 2 * kTileBytes);
-                __syncwarp();
-                int32_t kr[4], vr[4];
-                for (int i = 0; i < 4; ++i) {
-                    const int64_t tok = key_token(a, t, kv, j, lane * 4 + i);
-                    kr[i] = (int32_t)(kb + tok * ks);
-                    vr[i] = (int32_t)(vb + tok * vs);
+                // acquiring stage j implies block j-kStages was decided; a stop there ends the tile
+                if (j >= kStages && c.dec[(j - kStages) & 3] == 2) break;
+                if (lt == 0) {
+                    mbar_expect_tx(smem_u32(&c.k_full[st]), kTileBytes);
+                    mbar_expect_tx(smem_u32(&c.v_full[st]), kTileBytes);
                 }
-                const uint32_t kdst = sK + st * kTileBytes + lane * 512;
-                const uint32_t vdst = sV + st * kTileBytes + lane * 512;
-                for (int h = 0; h < 2; ++h) {
-                    tma_gather4(kdst + h * kHalf, &kmap, h * 64, kr[0], kr[1], kr[2], kr[3], smem_u32(&c.kv_full[st]));
-                    tma_gather4(vdst + h * kHalf, &vmap, h * 64, vr[0], vr[1], vr[2], vr[3], smem_u32(&c.kv_full[st]));
+                named_bar_sync(2, 96);
+                const uint32_t kdst = sK + st * kTileBytes;
+                const uint32_t vdst = sV + st * kTileBytes;
+                if (j < t.nd && p.kv_contig) {
+                    if (lt == 0) {
+                        const int64_t tok = t.sb + (int64_t)j * kBN;
+                        for (int h = 0; h < 2; ++h)
+                            tma_load2d(kdst + h * kHalf, &ktile, h * 64, (int32_t)(kb + tok), smem_u32(&c.k_full[st]));
+                        for (int h = 0; h < 2; ++h)
+                            tma_load2d(vdst + h * kHalf, &vtile, h * 64, (int32_t)(vb + tok), smem_u32(&c.v_full[st]));
+                    }
+                } else {
+                    // K first (Q K^T waits only for K), then V: 64 ops each, lt < 64 -> op 0/1
+                    for (int u = 0; u < 2; ++u) {
+                        const int op = lt + u * 96;  // ops [0,64): K, [64,128): V; op>>1 = group
+                        if (op >= 128) break;
+                        const int grp = (op >> 1) & 31, h = op & 1;
+                        const bool isv = op >= 64;
+                        tma_gather4((isv ? vdst : kdst) + h * kHalf + grp * 512, isv ? &vmap : &kmap, h * 64,
+                                    isv ? cv[u][0] : ck[u][0], isv ? cv[u][1] : ck[u][1],
+                                    isv ? cv[u][2] : ck[u][2], isv ? cv[u][3] : ck[u][3],
+                                    smem_u32(isv ? &c.v_full[st] : &c.k_full[st]));
+                    }
                 }
+                for (int u = 0; u < 2; ++u)
+                    for (int i = 0; i < 4; ++i) {
+                        ck[u][i] = nk[u][i];
+                        cv[u][i] = nv[u][i];
+                    }
                 ++loaded;
             }
             gblk += loaded;
         }
-    } else if (warp == 5) {
+    } else if (warp == 4) {
         // ============================== MMA issuer ==============================
         const uint32_t idesc_s = umma_idesc_bf16(kBM, kBN, false, false);
         const uint32_t idesc_o = umma_idesc_bf16(kBM, kD, false, true);
-        uint32_t gblk = 0, qcount = 0, gp = 0;
+        uint32_t gblk = 0, gq = 0, qcount = 0, gp = 0;  // loads, Q K^T (S buffer uses), p_full
         for (int64_t tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
             const TileInfo t = tile_info(a, tile);
             if (t.nb == 0) continue;
@@ -221,10 +276,11 @@ tc_pass_kernel(const TcParams p, const __grid_constant__ CUtensorMap qmap,
             int stop_at = -1;
             auto issue_qk = [&](int j) {
                 const uint32_t gi = gblk + j;
+                const uint32_t gs = gq + j;  // S buffer sequence (loads may run further ahead)
                 const int st = gi % kStages;
-                const int sb = gi & 1;
-                mbar_wait(smem_u32(&c.kv_full[st]), (gi / kStages) & 1, 2002);
-                mbar_wait(smem_u32(&c.s_empty[sb]), ((gi >> 1) & 1) ^ 1, 2003);
+                const int sb = gs & 1;
+                mbar_wait(smem_u32(&c.k_full[st]), (gi / kStages) & 1, 2002);
+                mbar_wait(smem_u32(&c.s_empty[sb]), ((gs >> 1) & 1) ^ 1, 2003);
                 tc_fence_after();
                 const uint32_t kbase = sK + st * kTileBytes;
                 for (int kk = 0; kk < kD / 16; ++kk) {
@@ -245,10 +301,13 @@ tc_pass_kernel(const TcParams p, const __grid_constant__ CUtensorMap qmap,
                     const uint32_t gi = gblk + j;
                     const int st = gi % kStages;
                     if (c.dec[j & 3] == 1) {
+                        mbar_wait(smem_u32(&c.v_full[st]), (gi / kStages) & 1, 2005);
+                        tc_fence_after();
                         const uint32_t vbase = sV + st * kTileBytes;
+                        const uint32_t pbase = sK + st * kTileBytes;  // P aliases K(j)
                         for (int kk = 0; kk < kBN / 16; ++kk) {
                             const uint32_t aoff = (kk / 4) * kHalf + (kk % 4) * 32;
-                            umma_bf16(tbase + kColO, umma_desc_sw128(sP + aoff, 16, 1024),
+                            umma_bf16(tbase + kColO, umma_desc_sw128(pbase + aoff, 16, 1024),
                                       umma_desc_sw128(vbase + kk * 16 * 128, kHalf, 1024), idesc_o, 1);
                         }
                         umma_commit(smem_u32(&c.kv_empty[st]));
@@ -259,10 +318,22 @@ tc_pass_kernel(const TcParams p, const __grid_constant__ CUtensorMap qmap,
                         // before publishing this decision, so barrier phases never run
                         // two ahead of their waiters)
                         stop_at = j;
+                        mbar_wait(smem_u32(&c.v_full[st]), (gi / kStages) & 1, 2006);
                         mbar_arrive(smem_u32(&c.kv_empty[st]));
                         if (j + 1 < t.nb) {
-                            // Q K^T of block j+1 was issued speculatively: free its stage once done
-                            umma_commit(smem_u32(&c.kv_empty[(gi + 1) % kStages]));
+                            // Q K^T of block j+1 was issued speculatively: its V must land before
+                            // the stage is freed (v_full phase accounting), then free it once done
+                            const uint32_t g1 = gi + 1;
+                            mbar_wait(smem_u32(&c.v_full[g1 % kStages]), (g1 / kStages) & 1, 2007);
+                            umma_commit(smem_u32(&c.kv_empty[g1 % kStages]));
+                        }
+                        // blocks j+2 .. j+kStages-1 were loaded (the loader runs kStages ahead of
+                        // the decisions) but never computed: consume and free them
+                        for (int jj = j + 2; jj < min(t.nb, j + kStages); ++jj) {
+                            const uint32_t g2 = gblk + jj;
+                            mbar_wait(smem_u32(&c.k_full[g2 % kStages]), (g2 / kStages) & 1, 2008);
+                            mbar_wait(smem_u32(&c.v_full[g2 % kStages]), (g2 / kStages) & 1, 2009);
+                            mbar_arrive(smem_u32(&c.kv_empty[g2 % kStages]));
                         }
                         umma_commit(smem_u32(&c.q_empty));
                         break;
@@ -271,13 +342,14 @@ tc_pass_kernel(const TcParams p, const __grid_constant__ CUtensorMap qmap,
             }
             __syncwarp();
             stop_at = __shfl_sync(0xffffffffu, stop_at, 0);
-            gblk += (stop_at >= 0) ? min(t.nb, stop_at + 2) : t.nb;
+            gblk += (stop_at >= 0) ? min(t.nb, stop_at + kStages) : t.nb;
+            gq += (stop_at >= 0) ? min(t.nb, stop_at + 2) : t.nb;
         }
     } else {
         // ============================== softmax / epilogue ==============================
         const int r = threadIdx.x;  // 0..127, TMEM lane
         const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
-        uint32_t gblk = 0, gp = 0, od = 0;
+        uint32_t gblk = 0, gq = 0, gp = 0, od = 0;
         for (int64_t tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
             const TileInfo t = tile_info(a, tile);
             const bool valid = r < t.tn;
@@ -315,9 +387,10 @@ tc_pass_kernel(const TcParams p, const __grid_constant__ CUtensorMap qmap,
             bool stopped = false;
             int stop_j = -1;
             for (int j = 0; j < t.nb; ++j) {
-                const uint32_t gi = gblk + j;
-                const int sb = gi & 1;
-                mbar_wait(smem_u32(&c.s_full[sb]), (gi >> 1) & 1, 3001);
+                const uint32_t gi = gblk + j;  // load sequence (K stage holding P)
+                const uint32_t gs = gq + j;    // S buffer sequence
+                const int sb = gs & 1;
+                mbar_wait(smem_u32(&c.s_full[sb]), (gs >> 1) & 1, 3001);
                 tc_fence_after();
                 uint32_t sv[kBN];
                 {
@@ -404,7 +477,7 @@ tc_pass_kernel(const TcParams p, const __grid_constant__ CUtensorMap qmap,
                     if (lane == 0) mbar_arrive(smem_u32(&c.p_full));
                     stopped = true;
                     if (j + 1 < t.nb) {  // drain the speculative Q K^T of block j+1
-                        const uint32_t gn = gi + 1;
+                        const uint32_t gn = gs + 1;
                         mbar_wait(smem_u32(&c.s_full[gn & 1]), (gn >> 1) & 1, 3002);
                         __syncwarp();
                         if (lane == 0) mbar_arrive(smem_u32(&c.s_empty[gn & 1]));
@@ -423,7 +496,7 @@ tc_pass_kernel(const TcParams p, const __grid_constant__ CUtensorMap qmap,
                     tmem_st_wait();
                 }
                 // P (bf16) -> smem, K-major SW128
-                unsigned char* prow = smem + kOffP + r * 128;
+                unsigned char* prow = smem + kOffK + (gi % kStages) * kTileBytes + r * 128;
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
 #pragma unroll
@@ -456,7 +529,8 @@ tc_pass_kernel(const TcParams p, const __grid_constant__ CUtensorMap qmap,
                 ++od;
                 tc_fence_after();
             }
-            gblk += (t.nb == 0) ? 0 : (stopped ? min(t.nb, stop_j + 2) : t.nb);
+            gblk += (t.nb == 0) ? 0 : (stopped ? min(t.nb, stop_j + kStages) : t.nb);
+            gq += (t.nb == 0) ? 0 : (stopped ? min(t.nb, stop_j + 2) : t.nb);
             // ---- read O, finalize / persist
             const float inv = 1.0f / ell;
             for (int c0 = 0; c0 < kD; c0 += 32) {
@@ -522,13 +596,14 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
     return fn;
 }
 
-// 2-D view of a [.., D] bf16 tensor as rows of D elements; box = 1 row x 64 columns (gather4).
-bool make_row_map(CUtensorMap* map, const void* base, int64_t rows) {
+// 2-D view of a [.., D] bf16 tensor as rows of D elements; box = box_rows x 64 columns
+// (1 row for tile::gather4, 128 rows for contiguous tile loads).
+bool make_row_map(CUtensorMap* map, const void* base, int64_t rows, uint32_t box_rows = 1) {
     auto enc = get_encode();
     if (!enc) return false;
     cuuint64_t dims[2] = {(cuuint64_t)kD, (cuuint64_t)rows};
     cuuint64_t strides[1] = {(cuuint64_t)kD * 2};
-    cuuint32_t box[2] = {64, 1};
+    cuuint32_t box[2] = {64, box_rows};
     cuuint32_t es[2] = {1, 1};
     return enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, es,
                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -559,15 +634,20 @@ bool tc_supported(const PassArgs& a) {
 
 cudaError_t launch_tc_pass(const PassArgs& a, cudaStream_t st) {
     const Geo& g = a.g;
-    CUtensorMap qmap, kmap, vmap;
-    if (!make_row_map(&qmap, a.q, span_rows(g.qs, g.z, g.hq, g.l)) ||
-        !make_row_map(&kmap, a.k, span_rows(g.ks, g.z, g.hkv, g.l)) ||
-        !make_row_map(&vmap, a.v, span_rows(g.vs, g.z, g.hkv, g.l)))
+    CUtensorMap qmap, kmap, vmap, qtile, ktile, vtile;
+    const int64_t qrows = span_rows(g.qs, g.z, g.hq, g.l);
+    const int64_t krows = span_rows(g.ks, g.z, g.hkv, g.l);
+    const int64_t vrows = span_rows(g.vs, g.z, g.hkv, g.l);
+    if (!make_row_map(&qmap, a.q, qrows) || !make_row_map(&kmap, a.k, krows) ||
+        !make_row_map(&vmap, a.v, vrows) || !make_row_map(&qtile, a.q, qrows, kBM) ||
+        !make_row_map(&ktile, a.k, krows, kBN) || !make_row_map(&vtile, a.v, vrows, kBN))
         return cudaErrorInvalidValue;
     TcParams p;
     std::memset(&p, 0, sizeof p);
     p.a = a;
     p.scale_log2 = (float)(a.scale * 1.4426950408889634);
+    p.q_contig = g.qs[2] == kD;
+    p.kv_contig = g.ks[2] == kD && g.vs[2] == kD;
     static bool attr_done = false;
     if (!attr_done) {
         cudaError_t e = cudaFuncSetAttribute(tc_pass_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
@@ -579,7 +659,7 @@ cudaError_t launch_tc_pass(const PassArgs& a, cudaStream_t st) {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const int64_t tiles = g.z * g.hq * a.tiles_per_head;
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, sms));
-    tc_pass_kernel<<<grid, kThreads, kSmemBytes, st>>>(p, qmap, kmap, vmap);
+    tc_pass_kernel<<<grid, kThreads, kSmemBytes, st>>>(p, qmap, kmap, vmap, qtile, ktile, vtile);
     return cudaGetLastError();
 }
 

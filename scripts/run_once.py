@@ -1,0 +1,14 @@
+"""One S2O forward at the C2/C3 shape (for ncu captures): plan, pass-1, pass-2."""
+import sys, os
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+import paper_2602_22575_b200 as s2o
+L = int(sys.argv[1]) if len(sys.argv) > 1 else 32768
+q, k, v = s2o.generate_synthetic("mixed", L // 64, 8.0, 0, 1, 32, L, 128)
+qd = torch.from_numpy(q).cuda().to(torch.bfloat16)
+kd = torch.from_numpy(k[:, :8]).cuda().to(torch.bfloat16)
+vd = torch.from_numpy(v[:, :8]).cuda().to(torch.bfloat16)
+cfg = s2o.KernelConfig(seg_len=2048, tau=0.005)
+res = s2o.s2o_attention(qd, kd, vd, cfg)
+torch.cuda.synchronize()
+print("pairs", res.trace.pass1_pairs.sum().item(), res.trace.pass2_pairs.sum().item())
