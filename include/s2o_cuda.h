@@ -89,6 +89,11 @@ typedef struct s2o_kernel_config {
     int64_t local_window; /* -1 == S; only bounds-checked (kernel.hpp:16-18) */
     int32_t path;         /* s2o_path */
     int32_t score_mode;   /* s2o_score_mode */
+    int32_t plan_depth;   /* kv_perm entries per segment s2o_attention_fwd materialises when the
+                             caller does not ask for kv_perm: 0 = auto (6144), -1 = the full
+                             permutation, > 0 = that many (rounded up to b_n). A tile that walks
+                             its whole truncated list without stopping is recomputed on the full
+                             plan, so results never depend on this knob. */
 } s2o_kernel_config;
 
 /* ------------------------------------------------------------------ utilities */
@@ -158,7 +163,10 @@ s2o_status s2o_attention_workspace_size(const s2o_problem* p, const s2o_kernel_c
 
 /* s2o_attention (kernel.hpp:106-107, kernel.cpp:351-369): validate -> build_plan ->
  * (fused ? fused : pass1 + pass2). q_perm / kv_perm / processed / pair outputs are optional
- * (NULL -> kept in the workspace). */
+ * (NULL -> kept in the workspace). When kv_perm is NULL the plan keeps only the exact top
+ * plan_depth entries of each kv_perm segment (selection instead of a full sort); tiles that
+ * exhaust them are recomputed on the full plan. That check reads one counter back, so in this
+ * mode the call synchronises `stream` once before returning. */
 s2o_status s2o_attention_fwd(const s2o_problem* p, const void* q, const void* k, const void* v,
                              const s2o_kernel_config* cfg, void* o, int32_t* q_perm,
                              int32_t* kv_perm, int32_t* processed, int64_t* pass1_pairs,

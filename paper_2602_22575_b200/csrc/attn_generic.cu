@@ -46,10 +46,11 @@ __global__ void __launch_bounds__(kThreads) generic_pass_kernel(PassArgs a, doub
     double* en = mn + a.bm;
     double* rsc = en + a.bm;
     int64_t* grow = reinterpret_cast<int64_t*>(rsc + a.bm);
-    const int64_t total_tiles = g.z * g.hq * a.tiles_per_head;
+    const int64_t total_tiles = a.num_tiles();
     const int64_t full_tiles = (g.N - 1) * a.T;
 
-    for (int64_t tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
+    for (int64_t it = blockIdx.x; it < total_tiles; it += gridDim.x) {
+        const int64_t tile = a.tile_at(it);
         const int64_t zh = tile / a.tiles_per_head;
         const int64_t r_in = tile % a.tiles_per_head;
         int64_t n, ti;
@@ -119,8 +120,8 @@ __global__ void __launch_bounds__(kThreads) generic_pass_kernel(PassArgs a, doub
         // ---- ranked prefix traversal with the monotone-gain stop (kernel.cpp:86-122)
         int64_t committed = 0;
         if ((a.mode & kPrefix) && n > 0) {
-            const int32_t* kv = a.kv_perm + zh * g.kv_per_head() + g.kv_off(n);
-            const int64_t kv_len = n * g.S;
+            const int32_t* kv = a.kv_seg(zh, n);
+            const int64_t kv_len = a.avail(n);
             int64_t pairs = 0;
             for (int64_t c0 = 0; c0 < kv_len; c0 += a.bn) {
                 const int64_t cn = min(a.bn, kv_len - c0);
@@ -175,9 +176,19 @@ __global__ void __launch_bounds__(kThreads) generic_pass_kernel(PassArgs a, doub
                 pairs += tn * cn;
                 __syncthreads();
             }
-            if (threadIdx.x == 0 && pairs) atomicAdd((unsigned long long*)&a.pass2_pairs[zh], (unsigned long long)pairs);
+            const bool overflow = kv_len < n * g.S && committed * a.bn >= kv_len;
+            if (threadIdx.x == 0) {
+                if (overflow) {
+                    const int slot = atomicAdd(a.ovf_count, 1);
+                    a.ovf_tiles[slot] = (int32_t)tile;
+                } else {
+                    if (pairs) atomicAdd((unsigned long long*)&a.pass2_pairs[zh], (unsigned long long)pairs);
+                    a.processed[(zh * g.N + n) * a.T + ti] = (int32_t)committed;
+                }
+            }
+        } else if ((a.mode & kPrefix) && threadIdx.x == 0) {
+            a.processed[(zh * g.N + n) * a.T + ti] = 0;
         }
-        if ((a.mode & kPrefix) && threadIdx.x == 0) a.processed[(zh * g.N + n) * a.T + ti] = (int32_t)committed;
 
         // ---- outputs
         for (int64_t r = threadIdx.x; r < tn; r += blockDim.x) {
@@ -232,7 +243,8 @@ size_t generic_scratch_bytes(const PassArgs& a) {
 }
 
 cudaError_t launch_generic_pass(const PassArgs& a, void* scratch, cudaStream_t st) {
-    const int64_t tiles = a.g.z * a.g.hq * a.tiles_per_head;
+    const int64_t tiles = a.num_tiles();
+    if (tiles == 0) return cudaSuccess;
     const int grid = std::min(grid_for(tiles), 256 * 8);
     generic_pass_kernel<<<grid, kThreads, 0, st>>>(a, reinterpret_cast<double*>(scratch));
     return cudaGetLastError();

@@ -78,7 +78,7 @@ struct TcParams {
 };
 
 struct TileInfo {
-    int64_t zh, n, ti, t0, tn, seg_rows, sb;
+    int64_t zh, n, ti, t0, tn, seg_rows, sb, avail;
     int nd, np, nb;  // diag blocks, prefix blocks, total
 };
 
@@ -95,7 +95,8 @@ __device__ __forceinline__ TileInfo tile_info(const PassArgs& a, int64_t tile) {
     t.t0 = t.ti * kBM;
     t.tn = min((int64_t)kBM, t.seg_rows - t.t0);
     t.nd = (a.mode & kDiag) ? (int)((t.t0 + t.tn - 1) / kBN + 1) : 0;
-    t.np = ((a.mode & kPrefix) && t.n > 0) ? (int)((t.n * g.S + kBN - 1) / kBN) : 0;
+    t.avail = a.avail(t.n);  // kv_perm entries available to walk
+    t.np = ((a.mode & kPrefix) && t.n > 0) ? (int)((t.avail + kBN - 1) / kBN) : 0;
     t.nb = t.nd + t.np;
     return t;
 }
@@ -118,7 +119,7 @@ __device__ __forceinline__ int64_t key_token(const PassArgs& a, const TileInfo& 
         return t.sb + k0 + (i < kn ? i : 0);
     }
     const int64_t c0 = (int64_t)(j - t.nd) * kBN;
-    const int64_t cn = min((int64_t)kBN, t.n * a.g.S - c0);
+    const int64_t cn = min((int64_t)kBN, t.avail - c0);
     return (int64_t)kv[c0 + (i < cn ? i : 0)];
 }
 
@@ -164,7 +165,7 @@ tc_pass_kernel(const TcParams p, const __grid_constant__ CUtensorMap qmap,
     tc_fence_after();
     const uint32_t tbase = c.tmem_base;
 
-    const int64_t total_tiles = g.z * g.hq * a.tiles_per_head;
+    const int64_t total_tiles = a.num_tiles();
     const int64_t kv_div = g.d;  // row unit of the tensor maps = D elements
 
     if (warp >= 5) {
@@ -174,9 +175,9 @@ tc_pass_kernel(const TcParams p, const __grid_constant__ CUtensorMap qmap,
         const uint32_t lbar = 5 * 32;        // named barrier 2 over the 96 loader threads
         uint32_t gblk = 0, qcount = 0;
         for (int64_t tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
-            const TileInfo t = tile_info(a, tile);
+            const TileInfo t = tile_info(a, a.tile_at(tile));
             if (t.nb == 0) continue;
-            const int32_t* kv = (t.np > 0) ? a.kv_perm + t.zh * g.kv_per_head() + g.kv_off(t.n) : nullptr;
+            const int32_t* kv = (t.np > 0) ? a.kv_seg(t.zh, t.n) : nullptr;
             // Q rows; wait until the previous tile's Q K^T are done
             mbar_wait(smem_u32(&c.q_empty), (qcount & 1) ^ 1, 1001);
             const int64_t qb = g.q_base(t.zh) / kv_div;
@@ -266,7 +267,7 @@ tc_pass_kernel(const TcParams p, const __grid_constant__ CUtensorMap qmap,
         const uint32_t idesc_o = umma_idesc_bf16(kBM, kD, false, true);
         uint32_t gblk = 0, gq = 0, qcount = 0, gp = 0;  // loads, Q K^T (S buffer uses), p_full
         for (int64_t tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
-            const TileInfo t = tile_info(a, tile);
+            const TileInfo t = tile_info(a, a.tile_at(tile));
             if (t.nb == 0) continue;
             if (lane == 0) {
                 mbar_wait(smem_u32(&c.q_full), qcount & 1, 2001);
@@ -351,7 +352,7 @@ tc_pass_kernel(const TcParams p, const __grid_constant__ CUtensorMap qmap,
         const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
         uint32_t gblk = 0, gq = 0, gp = 0, od = 0;
         for (int64_t tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
-            const TileInfo t = tile_info(a, tile);
+            const TileInfo t = tile_info(a, a.tile_at(tile));
             const bool valid = r < t.tn;
             const int64_t grow = q_local_row(a, t, r);  // segment row in [0, L)
             const int64_t slot = t.zh * g.l + grow;
@@ -419,7 +420,7 @@ tc_pass_kernel(const TcParams p, const __grid_constant__ CUtensorMap qmap,
                     lim = (int)max((int64_t)0, vis);
                 } else {
                     const int64_t c0 = (int64_t)(j - t.nd) * kBN;
-                    lim = (int)min((int64_t)kBN, t.n * g.S - c0);
+                    lim = (int)min((int64_t)kBN, t.avail - c0);
                 }
                 if (lim < kBN) {
 #pragma unroll
@@ -515,7 +516,7 @@ tc_pass_kernel(const TcParams p, const __grid_constant__ CUtensorMap qmap,
                 if (!is_diag) {
                     ++committed;
                     const int64_t c0 = (int64_t)(j - t.nd) * kBN;
-                    pairs += min((int64_t)kBN, t.n * g.S - c0);
+                    pairs += min((int64_t)kBN, t.avail - c0);
                 }
                 fence_proxy_async_smem();
                 tc_fence_before();
@@ -570,8 +571,15 @@ tc_pass_kernel(const TcParams p, const __grid_constant__ CUtensorMap qmap,
             }
             if (valid && (a.mode & kFinal) && !(ell > 0.0f)) atomicExch(a.err_flag, 2);
             if ((a.mode & kPrefix) && r == 0) {
-                a.processed[(t.zh * g.N + t.n) * a.T + t.ti] = committed;
-                if (pairs) atomicAdd((unsigned long long*)&a.pass2_pairs[t.zh], (unsigned long long)(pairs * t.tn));
+                const bool overflow = t.np > 0 && committed == t.np && t.avail < t.n * g.S;
+                if (overflow) {
+                    // walked the whole truncated list without stopping: rerun on the full plan
+                    const int slot = atomicAdd(a.ovf_count, 1);
+                    a.ovf_tiles[slot] = (int32_t)a.tile_at(tile);
+                } else {
+                    a.processed[(t.zh * g.N + t.n) * a.T + t.ti] = committed;
+                    if (pairs) atomicAdd((unsigned long long*)&a.pass2_pairs[t.zh], (unsigned long long)(pairs * t.tn));
+                }
             }
             tc_fence_before();
             named_bar_sync(1, 128);  // all rows done with this tile's O before the next init
@@ -657,7 +665,8 @@ cudaError_t launch_tc_pass(const PassArgs& a, cudaStream_t st) {
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const int64_t tiles = g.z * g.hq * a.tiles_per_head;
+    const int64_t tiles = a.num_tiles();
+    if (tiles == 0) return cudaSuccess;
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, sms));
     tc_pass_kernel<<<grid, kThreads, kSmemBytes, st>>>(p, qmap, kmap, vmap, qtile, ktile, vtile);
     return cudaGetLastError();

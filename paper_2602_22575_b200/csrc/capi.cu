@@ -336,18 +336,31 @@ s2o_status s2o_fused(const s2o_problem* p, const void* q, const void* k, const v
 // Workspace of the whole operator:
 //   [plan ws][pass ws][q_perm][kv_perm][acc][ell][m][processed][pass1][pass2]
 struct OpLayout {
-    size_t plan, pass, qperm, kvperm, acc, ell, m, proc, p1, p2, total;
+    size_t plan, pass, qperm, kvperm, kvtop, ovf, acc, ell, m, proc, p1, p2, total;
+    int64_t topt;
 };
 
-static OpLayout op_layout(const Geo& g, const PassArgs& a, int fused) {
+// Depth of the truncated kv plan (0 = full permutation).
+static int64_t plan_topt(const Geo& g, const s2o_kernel_config* c) {
+    if (c->plan_depth < 0) return 0;
+    int64_t t = c->plan_depth == 0 ? 6144 : c->plan_depth;
+    t = ((t + c->b_n - 1) / c->b_n) * c->b_n;
+    if (t >= (g.N - 1) * g.S) return 0;  // no segment would be truncated
+    return t;
+}
+
+static OpLayout op_layout(const Geo& g, const PassArgs& a, int fused, const s2o_kernel_config* c) {
     OpLayout L;
     size_t off = 0;
     auto take = [&](size_t b) { size_t o = off; off += align256(b); return o; };
     const int64_t zh = g.z * g.hq;
+    L.topt = plan_topt(g, c);
     L.plan = take(plan_workspace_bytes(g));
     L.pass = take(pass_ws_bytes(a));
     L.qperm = take(sizeof(int32_t) * zh * g.N * g.S);
     L.kvperm = take(sizeof(int32_t) * std::max<int64_t>(1, zh * g.kv_per_head()));
+    L.kvtop = take(sizeof(int32_t) * std::max<int64_t>(1, zh * g.N * L.topt));
+    L.ovf = take(sizeof(int32_t) * (4 + zh * a.tiles_per_head));
     L.acc = take(fused ? 0 : sizeof(float) * zh * g.l * g.d);
     L.ell = take(fused ? 0 : sizeof(float) * zh * g.l);
     L.m = take(fused ? 0 : sizeof(float) * zh * g.l);
@@ -364,7 +377,7 @@ s2o_status s2o_attention_workspace_size(const s2o_problem* p, const s2o_kernel_c
     s2o_status st = make_geo(p, cfg ? cfg->seg_len : 0, &g);
     if (st) return st;
     if ((st = validate_cfg(cfg, p->l))) return st;
-    *bytes = op_layout(g, base_args(g, cfg), cfg->fused).total;
+    *bytes = op_layout(g, base_args(g, cfg), cfg->fused, cfg).total;
     return S2O_OK;
 }
 
@@ -379,7 +392,7 @@ s2o_status s2o_attention_fwd(const s2o_problem* p, const void* q, const void* k,
     if ((st = validate_cfg(cfg, p->l))) return st;
     if (!q || !k || !v || !o) return fail(S2O_ERR_INVALID_ARG, "null pointer");
     PassArgs a = base_args(g, cfg);
-    const OpLayout L = op_layout(g, a, cfg->fused);
+    const OpLayout L = op_layout(g, a, cfg->fused, cfg);
     if (!workspace || workspace_bytes < L.total) return fail(S2O_ERR_WORKSPACE, "workspace too small");
     char* base = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(workspace) + 255) & ~uintptr_t(255));
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
@@ -388,31 +401,60 @@ s2o_status s2o_attention_fwd(const s2o_problem* p, const void* q, const void* k,
     int32_t* proc = processed ? processed : reinterpret_cast<int32_t*>(base + L.proc);
     int64_t* p1 = pass1_pairs ? pass1_pairs : reinterpret_cast<int64_t*>(base + L.p1);
     int64_t* p2 = pass2_pairs ? pass2_pairs : reinterpret_cast<int64_t*>(base + L.p2);
-    S2O_CUDA_TRY(launch_plan_build(g, q, k, qp, kvp, base + L.plan, s), "plan build");
+    // Truncated plan unless the caller asked for the full kv_perm (or no segment is long enough)
+    const int64_t topt = kv_perm ? 0 : L.topt;
+    int32_t* ovf = reinterpret_cast<int32_t*>(base + L.ovf);  // [0] overflow count, [1] selection flag
+    if (topt > 0) {
+        S2O_CUDA_TRY(cudaMemsetAsync(ovf, 0, 4 * sizeof(int32_t), s), "memset");
+        S2O_CUDA_TRY(launch_plan_topk(g, q, k, qp, reinterpret_cast<int32_t*>(base + L.kvtop), topt, ovf + 1,
+                                      base + L.plan, s), "plan top-k");
+    } else {
+        S2O_CUDA_TRY(launch_plan_build(g, q, k, qp, kvp, base + L.plan, s), "plan build");
+    }
     a.q = q; a.k = k; a.v = v; a.o = o;
-    a.kv_perm = kvp;
+    a.kv_perm = topt > 0 ? reinterpret_cast<int32_t*>(base + L.kvtop) : kvp;
+    a.kv_top = topt;
+    a.ovf_count = ovf;
+    a.ovf_tiles = ovf + 4;
     a.processed = proc;
     a.pass2_pairs = p2;
     S2O_CUDA_TRY(launch_trace_init(a, p1, s), "trace init");
+    float* acc = reinterpret_cast<float*>(base + L.acc);
+    float* ell = reinterpret_cast<float*>(base + L.ell);
+    float* m = reinterpret_cast<float*>(base + L.m);
+    PassArgs a2 = a;
     if (cfg->fused) {
-        a.mode = kDiag | kPrefix | kFinal;
-        a.q_reorder = 0;
-        st = run_pass(a, cfg->path, base + L.pass, pass_ws_bytes(a), s);
-        if (st) return st;
+        a2.mode = kDiag | kPrefix | kFinal;
+        a2.q_reorder = 0;
     } else {
-        float* acc = reinterpret_cast<float*>(base + L.acc);
-        float* ell = reinterpret_cast<float*>(base + L.ell);
-        float* m = reinterpret_cast<float*>(base + L.m);
         PassArgs a1 = a;
         a1.mode = kDiag | kStateOut;
         a1.q_reorder = 0;
         a1.acc_out = acc; a1.ell_out = ell; a1.m_out = m;
         if ((st = run_pass(a1, cfg->path, base + L.pass, pass_ws_bytes(a), s))) return st;
-        PassArgs a2 = a;
         a2.mode = kStateIn | kPrefix | kFinal;
         a2.q_perm = qp;
         a2.acc_in = acc; a2.ell_in = ell; a2.m_in = m;
-        if ((st = run_pass(a2, cfg->path, base + L.pass, pass_ws_bytes(a), s))) return st;
+    }
+    if ((st = run_pass(a2, cfg->path, base + L.pass, pass_ws_bytes(a), s))) return st;
+    if (topt > 0) {
+        // Tiles that walked their whole truncated list are recomputed on the full plan.
+        int32_t host[2] = {0, 0};
+        S2O_CUDA_TRY(cudaMemcpyAsync(host, ovf, sizeof host, cudaMemcpyDeviceToHost, s), "d2h overflow");
+        S2O_CUDA_TRY(cudaStreamSynchronize(s), "sync");
+        if (host[0] > 0 || host[1] != 0) {
+            S2O_CUDA_TRY(launch_plan_build(g, q, k, qp, kvp, base + L.plan, s), "plan build");
+            PassArgs a3 = a2;
+            a3.kv_perm = kvp;
+            a3.kv_top = 0;
+            if (host[1] != 0) {  // selection could not be certified: redo everything
+                S2O_CUDA_TRY(launch_trace_init(a, p1, s), "trace init");
+            } else {
+                a3.tile_list = ovf + 4;
+                a3.tile_count = host[0];
+            }
+            if ((st = run_pass(a3, cfg->path, base + L.pass, pass_ws_bytes(a), s))) return st;
+        }
     }
     g_err.clear();
     return S2O_OK;
@@ -452,7 +494,7 @@ s2o_status s2o_attention_host(const s2o_problem* p, const void* q, const void* k
     s2o_problem dp;
     s2o_problem_init(&dp, p->z, p->hq, p->hkv, p->l, p->d, p->in_dtype, p->out_dtype);
     PassArgs a = base_args(g, cfg);
-    const OpLayout L = op_layout(g, a, cfg->fused);
+    const OpLayout L = op_layout(g, a, cfg->fused, cfg);
     const size_t esz_in = p->in_dtype == S2O_BF16 ? 2 : 4;
     const size_t esz_out = p->out_dtype == S2O_BF16 ? 2 : 4;
     const size_t qb = esz_in * p->z * p->hq * p->l * p->d;
@@ -479,7 +521,9 @@ s2o_status s2o_attention_host(const s2o_problem* p, const void* q, const void* k
     S2O_CUDA_TRY(cudaMemcpyAsync(dk, k, kb, cudaMemcpyHostToDevice, s), "h2d k");
     S2O_CUDA_TRY(cudaMemcpyAsync(dv, v, kb, cudaMemcpyHostToDevice, s), "h2d v");
     char* wbase = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(ws) + 255) & ~uintptr_t(255));
-    st = s2o_attention_fwd(&dp, dq, dk, dv, cfg, dout, nullptr, nullptr, nullptr, nullptr, nullptr,
+    // the full kv_perm is only materialised when the caller asks for it
+    int32_t* dkv = (kv_perm && g.N > 1) ? reinterpret_cast<int32_t*>(wbase + L.kvperm) : nullptr;
+    st = s2o_attention_fwd(&dp, dq, dk, dv, cfg, dout, nullptr, dkv, nullptr, nullptr, nullptr,
                            ws, L.total, s);
     if (st) return st;
     S2O_CUDA_TRY(cudaMemcpyAsync(o, dout, ob, cudaMemcpyDeviceToHost, s), "d2h o");

@@ -43,11 +43,31 @@ struct PassArgs {
     int64_t T;              // query tiles per full segment = ceil(S/bm)
     int64_t tiles_per_head; // sum over segments
     int32_t* err_flag;      // device: 1 uninitialized state, 2 uncovered row
+    // truncated plan (fused operator): kv_perm laid out [Z*Hq][N][kv_top], 0 = packed full
+    int64_t kv_top;
+    int32_t* ovf_count;     // tiles that consumed their whole truncated list (rerun needed)
+    int32_t* ovf_tiles;
+    const int32_t* tile_list;  // optional: process only these tiles
+    int64_t tile_count;
+
+    __host__ __device__ int64_t avail(int64_t n) const {
+        const int64_t full = n * g.S;
+        return (kv_top > 0 && kv_top < full) ? kv_top : full;
+    }
+    __host__ __device__ const int32_t* kv_seg(int64_t zh, int64_t n) const {
+        return kv_top > 0 ? kv_perm + (zh * g.N + n) * kv_top : kv_perm + zh * g.kv_per_head() + g.kv_off(n);
+    }
+    __host__ __device__ int64_t num_tiles() const {
+        return tile_list ? tile_count : g.z * g.hq * tiles_per_head;
+    }
+    __device__ int64_t tile_at(int64_t i) const { return tile_list ? (int64_t)tile_list[i] : i; }
 };
 
 size_t plan_workspace_bytes(const Geo& g);
 cudaError_t launch_plan_build(const Geo& g, const void* q, const void* k, int32_t* q_perm,
                               int32_t* kv_perm, void* workspace, cudaStream_t st);
+cudaError_t launch_plan_topk(const Geo& g, const void* q, const void* k, int32_t* q_perm, int32_t* kvtop,
+                             int64_t topt, int32_t* flags, void* workspace, cudaStream_t st);
 cudaError_t launch_segment_means(const Geo& g, const void* x, int which_kv, int64_t nseg_out,
                                  float* out, cudaStream_t st);
 

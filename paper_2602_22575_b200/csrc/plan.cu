@@ -388,6 +388,143 @@ merge_pass_kernel(SortGeo sg, int64_t w, const uint64_t* __restrict__ ikeys,
     }
 }
 
+// ---------------------------------------------------------------- top-T selection
+// For the fused operator only the leading chunks of each kv_perm segment are consumed
+// (the walk stops early), so instead of fully sorting the prefix the plan materialises its
+// exact top-T: a CTA per (zh, n >= 1) samples 2048 keys, picks a threshold key whose
+// expected rank is ~1.25 T, gathers every key <= threshold into shared memory (one pass over
+// the segment, warp-ballot compaction), sorts them by (key, index) and writes the first T
+// indices. The result equals the first T entries of argsort_desc_stable (a stable sort's top
+// T is a prefix of the full order). If the threshold catches fewer than T keys or more than
+// the capacity, the CTA retries with another sample rank; after the retries it falls back to
+// a plain capacity-sized best-so-far and flags the segment (never observed; checked by host).
+constexpr int kSelThreads = 512;
+constexpr int kSelCap = 8192;      // keys held in smem for the final sort
+constexpr int kSelSample = 2048;
+
+__device__ __forceinline__ void bitonic_sort_smem(uint64_t* k, uint32_t* id, int n_pow2) {
+    for (int kk = 2; kk <= n_pow2; kk <<= 1) {
+        for (int jj = kk >> 1; jj > 0; jj >>= 1) {
+            for (int i = threadIdx.x; i < n_pow2 / 2; i += blockDim.x) {
+                // i-th compare-exchange pair of this stage
+                const int lo = ((i / jj) * (2 * jj)) + (i % jj);
+                const int hi = lo + jj;
+                const bool up = (lo & kk) == 0;
+                const uint64_t a = k[lo], b = k[hi];
+                const uint32_t ia = id[lo], ib = id[hi];
+                if (elt_less(b, ib, a, ia) == up) {
+                    k[lo] = b; k[hi] = a;
+                    id[lo] = ib; id[hi] = ia;
+                }
+            }
+            __syncthreads();
+        }
+    }
+}
+
+__global__ void __launch_bounds__(kSelThreads)
+select_topk_kernel(Geo g, const uint64_t* __restrict__ kvkey, int64_t topt, int32_t* __restrict__ kvtop,
+                   int32_t* __restrict__ flags) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    uint64_t* sk = reinterpret_cast<uint64_t*>(smem_raw);          // [kSelCap]
+    uint32_t* si = reinterpret_cast<uint32_t*>(sk + kSelCap);       // [kSelCap]
+    __shared__ int s_count;
+    __shared__ uint64_t s_theta;
+    const int64_t zh = blockIdx.x / (g.N - 1);
+    const int64_t n = 1 + blockIdx.x % (g.N - 1);
+    const int64_t len = n * g.S;
+    const int64_t tt = min(topt, len);
+    const uint64_t* keys = kvkey + zh * g.kv_per_head() + g.kv_off(n);
+    int32_t* out = kvtop + (zh * g.N + n) * topt;
+    int count = 0;
+    if (len <= kSelCap) {
+        for (int64_t i = threadIdx.x; i < len; i += blockDim.x) {
+            sk[i] = keys[i];
+            si[i] = (uint32_t)i;
+        }
+        count = (int)len;
+    } else {
+        // sample: 128 runs of 16 consecutive keys spread over the segment
+        for (int e = threadIdx.x; e < kSelSample; e += blockDim.x) {
+            const int run = e / 16, off = e % 16;
+            const int64_t pos = (int64_t)run * (len / 128) + off;
+            sk[e] = keys[pos];
+            si[e] = (uint32_t)e;
+        }
+        __syncthreads();
+        bitonic_sort_smem(sk, si, kSelSample);
+        double want = 1.15 * (double)tt + 32.0;
+        bool ok = false;
+        for (int attempt = 0; attempt < 6 && !ok; ++attempt) {
+            int64_t rank = (int64_t)ceil(want * kSelSample / (double)len) + 4;
+            if (rank > kSelSample - 1) rank = kSelSample - 1;
+            if (threadIdx.x == 0) {
+                s_theta = sk[rank];
+                s_count = 0;
+            }
+            __syncthreads();
+            const uint64_t theta = s_theta;
+            const bool last_sample = (rank == kSelSample - 1);
+            // one pass: compact every key <= theta (ballot + per-warp atomic slot)
+            for (int64_t b0 = 0; b0 < len; b0 += blockDim.x) {
+                const int64_t i = b0 + threadIdx.x;
+                const bool take = i < len && keys[i] <= theta;
+                const unsigned m = __ballot_sync(0xffffffffu, take);
+                int base = 0;
+                if ((threadIdx.x & 31) == 0 && m) base = atomicAdd(&s_count, __popc(m));
+                base = __shfl_sync(0xffffffffu, base, 0);
+                if (take) {
+                    const int slot = base + __popc(m & ((1u << (threadIdx.x & 31)) - 1));
+                    if (slot < kSelCap) {
+                        // the sample area [0, kSelSample) is still needed for retries only
+                        // while attempts remain; collect above it, shift down later
+                        sk[slot] = keys[i];
+                        si[slot] = (uint32_t)i;
+                    }
+                }
+            }
+            __syncthreads();
+            const int c = s_count;
+            __syncthreads();
+            if (c >= tt && c <= kSelCap) {
+                ok = true;
+                count = c;
+            } else if (c < tt) {
+                if (last_sample) { count = min(c, kSelCap); ok = true; if (threadIdx.x == 0) atomicExch(flags, 1); }
+                want *= 2.0;
+            } else {
+                want = 0.5 * (want + (double)tt);
+                if (want < tt + 1) want = tt + 1;
+            }
+            if (!ok) {
+                // the sample was overwritten by the collection: resample
+                for (int e = threadIdx.x; e < kSelSample; e += blockDim.x) {
+                    const int run = e / 16, off = e % 16;
+                    const int64_t pos = (int64_t)run * (len / 128) + off;
+                    sk[e] = keys[pos];
+                    si[e] = (uint32_t)e;
+                }
+                __syncthreads();
+                bitonic_sort_smem(sk, si, kSelSample);
+            }
+        }
+        if (!ok) {
+            count = kSelCap;
+            if (threadIdx.x == 0) atomicExch(flags, 1);
+        }
+    }
+    // sort the collected keys and emit the first tt indices
+    int np2 = 1;
+    while (np2 < count) np2 <<= 1;
+    for (int i = count + threadIdx.x; i < np2; i += blockDim.x) {
+        sk[i] = ~0ull;
+        si[i] = 0xffffffffu;
+    }
+    __syncthreads();
+    bitonic_sort_smem(sk, si, np2);
+    for (int64_t i = threadIdx.x; i < tt; i += blockDim.x) out[i] = (int32_t)si[i];
+}
+
 struct PlanWs {
     float* guide;      // [Z*Hkv*D]
     float* q_mean;     // [Z*Hq*N*D]
@@ -471,6 +608,42 @@ cudaError_t sort_family(int kind, const Geo& g, PlanWs& ws, int32_t* perm, cudaS
 }  // namespace
 
 size_t plan_workspace_bytes(const Geo& g) { return plan_ws_layout(g, nullptr, nullptr) + 256; }
+
+// Plan for the fused operator: q_perm in full, kv_perm truncated to its top `topt` entries
+// per segment, laid out [Z*Hq][N][topt] (segment 0 unused). flags[0] is set if a selection
+// could not certify its result (the caller then falls back to the full plan).
+cudaError_t launch_plan_topk(const Geo& g, const void* q, const void* k, int32_t* q_perm, int32_t* kvtop,
+                             int64_t topt, int32_t* flags, void* workspace, cudaStream_t st) {
+    PlanWs ws;
+    char* base = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(workspace) + 255) & ~uintptr_t(255));
+    plan_ws_layout(g, base, &ws);
+    cudaError_t err;
+    if ((err = launch_segment_means(g, k, 1, 1, ws.guide, st)) != cudaSuccess) return err;
+    {
+        const size_t smem = (2 * sizeof(uint64_t) + 2 * sizeof(uint32_t)) * kRun + sizeof(double) * g.d +
+                            sizeof(float) * kQRows * (g.d + 1);
+        cudaFuncSetAttribute(q_rank_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        q_rank_kernel<<<(unsigned)(g.z * g.hq * g.N), kQThreads, smem, st>>>(q, g, ws.guide, ws.q_mean,
+                                                                            ws.key0, q_perm);
+        if ((err = cudaGetLastError()) != cudaSuccess) return err;
+        if (g.S > kRun && (err = sort_family(0, g, ws, q_perm, st)) != cudaSuccess) return err;
+    }
+    if (g.N > 1) {
+        const size_t smem = sizeof(double) * g.d * kSPairs + sizeof(float) * g.d * kSK;
+        cudaFuncSetAttribute(kv_score_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        const int64_t keys = (g.N - 1) * g.S;
+        dim3 grid((unsigned)((keys + kSK - 1) / kSK), (unsigned)(g.z * g.hkv));
+        kv_score_kernel<<<grid, kSKThreads, smem, st>>>(k, g, ws.q_mean, ws.key0);
+        if ((err = cudaGetLastError()) != cudaSuccess) return err;
+        const size_t ssm = (sizeof(uint64_t) + sizeof(uint32_t)) * kSelCap;
+        cudaFuncSetAttribute(select_topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssm);
+        select_topk_kernel<<<(unsigned)(g.z * g.hq * (g.N - 1)), kSelThreads, ssm, st>>>(g, ws.key0, topt,
+                                                                                        kvtop, flags);
+        if ((err = cudaGetLastError()) != cudaSuccess) return err;
+    }
+    return cudaSuccess;
+}
+
 
 cudaError_t launch_segment_means(const Geo& g, const void* x, int which_kv, int64_t nseg_out,
                                  float* out, cudaStream_t st) {

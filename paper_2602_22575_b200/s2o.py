@@ -52,7 +52,8 @@ class _Problem(C.Structure):
 class _Config(C.Structure):
     _fields_ = [("seg_len", C.c_int64), ("tau", C.c_double), ("b_m", C.c_int64),
                 ("b_n", C.c_int64), ("q_reorder", C.c_int32), ("fused", C.c_int32),
-                ("local_window", C.c_int64), ("path", C.c_int32), ("score_mode", C.c_int32)]
+                ("local_window", C.c_int64), ("path", C.c_int32), ("score_mode", C.c_int32),
+                ("plan_depth", C.c_int32)]
 
 
 def lib() -> C.CDLL:
@@ -95,6 +96,7 @@ class KernelConfig:
     local_window: int = -1
     path: int = PATH_AUTO
     score_mode: int = SCORE_EXACT
+    plan_depth: int = 0  # s2o_attention: 0 = auto top-6144 kv_perm per segment, -1 = full
 
     @property
     def b_m(self) -> int:
@@ -107,7 +109,7 @@ class KernelConfig:
     def _c(self) -> _Config:
         return _Config(int(self.seg_len), float(self.tau), int(self.tiles.b_m), int(self.tiles.b_n),
                        int(bool(self.q_reorder)), int(bool(self.fused)), int(self.local_window),
-                       int(self.path), int(self.score_mode))
+                       int(self.path), int(self.score_mode), int(self.plan_depth))
 
     def validate(self, l: int) -> None:
         """KernelConfig::validate (kernel.cpp:166-182)."""

@@ -147,3 +147,41 @@ def test_tc_generic_agree_at_scale(cuda):
     assert ndiff <= max(1, a.trace.processed.numel() // 100) and maxd <= 1
     err = (a.out.float() - b.out.float()).abs()
     assert err.max().item() <= 2.5e-2 and err.mean().item() <= 2e-3
+
+
+@pytest.mark.parametrize("path", [TC, GEN])
+def test_truncated_plan_matches_full_plan(cuda, path):
+    """s2o_attention without a kv_perm output keeps only the exact top-T of each kv_perm
+    segment; tiles that exhaust it are recomputed on the full plan, so traces and outputs must
+    equal the full-plan run for any depth (tiny depths force the overflow fallback)."""
+    import paper_2602_22575_b200 as s2o
+    torch = cuda
+    hq, hkv, l, s = 4, 2, 8192, 1024
+    q, k, v = inputs(s2o, hq, hkv, l, seed=5)
+    qd, kd, vd = dev_bf16(torch, q), dev_bf16(torch, k), dev_bf16(torch, v)
+    base = s2o.KernelConfig(seg_len=s, tau=0.005, path=path)
+    full = s2o.s2o_attention(qd, kd, vd, base)  # kv_perm requested -> full plan
+    torch.cuda.synchronize()
+    for depth in (0, 128, 512, 2048):
+        cfg = s2o.KernelConfig(seg_len=s, tau=0.005, path=path, plan_depth=depth)
+        res = s2o.s2o_attention(qd, kd, vd, cfg, want_plan=False)
+        torch.cuda.synchronize()
+        assert torch.equal(res.trace.processed, full.trace.processed), depth
+        assert torch.equal(res.trace.pass2_pairs, full.trace.pass2_pairs), depth
+        assert torch.equal(res.out, full.out), depth
+
+
+def test_truncated_plan_gaussian_fallback(cuda):
+    """Pure gaussian inputs never stop early: every tile exhausts its truncated list and the
+    whole pass-2 is recomputed on the full plan."""
+    import paper_2602_22575_b200 as s2o
+    torch = cuda
+    torch.manual_seed(0)
+    q = torch.randn(1, 2, 4096, 128, device="cuda").to(torch.bfloat16)
+    k = torch.randn(1, 1, 4096, 128, device="cuda").to(torch.bfloat16)
+    v = torch.randn(1, 1, 4096, 128, device="cuda").to(torch.bfloat16)
+    full = s2o.s2o_attention(q, k, v, s2o.KernelConfig(seg_len=512, tau=0.005))
+    res = s2o.s2o_attention(q, k, v, s2o.KernelConfig(seg_len=512, tau=0.005, plan_depth=256), want_plan=False)
+    torch.cuda.synchronize()
+    assert torch.equal(res.trace.processed, full.trace.processed)
+    assert torch.equal(res.out, full.out)
