@@ -52,57 +52,61 @@ def peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
-
-    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    """SM clocks + throttle reasons sampled every 20 ms (NVML) during the timed region."""
 
     def __init__(self, index: int):
         self.index = index
-        self.proc = None
-        self.lines: list[str] = []
+        self.samples: list[tuple[float, float, int]] = []
+        self._stop = threading.Event()
+        self.ok = False
 
     def start(self):
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "200"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.thread = threading.Thread(target=self._read, daemon=True)
-            self.thread.start()
-        except FileNotFoundError:
-            self.proc = None
+            import pynvml
+            pynvml.nvmlInit()
+            self.nvml = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_mhz = float(pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM))
+            self.ok = True
+        except Exception:  # noqa: BLE001
+            return
+        self.thread = threading.Thread(target=self._run, daemon=True)
+        self.thread.start()
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.lines.append(line.strip())
+    def _run(self):
+        n = self.nvml
+        while not self._stop.is_set():
+            try:
+                sm = float(n.nvmlDeviceGetClockInfo(self.h, n.NVML_CLOCK_SM))
+                pw = n.nvmlDeviceGetPowerUsage(self.h) / 1000.0
+                rs = n.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                self.samples.append((sm, pw, rs))
+            except Exception:  # noqa: BLE001
+                pass
+            time.sleep(0.02)
 
     def stop(self) -> dict:
-        if self.proc is None:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        self.proc.terminate()
-        try:
-            self.proc.wait(timeout=5)
-        except subprocess.TimeoutExpired:
-            self.proc.kill()
-        sms, mx, reasons = [], None, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for line in self.lines:
-            parts = [x.strip() for x in line.split(",")]
-            if len(parts) < 8:
-                continue
-            try:
-                sms.append(float(parts[0]))
-                mx = float(parts[1])
-            except ValueError:
-                continue
-            for name, val in zip(names, parts[4:8]):
-                if val.lower() == "active":
+        if not self.ok:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml unavailable"], "samples": 0}
+        self._stop.set()
+        self.thread.join(timeout=2)
+        n = self.nvml
+        names = {
+            "hw_slowdown": getattr(n, "nvmlClocksEventReasonHwSlowdown", 0x8),
+            "sw_thermal_slowdown": getattr(n, "nvmlClocksEventReasonSwThermalSlowdown", 0x20),
+            "hw_thermal_slowdown": getattr(n, "nvmlClocksEventReasonHwThermalSlowdown", 0x40),
+            "sw_power_cap": getattr(n, "nvmlClocksEventReasonSwPowerCap", 0x4),
+        }
+        reasons = set()
+        for _, _, rs in self.samples:
+            for name, bit in names.items():
+                if rs & bit:
                     reasons.add(name)
-        sms.sort()
+        sms = sorted(x[0] for x in self.samples)
         med = sms[len(sms) // 2] if sms else None
-        return {"sm_mhz": med, "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sms)}
+        pmax = max((x[1] for x in self.samples), default=None)
+        return {"sm_mhz": med, "sm_max_mhz": self.max_mhz, "reasons": sorted(reasons),
+                "samples": len(sms), "power_w_max": pmax}
 
 
 def make_inputs(torch, s2o, l: int, seed: int, device):
@@ -140,13 +144,16 @@ def plan_sort_passes(l: int, s: int) -> int:
 
 
 def launches_per_step(l: int, s: int) -> int:
+    """Our kernels per s2o_attention_fwd call with the truncated plan (no overflow rerun):
+    guide means, q ranking (+ q sort when S > 2048), kv scoring, top-T selection, trace init,
+    pass-1, pass-2."""
     n = -(-l // s)
-    count = 2  # guide means, q ranking (+ in-CTA q sort)
+    count = 2
     if s > 2048:
         count += 2 + plan_sort_passes(l, s)
     if n > 1:
-        count += 1 + 2 + plan_sort_passes(l, s)  # kv scoring, table, run sort, merges
-    return count + 3  # trace init, pass-1, pass-2
+        count += 2
+    return count + 3
 
 
 # ------------------------------------------------------------------ reference (CPU) arm
@@ -287,7 +294,8 @@ def run_ours(args, rank: int, world: int):
     total_pairs = HQ * L * (L + 1) // 2
     sparsity = 1.0 - (p1 + p2) / total_pairs
     plan, _ = s2o.build_plan(q, k, S)
-    t_plan = cuda_time(torch, lambda: s2o.build_plan(q, k, S), 3)
+    t_plan_full = cuda_time(torch, lambda: s2o.build_plan(q, k, S), 2)
+    t_plan = cuda_time(torch, lambda: s2o.build_plan_truncated(q, k, S), 3)
     t_p1 = cuda_time(torch, lambda: s2o.pass1_dense_init(q, k, v, cfg), 3)
     bufs = s2o.pass1_dense_init(q, k, v, cfg)
     t_p2 = cuda_time(torch, lambda: s2o.pass2_sparse(q, k, v, bufs, plan, cfg, out=out), 3)
@@ -378,7 +386,8 @@ def run_ours(args, rank: int, world: int):
                        "seq_len": L, "seg_len": S, "tiles": [128, 128], "tau": args.tau,
                        "parallelism": f"layer-per-rank x{world}, no collective",
                        "l2": "inputs 1.6 GB > 126 MB L2 (no flush needed)", "path": {1: "generic", 2: "tcgen05"}[path]},
-            "breakdown_ms": {"plan": round(t_plan, 3), "pass1": round(t_p1, 3), "pass2": round(t_p2, 3)},
+            "breakdown_ms": {"plan_truncated": round(t_plan, 3), "pass1": round(t_p1, 3), "pass2": round(t_p2, 3),
+                             "plan_full_permutation": round(t_plan_full, 3)},
             "sparsity": round(sparsity, 5), "pairs": {"pass1": p1, "pass2": p2},
             "dense_ms": round(dense_ms, 3) if isinstance(dense_ms, float) else dense_ms,
             "speedup_vs_dense": round(dense_ms / ms_step, 2) if isinstance(dense_ms, float) else None,

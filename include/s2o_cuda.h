@@ -132,6 +132,16 @@ s2o_status s2o_plan_build(const s2o_problem* p, const void* q, const void* k,
                           const s2o_kernel_config* cfg, int32_t* q_perm, int32_t* kv_perm,
                           int64_t* cost2, void* workspace, size_t workspace_bytes, void* stream);
 
+/* Truncated plan for the fused operator: q_perm as above, and the exact top `depth` entries
+ * of every kv_perm segment (== the first min(nS, depth) entries of argsort_desc_stable), laid
+ * out int32 [Z, Hq, N, depth] (segment 0 unused). Selection instead of a full sort. The
+ * device int32 *flag is set to 1 if a segment's selection could not be certified (then use
+ * s2o_plan_build). Same workspace as s2o_plan_build. */
+s2o_status s2o_plan_build_truncated(const s2o_problem* p, const void* q, const void* k,
+                                    const s2o_kernel_config* cfg, int64_t depth, int32_t* q_perm,
+                                    int32_t* kv_top, int32_t* flag, void* workspace,
+                                    size_t workspace_bytes, void* stream);
+
 /* ------------------------------------------------------ Step 2: sparse attention passes */
 /* pass1_dense_init (kernel.hpp:70-71, kernel.cpp:184-218). */
 s2o_status s2o_pass1(const s2o_problem* p, const void* q, const void* k, const void* v,

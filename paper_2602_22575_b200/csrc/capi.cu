@@ -255,6 +255,26 @@ s2o_status s2o_plan_build(const s2o_problem* p, const void* q, const void* k,
     return S2O_OK;
 }
 
+s2o_status s2o_plan_build_truncated(const s2o_problem* p, const void* q, const void* k,
+                                    const s2o_kernel_config* cfg, int64_t depth, int32_t* q_perm,
+                                    int32_t* kv_top, int32_t* flag, void* workspace,
+                                    size_t workspace_bytes, void* stream) {
+    if (!cfg) return fail(S2O_ERR_INVALID_ARG, "null config");
+    Geo g;
+    s2o_status st = make_geo(p, cfg->seg_len, &g);
+    if (st) return st;
+    if (!q || !k || !q_perm || !flag || (g.N > 1 && !kv_top) || depth < 1)
+        return fail(S2O_ERR_INVALID_ARG, "null pointer or depth < 1");
+    if (!workspace || workspace_bytes < plan_workspace_bytes(g))
+        return fail(S2O_ERR_WORKSPACE, "workspace too small");
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    void* ws = reinterpret_cast<void*>((reinterpret_cast<uintptr_t>(workspace) + 255) & ~uintptr_t(255));
+    S2O_CUDA_TRY(cudaMemsetAsync(flag, 0, sizeof(int32_t), s), "memset");
+    S2O_CUDA_TRY(launch_plan_topk(g, q, k, q_perm, kv_top, depth, flag, ws, s), "plan top-k");
+    g_err.clear();
+    return S2O_OK;
+}
+
 s2o_status s2o_pass_workspace_size(const s2o_problem* p, const s2o_kernel_config* cfg,
                                    size_t* bytes) {
     Geo g;

@@ -329,6 +329,25 @@ def build_plan(q, k, seg_len: int, score_mode: int = SCORE_EXACT):
     return plan, RankingCost(int(cost[0]), int(cost[1]))
 
 
+def build_plan_truncated(q, k, seg_len: int, depth: int = 6144):
+    """Truncated plan (s2o_plan_build_truncated): (q_perm [Z,Hq,N,S], kv_top [Z,Hq,N,depth],
+    flag). kv_top[..., n, :min(nS, depth)] == the first entries of the full kv_perm segment."""
+    torch = _torch()
+    p = _problem(q, k)
+    seg = SegmentConfig.for_sequence(p.l, seg_len)
+    cfg = KernelConfig(seg_len=seg_len)._c()
+    nbytes = C.c_size_t(0)
+    _check(lib().s2o_plan_workspace_size(C.byref(p), C.c_int64(seg_len), C.byref(nbytes)))
+    ws = _workspace(nbytes.value, q.device)
+    qp = torch.empty((p.z, p.hq, seg.seg_count, seg.seg_len), dtype=torch.int32, device=q.device)
+    kv = torch.empty((p.z, p.hq, seg.seg_count, depth), dtype=torch.int32, device=q.device)
+    flag = torch.zeros(1, dtype=torch.int32, device=q.device)
+    _check(lib().s2o_plan_build_truncated(C.byref(p), _ptr(q), _ptr(k), C.byref(cfg), C.c_int64(depth),
+                                          _ptr(qp), _ptr(kv), _ptr(flag), _ptr(ws), C.c_size_t(ws.numel()),
+                                          _stream()))
+    return qp, kv, flag
+
+
 # ----------------------------------------------------------------------------- Step 2
 def _pass_ws(p: _Problem, c: _Config, device):
     nbytes = C.c_size_t(0)

@@ -22,7 +22,7 @@ __global__ void __launch_bounds__(512, 1) bench(int mode, int stages, int issuer
                                                 const int* rows, int nrows, long long* cycles) {
     extern __shared__ __align__(1024) unsigned char sm_raw[];
     unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(sm_raw) + 1023) & ~uintptr_t(1023));
-    uint64_t* bars = reinterpret_cast<uint64_t*>(sm + stages * kBlock);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sm + stages * kBlock);  // + rows after
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     if (threadIdx.x == 0) {
         for (int s = 0; s < stages; ++s) mbar_init(smem_u32(&bars[s]), mode == 3 ? 32 * issuers : 1);
@@ -47,6 +47,22 @@ __global__ void __launch_bounds__(512, 1) bench(int mode, int stages, int issuer
                     const int* r4 = rr + grp * 4;
                     tma_gather4(dst + (grp / 32) * 32768 + h * 16384 + (grp % 32) * 512, &gmap, h * 64, r4[0], r4[1],
                                 r4[2], r4[3], smem_u32(&bars[s]));
+                }
+            }
+        } else if (mode == 4) {
+            // one elected lane per issuing warp, warp-uniform operands from shared memory
+            int* srows = reinterpret_cast<int*>(bars + 8);
+            for (int e = threadIdx.x; e < 256; e += blockDim.x) srows[e] = rr[e];
+            __syncthreads();
+            if (warp == 0 && lane == 0) mbar_expect_tx(smem_u32(&bars[s]), kBlock);
+            if (warp < issuers) {
+                if (lane == 0) {
+                    for (int op = warp; op < 128; op += issuers) {
+                        const int grp = op / 2, h = op % 2;
+                        const int4 r4 = *reinterpret_cast<const int4*>(srows + grp * 4);
+                        tma_gather4(dst + (grp / 32) * 32768 + h * 16384 + (grp % 32) * 512, &gmap, h * 64, r4.x,
+                                    r4.y, r4.z, r4.w, smem_u32(&bars[s]));
+                    }
                 }
             }
         } else if (mode == 2) {
@@ -101,12 +117,12 @@ int main() {
         CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     enc(&tmap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, dbase, dims, str, bt, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
         CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    const char* names[4] = {"gather4", "gather4", "tile2d contiguous", "cp.async"};
-    for (int mode : {0, 2, 3}) {
+    const char* names[5] = {"gather4", "gather4", "tile2d contiguous", "cp.async", "gather4 1lane/warp"};
+    for (int mode : {4, 0}) {
       for (int issuers : {1, 2, 4, 8, 16}) {
         if (mode == 2 && issuers > 1) continue;
         for (int stages : {2}) {
-            const int smem = stages * kBlock + 2048;
+            const int smem = stages * kBlock + 4096;
             cudaFuncSetAttribute(bench, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
             bench<<<148, 512, smem>>>(mode, stages, issuers, gmap, tmap, dbase, drows, nrows, dcyc);
             cudaEvent_t a, b;

@@ -257,3 +257,23 @@ def test_plan_32k_bf16_bit_identical(cuda, port):
     want = port.build_plan(q, k, 2048)
     np.testing.assert_array_equal(plan.q_perm.reshape(1, 16, 2048).cpu().numpy(), want.q_perm)
     np.testing.assert_array_equal(plan.kv_perm.reshape(1, -1).cpu().numpy(), want.kv_perm)
+
+
+def test_truncated_plan_is_prefix_of_full_plan(cuda):
+    """s2o_plan_build_truncated returns exactly the first min(nS, depth) entries of each
+    full kv_perm segment (top-T of a stable sort == prefix of the full order)."""
+    import paper_2602_22575_b200 as s2o
+    torch = cuda
+    q, k, _ = s2o.generate_synthetic("mixed", 256, 8.0, 2, 1, 4, 16384, 128)
+    qd = dev(torch, bf16_round(q), torch.bfloat16)
+    kd = dev(torch, bf16_round(k[:, :2]), torch.bfloat16)
+    plan, _ = s2o.build_plan(qd, kd, 1024)
+    for depth in (128, 1000, 4096, 9000):
+        qp, kvt, flag = s2o.build_plan_truncated(qd, kd, 1024, depth)
+        torch.cuda.synchronize()
+        assert flag.item() == 0
+        assert torch.equal(qp, plan.q_perm)
+        for n in range(1, 16):
+            t = min(n * 1024, depth)
+            off = plan.seg.kv_offset(n)
+            assert torch.equal(kvt[:, :, n, :t], plan.kv_perm[:, :, off: off + t]), (depth, n)
