@@ -30,6 +30,8 @@ s2o_status cuda_fail(cudaError_t e, const char* where) {
 
 size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
+constexpr int64_t kMaxPlanDepth = 8192;  // select_topk_kernel smem capacity (kSelCap)
+
 // Geometry + generic argument checks shared by every entry point.
 s2o_status make_geo(const s2o_problem* p, int64_t seg_len, Geo* g) {
     if (!p) return fail(S2O_ERR_INVALID_ARG, "null problem");
@@ -265,6 +267,7 @@ s2o_status s2o_plan_build_truncated(const s2o_problem* p, const void* q, const v
     if (st) return st;
     if (!q || !k || !q_perm || !flag || (g.N > 1 && !kv_top) || depth < 1)
         return fail(S2O_ERR_INVALID_ARG, "null pointer or depth < 1");
+    if (depth > kMaxPlanDepth) return fail(S2O_ERR_UNSUPPORTED, "truncated plan depth must be <= 8192");
     if (!workspace || workspace_bytes < plan_workspace_bytes(g))
         return fail(S2O_ERR_WORKSPACE, "workspace too small");
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
@@ -365,6 +368,7 @@ static int64_t plan_topt(const Geo& g, const s2o_kernel_config* c) {
     if (c->plan_depth < 0) return 0;
     int64_t t = c->plan_depth == 0 ? 6144 : c->plan_depth;
     t = ((t + c->b_n - 1) / c->b_n) * c->b_n;
+    if (t > kMaxPlanDepth) return 0;  // beyond the selection capacity: build the full plan
     if (t >= (g.N - 1) * g.S) return 0;  // no segment would be truncated
     return t;
 }

@@ -268,7 +268,9 @@ def test_truncated_plan_is_prefix_of_full_plan(cuda):
     qd = dev(torch, bf16_round(q), torch.bfloat16)
     kd = dev(torch, bf16_round(k[:, :2]), torch.bfloat16)
     plan, _ = s2o.build_plan(qd, kd, 1024)
-    for depth in (128, 1000, 4096, 9000):
+    with pytest.raises(ValueError, match="depth"):
+        s2o.build_plan_truncated(qd, kd, 1024, 9000)
+    for depth in (128, 1000, 4096, 8192):
         qp, kvt, flag = s2o.build_plan_truncated(qd, kd, 1024, depth)
         torch.cuda.synchronize()
         assert flag.item() == 0
