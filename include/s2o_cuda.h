@@ -134,7 +134,7 @@ s2o_status s2o_plan_build(const s2o_problem* p, const void* q, const void* k,
 
 /* Truncated plan for the fused operator: q_perm as above, and the exact top `depth` entries
  * of every kv_perm segment (== the first min(nS, depth) entries of argsort_desc_stable), laid
- * out int32 [Z, Hq, N, depth] (segment 0 unused), depth <= 8192. Selection, not a full sort. The
+ * out int32 [Z, Hq, N, depth] (segment 0 unused), depth <= 6144. Selection, not a full sort. The
  * device int32 *flag is set to 1 if a segment's selection could not be certified (then use
  * s2o_plan_build). Same workspace as s2o_plan_build. */
 s2o_status s2o_plan_build_truncated(const s2o_problem* p, const void* q, const void* k,

@@ -30,7 +30,7 @@ s2o_status cuda_fail(cudaError_t e, const char* where) {
 
 size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
-constexpr int64_t kMaxPlanDepth = 8192;  // select_topk_kernel smem capacity (kSelCap)
+constexpr int64_t kMaxPlanDepth = 6144;  // 3/4 of select_topk_kernel smem capacity (kSelCap = 8192)
 
 // Geometry + generic argument checks shared by every entry point.
 s2o_status make_geo(const s2o_problem* p, int64_t seg_len, Geo* g) {
@@ -267,7 +267,7 @@ s2o_status s2o_plan_build_truncated(const s2o_problem* p, const void* q, const v
     if (st) return st;
     if (!q || !k || !q_perm || !flag || (g.N > 1 && !kv_top) || depth < 1)
         return fail(S2O_ERR_INVALID_ARG, "null pointer or depth < 1");
-    if (depth > kMaxPlanDepth) return fail(S2O_ERR_UNSUPPORTED, "truncated plan depth must be <= 8192");
+    if (depth > kMaxPlanDepth) return fail(S2O_ERR_UNSUPPORTED, "truncated plan depth must be <= 6144");
     if (!workspace || workspace_bytes < plan_workspace_bytes(g))
         return fail(S2O_ERR_WORKSPACE, "workspace too small");
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
