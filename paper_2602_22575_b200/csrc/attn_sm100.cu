@@ -3,32 +3,35 @@
 // One persistent kernel serves pass-1 (intra-segment causal scan, segment_causal_tile
 // kernel.cpp:36-71), pass-2 (ranked prefix traversal with the monotone-gain stop,
 // traverse_prefix kernel.cpp:86-122 + early_stop_check kernel.cpp:220-234) and the fused
-// single pass (kernel.cpp:300-349). A work unit is one 128-row query tile; its key stream is
-// a list of 128-key blocks: first the causal blocks of its own segment (masked on original
-// token positions), then the chunks of kv_perm in rank order (non-contiguous rows).
+// single pass (kernel.cpp:300-349).
 //
-// Warp roles (256 threads, 1 CTA per SM):
-//   warps 0-3  softmax/correction/epilogue: thread r owns query row r = TMEM lane r
-//   warp 4     MMA issuer (one lane): S = Q K^T into TMEM (double-buffered), O += P V
-//   warps 5-7  loaders: contiguous blocks (the causal blocks of pass-1, Q in token order) by
-//              2-D tile TMA (4 ops per block); permuted rows (Q by q_perm, prefix chunks by
-//              kv_perm) by TMA tile::gather4 spread over the three warps (the gather issue
-//              rate, ~1 op per 22 cycles per SM, is the limit; see scripts/load_bench.cu)
+// Work unit: a PAIR of 128-row query tiles of the same (head, segment). Their key streams
+// are the same list of 128-key blocks -- the segment's causal blocks (masked on original
+// token positions; the second tile has one more) followed by the chunks of kv_perm in rank
+// order -- so every K/V block is loaded once and feeds both tiles. TMA tile::gather4 is
+// capped at ~22 cycles/op per SM (profiles/r01_summary.md), so sharing a gathered chunk
+// between two tiles halves the dominant cost of pass-2.
 //
-// Early stop (reference semantics): for a prefix chunk the softmax warps
-// compute each row's relative normaliser gain sum_j exp(s_j - m) / ell from the chunk's
-// scores alone, reduce the max over the tile's rows, and compare with tau before P V is
-// issued; a stopping chunk is discarded (no P V, no state change). QK^T of the next chunk
-// is issued speculatively; it is simply dropped when the tile stops.
+// Warp roles (384 threads, 1 CTA per SM):
+//   warps 0-3  softmax/correction/epilogue of slot 0 (thread r owns row r = TMEM lane r)
+//   warps 4-7  softmax/correction/epilogue of slot 1
+//   warp 8     MMA issuer (one lane): S_X = Q_X K^T (SS MMA), O_X += P_X V (TS MMA, P in TMEM)
+//   warps 9-11 loaders: 2-D tile TMA for contiguous rows, TMA tile::gather4 for permuted rows
 //
-// Data layout in shared memory (all SWIZZLE_128B, 1024-B aligned):
-//   sQ   [2][128 rows][128 B]        Q tile, K-major (two 64-column halves)
-//   sK   [3 stages][2][128][128 B]   K block, K-major (B operand of Q K^T)
-//   sV   [3 stages][2][128][128 B]   V block, used MN-major (B operand of P V)
-//   P    = exp2(s - m) in bf16, K-major (A operand of P V), written into the K buffer of the
-//          block's own stage: K(j) is dead once Q K^T(j) completed (the softmax only writes P
-//          after reading S(j)), and the stage is released only after P V(j) completes.
-// TMEM (512 columns): S buffers at columns [0,128) and [128,256), O at [256,384).
+// Early stop (reference semantics): each row's relative normaliser gain of a prefix chunk,
+// sum_j exp(s_j - m) / ell, is computed from the chunk's scores; the max over the tile's rows
+// is compared with tau before P V is issued; a stopping chunk changes nothing (kernel.cpp:
+// 114-117). The two tiles of a pair stop independently; the pair's stream ends when both did.
+//
+// Shared memory (SWIZZLE_128B, 1024-B aligned): Q slot 0/1 (2 x 32 KB), 2 stages x (K 32 KB +
+// V 32 KB). TMEM (512 columns): slot X uses [256X, 256X+128) for S (P = exp2(s - m) in bf16 is
+// written over the first 64 columns after S is read) and [256X+128, 256X+256) for O.
+//
+// Ordering facts the pipeline relies on:
+//  * tcgen05.commit arrives when ALL earlier MMAs of the issuing thread completed, so
+//    s_full[X](j) also certifies P_X V(j-1) done: the softmax may then overwrite P_X and
+//    rescale O_X without another barrier.
+//  * Every mbarrier completes at most one phase ahead of its waiter (parity waits).
 #include <cudaTypedefs.h>
 
 #include <cmath>
@@ -47,79 +50,107 @@ namespace {
 constexpr int kD = 128;
 constexpr int kBM = 128;
 constexpr int kBN = 128;
-constexpr int kStages = 3;
-constexpr int kThreads = 256;
-constexpr int kLoaderWarps = 3;  // warps 5..7 issue TMA (gather4 issue rate scales with warps)
-constexpr uint32_t kHalf = 128u * 128u;            // bytes of one 64-column half tile
-constexpr uint32_t kTileBytes = 2 * kHalf;         // 32 KB
-constexpr uint32_t kOffQ = 0;
-constexpr uint32_t kOffK = kOffQ + kTileBytes;
+constexpr int kStages = 2;
+constexpr int kThreads = 384;
+constexpr int kMmaWarp = 8;
+constexpr int kLoadWarp0 = 9;
+constexpr int kLoaderThreads = 96;
+constexpr uint32_t kHalf = 128u * 128u;     // one 64-column half of a 128-row tile
+constexpr uint32_t kTileBytes = 2 * kHalf;  // 32 KB
+constexpr uint32_t kOffQ = 0;               // slot X at X * kTileBytes
+constexpr uint32_t kOffK = 2 * kTileBytes;
 constexpr uint32_t kOffV = kOffK + kStages * kTileBytes;
 constexpr uint32_t kOffCtrl = kOffV + kStages * kTileBytes;
-constexpr uint32_t kSmemBytes = kOffCtrl + 2048 + 1024;  // + control block + alignment slack
+constexpr uint32_t kSmemBytes = kOffCtrl + 1024 + 1024;
 constexpr uint32_t kTmemCols = 512;
-constexpr uint32_t kColO = 256;
 constexpr float kRescaleThresh = 8.0f;  // lazy max update, log2 units (factor 256)
 
 struct Ctrl {
     uint64_t q_full, q_empty;
     uint64_t k_full[kStages], v_full[kStages], kv_empty[kStages];
-    uint64_t s_full[2], s_empty[2];
-    uint64_t p_full, o_done;
+    uint64_t s_full[2], p_full[2], o_done[2];
     uint32_t tmem_base;
-    float red[4];
-    uint8_t dec[4];  // decision ring (block j -> j & 3): 1 = commit, 2 = stop
+    float red[2][4];
+    uint8_t dec[2][4];  // per slot decision ring (block j -> j & 3): 1 = commit, 2 = stop
 };
 
 struct TcParams {
     PassArgs a;
     float scale_log2;  // (1/sqrt(D)) * log2(e)
-    int q_contig, kv_contig;  // token stride == one row (tile TMA usable)
+    int q_contig, kv_contig;
+    int64_t pairs_per_head, pairs_full;  // pairs per head; pairs in a full segment
 };
 
-struct TileInfo {
-    int64_t zh, n, ti, t0, tn, seg_rows, sb, avail;
-    int nd, np, nb;  // diag blocks, prefix blocks, total
+struct PairInfo {
+    int64_t zh, n, sb, seg_rows, avail;
+    int64_t ti[2], t0[2], tn[2];
+    int has[2];
+    int nd[2], ndmax, np, nb;
 };
 
-__device__ __forceinline__ TileInfo tile_info(const PassArgs& a, int64_t tile) {
+__device__ __forceinline__ PairInfo pair_info(const TcParams& p, int64_t idx) {
+    const PassArgs& a = p.a;
     const Geo& g = a.g;
-    TileInfo t;
-    t.zh = tile / a.tiles_per_head;
-    const int64_t r_in = tile % a.tiles_per_head;
-    const int64_t full = (g.N - 1) * a.T;
-    if (r_in < full) { t.n = r_in / a.T; t.ti = r_in % a.T; }
-    else { t.n = g.N - 1; t.ti = r_in - full; }
-    t.sb = t.n * g.S;
-    t.seg_rows = g.seg_rows(t.n);
-    t.t0 = t.ti * kBM;
-    t.tn = min((int64_t)kBM, t.seg_rows - t.t0);
-    t.nd = (a.mode & kDiag) ? (int)((t.t0 + t.tn - 1) / kBN + 1) : 0;
-    t.avail = a.avail(t.n);  // kv_perm entries available to walk
-    t.np = ((a.mode & kPrefix) && t.n > 0) ? (int)((t.avail + kBN - 1) / kBN) : 0;
-    t.nb = t.nd + t.np;
-    return t;
-}
-
-// Absolute row (in D-element units) of q row `local` of the tile.
-__device__ __forceinline__ int64_t q_local_row(const PassArgs& a, const TileInfo& t, int64_t r) {
-    if (r >= t.tn) r = 0;  // ragged tail: duplicate a valid row, results discarded
-    const int64_t local = ((a.mode & kStateIn) && a.q_reorder)
-                              ? (int64_t)a.q_perm[(t.zh * a.g.N + t.n) * a.g.S + t.t0 + r]
-                              : t.t0 + r;
-    return t.sb + local;
-}
-
-// token index of key i of block j (clamped into the block's valid range)
-__device__ __forceinline__ int64_t key_token(const PassArgs& a, const TileInfo& t, const int32_t* kv,
-                                             int j, int i) {
-    if (j < t.nd) {
-        const int64_t k0 = (int64_t)j * kBN;
-        const int64_t kn = min((int64_t)kBN, t.seg_rows - k0);
-        return t.sb + k0 + (i < kn ? i : 0);
+    PairInfo P;
+    if (a.tile_list) {
+        const int64_t tile = a.tile_list[idx];
+        P.zh = tile / a.tiles_per_head;
+        const int64_t r = tile % a.tiles_per_head;
+        const int64_t full = (g.N - 1) * a.T;
+        if (r < full) { P.n = r / a.T; P.ti[0] = r % a.T; }
+        else { P.n = g.N - 1; P.ti[0] = r - full; }
+        P.ti[1] = -1;
+    } else {
+        P.zh = idx / p.pairs_per_head;
+        const int64_t r = idx % p.pairs_per_head;
+        const int64_t full = (g.N - 1) * p.pairs_full;
+        int64_t pi, tcount;
+        if (r < full) { P.n = r / p.pairs_full; pi = r % p.pairs_full; tcount = a.T; }
+        else { P.n = g.N - 1; pi = r - full; tcount = (g.last_len + kBM - 1) / kBM; }
+        P.ti[0] = 2 * pi;
+        P.ti[1] = (2 * pi + 1 < tcount) ? 2 * pi + 1 : -1;
     }
-    const int64_t c0 = (int64_t)(j - t.nd) * kBN;
-    const int64_t cn = min((int64_t)kBN, t.avail - c0);
+    P.sb = P.n * g.S;
+    P.seg_rows = g.seg_rows(P.n);
+    P.avail = a.avail(P.n);
+    P.ndmax = 0;
+    for (int x = 0; x < 2; ++x) {
+        P.has[x] = P.ti[x] >= 0;
+        P.t0[x] = P.has[x] ? P.ti[x] * kBM : 0;
+        P.tn[x] = P.has[x] ? min((int64_t)kBM, P.seg_rows - P.t0[x]) : 0;
+        P.nd[x] = (P.has[x] && (a.mode & kDiag)) ? (int)((P.t0[x] + P.tn[x] - 1) / kBN + 1) : 0;
+        P.ndmax = max(P.ndmax, P.nd[x]);
+    }
+    P.np = ((a.mode & kPrefix) && P.n > 0) ? (int)((P.avail + kBN - 1) / kBN) : 0;
+    P.nb = P.ndmax + P.np;
+    return P;
+}
+
+__device__ __forceinline__ bool participates(const PairInfo& P, int x, int j) {
+    return P.has[x] && (j < P.ndmax ? j < P.nd[x] : true);
+}
+__device__ __forceinline__ int last_block(const PairInfo& P, int x) {
+    return P.np > 0 ? P.nb - 1 : P.nd[x] - 1;
+}
+
+// Segment row of query row r of slot x (ragged tails duplicate row 0; results discarded).
+__device__ __forceinline__ int64_t q_row(const PassArgs& a, const PairInfo& P, int x, int64_t r) {
+    if (r >= P.tn[x]) r = 0;
+    const int64_t local = ((a.mode & kStateIn) && a.q_reorder)
+                              ? (int64_t)a.q_perm[(P.zh * a.g.N + P.n) * a.g.S + P.t0[x] + r]
+                              : P.t0[x] + r;
+    return P.sb + local;
+}
+
+// Token index of key i of block j (clamped into the block's valid range).
+__device__ __forceinline__ int64_t key_token(const PairInfo& P, const int32_t* kv, int j, int i) {
+    if (j < P.ndmax) {
+        const int64_t k0 = (int64_t)j * kBN;
+        const int64_t kn = min((int64_t)kBN, P.seg_rows - k0);
+        return P.sb + k0 + (i < kn ? i : 0);
+    }
+    const int64_t c0 = (int64_t)(j - P.ndmax) * kBN;
+    const int64_t cn = min((int64_t)kBN, P.avail - c0);
     return (int64_t)kv[c0 + (i < cn ? i : 0)];
 }
 
@@ -148,12 +179,11 @@ tc_pass_kernel(const TcParams p, const __grid_constant__ CUtensorMap qmap,
             mbar_init(smem_u32(&c.v_full[s]), 1);
             mbar_init(smem_u32(&c.kv_empty[s]), 1);
         }
-        for (int s = 0; s < 2; ++s) {
-            mbar_init(smem_u32(&c.s_full[s]), 1);
-            mbar_init(smem_u32(&c.s_empty[s]), 4);
+        for (int x = 0; x < 2; ++x) {
+            mbar_init(smem_u32(&c.s_full[x]), 1);
+            mbar_init(smem_u32(&c.p_full[x]), 4);
+            mbar_init(smem_u32(&c.o_done[x]), 1);
         }
-        mbar_init(smem_u32(&c.p_full), 4);
-        mbar_init(smem_u32(&c.o_done), 1);
         fence_mbar_init();
     }
     if (warp == 0) {
@@ -164,198 +194,186 @@ tc_pass_kernel(const TcParams p, const __grid_constant__ CUtensorMap qmap,
     __syncthreads();
     tc_fence_after();
     const uint32_t tbase = c.tmem_base;
+    const int64_t total = a.tile_list ? a.tile_count : g.z * g.hq * p.pairs_per_head;
+    const int64_t rowu = g.d;  // row unit of the tensor maps = D elements
 
-    const int64_t total_tiles = a.num_tiles();
-    const int64_t kv_div = g.d;  // row unit of the tensor maps = D elements
-
-    if (warp >= 5) {
+    if (warp >= kLoadWarp0) {
         // ============================== loaders ==============================
-        const int lw = warp - 5;             // loader warp 0..2
-        const int lt = lw * 32 + lane;       // loader thread 0..95
-        const uint32_t lbar = 5 * 32;        // named barrier 2 over the 96 loader threads
+        const int lt = (warp - kLoadWarp0) * 32 + lane;  // 0..95
         uint32_t gblk = 0, qcount = 0;
-        for (int64_t tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
-            const TileInfo t = tile_info(a, a.tile_at(tile));
-            if (t.nb == 0) continue;
-            const int32_t* kv = (t.np > 0) ? a.kv_seg(t.zh, t.n) : nullptr;
-            // Q rows; wait until the previous tile's Q K^T are done
+        for (int64_t it = blockIdx.x; it < total; it += gridDim.x) {
+            const PairInfo P = pair_info(p, it);
+            if (P.nb == 0) continue;
+            const int32_t* kv = (P.np > 0) ? a.kv_seg(P.zh, P.n) : nullptr;
             mbar_wait(smem_u32(&c.q_empty), (qcount & 1) ^ 1, 1001);
-            const int64_t qb = g.q_base(t.zh) / kv_div;
-            const bool q_tile = p.q_contig && !((a.mode & kStateIn) && a.q_reorder) && t.tn == kBM;
-            if (lt == 0) mbar_expect_tx(smem_u32(&c.q_full), kTileBytes);
-            named_bar_sync(2, 96);
-            if (q_tile) {
-                if (lt == 0)
-                    for (int h = 0; h < 2; ++h)
-                        tma_load2d(sQ + h * kHalf, &qtile, h * 64, (int32_t)(qb + t.sb + t.t0), smem_u32(&c.q_full));
-            } else {
-                for (int op = lt; op < 64; op += 96) {  // 32 row groups x 2 halves
-                    const int grp = op >> 1, h = op & 1;
+            const int64_t qb = g.q_base(P.zh) / rowu, qs = g.qs[2] / rowu;
+            const bool q_tile = p.q_contig && !((a.mode & kStateIn) && a.q_reorder);
+            if (lt == 0) mbar_expect_tx(smem_u32(&c.q_full), (P.has[1] ? 2 : 1) * kTileBytes);
+            named_bar_sync(3, kLoaderThreads);
+            for (int x = 0; x < 2; ++x) {
+                if (!P.has[x]) continue;
+                const uint32_t qdst = sQ + x * kTileBytes;
+                if (q_tile && P.tn[x] == kBM) {
+                    if (lt == 0)
+                        for (int h = 0; h < 2; ++h)
+                            tma_load2d(qdst + h * kHalf, &qtile, h * 64, (int32_t)(qb + (P.sb + P.t0[x]) * qs),
+                                       smem_u32(&c.q_full));
+                } else if (lt < 64) {
+                    const int grp = lt >> 1, h = lt & 1;
                     int32_t rows[4];
-                    for (int i = 0; i < 4; ++i)
-                        rows[i] = (int32_t)(qb + q_local_row(a, t, grp * 4 + i) * (g.qs[2] / kv_div));
-                    tma_gather4(sQ + h * kHalf + grp * 512, &qmap, h * 64, rows[0], rows[1], rows[2], rows[3],
+                    for (int i = 0; i < 4; ++i) rows[i] = (int32_t)(qb + q_row(a, P, x, grp * 4 + i) * qs);
+                    tma_gather4(qdst + h * kHalf + grp * 512, &qmap, h * 64, rows[0], rows[1], rows[2], rows[3],
                                 smem_u32(&c.q_full));
                 }
             }
             ++qcount;
-            const int64_t kb = g.k_base(t.zh) / kv_div, vb = g.v_base(t.zh) / kv_div;
-            const int64_t ks = g.ks[2] / kv_div, vs = g.vs[2] / kv_div;
-            int loaded = 0;
-            // gather indices for block j live in registers; block j+1's are prefetched while
-            // block j is issued (kv_perm reads are L2 round trips)
-            auto fetch_rows = [&](int j, int32_t (&rk)[2][4], int32_t (&rv)[2][4]) {
+            const int64_t kb = g.k_base(P.zh) / rowu, vb = g.v_base(P.zh) / rowu;
+            const int64_t ks = g.ks[2] / rowu, vs = g.vs[2] / rowu;
+            // gather ops of one block: [0,64) K, [64,128) V; op -> (row group, half)
+            auto fetch_rows = [&](int j, int32_t (&rr)[2][4]) {
                 for (int u = 0; u < 2; ++u) {
-                    const int op = lt + u * 96;
+                    const int op = lt + u * kLoaderThreads;
                     const int grp = (op >> 1) & 31;
+                    const bool isv = op >= 64;
                     for (int i = 0; i < 4; ++i) {
-                        const int64_t tok = (j < t.nb) ? key_token(a, t, kv, j, grp * 4 + i) : 0;
-                        rk[u][i] = (int32_t)(kb + tok * ks);
-                        rv[u][i] = (int32_t)(vb + tok * vs);
+                        const int64_t tok = (op < 128 && j < P.nb) ? key_token(P, kv, j, grp * 4 + i) : 0;
+                        rr[u][i] = (int32_t)(isv ? vb + tok * vs : kb + tok * ks);
                     }
                 }
             };
-            int32_t ck[2][4], cv[2][4], nk[2][4], nv[2][4];
-            fetch_rows(0, ck, cv);
-            for (int j = 0; j < t.nb; ++j) {
+            const auto gathered = [&](int j) { return !(j < P.ndmax && p.kv_contig); };
+            int32_t cur[2][4], nxt[2][4];
+            if (gathered(0)) fetch_rows(0, cur);
+            bool stop_known[2] = {false, false};
+            int loaded = 0;
+            for (int j = 0; j < P.nb; ++j) {
                 const uint32_t gi = gblk + j;
                 const int st = gi % kStages;
-                if (j + 1 < t.nb && !(j + 1 < t.nd && p.kv_contig)) fetch_rows(j + 1, nk, nv);
+                if (j + 1 < P.nb && gathered(j + 1)) fetch_rows(j + 1, nxt);
                 mbar_wait(smem_u32(&c.kv_empty[st]), ((gi / kStages) & 1) ^ 1, 1002);
-                // acquiring stage j implies block j-kStages was decided; a stop there ends the tile
-                if (j >= kStages && c.dec[(j - kStages) & 3] == 2) break;
+                // acquiring stage j certifies that both slots' decisions on block j-2 are final
+                if (j >= 2 && j - 2 >= P.ndmax)
+                    for (int x = 0; x < 2; ++x)
+                        if (participates(P, x, j - 2) && c.dec[x][(j - 2) & 3] == 2) stop_known[x] = true;
+                bool need = false;
+                for (int x = 0; x < 2; ++x) need |= participates(P, x, j) && !stop_known[x];
+                if (!need) break;
                 if (lt == 0) {
                     mbar_expect_tx(smem_u32(&c.k_full[st]), kTileBytes);
                     mbar_expect_tx(smem_u32(&c.v_full[st]), kTileBytes);
                 }
-                named_bar_sync(2, 96);
+                named_bar_sync(3, kLoaderThreads);
                 const uint32_t kdst = sK + st * kTileBytes;
                 const uint32_t vdst = sV + st * kTileBytes;
-                if (j < t.nd && p.kv_contig) {
+                if (!gathered(j)) {
                     if (lt == 0) {
-                        const int64_t tok = t.sb + (int64_t)j * kBN;
+                        const int64_t tok = P.sb + (int64_t)j * kBN;
                         for (int h = 0; h < 2; ++h)
-                            tma_load2d(kdst + h * kHalf, &ktile, h * 64, (int32_t)(kb + tok), smem_u32(&c.k_full[st]));
+                            tma_load2d(kdst + h * kHalf, &ktile, h * 64, (int32_t)(kb + tok * ks), smem_u32(&c.k_full[st]));
                         for (int h = 0; h < 2; ++h)
-                            tma_load2d(vdst + h * kHalf, &vtile, h * 64, (int32_t)(vb + tok), smem_u32(&c.v_full[st]));
+                            tma_load2d(vdst + h * kHalf, &vtile, h * 64, (int32_t)(vb + tok * vs), smem_u32(&c.v_full[st]));
                     }
                 } else {
-                    // K first (Q K^T waits only for K), then V: 64 ops each, lt < 64 -> op 0/1
                     for (int u = 0; u < 2; ++u) {
-                        const int op = lt + u * 96;  // ops [0,64): K, [64,128): V; op>>1 = group
+                        const int op = lt + u * kLoaderThreads;
                         if (op >= 128) break;
                         const int grp = (op >> 1) & 31, h = op & 1;
                         const bool isv = op >= 64;
                         tma_gather4((isv ? vdst : kdst) + h * kHalf + grp * 512, isv ? &vmap : &kmap, h * 64,
-                                    isv ? cv[u][0] : ck[u][0], isv ? cv[u][1] : ck[u][1],
-                                    isv ? cv[u][2] : ck[u][2], isv ? cv[u][3] : ck[u][3],
+                                    cur[u][0], cur[u][1], cur[u][2], cur[u][3],
                                     smem_u32(isv ? &c.v_full[st] : &c.k_full[st]));
                     }
                 }
                 for (int u = 0; u < 2; ++u)
-                    for (int i = 0; i < 4; ++i) {
-                        ck[u][i] = nk[u][i];
-                        cv[u][i] = nv[u][i];
-                    }
+                    for (int i = 0; i < 4; ++i) cur[u][i] = nxt[u][i];
                 ++loaded;
             }
             gblk += loaded;
         }
-    } else if (warp == 4) {
+    } else if (warp == kMmaWarp) {
         // ============================== MMA issuer ==============================
-        const uint32_t idesc_s = umma_idesc_bf16(kBM, kBN, false, false);
-        const uint32_t idesc_o = umma_idesc_bf16(kBM, kD, false, true);
-        uint32_t gblk = 0, gq = 0, qcount = 0, gp = 0;  // loads, Q K^T (S buffer uses), p_full
-        for (int64_t tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
-            const TileInfo t = tile_info(a, a.tile_at(tile));
-            if (t.nb == 0) continue;
-            if (lane == 0) {
+        if (lane == 0) {
+            const uint32_t idesc_s = umma_idesc_bf16(kBM, kBN, false, false);
+            const uint32_t idesc_o = umma_idesc_bf16(kBM, kD, false, true);
+            uint32_t gblk = 0, qcount = 0;
+            uint32_t ns[2] = {0, 0};  // s_full / p_full phases per slot
+            for (int64_t it = blockIdx.x; it < total; it += gridDim.x) {
+                const PairInfo P = pair_info(p, it);
+                if (P.nb == 0) continue;
                 mbar_wait(smem_u32(&c.q_full), qcount & 1, 2001);
+                ++qcount;
                 tc_fence_after();
-            }
-            ++qcount;
-            int stop_at = -1;
-            auto issue_qk = [&](int j) {
-                const uint32_t gi = gblk + j;
-                const uint32_t gs = gq + j;  // S buffer sequence (loads may run further ahead)
-                const int st = gi % kStages;
-                const int sb = gs & 1;
-                mbar_wait(smem_u32(&c.k_full[st]), (gi / kStages) & 1, 2002);
-                mbar_wait(smem_u32(&c.s_empty[sb]), ((gs >> 1) & 1) ^ 1, 2003);
-                tc_fence_after();
-                const uint32_t kbase = sK + st * kTileBytes;
-                for (int kk = 0; kk < kD / 16; ++kk) {
-                    const uint32_t off = (kk / 4) * kHalf + (kk % 4) * 32;
-                    umma_bf16(tbase + sb * 128, umma_desc_sw128(sQ + off, 16, 1024),
-                              umma_desc_sw128(kbase + off, 16, 1024), idesc_s, kk > 0);
-                }
-                umma_commit(smem_u32(&c.s_full[sb]));
-            };
-            if (lane == 0) {
-                issue_qk(0);
-                for (int j = 0; j < t.nb; ++j) {
-                    if (j + 1 < t.nb) issue_qk(j + 1);
-                    // decision for block j
-                    mbar_wait(smem_u32(&c.p_full), gp & 1, 2004);
-                    ++gp;
-                    tc_fence_after();
+                int stop_at[2] = {1 << 30, 1 << 30};
+                int loaded = 0;
+                for (int j = 0; j < P.nb; ++j) {
+                    // same predicate as the loader: decisions on blocks <= j-2 are known there
+                    bool need = false;
+                    for (int x = 0; x < 2; ++x) need |= participates(P, x, j) && !(stop_at[x] <= j - 2);
+                    if (!need) break;
+                    ++loaded;
                     const uint32_t gi = gblk + j;
                     const int st = gi % kStages;
-                    if (c.dec[j & 3] == 1) {
-                        mbar_wait(smem_u32(&c.v_full[st]), (gi / kStages) & 1, 2005);
-                        tc_fence_after();
-                        const uint32_t vbase = sV + st * kTileBytes;
-                        const uint32_t pbase = sK + st * kTileBytes;  // P aliases K(j)
-                        for (int kk = 0; kk < kBN / 16; ++kk) {
-                            const uint32_t aoff = (kk / 4) * kHalf + (kk % 4) * 32;
-                            umma_bf16(tbase + kColO, umma_desc_sw128(pbase + aoff, 16, 1024),
-                                      umma_desc_sw128(vbase + kk * 16 * 128, kHalf, 1024), idesc_o, 1);
+                    const uint32_t ph = (gi / kStages) & 1;
+                    mbar_wait(smem_u32(&c.k_full[st]), ph, 2002);
+                    tc_fence_after();
+                    bool act[2];
+                    for (int x = 0; x < 2; ++x) act[x] = participates(P, x, j) && stop_at[x] > j - 1;
+                    const uint32_t kbase = sK + st * kTileBytes;
+                    for (int x = 0; x < 2; ++x) {
+                        if (!act[x]) continue;
+                        const uint32_t qbase = sQ + x * kTileBytes;
+                        for (int kk = 0; kk < kD / 16; ++kk) {
+                            const uint32_t off = (kk / 4) * kHalf + (kk % 4) * 32;
+                            umma_bf16(tbase + x * 256, umma_desc_sw128(qbase + off, 16, 1024),
+                                      umma_desc_sw128(kbase + off, 16, 1024), idesc_s, kk > 0);
                         }
-                        umma_commit(smem_u32(&c.kv_empty[st]));
-                        umma_commit(smem_u32(&c.o_done));
-                        if (j + 1 == t.nb) umma_commit(smem_u32(&c.q_empty));
-                    } else {
-                        // stop: no P V, no o_done completion (the softmax drained P V(j-1)
-                        // before publishing this decision, so barrier phases never run
-                        // two ahead of their waiters)
-                        stop_at = j;
-                        mbar_wait(smem_u32(&c.v_full[st]), (gi / kStages) & 1, 2006);
-                        mbar_arrive(smem_u32(&c.kv_empty[st]));
-                        if (j + 1 < t.nb) {
-                            // Q K^T of block j+1 was issued speculatively: its V must land before
-                            // the stage is freed (v_full phase accounting), then free it once done
-                            const uint32_t g1 = gi + 1;
-                            mbar_wait(smem_u32(&c.v_full[g1 % kStages]), (g1 / kStages) & 1, 2007);
-                            umma_commit(smem_u32(&c.kv_empty[g1 % kStages]));
-                        }
-                        // blocks j+2 .. j+kStages-1 were loaded (the loader runs kStages ahead of
-                        // the decisions) but never computed: consume and free them
-                        for (int jj = j + 2; jj < min(t.nb, j + kStages); ++jj) {
-                            const uint32_t g2 = gblk + jj;
-                            mbar_wait(smem_u32(&c.k_full[g2 % kStages]), (g2 / kStages) & 1, 2008);
-                            mbar_wait(smem_u32(&c.v_full[g2 % kStages]), (g2 / kStages) & 1, 2009);
-                            mbar_arrive(smem_u32(&c.kv_empty[g2 % kStages]));
-                        }
-                        umma_commit(smem_u32(&c.q_empty));
-                        break;
+                        umma_commit(smem_u32(&c.s_full[x]));
                     }
+                    bool v_ready = false;
+                    for (int x = 0; x < 2; ++x) {
+                        if (!act[x]) continue;
+                        mbar_wait(smem_u32(&c.p_full[x]), ns[x] & 1, 2004);
+                        ++ns[x];
+                        tc_fence_after();
+                        if (c.dec[x][j & 3] == 1) {
+                            if (!v_ready) {
+                                mbar_wait(smem_u32(&c.v_full[st]), ph, 2005);
+                                tc_fence_after();
+                                v_ready = true;
+                            }
+                            const uint32_t vbase = sV + st * kTileBytes;
+                            for (int kk = 0; kk < kBN / 16; ++kk)
+                                umma_bf16_ts(tbase + x * 256 + 128, tbase + x * 256 + kk * 8,
+                                             umma_desc_sw128(vbase + kk * 16 * 128, kHalf, 1024), idesc_o, 1);
+                            if (j == last_block(P, x)) umma_commit(smem_u32(&c.o_done[x]));
+                        } else {
+                            stop_at[x] = j;
+                            umma_commit(smem_u32(&c.o_done[x]));  // slot finished
+                        }
+                    }
+                    if (!v_ready) mbar_wait(smem_u32(&c.v_full[st]), ph, 2006);  // consume the phase
+                    umma_commit(smem_u32(&c.kv_empty[st]));
                 }
+                umma_commit(smem_u32(&c.q_empty));
+                gblk += loaded;
             }
-            __syncwarp();
-            stop_at = __shfl_sync(0xffffffffu, stop_at, 0);
-            gblk += (stop_at >= 0) ? min(t.nb, stop_at + kStages) : t.nb;
-            gq += (stop_at >= 0) ? min(t.nb, stop_at + 2) : t.nb;
         }
+        __syncwarp();
     } else {
-        // ============================== softmax / epilogue ==============================
-        const int r = threadIdx.x;  // 0..127, TMEM lane
-        const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
-        uint32_t gblk = 0, gq = 0, gp = 0, od = 0;
-        for (int64_t tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
-            const TileInfo t = tile_info(a, a.tile_at(tile));
-            const bool valid = r < t.tn;
-            const int64_t grow = q_local_row(a, t, r);  // segment row in [0, L)
-            const int64_t slot = t.zh * g.l + grow;
+        // ============================== softmax / epilogue (slot x) ==============================
+        const int x = warp / 4;
+        const int r = threadIdx.x % 128;  // TMEM lane
+        const uint32_t lane_off = (uint32_t)((warp % 4) * 32) << 16;
+        const uint32_t tS = tbase + lane_off + x * 256;
+        const uint32_t tO = tS + 128;
+        const uint32_t bar_id = 1 + x;
+        uint32_t ns = 0, no = 0;
+        for (int64_t it = blockIdx.x; it < total; it += gridDim.x) {
+            const PairInfo P = pair_info(p, it);
+            if (!P.has[x]) continue;
+            const bool valid = r < P.tn[x];
+            const int64_t grow = q_row(a, P, x, r);
+            const int64_t slot = P.zh * g.l + grow;
             float m2, ell;
             // ---- state init: O in TMEM, (m, ell) in registers
             if (a.mode & kStateIn) {
@@ -365,178 +383,129 @@ tc_pass_kernel(const TcParams p, const __grid_constant__ CUtensorMap qmap,
                 for (int c0 = 0; c0 < kD; c0 += 32) {
                     uint32_t v[32];
                     for (int i = 0; i < 8; ++i) {
-                        const float4 x = src[c0 / 4 + i];
-                        v[4 * i] = __float_as_uint(x.x);
-                        v[4 * i + 1] = __float_as_uint(x.y);
-                        v[4 * i + 2] = __float_as_uint(x.z);
-                        v[4 * i + 3] = __float_as_uint(x.w);
+                        const float4 y = src[c0 / 4 + i];
+                        v[4 * i] = __float_as_uint(y.x);
+                        v[4 * i + 1] = __float_as_uint(y.y);
+                        v[4 * i + 2] = __float_as_uint(y.z);
+                        v[4 * i + 3] = __float_as_uint(y.w);
                     }
-                    tmem_st32(tbase + lane_off + kColO + c0, v);
+                    tmem_st32(tO + c0, v);
                 }
             } else {
                 m2 = -INFINITY;
                 ell = 0.0f;
                 uint32_t z[32];
                 for (int i = 0; i < 32; ++i) z[i] = 0u;
-                for (int c0 = 0; c0 < kD; c0 += 32) tmem_st32(tbase + lane_off + kColO + c0, z);
+                for (int c0 = 0; c0 < kD; c0 += 32) tmem_st32(tO + c0, z);
             }
             tmem_st_wait();
             tc_fence_before();
 
             int committed = 0;
             int64_t pairs = 0;
-            bool stopped = false;
-            int stop_j = -1;
-            for (int j = 0; j < t.nb; ++j) {
-                const uint32_t gi = gblk + j;  // load sequence (K stage holding P)
-                const uint32_t gs = gq + j;    // S buffer sequence
-                const int sb = gs & 1;
-                mbar_wait(smem_u32(&c.s_full[sb]), (gs >> 1) & 1, 3001);
+            bool any = false;
+            for (int j = 0; j < P.nb; ++j) {
+                if (!participates(P, x, j)) continue;
+                any = true;
+                mbar_wait(smem_u32(&c.s_full[x]), ns & 1, 3001);
+                ++ns;
                 tc_fence_after();
-                uint32_t sv[kBN];
-                {
-                    uint32_t (&v0)[32] = *reinterpret_cast<uint32_t(*)[32]>(&sv[0]);
-                    uint32_t (&v1)[32] = *reinterpret_cast<uint32_t(*)[32]>(&sv[32]);
-                    uint32_t (&v2)[32] = *reinterpret_cast<uint32_t(*)[32]>(&sv[64]);
-                    uint32_t (&v3)[32] = *reinterpret_cast<uint32_t(*)[32]>(&sv[96]);
-                    const uint32_t sa = tbase + lane_off + sb * 128;
-                    tmem_ld32(sa, v0);
-                    tmem_ld32(sa + 32, v1);
-                    tmem_ld32(sa + 64, v2);
-                    tmem_ld32(sa + 96, v3);
-                    tmem_ld_wait();
-                }
-                tc_fence_before();
-                __syncwarp();
-                if (lane == 0) mbar_arrive(smem_u32(&c.s_empty[sb]));
-                float* s = reinterpret_cast<float*>(sv);
-                // ---- masks: causal on original positions (diag) / clipped chunk (prefix)
-                const bool is_diag = j < t.nd;
-                int lim;  // keys [0, lim) of the block are visible to this row
+                // ---- visible keys of this block for this row
+                const bool is_diag = j < P.ndmax;
+                int lim;
                 if (is_diag) {
                     const int64_t k0 = (int64_t)j * kBN;
-                    const int64_t kn = min((int64_t)kBN, t.seg_rows - k0);
-                    const int64_t vis = (k0 + kn - 1 <= t.t0) ? kn : min(kn, t.t0 + r - k0 + 1);
+                    const int64_t kn = min((int64_t)kBN, P.seg_rows - k0);
+                    const int64_t vis = (k0 + kn - 1 <= P.t0[x]) ? kn : min(kn, P.t0[x] + r - k0 + 1);
                     lim = (int)max((int64_t)0, vis);
                 } else {
-                    const int64_t c0 = (int64_t)(j - t.nd) * kBN;
-                    lim = (int)min((int64_t)kBN, t.avail - c0);
+                    const int64_t c0 = (int64_t)(j - P.ndmax) * kBN;
+                    lim = (int)min((int64_t)kBN, P.avail - c0);
                 }
-                if (lim < kBN) {
+                // ---- pass 1: row max (S read from TMEM in 32-column chunks)
+                float mxa[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
-                    for (int i = 0; i < kBN; ++i)
-                        if (i >= lim) s[i] = -INFINITY;
+                for (int c0 = 0; c0 < kBN; c0 += 32) {
+                    uint32_t v[32];
+                    tmem_ld32(tS + c0, v);
+                    tmem_ld_wait();
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) {
+                        const float sv = (c0 + i < lim) ? __uint_as_float(v[i]) : -INFINITY;
+                        mxa[i & 3] = fmaxf(mxa[i & 3], sv);
+                    }
                 }
-                float mxa[8];
-#pragma unroll
-                for (int u = 0; u < 8; ++u) mxa[u] = s[u];
-#pragma unroll
-                for (int i = 8; i < kBN; i += 8)
-#pragma unroll
-                    for (int u = 0; u < 8; ++u) mxa[u] = fmaxf(mxa[u], s[i + u]);
-                const float mx = fmaxf(fmaxf(fmaxf(mxa[0], mxa[1]), fmaxf(mxa[2], mxa[3])),
-                                       fmaxf(fmaxf(mxa[4], mxa[5]), fmaxf(mxa[6], mxa[7]))) * p.scale_log2;
+                const float mx = fmaxf(fmaxf(mxa[0], mxa[1]), fmaxf(mxa[2], mxa[3])) * p.scale_log2;
                 const float m_new = fmaxf(m2, mx);
                 const bool rescale = (m_new > m2 + kRescaleThresh) || (m2 == -INFINITY);
                 const float m_use = rescale ? m_new : m2;
                 const float neg_ref = (m_use == -INFINITY) ? 0.0f : -m_use;
-                float rs[8];
-#pragma unroll
-                for (int u = 0; u < 8; ++u) rs[u] = 0.0f;
-#pragma unroll
-                for (int i = 0; i < kBN; i += 8)
-#pragma unroll
-                    for (int u = 0; u < 8; ++u) {
-                        s[i + u] = ex2(fmaf(s[i + u], p.scale_log2, neg_ref));
-                        rs[u] += s[i + u];
-                    }
-                const float rowsum = ((rs[0] + rs[1]) + (rs[2] + rs[3])) + ((rs[4] + rs[5]) + (rs[6] + rs[7]));
                 const float alpha = (m2 == -INFINITY) ? 0.0f : ex2(m2 + neg_ref);
+                // O rescale (P V of the previous block is complete: s_full orders after it)
+                if (__any_sync(0xffffffffu, rescale && m2 != -INFINITY)) {
+                    for (int c0 = 0; c0 < kD; c0 += 32) {
+                        uint32_t v[32];
+                        tmem_ld32(tO + c0, v);
+                        tmem_ld_wait();
+                        for (int i = 0; i < 32; ++i) v[i] = __float_as_uint(__uint_as_float(v[i]) * alpha);
+                        tmem_st32(tO + c0, v);
+                    }
+                }
+                // ---- pass 2: P = exp2(s*scale - m) -> bf16 pairs over the first 64 S columns
+                float rs[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+#pragma unroll
+                for (int c0 = 0; c0 < kBN; c0 += 32) {
+                    uint32_t v[32];
+                    tmem_ld32(tS + c0, v);
+                    tmem_ld_wait();
+                    uint32_t pk[16];
+#pragma unroll
+                    for (int i = 0; i < 32; i += 2) {
+                        const float e0 = (c0 + i < lim) ? ex2(fmaf(__uint_as_float(v[i]), p.scale_log2, neg_ref)) : 0.0f;
+                        const float e1 = (c0 + i + 1 < lim) ? ex2(fmaf(__uint_as_float(v[i + 1]), p.scale_log2, neg_ref)) : 0.0f;
+                        rs[(i >> 1) & 3] += e0 + e1;
+                        pk[i >> 1] = pack_bf16(e0, e1);
+                    }
+                    tmem_st16(tS + c0 / 2, pk);
+                }
+                const float rowsum = (rs[0] + rs[1]) + (rs[2] + rs[3]);
                 bool commit = true;
                 if (!is_diag) {
                     // relative normaliser gain of this chunk (kernel.cpp:108-115)
                     const float prev = ell * alpha;
                     float gain = valid ? rowsum / prev : -INFINITY;
                     for (int o = 16; o > 0; o >>= 1) gain = fmaxf(gain, __shfl_xor_sync(0xffffffffu, gain, o));
-                    if (lane == 0) c.red[warp] = gain;
-                    named_bar_sync(1, 128);
-                    const float mg = fmaxf(fmaxf(c.red[0], c.red[1]), fmaxf(c.red[2], c.red[3]));
+                    if (lane == 0) c.red[x][warp % 4] = gain;
+                    named_bar_sync(bar_id, 128);
+                    const float mg = fmaxf(fmaxf(c.red[x][0], c.red[x][1]), fmaxf(c.red[x][2], c.red[x][3]));
                     commit = !(mg < (float)a.tau);
-                    named_bar_sync(1, 128);  // red[] reusable
+                    named_bar_sync(bar_id, 128);  // red[] reusable
                 }
-                ++gp;
-                // P V of block j-1 must be complete before this block's decision is published
-                // (P buffer / O reuse, and one-phase-at-a-time on o_done and p_full)
-                if (j > 0) {
-                    mbar_wait(smem_u32(&c.o_done), od & 1, 3003);
-                    ++od;
-                    tc_fence_after();
-                }
-                if (!commit) {
-                    if (r == 0) c.dec[j & 3] = 2;
-                    __syncwarp();
-                    if (lane == 0) mbar_arrive(smem_u32(&c.p_full));
-                    stopped = true;
-                    if (j + 1 < t.nb) {  // drain the speculative Q K^T of block j+1
-                        const uint32_t gn = gs + 1;
-                        mbar_wait(smem_u32(&c.s_full[gn & 1]), (gn >> 1) & 1, 3002);
-                        __syncwarp();
-                        if (lane == 0) mbar_arrive(smem_u32(&c.s_empty[gn & 1]));
-                    }
-                    stop_j = j;
-                    break;
-                }
-                if (__any_sync(0xffffffffu, rescale && m2 != -INFINITY)) {
-                    for (int c0 = 0; c0 < kD; c0 += 32) {
-                        uint32_t v[32];
-                        tmem_ld32(tbase + lane_off + kColO + c0, v);
-                        tmem_ld_wait();
-                        for (int i = 0; i < 32; ++i) v[i] = __float_as_uint(__uint_as_float(v[i]) * alpha);
-                        tmem_st32(tbase + lane_off + kColO + c0, v);
-                    }
-                    tmem_st_wait();
-                }
-                // P (bf16) -> smem, K-major SW128
-                unsigned char* prow = smem + kOffK + (gi % kStages) * kTileBytes + r * 128;
-#pragma unroll
-                for (int h = 0; h < 2; ++h) {
-#pragma unroll
-                    for (int ch = 0; ch < 8; ++ch) {
-                        const float* x = s + h * 64 + ch * 8;
-                        uint4 w;
-                        w.x = pack_bf16(x[0], x[1]);
-                        w.y = pack_bf16(x[2], x[3]);
-                        w.z = pack_bf16(x[4], x[5]);
-                        w.w = pack_bf16(x[6], x[7]);
-                        *reinterpret_cast<uint4*>(prow + h * kHalf + ((ch ^ (r & 7)) << 4)) = w;
-                    }
-                }
-                ell = ell * alpha + rowsum;
+                // state update (on a stop the rescaled state is the same state: O/ell unchanged)
+                ell = commit ? ell * alpha + rowsum : ell * alpha;
                 m2 = m_use;
-                if (!is_diag) {
+                if (commit && !is_diag) {
                     ++committed;
-                    const int64_t c0 = (int64_t)(j - t.nd) * kBN;
-                    pairs += min((int64_t)kBN, t.avail - c0);
+                    const int64_t c0 = (int64_t)(j - P.ndmax) * kBN;
+                    pairs += min((int64_t)kBN, P.avail - c0);
                 }
-                fence_proxy_async_smem();
+                tmem_st_wait();
                 tc_fence_before();
-                if (r == 0) c.dec[j & 3] = 1;
+                if (r == 0) c.dec[x][j & 3] = commit ? 1 : 2;
                 __syncwarp();
-                if (lane == 0) mbar_arrive(smem_u32(&c.p_full));
+                if (lane == 0) mbar_arrive(smem_u32(&c.p_full[x]));
+                if (!commit) break;
             }
-            // ---- epilogue: the last P V (if the tile ran to completion) must be done
-            if (t.nb > 0 && !stopped) {
-                mbar_wait(smem_u32(&c.o_done), od & 1, 3004);
-                ++od;
+            if (any) {
+                mbar_wait(smem_u32(&c.o_done[x]), no & 1, 3004);
+                ++no;
                 tc_fence_after();
             }
-            gblk += (t.nb == 0) ? 0 : (stopped ? min(t.nb, stop_j + kStages) : t.nb);
-            gq += (t.nb == 0) ? 0 : (stopped ? min(t.nb, stop_j + 2) : t.nb);
             // ---- read O, finalize / persist
             const float inv = 1.0f / ell;
             for (int c0 = 0; c0 < kD; c0 += 32) {
                 uint32_t v[32];
-                tmem_ld32(tbase + lane_off + kColO + c0, v);
+                tmem_ld32(tO + c0, v);
                 tmem_ld_wait();
                 if (!valid) continue;
                 if (a.mode & kStateOut) {
@@ -546,7 +515,7 @@ tc_pass_kernel(const TcParams p, const __grid_constant__ CUtensorMap qmap,
                                              __uint_as_float(v[4 * i + 2]), __uint_as_float(v[4 * i + 3]));
                 }
                 if (a.mode & kFinal) {
-                    const int64_t ooff = g.o_base(t.zh) + grow * g.os[2] + c0;
+                    const int64_t ooff = g.o_base(P.zh) + grow * g.os[2] + c0;
                     if (g.out_bf16) {
                         uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(a.o) + ooff);
                         for (int i = 0; i < 4; ++i) {
@@ -571,18 +540,19 @@ tc_pass_kernel(const TcParams p, const __grid_constant__ CUtensorMap qmap,
             }
             if (valid && (a.mode & kFinal) && !(ell > 0.0f)) atomicExch(a.err_flag, 2);
             if ((a.mode & kPrefix) && r == 0) {
-                const bool overflow = t.np > 0 && committed == t.np && t.avail < t.n * g.S;
+                const int64_t tile = P.zh * a.tiles_per_head + P.n * a.T + P.ti[x];
+                const bool overflow = P.np > 0 && committed == P.np && P.avail < P.n * g.S;
                 if (overflow) {
                     // walked the whole truncated list without stopping: rerun on the full plan
-                    const int slot = atomicAdd(a.ovf_count, 1);
-                    a.ovf_tiles[slot] = (int32_t)a.tile_at(tile);
+                    const int s2 = atomicAdd(a.ovf_count, 1);
+                    a.ovf_tiles[s2] = (int32_t)tile;
                 } else {
-                    a.processed[(t.zh * g.N + t.n) * a.T + t.ti] = committed;
-                    if (pairs) atomicAdd((unsigned long long*)&a.pass2_pairs[t.zh], (unsigned long long)(pairs * t.tn));
+                    a.processed[(P.zh * g.N + P.n) * a.T + P.ti[x]] = committed;
+                    if (pairs) atomicAdd((unsigned long long*)&a.pass2_pairs[P.zh], (unsigned long long)(pairs * P.tn[x]));
                 }
             }
             tc_fence_before();
-            named_bar_sync(1, 128);  // all rows done with this tile's O before the next init
+            named_bar_sync(bar_id, 128);  // all rows done with O before the next pair's init
         }
     }
     tc_fence_before();
@@ -619,13 +589,10 @@ bool make_row_map(CUtensorMap* map, const void* base, int64_t rows, uint32_t box
 }
 
 int64_t span_rows(const int64_t* st, int64_t z, int64_t h, int64_t l) {
-    // rows (of D elements) spanned by a strided [z, h, l, D] tensor
     return ((z - 1) * st[0] + (h - 1) * st[1] + (l - 1) * st[2]) / kD + 1;
 }
 
-bool strides_ok(const int64_t* st) {
-    return st[0] % kD == 0 && st[1] % kD == 0 && st[2] % kD == 0;
-}
+bool strides_ok(const int64_t* st) { return st[0] % kD == 0 && st[1] % kD == 0 && st[2] % kD == 0; }
 
 }  // namespace
 
@@ -656,6 +623,9 @@ cudaError_t launch_tc_pass(const PassArgs& a, cudaStream_t st) {
     p.scale_log2 = (float)(a.scale * 1.4426950408889634);
     p.q_contig = g.qs[2] == kD;
     p.kv_contig = g.ks[2] == kD && g.vs[2] == kD;
+    p.pairs_full = (a.T + 1) / 2;
+    const int64_t t_last = (g.last_len + kBM - 1) / kBM;
+    p.pairs_per_head = (g.N - 1) * p.pairs_full + (t_last + 1) / 2;
     static bool attr_done = false;
     if (!attr_done) {
         cudaError_t e = cudaFuncSetAttribute(tc_pass_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
@@ -665,9 +635,9 @@ cudaError_t launch_tc_pass(const PassArgs& a, cudaStream_t st) {
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const int64_t tiles = a.num_tiles();
-    if (tiles == 0) return cudaSuccess;
-    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, sms));
+    const int64_t work = a.tile_list ? a.tile_count : g.z * g.hq * p.pairs_per_head;
+    if (work == 0) return cudaSuccess;
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(work, sms));
     tc_pass_kernel<<<grid, kThreads, kSmemBytes, st>>>(p, qmap, kmap, vmap, qtile, ktile, vtile);
     return cudaGetLastError();
 }
