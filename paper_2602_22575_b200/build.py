@@ -23,8 +23,12 @@ CU_SRCS = ["capi.cu", "plan.cu", "attn_generic.cu", "attn_sm100.cu"]
 CPP_SRCS = ["synthetic.cpp"]
 
 
+EXTRA = os.environ.get("S2O_NVCC_FLAGS", "").split()  # e.g. -DS2O_TIMELINE (profiling aid)
+
+
 def _stamp() -> str:
     h = hashlib.sha1()
+    h.update(" ".join(EXTRA).encode())
     for name in sorted(os.listdir(CSRC)) + ["../../include/s2o_cuda.h", "../build.py"]:
         path = os.path.join(CSRC, name)
         if os.path.isfile(path):
@@ -50,7 +54,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         obj = os.path.join(obj_dir, src + ".o")
         cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
                "-Xptxas", "-v" if verbose else "-O3", "--expt-relaxed-constexpr",
-               *inc, "-c", os.path.join(CSRC, src), "-o", obj]
+               *EXTRA, *inc, "-c", os.path.join(CSRC, src), "-o", obj]
         procs.append((src, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT)))
         objs.append(obj)
     for src in CPP_SRCS:

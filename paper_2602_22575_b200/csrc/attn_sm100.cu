@@ -50,27 +50,37 @@ namespace {
 constexpr int kD = 128;
 constexpr int kBM = 128;
 constexpr int kBN = 128;
-constexpr int kStages = 2;
-constexpr int kThreads = 384;
+constexpr int kKStages = 3;  // K ring: block j may load once decisions <= j-3 are known
+constexpr int kVStages = 2;  // V ring: block j may load once decisions <= j-2 are known
+constexpr int kThreads = 512;
 constexpr int kMmaWarp = 8;
-constexpr int kLoadWarp0 = 9;
-constexpr int kLoaderThreads = 96;
+constexpr int kKWarp0 = 9;    // K loader group: warps 9-12 (also loads Q)
+constexpr int kVWarp0 = 13;   // V loader group: warps 13-15
+constexpr int kKThreads = 128;
+constexpr int kVThreads = 96;
 constexpr uint32_t kHalf = 128u * 128u;     // one 64-column half of a 128-row tile
 constexpr uint32_t kTileBytes = 2 * kHalf;  // 32 KB
 constexpr uint32_t kOffQ = 0;               // slot X at X * kTileBytes
 constexpr uint32_t kOffK = 2 * kTileBytes;
-constexpr uint32_t kOffV = kOffK + kStages * kTileBytes;
-constexpr uint32_t kOffCtrl = kOffV + kStages * kTileBytes;
-constexpr uint32_t kSmemBytes = kOffCtrl + 1024 + 1024;
+constexpr uint32_t kOffV = kOffK + kKStages * kTileBytes;
+constexpr uint32_t kOffCtrl = kOffV + kVStages * kTileBytes;
+constexpr uint32_t kOffTok = kOffCtrl + 256;  // token rings: K group int32 [2][128], V group [2][128]
+constexpr uint32_t kSmemBytes = kOffTok + 2048;  // 226.25 KB (base must be 1024-B aligned)
 constexpr uint32_t kTmemCols = 512;
+constexpr int kSoftmaxRegs = 192;   // setmaxnreg: softmax warpgroups (0, 1)
+constexpr int kOtherRegs = 64;      // MMA + loader warpgroups (2, 3)
+constexpr int kLaunchRegs = 65536 / kThreads / 8 * 8;  // 128: what __launch_bounds__(512, 1) allots
+// setmaxnreg.inc blocks until the pool has the registers: the decrements must cover it
+static_assert(kSoftmaxRegs - kLaunchRegs <= kLaunchRegs - kOtherRegs, "register pool overcommitted");
+static_assert(sizeof(uint64_t) * 19 + 4 + 64 + 8 <= 256, "Ctrl exceeds its 256 B");
 constexpr float kRescaleThresh = 8.0f;  // lazy max update, log2 units (factor 256)
 
 struct Ctrl {
     uint64_t q_full, q_empty;
-    uint64_t k_full[kStages], v_full[kStages], kv_empty[kStages];
+    uint64_t k_full[kKStages], k_empty[kKStages], v_full[kVStages], v_empty[kVStages];
     uint64_t s_full[2], p_full[2], o_done[2];
     uint32_t tmem_base;
-    float red[2][4];
+    uint32_t red[2][2][4];  // continue votes [slot][block parity][warp]
     uint8_t dec[2][4];  // per slot decision ring (block j -> j & 3): 1 = commit, 2 = stop
 };
 
@@ -79,7 +89,25 @@ struct TcParams {
     float scale_log2;  // (1/sqrt(D)) * log2(e)
     int q_contig, kv_contig;
     int64_t pairs_per_head, pairs_full;  // pairs per head; pairs in a full segment
+    unsigned long long* tl;              // optional timeline (CTA 0), see s2o_debug_timeline
 };
+
+// Timeline events (profiling aid): tl[ev * kTlCap + seq] = clock64() in CTA 0.
+constexpr int kTlCap = 1024;
+// Compiled in only with -DS2O_TIMELINE (S2O_NVCC_FLAGS=-DS2O_TIMELINE python -m ...build).
+__device__ __forceinline__ void tl_mark(const TcParams& p, int ev, uint32_t seq) {
+#ifdef S2O_TIMELINE
+    if (p.tl != nullptr && blockIdx.x == 0 && seq < (uint32_t)kTlCap)
+        p.tl[ev * kTlCap + seq] = clock64();
+#endif
+}
+
+// Early-stop decision from the four per-warp votes (early_stop_check kernel.cpp:220-234: stop iff
+// max gain < tau, strictly, NaN gains dropped <=> continue iff some row has gain >= tau).
+__device__ __forceinline__ bool chunk_commit(const uint32_t* red) {
+    const volatile uint32_t* rv = red;
+    return (rv[0] | rv[1] | rv[2] | rv[3]) != 0u;
+}
 
 struct PairInfo {
     int64_t zh, n, sb, seg_rows, avail;
@@ -160,8 +188,8 @@ tc_pass_kernel(const TcParams p, const __grid_constant__ CUtensorMap qmap,
                const __grid_constant__ CUtensorMap qtile, const __grid_constant__ CUtensorMap ktile,
                const __grid_constant__ CUtensorMap vtile) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
-    unsigned char* smem = reinterpret_cast<unsigned char*>(
-        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    unsigned char* smem = smem_raw;
+    if ((smem_u32(smem) & 1023u) != 0) __trap();  // SWIZZLE_128B tiles need a 1024-B aligned base
     Ctrl& c = *reinterpret_cast<Ctrl*>(smem + kOffCtrl);
     const PassArgs& a = p.a;
     const Geo& g = a.g;
@@ -172,12 +200,17 @@ tc_pass_kernel(const TcParams p, const __grid_constant__ CUtensorMap qmap,
     const uint32_t sV = smem_u32(smem + kOffV);
 
     if (threadIdx.x == 0) {
-        mbar_init(smem_u32(&c.q_full), 1);
+        // full barriers: every loader thread arrives once per phase (TMA expect_tx by one
+        // thread + plain arrives, or cp.async.mbarrier.arrive.noinc by all)
+        mbar_init(smem_u32(&c.q_full), kKThreads);
         mbar_init(smem_u32(&c.q_empty), 1);
-        for (int s = 0; s < kStages; ++s) {
-            mbar_init(smem_u32(&c.k_full[s]), 1);
-            mbar_init(smem_u32(&c.v_full[s]), 1);
-            mbar_init(smem_u32(&c.kv_empty[s]), 1);
+        for (int s = 0; s < kKStages; ++s) {
+            mbar_init(smem_u32(&c.k_full[s]), kKThreads);
+            mbar_init(smem_u32(&c.k_empty[s]), 1);
+        }
+        for (int s = 0; s < kVStages; ++s) {
+            mbar_init(smem_u32(&c.v_full[s]), kVThreads);
+            mbar_init(smem_u32(&c.v_empty[s]), 1);
         }
         for (int x = 0; x < 2; ++x) {
             mbar_init(smem_u32(&c.s_full[x]), 1);
@@ -197,191 +230,275 @@ tc_pass_kernel(const TcParams p, const __grid_constant__ CUtensorMap qmap,
     const int64_t total = a.tile_list ? a.tile_count : g.z * g.hq * p.pairs_per_head;
     const int64_t rowu = g.d;  // row unit of the tensor maps = D elements
 
-    if (warp >= kLoadWarp0) {
+    if (warp >= kMmaWarp) setmaxnreg_dec<kOtherRegs>();  // warpgroups 2-3
+    if (warp >= kKWarp0) {
         // ============================== loaders ==============================
-        const int lt = (warp - kLoadWarp0) * 32 + lane;  // 0..95
-        uint32_t gblk = 0, qcount = 0;
+        // Two independent groups: K (+ Q) and V, so K(j+1) never waits behind V(j)'s gating.
+        // Gathered rows (permuted Q rows, ranked prefix keys) move with 16-byte cp.async into
+        // the SWIZZLE_128B layout: a thread owns one 16-B column chunk and a fixed row stride,
+        // so a warp instruction moves 2 rows x 256 B with no per-lane TMA issue loop.
+        // Contiguous 128-row blocks move with one 2-D TMA tile per 64-column half.
+        const bool kgrp = warp < kVWarp0;
+        const int nthr = kgrp ? kKThreads : kVThreads;
+        const int lt = (warp - (kgrp ? kKWarp0 : kVWarp0)) * 32 + lane;
+        const uint32_t gbar = kgrp ? 3 : 4;
+        int32_t* ring0 = reinterpret_cast<int32_t*>(smem + kOffTok) + (kgrp ? 0 : 2 * kBN);
+        const int rstep = nthr / 16;                 // rows between a thread's chunks
+        const int ch = lt & 15, r0 = lt >> 4;
+        const uint32_t ch_off = (uint32_t)(ch >> 3) * kHalf;
+        auto gather_tile = [&](uint32_t dst, const __nv_bfloat16* base, int64_t rstride, const int32_t* tok) {
+            for (int row = r0; row < kBM; row += rstep) {
+                const __nv_bfloat16* src = base + (int64_t)tok[row] * rstride + ch * 8;
+                cp_async16(dst + ch_off + row * 128 + ((((uint32_t)ch & 7u) ^ ((uint32_t)row & 7u)) << 4), src, 16);
+            }
+        };
+        const __nv_bfloat16* qg = reinterpret_cast<const __nv_bfloat16*>(a.q);
+        const __nv_bfloat16* xg = reinterpret_cast<const __nv_bfloat16*>(kgrp ? a.k : a.v);
+        const CUtensorMap* xtile = kgrp ? &ktile : &vtile;
+        const uint32_t xbase = kgrp ? sK : sV;
+        const int nst = kgrp ? kKStages : kVStages;
+        const int lag = kgrp ? 3 : 2;  // decisions <= j-lag are final when stage j is acquired
+        uint64_t* xfull = kgrp ? c.k_full : c.v_full;
+        uint64_t* xempty = kgrp ? c.k_empty : c.v_empty;
+        uint32_t gx = 0, qcount = 0;
         for (int64_t it = blockIdx.x; it < total; it += gridDim.x) {
             const PairInfo P = pair_info(p, it);
             if (P.nb == 0) continue;
             const int32_t* kv = (P.np > 0) ? a.kv_seg(P.zh, P.n) : nullptr;
-            mbar_wait(smem_u32(&c.q_empty), (qcount & 1) ^ 1, 1001);
-            const int64_t qb = g.q_base(P.zh) / rowu, qs = g.qs[2] / rowu;
-            const bool q_tile = p.q_contig && !((a.mode & kStateIn) && a.q_reorder);
-            if (lt == 0) mbar_expect_tx(smem_u32(&c.q_full), (P.has[1] ? 2 : 1) * kTileBytes);
-            named_bar_sync(3, kLoaderThreads);
-            for (int x = 0; x < 2; ++x) {
-                if (!P.has[x]) continue;
-                const uint32_t qdst = sQ + x * kTileBytes;
-                if (q_tile && P.tn[x] == kBM) {
-                    if (lt == 0)
-                        for (int h = 0; h < 2; ++h)
-                            tma_load2d(qdst + h * kHalf, &qtile, h * 64, (int32_t)(qb + (P.sb + P.t0[x]) * qs),
-                                       smem_u32(&c.q_full));
-                } else if (lt < 64) {
-                    const int grp = lt >> 1, h = lt & 1;
-                    int32_t rows[4];
-                    for (int i = 0; i < 4; ++i) rows[i] = (int32_t)(qb + q_row(a, P, x, grp * 4 + i) * qs);
-                    tma_gather4(qdst + h * kHalf + grp * 512, &qmap, h * 64, rows[0], rows[1], rows[2], rows[3],
-                                smem_u32(&c.q_full));
-                }
-            }
-            ++qcount;
-            const int64_t kb = g.k_base(P.zh) / rowu, vb = g.v_base(P.zh) / rowu;
-            const int64_t ks = g.ks[2] / rowu, vs = g.vs[2] / rowu;
-            // gather ops of one block: [0,64) K, [64,128) V; op -> (row group, half)
-            auto fetch_rows = [&](int j, int32_t (&rr)[2][4]) {
-                for (int u = 0; u < 2; ++u) {
-                    const int op = lt + u * kLoaderThreads;
-                    const int grp = (op >> 1) & 31;
-                    const bool isv = op >= 64;
-                    for (int i = 0; i < 4; ++i) {
-                        const int64_t tok = (op < 128 && j < P.nb) ? key_token(P, kv, j, grp * 4 + i) : 0;
-                        rr[u][i] = (int32_t)(isv ? vb + tok * vs : kb + tok * ks);
-                    }
-                }
-            };
-            const auto gathered = [&](int j) { return !(j < P.ndmax && p.kv_contig); };
-            int32_t cur[2][4], nxt[2][4];
-            if (gathered(0)) fetch_rows(0, cur);
-            bool stop_known[2] = {false, false};
-            int loaded = 0;
-            for (int j = 0; j < P.nb; ++j) {
-                const uint32_t gi = gblk + j;
-                const int st = gi % kStages;
-                if (j + 1 < P.nb && gathered(j + 1)) fetch_rows(j + 1, nxt);
-                mbar_wait(smem_u32(&c.kv_empty[st]), ((gi / kStages) & 1) ^ 1, 1002);
-                // acquiring stage j certifies that both slots' decisions on block j-2 are final
-                if (j >= 2 && j - 2 >= P.ndmax)
-                    for (int x = 0; x < 2; ++x)
-                        if (participates(P, x, j - 2) && c.dec[x][(j - 2) & 3] == 2) stop_known[x] = true;
-                bool need = false;
-                for (int x = 0; x < 2; ++x) need |= participates(P, x, j) && !stop_known[x];
-                if (!need) break;
-                if (lt == 0) {
-                    mbar_expect_tx(smem_u32(&c.k_full[st]), kTileBytes);
-                    mbar_expect_tx(smem_u32(&c.v_full[st]), kTileBytes);
-                }
-                named_bar_sync(3, kLoaderThreads);
-                const uint32_t kdst = sK + st * kTileBytes;
-                const uint32_t vdst = sV + st * kTileBytes;
-                if (!gathered(j)) {
+            named_bar_sync(gbar, nthr);  // every thread of the group is done with its ring
+            if (kgrp) {
+                // ---- Q (both slots)
+                mbar_wait(smem_u32(&c.q_empty), (qcount & 1) ^ 1, 1001);
+                const int64_t qb = g.q_base(P.zh) / rowu, qs = g.qs[2] / rowu;
+                const bool q_tile = p.q_contig && !((a.mode & kStateIn) && a.q_reorder) && P.tn[0] == kBM &&
+                                    (!P.has[1] || P.tn[1] == kBM);
+                if (q_tile) {
                     if (lt == 0) {
-                        const int64_t tok = P.sb + (int64_t)j * kBN;
-                        for (int h = 0; h < 2; ++h)
-                            tma_load2d(kdst + h * kHalf, &ktile, h * 64, (int32_t)(kb + tok * ks), smem_u32(&c.k_full[st]));
-                        for (int h = 0; h < 2; ++h)
-                            tma_load2d(vdst + h * kHalf, &vtile, h * 64, (int32_t)(vb + tok * vs), smem_u32(&c.v_full[st]));
+                        mbar_expect_tx(smem_u32(&c.q_full), (P.has[1] ? 2 : 1) * kTileBytes);
+                        for (int x = 0; x < 2; ++x)
+                            if (P.has[x])
+                                for (int h = 0; h < 2; ++h)
+                                    tma_load2d(sQ + x * kTileBytes + h * kHalf, &qtile, h * 64,
+                                               (int32_t)(qb + (P.sb + P.t0[x]) * qs), smem_u32(&c.q_full));
+                    } else {
+                        mbar_arrive(smem_u32(&c.q_full));
                     }
                 } else {
-                    for (int u = 0; u < 2; ++u) {
-                        const int op = lt + u * kLoaderThreads;
-                        if (op >= 128) break;
-                        const int grp = (op >> 1) & 31, h = op & 1;
-                        const bool isv = op >= 64;
-                        tma_gather4((isv ? vdst : kdst) + h * kHalf + grp * 512, isv ? &vmap : &kmap, h * 64,
-                                    cur[u][0], cur[u][1], cur[u][2], cur[u][3],
-                                    smem_u32(isv ? &c.v_full[st] : &c.k_full[st]));
+                    for (int e = lt; e < 2 * kBM; e += nthr) {
+                        const int x = e >> 7;
+                        ring0[e] = P.has[x] ? (int32_t)(qb + q_row(a, P, x, e & 127) * qs) : 0;
                     }
+                    named_bar_sync(gbar, nthr);
+                    for (int x = 0; x < 2; ++x)
+                        if (P.has[x]) gather_tile(sQ + x * kTileBytes, qg, kD, ring0 + x * kBM);
+                    cp_async_arrive_noinc(smem_u32(&c.q_full));
+                    named_bar_sync(gbar, nthr);  // ring reusable
                 }
-                for (int u = 0; u < 2; ++u)
-                    for (int i = 0; i < 4; ++i) cur[u][i] = nxt[u][i];
-                ++loaded;
+                ++qcount;
             }
-            gblk += loaded;
+            const int64_t xb = (kgrp ? g.k_base(P.zh) : g.v_base(P.zh)) / rowu;
+            const int64_t xs = (kgrp ? g.ks[2] : g.vs[2]) / rowu;
+            const auto gathered = [&](int j) { return !(j < P.ndmax && p.kv_contig); };
+            // tokens of block j: entries lt and lt + nthr (< 128) in registers, one block ahead
+            auto fetch_tok = [&](int j, int32_t (&tk)[2]) {
+                for (int u = 0; u < 2; ++u) {
+                    const int i = lt + u * nthr;
+                    tk[u] = (i < kBN && j < P.nb && gathered(j)) ? (int32_t)key_token(P, kv, j, i) : 0;
+                }
+            };
+            int32_t tk[2];
+            fetch_tok(0, tk);
+            int stop_at[2] = {1 << 30, 1 << 30};
+            int known = -1;  // decisions of blocks <= known have been read
+            int nx = 0;
+            for (int j = 0; j < P.nb; ++j) {
+                const bool gat = gathered(j);
+                int32_t* ring = ring0 + (j & 1) * kBN;
+                if (gat)
+                    for (int u = 0; u < 2; ++u)
+                        if (lt + u * nthr < kBN) ring[lt + u * nthr] = tk[u];
+                fetch_tok(j + 1, tk);  // prefetch (latency overlaps the stage wait)
+                if (gat) named_bar_sync(gbar, nthr);
+                const uint32_t gi = gx + j;
+                const int st = gi % nst;
+                mbar_wait(smem_u32(&xempty[st]), ((gi / nst) & 1) ^ 1, kgrp ? 1002 : 1003);
+                if (kgrp && lt == 0) tl_mark(p, 9, gi);
+                // stage reuse certifies both slots' decisions on blocks <= j - lag
+                for (; known < j - lag;) {
+                    ++known;
+                    if (known >= P.ndmax)
+                        for (int x = 0; x < 2; ++x)
+                            if (participates(P, x, known) && stop_at[x] > known && c.dec[x][known & 3] == 2)
+                                stop_at[x] = known;
+                }
+                bool need = false;
+                for (int x = 0; x < 2; ++x) need |= participates(P, x, j) && !(stop_at[x] <= j - lag);
+                if (!need) break;
+                const uint32_t dst = xbase + st * kTileBytes;
+                if (!gat) {
+                    if (lt == 0) {
+                        mbar_expect_tx(smem_u32(&xfull[st]), kTileBytes);
+                        const int64_t tok = P.sb + (int64_t)j * kBN;
+                        for (int h = 0; h < 2; ++h)
+                            tma_load2d(dst + h * kHalf, xtile, h * 64, (int32_t)(xb + tok * xs), smem_u32(&xfull[st]));
+                    } else {
+                        mbar_arrive(smem_u32(&xfull[st]));
+                    }
+                } else {
+                    gather_tile(dst, xg + xb * kD, xs * kD, ring);
+                    cp_async_arrive_noinc(smem_u32(&xfull[st]));
+                }
+                if (kgrp && lt == 0) tl_mark(p, 10, gi);
+                ++nx;
+            }
+            gx += nx;
         }
     } else if (warp == kMmaWarp) {
         // ============================== MMA issuer ==============================
-        if (lane == 0) {
+        // Ping-pong order (per block j, per slot x): wait P_x(j) -> O_x += P_x V(j) -> S_x(j+1)
+        // = Q_x K(j+1)^T. The tensor pipe runs slot 1's PV/S while slot 0's softmax works and
+        // vice versa. S_x(j+1) overwrites P_x(j) only after the in-order pipe consumed it.
+        // Blocks loaded (must match the loader): K(j) iff need(j, 3), V(j) iff need(j, 2).
+        // The whole warp runs the control flow (warp-uniform values stay in uniform registers);
+        // one elected lane issues each tcgen05 instruction.
+        const bool leader = elect_one();
+        {
             const uint32_t idesc_s = umma_idesc_bf16(kBM, kBN, false, false);
             const uint32_t idesc_o = umma_idesc_bf16(kBM, kD, false, true);
-            uint32_t gblk = 0, qcount = 0;
-            uint32_t ns[2] = {0, 0};  // s_full / p_full phases per slot
+            uint32_t gk = 0, gv = 0, qcount = 0;
+            uint32_t ns[2] = {0, 0};  // p_full phases per slot
+            // descriptor address field is addr >> 4 in the low bits: desc(a + off) = desc(a) + off/16
+            const uint64_t dq0 = umma_desc_sw128(sQ, 16, 1024);
+            const uint64_t dk0 = umma_desc_sw128(sK, 16, 1024);
+            const uint64_t dv0 = umma_desc_sw128(sV, kHalf, 1024);
+            auto issue_s = [&](int x, int st) {
+                x = __shfl_sync(0xffffffffu, x, 0);  // warp-uniform: descriptors stay in uniform registers
+                st = __shfl_sync(0xffffffffu, st, 0);
+                const uint64_t dq = dq0 + ((x * kTileBytes) >> 4);
+                const uint64_t dk = dk0 + ((st * kTileBytes) >> 4);
+#pragma unroll
+                for (int kk = 0; kk < kD / 16; ++kk) {
+                    const uint32_t off = ((kk / 4) * kHalf + (kk % 4) * 32) >> 4;
+                    if (leader) umma_bf16(tbase + x * 256, dq + off, dk + off, idesc_s, kk > 0);
+                }
+                if (leader) umma_commit(smem_u32(&c.s_full[x]));
+            };
+            auto wait_k = [&](uint32_t gki) {
+                mbar_wait(smem_u32(&c.k_full[gki % kKStages]), (gki / kKStages) & 1, 2002);
+                tl_mark(p, 5, gki);
+                fence_proxy_async_smem();  // cp.async (generic proxy) writes -> UMMA reads
+                tc_fence_after();
+            };
             for (int64_t it = blockIdx.x; it < total; it += gridDim.x) {
                 const PairInfo P = pair_info(p, it);
                 if (P.nb == 0) continue;
                 mbar_wait(smem_u32(&c.q_full), qcount & 1, 2001);
                 ++qcount;
-                tc_fence_after();
                 int stop_at[2] = {1 << 30, 1 << 30};
-                int loaded = 0;
-                for (int j = 0; j < P.nb; ++j) {
-                    // same predicate as the loader: decisions on blocks <= j-2 are known there
-                    bool need = false;
-                    for (int x = 0; x < 2; ++x) need |= participates(P, x, j) && !(stop_at[x] <= j - 2);
-                    if (!need) break;
-                    ++loaded;
-                    const uint32_t gi = gblk + j;
-                    const int st = gi % kStages;
-                    const uint32_t ph = (gi / kStages) & 1;
-                    mbar_wait(smem_u32(&c.k_full[st]), ph, 2002);
-                    tc_fence_after();
-                    bool act[2];
-                    for (int x = 0; x < 2; ++x) act[x] = participates(P, x, j) && stop_at[x] > j - 1;
-                    const uint32_t kbase = sK + st * kTileBytes;
+                auto need = [&](int j, int lag) {
+                    bool n = false;
+                    for (int x = 0; x < 2; ++x) n |= participates(P, x, j) && !(stop_at[x] <= j - lag);
+                    return n;
+                };
+                wait_k(gk);
+                for (int x = 0; x < 2; ++x)
+                    if (participates(P, x, 0)) issue_s(x, gk % kKStages);
+                int nk = 0, nv = 0;
+                for (int j = 0;; ++j) {
+                    const uint32_t gki = gk + j, gvi = gv + j;
+                    const bool has_v = need(j, 2);
+                    const bool has_kn = (j + 1 < P.nb) && need(j + 1, 3);
+                    bool v_ready = false, kn_ready = false;
                     for (int x = 0; x < 2; ++x) {
-                        if (!act[x]) continue;
-                        const uint32_t qbase = sQ + x * kTileBytes;
-                        for (int kk = 0; kk < kD / 16; ++kk) {
-                            const uint32_t off = (kk / 4) * kHalf + (kk % 4) * 32;
-                            umma_bf16(tbase + x * 256, umma_desc_sw128(qbase + off, 16, 1024),
-                                      umma_desc_sw128(kbase + off, 16, 1024), idesc_s, kk > 0);
-                        }
-                        umma_commit(smem_u32(&c.s_full[x]));
-                    }
-                    bool v_ready = false;
-                    for (int x = 0; x < 2; ++x) {
-                        if (!act[x]) continue;
-                        mbar_wait(smem_u32(&c.p_full[x]), ns[x] & 1, 2004);
-                        ++ns[x];
-                        tc_fence_after();
-                        if (c.dec[x][j & 3] == 1) {
-                            if (!v_ready) {
-                                mbar_wait(smem_u32(&c.v_full[st]), ph, 2005);
-                                tc_fence_after();
-                                v_ready = true;
+                        if (participates(P, x, j) && stop_at[x] > j - 1) {
+                            mbar_wait(smem_u32(&c.p_full[x]), ns[x] & 1, 2004);
+                            tl_mark(p, 6 + x, gki);
+                            ++ns[x];
+                            tc_fence_after();
+                            const bool commit = j < P.ndmax || chunk_commit(c.red[x][j & 1]);
+                            __syncwarp();
+                            if (leader) c.dec[x][j & 3] = commit ? 1 : 2;  // for the loaders' stop tracking
+                            if (commit) {
+                                if (!v_ready) {
+                                    mbar_wait(smem_u32(&c.v_full[gvi % kVStages]), (gvi / kVStages) & 1, 2005);
+                                    fence_proxy_async_smem();
+                                    tc_fence_after();
+                                    v_ready = true;
+                                }
+                                const int vst = __shfl_sync(0xffffffffu, (int)(gvi % kVStages), 0);
+                                const int xu = __shfl_sync(0xffffffffu, x, 0);
+                                const uint64_t dv = dv0 + ((vst * kTileBytes) >> 4);
+#pragma unroll
+                                for (int kk = 0; kk < kBN / 16; ++kk)
+                                    if (leader)
+                                        umma_bf16_ts(tbase + xu * 256 + 128, tbase + xu * 256 + kk * 8,
+                                                     dv + ((kk * 16 * 128) >> 4), idesc_o, 1);
+                                if (leader && j == last_block(P, x)) umma_commit(smem_u32(&c.o_done[x]));
+                            } else {
+                                stop_at[x] = j;
+                                if (leader) umma_commit(smem_u32(&c.o_done[x]));  // slot finished
                             }
-                            const uint32_t vbase = sV + st * kTileBytes;
-                            for (int kk = 0; kk < kBN / 16; ++kk)
-                                umma_bf16_ts(tbase + x * 256 + 128, tbase + x * 256 + kk * 8,
-                                             umma_desc_sw128(vbase + kk * 16 * 128, kHalf, 1024), idesc_o, 1);
-                            if (j == last_block(P, x)) umma_commit(smem_u32(&c.o_done[x]));
-                        } else {
-                            stop_at[x] = j;
-                            umma_commit(smem_u32(&c.o_done[x]));  // slot finished
+                        }
+                        if (has_kn && participates(P, x, j + 1) && stop_at[x] > j) {
+                            if (!kn_ready) {
+                                wait_k(gki + 1);
+                                kn_ready = true;
+                            }
+                            issue_s(x, (gki + 1) % kKStages);
                         }
                     }
-                    if (!v_ready) mbar_wait(smem_u32(&c.v_full[st]), ph, 2006);  // consume the phase
-                    umma_commit(smem_u32(&c.kv_empty[st]));
+                    if (has_v && !v_ready) mbar_wait(smem_u32(&c.v_full[gvi % kVStages]), (gvi / kVStages) & 1, 2006);
+                    // both slots' decisions on block j are read: the loader may reuse its stages
+                    if (leader) {
+                        umma_commit(smem_u32(&c.k_empty[gki % kKStages]));
+                        if (has_v) umma_commit(smem_u32(&c.v_empty[gvi % kVStages]));
+                    }
+                    tl_mark(p, 8, gki);
+                    ++nk;
+                    nv += has_v ? 1 : 0;
+                    if (!has_kn) break;
+                    if (!kn_ready) wait_k(gki + 1);
                 }
-                umma_commit(smem_u32(&c.q_empty));
-                gblk += loaded;
+                if (leader) umma_commit(smem_u32(&c.q_empty));
+                gk += nk;
+                gv += nv;
             }
         }
         __syncwarp();
     } else {
         // ============================== softmax / epilogue (slot x) ==============================
+        setmaxnreg_inc<kSoftmaxRegs>();
         const int x = warp / 4;
         const int r = threadIdx.x % 128;  // TMEM lane
         const uint32_t lane_off = (uint32_t)((warp % 4) * 32) << 16;
         const uint32_t tS = tbase + lane_off + x * 256;
         const uint32_t tO = tS + 128;
         const uint32_t bar_id = 1 + x;
-        uint32_t ns = 0, no = 0;
+        const float sc = p.scale_log2;
+        uint32_t ns = 0, no = 0, npf = 0;
         for (int64_t it = blockIdx.x; it < total; it += gridDim.x) {
+            float m2, ell;
+            int committed = 0, pairs = 0;
+            bool any = false;
+            const bool tl_on = r == 0;
+            {
+            // 32-bit copies of what the block loop needs (keeps the 128 scores in registers)
             const PairInfo P = pair_info(p, it);
             if (!P.has[x]) continue;
+            if (tl_on) tl_mark(p, 11 + 4 * x, no);
+            const int nd_x = P.nd[x], ndmax = P.ndmax, nb = P.nb;
+            const int t0x = (int)P.t0[x], segr = (int)P.seg_rows, avail = (int)P.avail;
             const bool valid = r < P.tn[x];
-            const int64_t grow = q_row(a, P, x, r);
-            const int64_t slot = P.zh * g.l + grow;
-            float m2, ell;
+            const int64_t slot = P.zh * g.l + q_row(a, P, x, r);
             // ---- state init: O in TMEM, (m, ell) in registers
             if (a.mode & kStateIn) {
                 m2 = a.m_in[slot] * 1.4426950408889634f;
                 ell = a.ell_in[slot];
                 const float4* src = reinterpret_cast<const float4*>(a.acc_in + slot * kD);
+#pragma unroll
                 for (int c0 = 0; c0 < kD; c0 += 32) {
                     uint32_t v[32];
+#pragma unroll
                     for (int i = 0; i < 8; ++i) {
                         const float4 y = src[c0 / 4 + i];
                         v[4 * i] = __float_as_uint(y.x);
@@ -395,143 +512,179 @@ tc_pass_kernel(const TcParams p, const __grid_constant__ CUtensorMap qmap,
                 m2 = -INFINITY;
                 ell = 0.0f;
                 uint32_t z[32];
+#pragma unroll
                 for (int i = 0; i < 32; ++i) z[i] = 0u;
+#pragma unroll
                 for (int c0 = 0; c0 < kD; c0 += 32) tmem_st32(tO + c0, z);
             }
             tmem_st_wait();
             tc_fence_before();
+            if (tl_on) tl_mark(p, 12 + 4 * x, no);
 
-            int committed = 0;
-            int64_t pairs = 0;
-            bool any = false;
-            for (int j = 0; j < P.nb; ++j) {
-                if (!participates(P, x, j)) continue;
+            for (int j = 0; j < nb; ++j) {
+                if (j < ndmax && j >= nd_x) continue;  // !participates
                 any = true;
                 mbar_wait(smem_u32(&c.s_full[x]), ns & 1, 3001);
+                if (tl_on) tl_mark(p, 19 + 3 * x, ns);
                 ++ns;
                 tc_fence_after();
+                // ---- all 128 scores of this row in registers (one TMEM round trip)
+                uint32_t sv[kBN];
+#pragma unroll
+                for (int c0 = 0; c0 < kBN; c0 += 32) tmem_ld32(tS + c0, *reinterpret_cast<uint32_t(*)[32]>(&sv[c0]));
+                tmem_ld_wait();
+                if (tl_on) tl_mark(p, 25 + 3 * x, ns - 1);
                 // ---- visible keys of this block for this row
-                const bool is_diag = j < P.ndmax;
+                const bool is_diag = j < ndmax;
                 int lim;
                 if (is_diag) {
-                    const int64_t k0 = (int64_t)j * kBN;
-                    const int64_t kn = min((int64_t)kBN, P.seg_rows - k0);
-                    const int64_t vis = (k0 + kn - 1 <= P.t0[x]) ? kn : min(kn, P.t0[x] + r - k0 + 1);
-                    lim = (int)max((int64_t)0, vis);
+                    const int k0 = j * kBN;
+                    const int kn = min(kBN, segr - k0);
+                    const int vis = (k0 + kn - 1 <= t0x) ? kn : min(kn, t0x + r - k0 + 1);
+                    lim = max(0, vis);
                 } else {
-                    const int64_t c0 = (int64_t)(j - P.ndmax) * kBN;
-                    lim = (int)min((int64_t)kBN, P.avail - c0);
+                    lim = min(kBN, avail - (j - ndmax) * kBN);
                 }
-                // ---- pass 1: row max (S read from TMEM in 32-column chunks)
-                float mxa[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+                const bool full = __all_sync(0xffffffffu, lim >= kBN);
+                float mxa[8];
 #pragma unroll
-                for (int c0 = 0; c0 < kBN; c0 += 32) {
-                    uint32_t v[32];
-                    tmem_ld32(tS + c0, v);
-                    tmem_ld_wait();
+                for (int i = 0; i < 8; ++i) mxa[i] = -INFINITY;
+                if (full) {
 #pragma unroll
-                    for (int i = 0; i < 32; ++i) {
-                        const float sv = (c0 + i < lim) ? __uint_as_float(v[i]) : -INFINITY;
-                        mxa[i & 3] = fmaxf(mxa[i & 3], sv);
-                    }
+                    for (int i = 0; i < kBN; ++i) mxa[i & 7] = fmaxf(mxa[i & 7], __uint_as_float(sv[i]));
+                } else {
+#pragma unroll
+                    for (int i = 0; i < kBN; ++i)
+                        mxa[i & 7] = fmaxf(mxa[i & 7], i < lim ? __uint_as_float(sv[i]) : -INFINITY);
                 }
-                const float mx = fmaxf(fmaxf(mxa[0], mxa[1]), fmaxf(mxa[2], mxa[3])) * p.scale_log2;
+                const float mx = fmaxf(fmaxf(fmaxf(mxa[0], mxa[1]), fmaxf(mxa[2], mxa[3])),
+                                       fmaxf(fmaxf(mxa[4], mxa[5]), fmaxf(mxa[6], mxa[7]))) * sc;
                 const float m_new = fmaxf(m2, mx);
                 const bool rescale = (m_new > m2 + kRescaleThresh) || (m2 == -INFINITY);
                 const float m_use = rescale ? m_new : m2;
                 const float neg_ref = (m_use == -INFINITY) ? 0.0f : -m_use;
                 const float alpha = (m2 == -INFINITY) ? 0.0f : ex2(m2 + neg_ref);
-                // O rescale (P V of the previous block is complete: s_full orders after it)
+                if (tl_on) tl_mark(p, 26 + 3 * x, ns - 1);
+                // ---- P = exp2(s*scale - m) in bf16 over the first 64 S columns; on full blocks a
+                // quarter of the exponentials run on the FMA pipe (MUFU and FMA in parallel)
+                if (tl_on) tl_mark(p, 27 + 3 * x, ns - 1);
+                float rs[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+                if (full) {
+#pragma unroll
+                    for (int c0 = 0; c0 < kBN; c0 += 32) {
+                        uint32_t pk[16];
+#pragma unroll
+                        for (int i = 0; i < 32; i += 2) {
+                            const float x0 = fmaf(__uint_as_float(sv[c0 + i]), sc, neg_ref);
+                            const float x1 = fmaf(__uint_as_float(sv[c0 + i + 1]), sc, neg_ref);
+                            const float e0 = (i >= 24) ? ex2_poly(x0) : ex2(x0);
+                            const float e1 = (i >= 24) ? ex2_poly(x1) : ex2(x1);
+                            rs[(i >> 1) & 3] += e0 + e1;
+                            pk[i >> 1] = pack_bf16(e0, e1);
+                        }
+                        tmem_st16(tS + c0 / 2, pk);
+                    }
+                } else {
+#pragma unroll
+                    for (int c0 = 0; c0 < kBN; c0 += 32) {
+                        uint32_t pk[16];
+#pragma unroll
+                        for (int i = 0; i < 32; i += 2) {
+                            const float e0 = c0 + i < lim ? ex2(fmaf(__uint_as_float(sv[c0 + i]), sc, neg_ref)) : 0.0f;
+                            const float e1 = c0 + i + 1 < lim ? ex2(fmaf(__uint_as_float(sv[c0 + i + 1]), sc, neg_ref)) : 0.0f;
+                            rs[(i >> 1) & 3] += e0 + e1;
+                            pk[i >> 1] = pack_bf16(e0, e1);
+                        }
+                        tmem_st16(tS + c0 / 2, pk);
+                    }
+                }
+                const float rowsum = (rs[0] + rs[1]) + (rs[2] + rs[3]);
+                // O rescale after the scores are dead (P V(j-1) is complete: s_full orders after it;
+                // P V(j) is issued only after p_full)
                 if (__any_sync(0xffffffffu, rescale && m2 != -INFINITY)) {
+#pragma unroll
                     for (int c0 = 0; c0 < kD; c0 += 32) {
                         uint32_t v[32];
                         tmem_ld32(tO + c0, v);
                         tmem_ld_wait();
+#pragma unroll
                         for (int i = 0; i < 32; ++i) v[i] = __float_as_uint(__uint_as_float(v[i]) * alpha);
                         tmem_st32(tO + c0, v);
                     }
                 }
-                // ---- pass 2: P = exp2(s*scale - m) -> bf16 pairs over the first 64 S columns
-                float rs[4] = {0.0f, 0.0f, 0.0f, 0.0f};
-#pragma unroll
-                for (int c0 = 0; c0 < kBN; c0 += 32) {
-                    uint32_t v[32];
-                    tmem_ld32(tS + c0, v);
-                    tmem_ld_wait();
-                    uint32_t pk[16];
-#pragma unroll
-                    for (int i = 0; i < 32; i += 2) {
-                        const float e0 = (c0 + i < lim) ? ex2(fmaf(__uint_as_float(v[i]), p.scale_log2, neg_ref)) : 0.0f;
-                        const float e1 = (c0 + i + 1 < lim) ? ex2(fmaf(__uint_as_float(v[i + 1]), p.scale_log2, neg_ref)) : 0.0f;
-                        rs[(i >> 1) & 3] += e0 + e1;
-                        pk[i >> 1] = pack_bf16(e0, e1);
-                    }
-                    tmem_st16(tS + c0 / 2, pk);
+                if (tl_on) tl_mark(p, 20 + 3 * x, ns - 1);
+                // relative normaliser gain of this chunk (kernel.cpp:108-115): per-warp max into
+                // red[] (double-buffered by block parity), then one arrive per warp on p_full; the
+                // MMA issuer and these warps both take the decision from the four warp maxima
+                // (gain >= tau  <=>  rowsum >= tau * prev; NaN rows never vote to continue)
+                if (!is_diag) {
+                    const bool cont = valid && (rowsum >= (float)a.tau * (ell * alpha));
+                    const unsigned vote = __ballot_sync(0xffffffffu, cont);
+                    if (lane == 0) c.red[x][j & 1][warp % 4] = vote != 0u;
                 }
-                const float rowsum = (rs[0] + rs[1]) + (rs[2] + rs[3]);
+                tmem_st_wait();
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(smem_u32(&c.p_full[x]));
                 bool commit = true;
                 if (!is_diag) {
-                    // relative normaliser gain of this chunk (kernel.cpp:108-115)
-                    const float prev = ell * alpha;
-                    float gain = valid ? rowsum / prev : -INFINITY;
-                    for (int o = 16; o > 0; o >>= 1) gain = fmaxf(gain, __shfl_xor_sync(0xffffffffu, gain, o));
-                    if (lane == 0) c.red[x][warp % 4] = gain;
-                    named_bar_sync(bar_id, 128);
-                    const float mg = fmaxf(fmaxf(c.red[x][0], c.red[x][1]), fmaxf(c.red[x][2], c.red[x][3]));
-                    commit = !(mg < (float)a.tau);
-                    named_bar_sync(bar_id, 128);  // red[] reusable
+                    mbar_wait(smem_u32(&c.p_full[x]), npf & 1, 3002);
+                    commit = chunk_commit(c.red[x][j & 1]);
                 }
+                ++npf;
                 // state update (on a stop the rescaled state is the same state: O/ell unchanged)
                 ell = commit ? ell * alpha + rowsum : ell * alpha;
                 m2 = m_use;
                 if (commit && !is_diag) {
                     ++committed;
-                    const int64_t c0 = (int64_t)(j - P.ndmax) * kBN;
-                    pairs += min((int64_t)kBN, P.avail - c0);
+                    pairs += min(kBN, avail - (j - ndmax) * kBN);
                 }
-                tmem_st_wait();
-                tc_fence_before();
-                if (r == 0) c.dec[x][j & 3] = commit ? 1 : 2;
-                __syncwarp();
-                if (lane == 0) mbar_arrive(smem_u32(&c.p_full[x]));
+                if (tl_on) tl_mark(p, 21 + 3 * x, ns - 1);
                 if (!commit) break;
             }
+            }  // block loop scope
+            const PairInfo P = pair_info(p, it);
+            const bool valid = r < P.tn[x];
+            const int64_t grow = q_row(a, P, x, r);
+            const int64_t slot = P.zh * g.l + grow;
             if (any) {
                 mbar_wait(smem_u32(&c.o_done[x]), no & 1, 3004);
                 ++no;
                 tc_fence_after();
             }
+            if (tl_on) tl_mark(p, 13 + 4 * x, no);
             // ---- read O, finalize / persist
+            uint32_t ov[kD];
+#pragma unroll
+            for (int c0 = 0; c0 < kD; c0 += 32) tmem_ld32(tO + c0, *reinterpret_cast<uint32_t(*)[32]>(&ov[c0]));
+            tmem_ld_wait();
             const float inv = 1.0f / ell;
-            for (int c0 = 0; c0 < kD; c0 += 32) {
-                uint32_t v[32];
-                tmem_ld32(tO + c0, v);
-                tmem_ld_wait();
-                if (!valid) continue;
-                if (a.mode & kStateOut) {
-                    float4* dst = reinterpret_cast<float4*>(a.acc_out + slot * kD + c0);
-                    for (int i = 0; i < 8; ++i)
-                        dst[i] = make_float4(__uint_as_float(v[4 * i]), __uint_as_float(v[4 * i + 1]),
-                                             __uint_as_float(v[4 * i + 2]), __uint_as_float(v[4 * i + 3]));
-                }
-                if (a.mode & kFinal) {
-                    const int64_t ooff = g.o_base(P.zh) + grow * g.os[2] + c0;
-                    if (g.out_bf16) {
-                        uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(a.o) + ooff);
-                        for (int i = 0; i < 4; ++i) {
-                            uint4 w;
-                            w.x = pack_bf16(__uint_as_float(v[8 * i]) * inv, __uint_as_float(v[8 * i + 1]) * inv);
-                            w.y = pack_bf16(__uint_as_float(v[8 * i + 2]) * inv, __uint_as_float(v[8 * i + 3]) * inv);
-                            w.z = pack_bf16(__uint_as_float(v[8 * i + 4]) * inv, __uint_as_float(v[8 * i + 5]) * inv);
-                            w.w = pack_bf16(__uint_as_float(v[8 * i + 6]) * inv, __uint_as_float(v[8 * i + 7]) * inv);
-                            dst[i] = w;
-                        }
-                    } else {
-                        float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(a.o) + ooff);
-                        for (int i = 0; i < 8; ++i)
-                            dst[i] = make_float4(__uint_as_float(v[4 * i]) * inv, __uint_as_float(v[4 * i + 1]) * inv,
-                                                 __uint_as_float(v[4 * i + 2]) * inv, __uint_as_float(v[4 * i + 3]) * inv);
+            if (valid && (a.mode & kStateOut)) {
+                float4* dst = reinterpret_cast<float4*>(a.acc_out + slot * kD);
+#pragma unroll
+                for (int i = 0; i < kD / 4; ++i)
+                    dst[i] = make_float4(__uint_as_float(ov[4 * i]), __uint_as_float(ov[4 * i + 1]),
+                                         __uint_as_float(ov[4 * i + 2]), __uint_as_float(ov[4 * i + 3]));
+            }
+            if (valid && (a.mode & kFinal)) {
+                const int64_t ooff = g.o_base(P.zh) + grow * g.os[2];
+                if (g.out_bf16) {
+                    uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(a.o) + ooff);
+#pragma unroll
+                    for (int i = 0; i < kD / 8; ++i) {
+                        uint4 w;
+                        w.x = pack_bf16(__uint_as_float(ov[8 * i]) * inv, __uint_as_float(ov[8 * i + 1]) * inv);
+                        w.y = pack_bf16(__uint_as_float(ov[8 * i + 2]) * inv, __uint_as_float(ov[8 * i + 3]) * inv);
+                        w.z = pack_bf16(__uint_as_float(ov[8 * i + 4]) * inv, __uint_as_float(ov[8 * i + 5]) * inv);
+                        w.w = pack_bf16(__uint_as_float(ov[8 * i + 6]) * inv, __uint_as_float(ov[8 * i + 7]) * inv);
+                        dst[i] = w;
                     }
+                } else {
+                    float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(a.o) + ooff);
+#pragma unroll
+                    for (int i = 0; i < kD / 4; ++i)
+                        dst[i] = make_float4(__uint_as_float(ov[4 * i]) * inv, __uint_as_float(ov[4 * i + 1]) * inv,
+                                             __uint_as_float(ov[4 * i + 2]) * inv, __uint_as_float(ov[4 * i + 3]) * inv);
                 }
             }
             if (valid && (a.mode & kStateOut)) {
@@ -548,9 +701,10 @@ tc_pass_kernel(const TcParams p, const __grid_constant__ CUtensorMap qmap,
                     a.ovf_tiles[s2] = (int32_t)tile;
                 } else {
                     a.processed[(P.zh * g.N + P.n) * a.T + P.ti[x]] = committed;
-                    if (pairs) atomicAdd((unsigned long long*)&a.pass2_pairs[P.zh], (unsigned long long)(pairs * P.tn[x]));
+                    if (pairs) atomicAdd((unsigned long long*)&a.pass2_pairs[P.zh], (unsigned long long)pairs * P.tn[x]);
                 }
             }
+            if (tl_on) tl_mark(p, 14 + 4 * x, no);
             tc_fence_before();
             named_bar_sync(bar_id, 128);  // all rows done with O before the next pair's init
         }
@@ -592,6 +746,8 @@ int64_t span_rows(const int64_t* st, int64_t z, int64_t h, int64_t l) {
     return ((z - 1) * st[0] + (h - 1) * st[1] + (l - 1) * st[2]) / kD + 1;
 }
 
+unsigned long long* g_timeline = nullptr;
+
 bool strides_ok(const int64_t* st) { return st[0] % kD == 0 && st[1] % kD == 0 && st[2] % kD == 0; }
 
 }  // namespace
@@ -624,6 +780,7 @@ cudaError_t launch_tc_pass(const PassArgs& a, cudaStream_t st) {
     p.q_contig = g.qs[2] == kD;
     p.kv_contig = g.ks[2] == kD && g.vs[2] == kD;
     p.pairs_full = (a.T + 1) / 2;
+    p.tl = g_timeline;
     const int64_t t_last = (g.last_len + kBM - 1) / kBM;
     p.pairs_per_head = (g.N - 1) * p.pairs_full + (t_last + 1) / 2;
     static bool attr_done = false;
@@ -643,3 +800,9 @@ cudaError_t launch_tc_pass(const PassArgs& a, cudaStream_t st) {
 }
 
 }  // namespace s2o
+
+// Profiling aid (not part of the operator ABI): record clock64() pipeline events of CTA 0 of
+// subsequent tcgen05 pass launches into a device buffer of 32 * 1024 uint64 (nullptr = off).
+extern "C" void s2o_debug_timeline(void* dev_buf) {
+    s2o::g_timeline = reinterpret_cast<unsigned long long*>(dev_buf);
+}

@@ -51,6 +51,17 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity, int tag
     }
 }
 
+// One lane of the (converged) warp returns true.
+__device__ __forceinline__ bool elect_one() {
+    uint32_t pred;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "elect.sync _|p, 0xffffffff;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(pred));
+    return pred != 0;
+}
+
 // ------------------------------------------------------------------ fences / barriers
 __device__ __forceinline__ void fence_proxy_async_smem() {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -207,6 +218,32 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
     uint32_t r;
     asm("cvt.rn.bf16x2.f32 %0, %2, %1;" : "=r"(r) : "f"(lo), "f"(hi));
     return r;
+}
+
+// Warpgroup register reallocation (all 4 warps of a warpgroup execute it).
+template <int N>
+__device__ __forceinline__ void setmaxnreg_inc() {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(N));
+}
+template <int N>
+__device__ __forceinline__ void setmaxnreg_dec() {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(N));
+}
+
+// 2^x on the FMA pipe (offloads MUFU): round-to-nearest split x = j + f, f in [-0.5, 0.5],
+// degree-5 fit of 2^f (max rel. error 2.5e-7 in fp32, same order as ex2.approx), exponent
+// added as an integer. x is clamped to >= -126 (result >= 2^-126.5 instead of a denormal).
+__device__ __forceinline__ float ex2_poly(float x) {
+    const float xc = fmaxf(x, -126.0f);
+    const float t = xc + 12582912.0f;  // 1.5 * 2^23: low mantissa bits hold round(xc)
+    const float f = xc - (t - 12582912.0f);
+    float p = 1.3277226826176047e-3f;
+    p = fmaf(p, f, 9.675547480583191e-3f);
+    p = fmaf(p, f, 5.55071085691452e-2f);
+    p = fmaf(p, f, 2.4022120237350464e-1f);
+    p = fmaf(p, f, 6.931469440460205e-1f);
+    p = fmaf(p, f, 1.0000001192092896f);
+    return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
 }
 
 __device__ __forceinline__ float ex2(float x) {
