@@ -14,8 +14,10 @@ import sys
 
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
-CSRC = os.path.join(PKG, "csrc")
-LIB_DIR = os.path.join(PKG, "lib")
+# S2O_VARIANT_DIR (dev A/B aid): build csrc/ found there into <dir>/lib instead of the package's
+_VARIANT = os.environ.get("S2O_VARIANT_DIR")
+CSRC = os.path.join(_VARIANT, "csrc") if _VARIANT else os.path.join(PKG, "csrc")
+LIB_DIR = os.path.join(_VARIANT, "lib") if _VARIANT else os.path.join(PKG, "lib")
 LIB = os.path.join(LIB_DIR, "libs2o_cuda.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

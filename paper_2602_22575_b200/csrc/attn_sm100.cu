@@ -64,8 +64,8 @@ constexpr uint32_t kOffQ = 0;               // slot X at X * kTileBytes
 constexpr uint32_t kOffK = 2 * kTileBytes;
 constexpr uint32_t kOffV = kOffK + kKStages * kTileBytes;
 constexpr uint32_t kOffCtrl = kOffV + kVStages * kTileBytes;
-constexpr uint32_t kOffTok = kOffCtrl + 256;  // token rings: K group int32 [2][128], V group [2][128]
-constexpr uint32_t kSmemBytes = kOffTok + 2048;  // 226.25 KB (base must be 1024-B aligned)
+constexpr uint32_t kOffTok = kOffCtrl + 256;  // token rings: K group int32 [2][128], V group [2][144]
+constexpr uint32_t kSmemBytes = kOffTok + 2304;  // 226.5 KB (base must be 1024-B aligned)
 constexpr uint32_t kTmemCols = 512;
 constexpr int kSoftmaxRegs = 192;   // setmaxnreg: softmax warpgroups (0, 1)
 constexpr int kOtherRegs = 64;      // MMA + loader warpgroups (2, 3)
@@ -100,6 +100,39 @@ __device__ __forceinline__ void tl_mark(const TcParams& p, int ev, uint32_t seq)
     if (p.tl != nullptr && blockIdx.x == 0 && seq < (uint32_t)kTlCap)
         p.tl[ev * kTlCap + seq] = clock64();
 #endif
+}
+
+// Token rings: the loader thread owning rows r0, r0 + STEP, ... reads its tokens as int4 vectors,
+// so a ring stores row `row` at (row % STEP) * rows_per_thread + row / STEP.
+template <int STEP>
+struct TokRing {
+    static constexpr int kRpt = ((kBM + STEP - 1) / STEP + 3) / 4 * 4;  // rows per thread, padded
+    static constexpr int kSize = STEP * kRpt;                           // ints per block
+    __device__ static int pos(int row) { return (row % STEP) * kRpt + row / STEP; }
+};
+
+// cp.async of one 16-B column chunk `ch` of rows r0, r0 + STEP, ... (< 128) of a 128-row tile into
+// the SWIZZLE_128B layout; byte offset tok * rbytes from bch.
+template <int STEP>
+__device__ __forceinline__ void gather_rows(uint32_t dst, const char* bch, uint32_t rbytes, const int32_t* ring,
+                                            int r0, uint32_t ch) {
+    using R = TokRing<STEP>;
+    const uint32_t xr = ch & 7u;
+    const int4* tv = reinterpret_cast<const int4*>(ring + r0 * R::kRpt);
+#pragma unroll
+    for (int q = 0; q < R::kRpt / 4; ++q) {
+        const int4 t4 = tv[q];
+        const int tt[4] = {t4.x, t4.y, t4.z, t4.w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const int i = 4 * q + e;
+            const int row = r0 + STEP * i;
+            if (STEP * (i + 1) <= kBM || row < kBM) {
+                const char* src = bch + (uint64_t)(uint32_t)tt[e] * rbytes;
+                sm100::cp_async16(dst + row * 128 + ((xr ^ ((uint32_t)row & 7u)) << 4), src, 16);
+            }
+        }
+    }
 }
 
 // Early-stop decision from the four per-warp votes (early_stop_check kernel.cpp:220-234: stop iff
@@ -242,15 +275,17 @@ tc_pass_kernel(const TcParams p, const __grid_constant__ CUtensorMap qmap,
         const int nthr = kgrp ? kKThreads : kVThreads;
         const int lt = (warp - (kgrp ? kKWarp0 : kVWarp0)) * 32 + lane;
         const uint32_t gbar = kgrp ? 3 : 4;
-        int32_t* ring0 = reinterpret_cast<int32_t*>(smem + kOffTok) + (kgrp ? 0 : 2 * kBN);
-        const int rstep = nthr / 16;                 // rows between a thread's chunks
-        const int ch = lt & 15, r0 = lt >> 4;
+        constexpr int kKStep = kKThreads / 16, kVStep = kVThreads / 16;
+        const int ring_sz = kgrp ? TokRing<kKStep>::kSize : TokRing<kVStep>::kSize;
+        int32_t* ring0 = reinterpret_cast<int32_t*>(smem + kOffTok) + (kgrp ? 0 : 2 * TokRing<kKStep>::kSize);
+        auto ring_pos = [&](int row) { return kgrp ? TokRing<kKStep>::pos(row) : TokRing<kVStep>::pos(row); };
+        const int ch = lt & 15, r0 = lt >> 4;  // rows r0, r0 + nthr/16, ...
         const uint32_t ch_off = (uint32_t)(ch >> 3) * kHalf;
         auto gather_tile = [&](uint32_t dst, const __nv_bfloat16* base, int64_t rstride, const int32_t* tok) {
-            for (int row = r0; row < kBM; row += rstep) {
-                const __nv_bfloat16* src = base + (int64_t)tok[row] * rstride + ch * 8;
-                cp_async16(dst + ch_off + row * 128 + ((((uint32_t)ch & 7u) ^ ((uint32_t)row & 7u)) << 4), src, 16);
-            }
+            const char* bch = reinterpret_cast<const char*>(base) + ch * 16;
+            const uint32_t rbytes = (uint32_t)(rstride * 2);
+            if (kgrp) gather_rows<kKStep>(dst + ch_off, bch, rbytes, tok, r0, (uint32_t)ch);
+            else gather_rows<kVStep>(dst + ch_off, bch, rbytes, tok, r0, (uint32_t)ch);
         };
         const __nv_bfloat16* qg = reinterpret_cast<const __nv_bfloat16*>(a.q);
         const __nv_bfloat16* xg = reinterpret_cast<const __nv_bfloat16*>(kgrp ? a.k : a.v);
@@ -266,6 +301,7 @@ tc_pass_kernel(const TcParams p, const __grid_constant__ CUtensorMap qmap,
             if (P.nb == 0) continue;
             const int32_t* kv = (P.np > 0) ? a.kv_seg(P.zh, P.n) : nullptr;
             named_bar_sync(gbar, nthr);  // every thread of the group is done with its ring
+            if (kgrp && lt == 0) tl_mark(p, 30, qcount);
             if (kgrp) {
                 // ---- Q (both slots)
                 mbar_wait(smem_u32(&c.q_empty), (qcount & 1) ^ 1, 1001);
@@ -286,7 +322,7 @@ tc_pass_kernel(const TcParams p, const __grid_constant__ CUtensorMap qmap,
                 } else {
                     for (int e = lt; e < 2 * kBM; e += nthr) {
                         const int x = e >> 7;
-                        ring0[e] = P.has[x] ? (int32_t)(qb + q_row(a, P, x, e & 127) * qs) : 0;
+                        ring0[x * kBM + ring_pos(e & 127)] = P.has[x] ? (int32_t)(qb + q_row(a, P, x, e & 127) * qs) : 0;
                     }
                     named_bar_sync(gbar, nthr);
                     for (int x = 0; x < 2; ++x)
@@ -294,6 +330,7 @@ tc_pass_kernel(const TcParams p, const __grid_constant__ CUtensorMap qmap,
                     cp_async_arrive_noinc(smem_u32(&c.q_full));
                     named_bar_sync(gbar, nthr);  // ring reusable
                 }
+                if (lt == 0) tl_mark(p, 29, qcount);
                 ++qcount;
             }
             const int64_t xb = (kgrp ? g.k_base(P.zh) : g.v_base(P.zh)) / rowu;
@@ -313,10 +350,10 @@ tc_pass_kernel(const TcParams p, const __grid_constant__ CUtensorMap qmap,
             int nx = 0;
             for (int j = 0; j < P.nb; ++j) {
                 const bool gat = gathered(j);
-                int32_t* ring = ring0 + (j & 1) * kBN;
+                int32_t* ring = ring0 + (j & 1) * ring_sz;
                 if (gat)
                     for (int u = 0; u < 2; ++u)
-                        if (lt + u * nthr < kBN) ring[lt + u * nthr] = tk[u];
+                        if (lt + u * nthr < kBN) ring[ring_pos(lt + u * nthr)] = tk[u];
                 fetch_tok(j + 1, tk);  // prefetch (latency overlaps the stage wait)
                 if (gat) named_bar_sync(gbar, nthr);
                 const uint32_t gi = gx + j;
@@ -393,8 +430,10 @@ tc_pass_kernel(const TcParams p, const __grid_constant__ CUtensorMap qmap,
                 const PairInfo P = pair_info(p, it);
                 if (P.nb == 0) continue;
                 mbar_wait(smem_u32(&c.q_full), qcount & 1, 2001);
+                tl_mark(p, 26, qcount);
                 ++qcount;
                 int stop_at[2] = {1 << 30, 1 << 30};
+                bool pv_any[2] = {false, false};  // first P V of a slot overwrites O (accumulate = 0)
                 auto need = [&](int j, int lag) {
                     bool n = false;
                     for (int x = 0; x < 2; ++x) n |= participates(P, x, j) && !(stop_at[x] <= j - lag);
@@ -403,6 +442,7 @@ tc_pass_kernel(const TcParams p, const __grid_constant__ CUtensorMap qmap,
                 wait_k(gk);
                 for (int x = 0; x < 2; ++x)
                     if (participates(P, x, 0)) issue_s(x, gk % kKStages);
+                tl_mark(p, 27, qcount - 1);
                 int nk = 0, nv = 0;
                 for (int j = 0;; ++j) {
                     const uint32_t gki = gk + j, gvi = gv + j;
@@ -421,6 +461,7 @@ tc_pass_kernel(const TcParams p, const __grid_constant__ CUtensorMap qmap,
                             if (commit) {
                                 if (!v_ready) {
                                     mbar_wait(smem_u32(&c.v_full[gvi % kVStages]), (gvi / kVStages) & 1, 2005);
+                                    tl_mark(p, 28, gki);
                                     fence_proxy_async_smem();
                                     tc_fence_after();
                                     v_ready = true;
@@ -432,7 +473,8 @@ tc_pass_kernel(const TcParams p, const __grid_constant__ CUtensorMap qmap,
                                 for (int kk = 0; kk < kBN / 16; ++kk)
                                     if (leader)
                                         umma_bf16_ts(tbase + xu * 256 + 128, tbase + xu * 256 + kk * 8,
-                                                     dv + ((kk * 16 * 128) >> 4), idesc_o, 1);
+                                                     dv + ((kk * 16 * 128) >> 4), idesc_o, (kk > 0 || pv_any[x]) ? 1 : 0);
+                                pv_any[x] = true;
                                 if (leader && j == last_block(P, x)) umma_commit(smem_u32(&c.o_done[x]));
                             } else {
                                 stop_at[x] = j;
@@ -478,6 +520,8 @@ tc_pass_kernel(const TcParams p, const __grid_constant__ CUtensorMap qmap,
         uint32_t ns = 0, no = 0, npf = 0;
         for (int64_t it = blockIdx.x; it < total; it += gridDim.x) {
             float m2, ell;
+            float sacc = 1.0f;    // scale of the resumed accumulator (kStateIn)
+            bool pv_any = false;  // a P V has been issued into O_x for this pair
             int committed = 0, pairs = 0;
             bool any = false;
             const bool tl_on = r == 0;
@@ -490,35 +534,20 @@ tc_pass_kernel(const TcParams p, const __grid_constant__ CUtensorMap qmap,
             const int t0x = (int)P.t0[x], segr = (int)P.seg_rows, avail = (int)P.avail;
             const bool valid = r < P.tn[x];
             const int64_t slot = P.zh * g.l + q_row(a, P, x, r);
-            // ---- state init: O in TMEM, (m, ell) in registers
+            // ---- state init: (m, ell) in registers. O in TMEM starts from the first P V (issued
+            // with accumulate = 0); a resumed pass-1 accumulator is added in the epilogue with the
+            // product of the rescale factors applied since (sacc), so its HBM read is off the
+            // critical path (L2 prefetch now, load at the end).
             if (a.mode & kStateIn) {
                 m2 = a.m_in[slot] * 1.4426950408889634f;
                 ell = a.ell_in[slot];
-                const float4* src = reinterpret_cast<const float4*>(a.acc_in + slot * kD);
+                const char* arow = reinterpret_cast<const char*>(a.acc_in + slot * kD);
 #pragma unroll
-                for (int c0 = 0; c0 < kD; c0 += 32) {
-                    uint32_t v[32];
-#pragma unroll
-                    for (int i = 0; i < 8; ++i) {
-                        const float4 y = src[c0 / 4 + i];
-                        v[4 * i] = __float_as_uint(y.x);
-                        v[4 * i + 1] = __float_as_uint(y.y);
-                        v[4 * i + 2] = __float_as_uint(y.z);
-                        v[4 * i + 3] = __float_as_uint(y.w);
-                    }
-                    tmem_st32(tO + c0, v);
-                }
+                for (int i = 0; i < 4; ++i) asm volatile("prefetch.global.L2 [%0];" ::"l"(arow + 128 * i));
             } else {
                 m2 = -INFINITY;
                 ell = 0.0f;
-                uint32_t z[32];
-#pragma unroll
-                for (int i = 0; i < 32; ++i) z[i] = 0u;
-#pragma unroll
-                for (int c0 = 0; c0 < kD; c0 += 32) tmem_st32(tO + c0, z);
             }
-            tmem_st_wait();
-            tc_fence_before();
             if (tl_on) tl_mark(p, 12 + 4 * x, no);
 
             for (int j = 0; j < nb; ++j) {
@@ -533,7 +562,7 @@ tc_pass_kernel(const TcParams p, const __grid_constant__ CUtensorMap qmap,
 #pragma unroll
                 for (int c0 = 0; c0 < kBN; c0 += 32) tmem_ld32(tS + c0, *reinterpret_cast<uint32_t(*)[32]>(&sv[c0]));
                 tmem_ld_wait();
-                if (tl_on) tl_mark(p, 25 + 3 * x, ns - 1);
+                if (tl_on && x == 0) tl_mark(p, 25, ns - 1);
                 // ---- visible keys of this block for this row
                 const bool is_diag = j < ndmax;
                 int lim;
@@ -546,62 +575,64 @@ tc_pass_kernel(const TcParams p, const __grid_constant__ CUtensorMap qmap,
                     lim = min(kBN, avail - (j - ndmax) * kBN);
                 }
                 const bool full = __all_sync(0xffffffffu, lim >= kBN);
-                float mxa[8];
-#pragma unroll
-                for (int i = 0; i < 8; ++i) mxa[i] = -INFINITY;
-                if (full) {
-#pragma unroll
-                    for (int i = 0; i < kBN; ++i) mxa[i & 7] = fmaxf(mxa[i & 7], __uint_as_float(sv[i]));
-                } else {
-#pragma unroll
-                    for (int i = 0; i < kBN; ++i)
-                        mxa[i & 7] = fmaxf(mxa[i & 7], i < lim ? __uint_as_float(sv[i]) : -INFINITY);
-                }
-                const float mx = fmaxf(fmaxf(fmaxf(mxa[0], mxa[1]), fmaxf(mxa[2], mxa[3])),
-                                       fmaxf(fmaxf(mxa[4], mxa[5]), fmaxf(mxa[6], mxa[7]))) * sc;
-                const float m_new = fmaxf(m2, mx);
-                const bool rescale = (m_new > m2 + kRescaleThresh) || (m2 == -INFINITY);
-                const float m_use = rescale ? m_new : m2;
-                const float neg_ref = (m_use == -INFINITY) ? 0.0f : -m_use;
-                const float alpha = (m2 == -INFINITY) ? 0.0f : ex2(m2 + neg_ref);
-                if (tl_on) tl_mark(p, 26 + 3 * x, ns - 1);
-                // ---- P = exp2(s*scale - m) in bf16 over the first 64 S columns; on full blocks a
-                // quarter of the exponentials run on the FMA pipe (MUFU and FMA in parallel)
-                if (tl_on) tl_mark(p, 27 + 3 * x, ns - 1);
+                float m_use, alpha;
+                bool rescale;
                 float rs[4] = {0.0f, 0.0f, 0.0f, 0.0f};
-                if (full) {
+                {
+                    float mxa[8];
 #pragma unroll
-                    for (int c0 = 0; c0 < kBN; c0 += 32) {
-                        uint32_t pk[16];
+                    for (int i = 0; i < 8; ++i) mxa[i] = -INFINITY;
+                    if (full) {
 #pragma unroll
-                        for (int i = 0; i < 32; i += 2) {
-                            const float x0 = fmaf(__uint_as_float(sv[c0 + i]), sc, neg_ref);
-                            const float x1 = fmaf(__uint_as_float(sv[c0 + i + 1]), sc, neg_ref);
-                            const float e0 = (i >= 24) ? ex2_poly(x0) : ex2(x0);
-                            const float e1 = (i >= 24) ? ex2_poly(x1) : ex2(x1);
-                            rs[(i >> 1) & 3] += e0 + e1;
-                            pk[i >> 1] = pack_bf16(e0, e1);
-                        }
-                        tmem_st16(tS + c0 / 2, pk);
+                        for (int i = 0; i < kBN; ++i) mxa[i & 7] = fmaxf(mxa[i & 7], __uint_as_float(sv[i]));
+                    } else {
+#pragma unroll
+                        for (int i = 0; i < kBN; ++i)
+                            mxa[i & 7] = fmaxf(mxa[i & 7], i < lim ? __uint_as_float(sv[i]) : -INFINITY);
                     }
-                } else {
+                    const float mx = fmaxf(fmaxf(fmaxf(mxa[0], mxa[1]), fmaxf(mxa[2], mxa[3])),
+                                           fmaxf(fmaxf(mxa[4], mxa[5]), fmaxf(mxa[6], mxa[7]))) * sc;
+                    const float m_new = fmaxf(m2, mx);
+                    rescale = (m_new > m2 + kRescaleThresh) || (m2 == -INFINITY);
+                    m_use = rescale ? m_new : m2;
+                    const float neg_ref = (m_use == -INFINITY) ? 0.0f : -m_use;
+                    alpha = (m2 == -INFINITY) ? 0.0f : ex2(m2 + neg_ref);
+                    // P = exp2(s*scale - m) in bf16 over the first 64 S columns. (All on MUFU: an
+                    // FMA-pipe polynomial for part of the row measured slower -- the softmax is
+                    // latency- not MUFU-throughput-bound here, profiles/r01_summary.md.)
+                    if (full) {
 #pragma unroll
-                    for (int c0 = 0; c0 < kBN; c0 += 32) {
-                        uint32_t pk[16];
+                        for (int c0 = 0; c0 < kBN; c0 += 32) {
+                            uint32_t pk[16];
 #pragma unroll
-                        for (int i = 0; i < 32; i += 2) {
-                            const float e0 = c0 + i < lim ? ex2(fmaf(__uint_as_float(sv[c0 + i]), sc, neg_ref)) : 0.0f;
-                            const float e1 = c0 + i + 1 < lim ? ex2(fmaf(__uint_as_float(sv[c0 + i + 1]), sc, neg_ref)) : 0.0f;
-                            rs[(i >> 1) & 3] += e0 + e1;
-                            pk[i >> 1] = pack_bf16(e0, e1);
+                            for (int i = 0; i < 32; i += 2) {
+                                const float e0 = ex2(fmaf(__uint_as_float(sv[c0 + i]), sc, neg_ref));
+                                const float e1 = ex2(fmaf(__uint_as_float(sv[c0 + i + 1]), sc, neg_ref));
+                                rs[(i >> 1) & 3] += e0 + e1;
+                                pk[i >> 1] = pack_bf16(e0, e1);
+                            }
+                            tmem_st16(tS + c0 / 2, pk);
                         }
-                        tmem_st16(tS + c0 / 2, pk);
+                    } else {
+#pragma unroll
+                        for (int c0 = 0; c0 < kBN; c0 += 32) {
+                            uint32_t pk[16];
+#pragma unroll
+                            for (int i = 0; i < 32; i += 2) {
+                                const float e0 = c0 + i < lim ? ex2(fmaf(__uint_as_float(sv[c0 + i]), sc, neg_ref)) : 0.0f;
+                                const float e1 = c0 + i + 1 < lim ? ex2(fmaf(__uint_as_float(sv[c0 + i + 1]), sc, neg_ref)) : 0.0f;
+                                rs[(i >> 1) & 3] += e0 + e1;
+                                pk[i >> 1] = pack_bf16(e0, e1);
+                            }
+                            tmem_st16(tS + c0 / 2, pk);
+                        }
                     }
                 }
                 const float rowsum = (rs[0] + rs[1]) + (rs[2] + rs[3]);
                 // O rescale after the scores are dead (P V(j-1) is complete: s_full orders after it;
                 // P V(j) is issued only after p_full)
-                if (__any_sync(0xffffffffu, rescale && m2 != -INFINITY)) {
+                if (rescale) sacc *= alpha;
+                if (__any_sync(0xffffffffu, pv_any && rescale && m2 != -INFINITY)) {
 #pragma unroll
                     for (int c0 = 0; c0 < kD; c0 += 32) {
                         uint32_t v[32];
@@ -634,6 +665,7 @@ tc_pass_kernel(const TcParams p, const __grid_constant__ CUtensorMap qmap,
                 ++npf;
                 // state update (on a stop the rescaled state is the same state: O/ell unchanged)
                 ell = commit ? ell * alpha + rowsum : ell * alpha;
+                pv_any |= commit;
                 m2 = m_use;
                 if (commit && !is_diag) {
                     ++committed;
@@ -658,6 +690,21 @@ tc_pass_kernel(const TcParams p, const __grid_constant__ CUtensorMap qmap,
 #pragma unroll
             for (int c0 = 0; c0 < kD; c0 += 32) tmem_ld32(tO + c0, *reinterpret_cast<uint32_t(*)[32]>(&ov[c0]));
             tmem_ld_wait();
+            if (!pv_any) {
+#pragma unroll
+                for (int i = 0; i < kD; ++i) ov[i] = 0u;
+            }
+            if (a.mode & kStateIn) {
+                const float4* src = reinterpret_cast<const float4*>(a.acc_in + slot * kD);
+#pragma unroll
+                for (int i = 0; i < kD / 4; ++i) {
+                    const float4 y = src[i];
+                    ov[4 * i] = __float_as_uint(fmaf(y.x, sacc, __uint_as_float(ov[4 * i])));
+                    ov[4 * i + 1] = __float_as_uint(fmaf(y.y, sacc, __uint_as_float(ov[4 * i + 1])));
+                    ov[4 * i + 2] = __float_as_uint(fmaf(y.z, sacc, __uint_as_float(ov[4 * i + 2])));
+                    ov[4 * i + 3] = __float_as_uint(fmaf(y.w, sacc, __uint_as_float(ov[4 * i + 3])));
+                }
+            }
             const float inv = 1.0f / ell;
             if (valid && (a.mode & kStateOut)) {
                 float4* dst = reinterpret_cast<float4*>(a.acc_out + slot * kD);

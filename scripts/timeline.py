@@ -22,8 +22,8 @@ CAP = 1024
 NAMES = {5: "k_full", 6: "p0_seen", 7: "p1_seen", 8: "kv_empty", 9: "ld_acq", 10: "ld_iss",
          11: "s0_pair", 12: "s0_init", 13: "s0_odone", 14: "s0_epi", 15: "s1_pair", 16: "s1_init",
          17: "s1_odone", 18: "s1_epi", 19: "s0_sfull", 20: "s0_exps", 21: "s0_arrive",
-         22: "s1_sfull", 23: "s1_exps", 24: "s1_arrive", 25: "s0_ldwait", 26: "s0_max", 27: "s0_resc",
-         28: "s1_ldwait", 29: "s1_max", 30: "s1_resc"}
+         22: "s1_sfull", 23: "s1_exps", 24: "s1_arrive", 25: "s0_ldwait", 26: "mma_qfull", 27: "mma_s0iss",
+         28: "v_full", 29: "kq_issued", 30: "kq_start"}
 
 
 def dump(tag, buf):
@@ -32,12 +32,12 @@ def dump(tag, buf):
     rel = np.where(t > 0, t - t0, -1)
     np.save(os.path.join("gpurun_out", f"timeline_{tag}.npy"), rel)
     print(f"== {tag}: total span {rel.max()} clk")
-    for ev in (9, 10, 5, 19, 25, 26, 27, 20, 21, 6, 22, 28, 29, 30, 23, 24, 7, 8):
+    for ev in (9, 10, 5, 28, 19, 25, 20, 21, 6, 22, 23, 24, 7, 8):
         row = rel[ev]
         n = int((row >= 0).sum())
         first = row[:24]
         print(f"{NAMES[ev]:>10} n={n:4d} " + " ".join(f"{v:7d}" for v in first))
-    for ev in (11, 12, 13, 14, 15, 16, 17, 18):
+    for ev in (30, 29, 26, 27, 11, 12, 13, 14, 15, 16, 17, 18):
         row = rel[ev]
         print(f"{NAMES[ev]:>10} " + " ".join(f"{v:7d}" for v in row[:12]))
 
