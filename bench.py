@@ -121,16 +121,20 @@ def make_inputs(torch, s2o, l: int, seed: int, device):
 
 
 def cuda_time(torch, fn, reps: int, stream=None) -> float:
-    """Mean ms of fn() over reps, CUDA events on the current stream, synchronized."""
+    """Min ms of fn() over reps (after one untimed call that absorbs allocator / first-touch
+    effects), CUDA events on the current stream, synchronized around each call."""
+    fn()
     torch.cuda.synchronize()
-    a = torch.cuda.Event(enable_timing=True)
-    b = torch.cuda.Event(enable_timing=True)
-    a.record()
+    best = float("inf")
     for _ in range(reps):
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record()
         fn()
-    b.record()
-    torch.cuda.synchronize()
-    return a.elapsed_time(b) / reps
+        b.record()
+        torch.cuda.synchronize()
+        best = min(best, a.elapsed_time(b))
+    return best
 
 
 def plan_sort_passes(l: int, s: int) -> int:

@@ -95,10 +95,13 @@ bool path_is_tc(const PassArgs& a, int32_t path) {
 // Pass scratch: generic path scratch + error flag.
 size_t pass_ws_bytes(const PassArgs& a) { return align256(generic_scratch_bytes(a)) + 256; }
 
-s2o_status run_pass(PassArgs a, int32_t path, void* ws, size_t ws_bytes, cudaStream_t st) {
+// The error flag lives in the (caller-owned, uninitialised) pass scratch; every pass clears it
+// except a tile-list rerun, which must keep the flags of the tiles it does not revisit.
+s2o_status run_pass(PassArgs a, int32_t path, void* ws, size_t ws_bytes, cudaStream_t st, bool clear_flag = true) {
     char* base = reinterpret_cast<char*>(ws);
     if (!ws || ws_bytes < pass_ws_bytes(a)) return fail(S2O_ERR_WORKSPACE, "workspace too small");
     a.err_flag = reinterpret_cast<int32_t*>(base + align256(generic_scratch_bytes(a)));
+    if (clear_flag) S2O_CUDA_TRY(cudaMemsetAsync(a.err_flag, 0, sizeof(int32_t), st), "memset");
     if (path == S2O_PATH_TCGEN05 && !tc_supported(a))
         return fail(S2O_ERR_UNSUPPORTED,
                     "tcgen05 path needs bf16 inputs, D=128, b_m=128, b_n in {64,128}");
@@ -113,9 +116,13 @@ s2o_status run_pass(PassArgs a, int32_t path, void* ws, size_t ws_bytes, cudaStr
 // Stream/arena for the host-buffer entry point.
 struct HostArena {
     std::mutex mu;
-    cudaStream_t stream = nullptr;
+    cudaStream_t stream = nullptr;           // compute
+    cudaStream_t s_in = nullptr, s_out = nullptr;  // host->device / device->host copies
+    cudaEvent_t ev_h2d[2] = {}, ev_comp[2] = {}, ev_d2h[2] = {};
     void* dev = nullptr;
     size_t bytes = 0;
+    int32_t* flags = nullptr;  // pinned, one per chunk
+    int64_t nflags = 0;
 } g_host;
 
 }  // namespace
@@ -477,7 +484,7 @@ s2o_status s2o_attention_fwd(const s2o_problem* p, const void* q, const void* k,
                 a3.tile_list = ovf + 4;
                 a3.tile_count = host[0];
             }
-            if ((st = run_pass(a3, cfg->path, base + L.pass, pass_ws_bytes(a), s))) return st;
+            if ((st = run_pass(a3, cfg->path, base + L.pass, pass_ws_bytes(a), s, host[1] != 0))) return st;
         }
     }
     g_err.clear();
@@ -505,6 +512,129 @@ s2o_status s2o_dense_causal_fwd(const s2o_problem* p, const void* q, const void*
     return st;
 }
 
+// Host-buffer operator, pipelined over (batch, kv head) chunks -- heads are independent: chunk
+// c+1 moves host->device while chunk c computes and chunk c-1 moves device->host, on three
+// streams with double-buffered device chunk sets. Each chunk is the sub-problem
+// {Z=1, Hq=group, Hkv=1} through s2o_attention_fwd, so results equal the one-shot call.
+static s2o_status attention_host_pipelined(const s2o_problem* p, const Geo& g, const void* q, const void* k,
+                                           const void* v, const s2o_kernel_config* cfg, void* o,
+                                           int32_t* q_perm, int32_t* kv_perm, int32_t* processed,
+                                           int64_t* pass1_pairs, int64_t* pass2_pairs) {
+    const int64_t grp = p->hq / p->hkv;
+    const int64_t nchunks = p->z * p->hkv;
+    s2o_problem sp;
+    s2o_problem_init(&sp, 1, grp, 1, p->l, p->d, p->in_dtype, p->out_dtype);
+    Geo sg;
+    s2o_status st = make_geo(&sp, cfg->seg_len, &sg);
+    if (st) return st;
+    PassArgs sa = base_args(sg, cfg);
+    const OpLayout SL = op_layout(sg, sa, cfg->fused, cfg);
+    const size_t esz_in = p->in_dtype == S2O_BF16 ? 2 : 4;
+    const size_t esz_out = p->out_dtype == S2O_BF16 ? 2 : 4;
+    const size_t row = (size_t)p->l * p->d;
+    const size_t qb = esz_in * grp * row, kb = esz_in * row, ob = esz_out * grp * row;
+    const size_t qpb = sizeof(int32_t) * grp * sg.N * sg.S;
+    const size_t kvpb = kv_perm && sg.N > 1 ? sizeof(int32_t) * grp * sg.kv_per_head() : 0;
+    const size_t prb = sizeof(int32_t) * grp * sg.N * sa.T;
+    const size_t pairb = sizeof(int64_t) * grp;
+    // chunk set: q k v o q_perm kv_perm processed pass1 pass2
+    const size_t off_q = 0, off_k = align256(qb), off_v = off_k + align256(kb), off_o = off_v + align256(kb);
+    const size_t off_qp = off_o + align256(ob), off_kvp = off_qp + align256(qpb);
+    const size_t off_pr = off_kvp + align256(kvpb), off_p1 = off_pr + align256(prb), off_p2 = off_p1 + align256(pairb);
+    const size_t set_bytes = off_p2 + align256(pairb);
+    const size_t need = 2 * set_bytes + SL.total + 256;
+    std::lock_guard<std::mutex> lock(g_host.mu);
+    if (!g_host.stream) S2O_CUDA_TRY(cudaStreamCreateWithFlags(&g_host.stream, cudaStreamNonBlocking), "stream");
+    if (!g_host.s_in) {
+        S2O_CUDA_TRY(cudaStreamCreateWithFlags(&g_host.s_in, cudaStreamNonBlocking), "stream");
+        S2O_CUDA_TRY(cudaStreamCreateWithFlags(&g_host.s_out, cudaStreamNonBlocking), "stream");
+        for (int b = 0; b < 2; ++b) {
+            S2O_CUDA_TRY(cudaEventCreateWithFlags(&g_host.ev_h2d[b], cudaEventDisableTiming), "event");
+            S2O_CUDA_TRY(cudaEventCreateWithFlags(&g_host.ev_comp[b], cudaEventDisableTiming), "event");
+            S2O_CUDA_TRY(cudaEventCreateWithFlags(&g_host.ev_d2h[b], cudaEventDisableTiming), "event");
+        }
+    }
+    if (g_host.bytes < need) {
+        if (g_host.dev) cudaFree(g_host.dev);
+        g_host.dev = nullptr;
+        g_host.bytes = 0;
+        S2O_CUDA_TRY(cudaMalloc(&g_host.dev, need), "arena alloc");
+        g_host.bytes = need;
+    }
+    if (g_host.nflags < nchunks) {
+        if (g_host.flags) cudaFreeHost(g_host.flags);
+        g_host.flags = nullptr;
+        g_host.nflags = 0;
+        S2O_CUDA_TRY(cudaMallocHost(&g_host.flags, sizeof(int32_t) * nchunks), "pinned flags");
+        g_host.nflags = nchunks;
+    }
+    char* set[2] = {reinterpret_cast<char*>(g_host.dev), reinterpret_cast<char*>(g_host.dev) + set_bytes};
+    char* ws = reinterpret_cast<char*>(g_host.dev) + 2 * set_bytes;
+    char* wbase = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(ws) + 255) & ~uintptr_t(255));
+    const int32_t* dflag = reinterpret_cast<const int32_t*>(wbase + SL.pass + align256(generic_scratch_bytes(sa)));
+    cudaStream_t sc = g_host.stream, si = g_host.s_in, so = g_host.s_out;
+    auto hq_off = [&](int64_t c) { return (c / p->hkv) * p->hq + (c % p->hkv) * grp; };  // first q head
+    auto enqueue_in = [&](int64_t c) -> s2o_status {
+        const int b = (int)(c & 1);
+        if (c >= 2) S2O_CUDA_TRY(cudaStreamWaitEvent(si, g_host.ev_comp[b], 0), "wait");
+        const char* hq = reinterpret_cast<const char*>(q) + esz_in * row * hq_off(c);
+        const char* hk = reinterpret_cast<const char*>(k) + esz_in * row * c;
+        const char* hv = reinterpret_cast<const char*>(v) + esz_in * row * c;
+        S2O_CUDA_TRY(cudaMemcpyAsync(set[b] + off_q, hq, qb, cudaMemcpyHostToDevice, si), "h2d q");
+        S2O_CUDA_TRY(cudaMemcpyAsync(set[b] + off_k, hk, kb, cudaMemcpyHostToDevice, si), "h2d k");
+        S2O_CUDA_TRY(cudaMemcpyAsync(set[b] + off_v, hv, kb, cudaMemcpyHostToDevice, si), "h2d v");
+        S2O_CUDA_TRY(cudaEventRecord(g_host.ev_h2d[b], si), "record");
+        return S2O_OK;
+    };
+    auto drain = [&]() {
+        cudaStreamSynchronize(si);
+        cudaStreamSynchronize(sc);
+        cudaStreamSynchronize(so);
+    };
+    if ((st = enqueue_in(0))) return st;
+    for (int64_t c = 0; c < nchunks; ++c) {
+        const int b = (int)(c & 1);
+        if (c + 1 < nchunks && (st = enqueue_in(c + 1))) { drain(); return st; }
+        S2O_CUDA_TRY(cudaStreamWaitEvent(sc, g_host.ev_h2d[b], 0), "wait");
+        if (c >= 2) S2O_CUDA_TRY(cudaStreamWaitEvent(sc, g_host.ev_d2h[b], 0), "wait");
+        char* cs = set[b];
+        st = s2o_attention_fwd(&sp, cs + off_q, cs + off_k, cs + off_v, cfg, cs + off_o,
+                               reinterpret_cast<int32_t*>(cs + off_qp),
+                               kvpb ? reinterpret_cast<int32_t*>(cs + off_kvp) : nullptr,
+                               reinterpret_cast<int32_t*>(cs + off_pr), reinterpret_cast<int64_t*>(cs + off_p1),
+                               reinterpret_cast<int64_t*>(cs + off_p2), ws, SL.total + 256, sc);
+        if (st) { drain(); return st; }
+        S2O_CUDA_TRY(cudaMemcpyAsync(&g_host.flags[c], dflag, sizeof(int32_t), cudaMemcpyDeviceToHost, sc), "d2h flag");
+        S2O_CUDA_TRY(cudaEventRecord(g_host.ev_comp[b], sc), "record");
+        S2O_CUDA_TRY(cudaStreamWaitEvent(so, g_host.ev_comp[b], 0), "wait");
+        const int64_t h0 = hq_off(c);
+        S2O_CUDA_TRY(cudaMemcpyAsync(reinterpret_cast<char*>(o) + esz_out * row * h0, cs + off_o, ob,
+                                     cudaMemcpyDeviceToHost, so), "d2h o");
+        if (q_perm)
+            S2O_CUDA_TRY(cudaMemcpyAsync(q_perm + h0 * sg.N * sg.S, cs + off_qp, qpb, cudaMemcpyDeviceToHost, so),
+                         "d2h q_perm");
+        if (kvpb)
+            S2O_CUDA_TRY(cudaMemcpyAsync(kv_perm + h0 * sg.kv_per_head(), cs + off_kvp, kvpb,
+                                         cudaMemcpyDeviceToHost, so), "d2h kv_perm");
+        if (processed)
+            S2O_CUDA_TRY(cudaMemcpyAsync(processed + h0 * sg.N * sa.T, cs + off_pr, prb, cudaMemcpyDeviceToHost, so),
+                         "d2h trace");
+        if (pass1_pairs)
+            S2O_CUDA_TRY(cudaMemcpyAsync(pass1_pairs + h0, cs + off_p1, pairb, cudaMemcpyDeviceToHost, so), "d2h pairs");
+        if (pass2_pairs)
+            S2O_CUDA_TRY(cudaMemcpyAsync(pass2_pairs + h0, cs + off_p2, pairb, cudaMemcpyDeviceToHost, so), "d2h pairs");
+        S2O_CUDA_TRY(cudaEventRecord(g_host.ev_d2h[b], so), "record");
+    }
+    S2O_CUDA_TRY(cudaStreamSynchronize(so), "sync");
+    S2O_CUDA_TRY(cudaStreamSynchronize(sc), "sync");
+    for (int64_t c = 0; c < nchunks; ++c) {
+        if (g_host.flags[c] == 1) return fail(S2O_ERR_UNINIT_STATE, "uninitialized state");
+        if (g_host.flags[c] == 2) return fail(S2O_ERR_UNCOVERED_ROW, "uncovered query row");
+    }
+    g_err.clear();
+    return S2O_OK;
+}
+
 s2o_status s2o_attention_host(const s2o_problem* p, const void* q, const void* k, const void* v,
                               const s2o_kernel_config* cfg, void* o, int32_t* q_perm,
                               int32_t* kv_perm, int32_t* processed, int64_t* pass1_pairs,
@@ -515,6 +645,9 @@ s2o_status s2o_attention_host(const s2o_problem* p, const void* q, const void* k
     if ((st = validate_cfg(cfg, p->l))) return st;
     if (!q || !k || !v || !o) return fail(S2O_ERR_INVALID_ARG, "null pointer");
     // host buffers are dense [Z,H,L,D]
+    if (p->z * p->hkv >= 2)
+        return attention_host_pipelined(p, g, q, k, v, cfg, o, q_perm, kv_perm, processed, pass1_pairs,
+                                        pass2_pairs);
     s2o_problem dp;
     s2o_problem_init(&dp, p->z, p->hq, p->hkv, p->l, p->d, p->in_dtype, p->out_dtype);
     PassArgs a = base_args(g, cfg);
@@ -582,8 +715,18 @@ void s2o_host_release(void) {
     if (g_host.dev) cudaFree(g_host.dev);
     g_host.dev = nullptr;
     g_host.bytes = 0;
-    if (g_host.stream) cudaStreamDestroy(g_host.stream);
-    g_host.stream = nullptr;
+    if (g_host.flags) cudaFreeHost(g_host.flags);
+    g_host.flags = nullptr;
+    g_host.nflags = 0;
+    for (cudaStream_t* s : {&g_host.stream, &g_host.s_in, &g_host.s_out}) {
+        if (*s) cudaStreamDestroy(*s);
+        *s = nullptr;
+    }
+    for (int b = 0; b < 2; ++b)
+        for (cudaEvent_t* e : {&g_host.ev_h2d[b], &g_host.ev_comp[b], &g_host.ev_d2h[b]}) {
+            if (*e) cudaEventDestroy(*e);
+            *e = nullptr;
+        }
 }
 
 }  // extern "C"
