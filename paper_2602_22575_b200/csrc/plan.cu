@@ -156,6 +156,176 @@ q_rank_kernel(const void* __restrict__ q, Geo g, const float* __restrict__ guide
     for (int64_t i = threadIdx.x; i < len; i += blockDim.x) out[i] = (int32_t)res[i];
 }
 
+// Fast q ranking for the product shape (bf16, D = 128, 16-B aligned rows): 512 threads per
+// (zh, n). Rows stream through two shared buffers of 256 rows (odd 65-word row stride: the
+// per-row dot and the per-column sum both read conflict-free). Every thread prefetches 1/512
+// of chunk c+1 into registers (64 KB in flight per SM) while warps 0-7 score the 256 rows of
+// chunk c (one row per thread, fp64 sequential over d) and warps 8-11 extend the 128 column
+// sums (fp64 sequential over rows). Same arithmetic, same order as q_rank_kernel /
+// mean_pool_rows + dot_f.
+constexpr int kQF_Threads = 512;
+constexpr int kQF_Rows = 256;
+constexpr int kQF_W = 65;  // 32-bit words per staged row (64 used)
+constexpr int kQF_Per = kQF_Rows * 16 / kQF_Threads;  // 16-B pieces per thread per chunk (8)
+constexpr size_t kQF_Smem = sizeof(uint32_t) * 2 * kQF_Rows * kQF_W + (2 * sizeof(uint64_t) + 2 * sizeof(uint32_t)) * kRun +
+                            sizeof(double) * 128;
+
+// Register-prefetched staging of 256 bf16 rows of 128 columns (row stride `rs` elements).
+struct RowStager {
+    uint4 reg[kQF_Per];
+    __device__ void fetch(const __nv_bfloat16* base, int64_t rs, int r0, int len) {
+#pragma unroll
+        for (int i = 0; i < kQF_Per; ++i) {
+            const int e = threadIdx.x + i * kQF_Threads;
+            const int r = e >> 4, p = e & 15;
+            reg[i] = (r0 + r < len) ? *reinterpret_cast<const uint4*>(base + (int64_t)(r0 + r) * rs + p * 8)
+                                    : make_uint4(0, 0, 0, 0);
+        }
+    }
+    __device__ void stash(uint32_t* dst) const {
+#pragma unroll
+        for (int i = 0; i < kQF_Per; ++i) {
+            const int e = threadIdx.x + i * kQF_Threads;
+            const int r = e >> 4, p = e & 15;
+            uint32_t* d = dst + r * kQF_W + p * 4;
+            d[0] = reg[i].x; d[1] = reg[i].y; d[2] = reg[i].z; d[3] = reg[i].w;
+        }
+    }
+};
+
+// fp64 running sum of column `col` over rows [0, cn) of a staged chunk, in row order.
+__device__ __forceinline__ double column_sum(const uint32_t* buf, int col, int cn, double acc) {
+    const uint32_t* cp = buf + (col >> 1);
+    const int sh = (col & 1) ? 0 : 16;
+    int r = 0;
+    for (; r + 8 <= cn; r += 8) {
+        float v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = __uint_as_float((cp[(r + u) * kQF_W] << sh) & 0xffff0000u);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) acc += (double)v[u];
+    }
+    for (; r < cn; ++r) acc += (double)__uint_as_float((cp[r * kQF_W] << sh) & 0xffff0000u);
+    return acc;
+}
+
+__global__ void __launch_bounds__(kQF_Threads, 1)
+q_rank128_kernel(const __nv_bfloat16* __restrict__ q, Geo g, const float* __restrict__ guide,
+                 float* __restrict__ q_mean, uint64_t* __restrict__ qkey, int32_t* __restrict__ q_perm) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    uint32_t* stage = reinterpret_cast<uint32_t*>(smem_raw);                  // [2][256][65]
+    uint64_t* sk0 = reinterpret_cast<uint64_t*>(stage + 2 * kQF_Rows * kQF_W);  // [kRun]
+    uint64_t* sk1 = sk0 + kRun;
+    uint32_t* si0 = reinterpret_cast<uint32_t*>(sk1 + kRun);
+    uint32_t* si1 = si0 + kRun;
+    double* gd = reinterpret_cast<double*>(si1 + kRun);                         // [128]
+    const int tid = threadIdx.x;
+    const int64_t zh = blockIdx.x / g.N;
+    const int64_t n = blockIdx.x % g.N;
+    const int len = (int)g.seg_rows(n);
+    const bool local_sort = len <= kRun;
+    const int64_t z = zh / g.hq;
+    const float* gsrc = guide + (z * g.hkv + g.kvh(zh)) * 128;
+    if (tid < 128) gd[tid] = (double)gsrc[tid];
+    const __nv_bfloat16* qseg = q + g.q_base(zh) + n * g.S * g.qs[2];
+    const int nchunks = (len + kQF_Rows - 1) / kQF_Rows;
+    RowStager rows;
+    rows.fetch(qseg, g.qs[2], 0, len);
+    rows.stash(stage);
+    __syncthreads();
+    double col_acc = 0.0;
+    for (int c = 0; c < nchunks; ++c) {
+        const int r0 = c * kQF_Rows;
+        const int cn = min(kQF_Rows, len - r0);
+        const uint32_t* buf = stage + (c & 1) * kQF_Rows * kQF_W;
+        if (c + 1 < nchunks) rows.fetch(qseg, g.qs[2], r0 + kQF_Rows, len);
+        if (tid < 256) {
+            if (tid < cn) {
+                const uint32_t* row = buf + tid * kQF_W;
+                double acc = 0.0;
+#pragma unroll 8
+                for (int w = 0; w < 64; ++w) {
+                    const uint32_t x = row[w];
+                    acc = fma((double)__uint_as_float(x << 16), gd[2 * w], acc);
+                    acc = fma((double)__uint_as_float(x & 0xffff0000u), gd[2 * w + 1], acc);
+                }
+                const uint64_t key = desc_key(acc);
+                const int pos = r0 + tid;
+                if (local_sort) {
+                    sk0[pos] = key;
+                    si0[pos] = (uint32_t)pos;
+                } else {
+                    qkey[zh * g.N * g.S + n * g.S + pos] = key;
+                }
+            }
+        } else if (tid < 384) {
+            col_acc = column_sum(buf, tid - 256, cn, col_acc);
+        }
+        if (c + 1 < nchunks) rows.stash(stage + ((c + 1) & 1) * kQF_Rows * kQF_W);
+        __syncthreads();
+    }
+    if (tid >= 256 && tid < 384) q_mean[(zh * g.N + n) * 128 + (tid - 256)] = (float)(col_acc * (1.0 / (double)len));
+    if (!local_sort) return;
+    for (int i = len + tid; i < kRun; i += kQF_Threads) {
+        sk0[i] = ~0ull;
+        si0[i] = 0xffffffffu;
+    }
+    __syncthreads();
+    const int which = block_merge_sort<kQF_Threads, kRun / kQF_Threads>(sk0, si0, sk1, si1);
+    const uint32_t* res = which ? si1 : si0;
+    int32_t* out = q_perm + (zh * g.N + n) * g.S;
+    for (int i = tid; i < len; i += kQF_Threads) out[i] = (int32_t)res[i];
+}
+
+// Segment means for the product shape (bf16, D = 128): the same staged stream, column sums only.
+// grid (z * heads, nseg_out).
+__global__ void __launch_bounds__(kQF_Threads, 1)
+seg_mean128_kernel(const __nv_bfloat16* __restrict__ x, int64_t heads_per_z, int64_t s0, int64_t s1, int64_t s2,
+                   int64_t S, int64_t N, int64_t last_len, int64_t nseg_out, float* __restrict__ out) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    uint32_t* stage = reinterpret_cast<uint32_t*>(smem_raw);
+    const int tid = threadIdx.x;
+    const int64_t slice = blockIdx.x, n = blockIdx.y;
+    const int len = (int)((n + 1 == N) ? last_len : S);
+    const __nv_bfloat16* seg = x + (slice / heads_per_z) * s0 + (slice % heads_per_z) * s1 + n * S * s2;
+    const int nchunks = (len + kQF_Rows - 1) / kQF_Rows;
+    RowStager rows;
+    rows.fetch(seg, s2, 0, len);
+    rows.stash(stage);
+    __syncthreads();
+    double acc = 0.0;
+    for (int c = 0; c < nchunks; ++c) {
+        const int r0 = c * kQF_Rows;
+        const int cn = min(kQF_Rows, len - r0);
+        if (c + 1 < nchunks) rows.fetch(seg, s2, r0 + kQF_Rows, len);
+        if (tid < 128) acc = column_sum(stage + (c & 1) * kQF_Rows * kQF_W, tid, cn, acc);
+        if (c + 1 < nchunks) rows.stash(stage + ((c + 1) & 1) * kQF_Rows * kQF_W);
+        __syncthreads();
+    }
+    if (tid < 128) out[(slice * nseg_out + n) * 128 + tid] = (float)(acc * (1.0 / (double)len));
+}
+
+bool q_rank128_ok(const Geo& g, const void* q) {
+    return g.in_bf16 && g.d == 128 && g.qs[0] % 8 == 0 && g.qs[1] % 8 == 0 && g.qs[2] % 8 == 0 &&
+           (reinterpret_cast<uintptr_t>(q) & 15) == 0;
+}
+
+// q ranking dispatch: fast kernel for the product shape, generic kernel otherwise.
+cudaError_t launch_q_rank(const Geo& g, const void* q, const float* guide, float* q_mean, uint64_t* qkey,
+                          int32_t* q_perm, cudaStream_t st) {
+    if (q_rank128_ok(g, q)) {
+        cudaFuncSetAttribute(q_rank128_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kQF_Smem);
+        q_rank128_kernel<<<(unsigned)(g.z * g.hq * g.N), kQF_Threads, kQF_Smem, st>>>(
+            reinterpret_cast<const __nv_bfloat16*>(q), g, guide, q_mean, qkey, q_perm);
+        return cudaGetLastError();
+    }
+    const size_t smem = (2 * sizeof(uint64_t) + 2 * sizeof(uint32_t)) * kRun + sizeof(double) * g.d +
+                        sizeof(float) * kQRows * (g.d + 1);
+    cudaFuncSetAttribute(q_rank_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    q_rank_kernel<<<(unsigned)(g.z * g.hq * g.N), kQThreads, smem, st>>>(q, g, guide, q_mean, qkey, q_perm);
+    return cudaGetLastError();
+}
+
 // ---------------------------------------------------------------- kv scoring
 // One CTA (128 threads) per (z, kv head, block of 128 keys). Register tile per thread:
 // 4 keys x 8 (q head, segment) pairs = 32 fp64 accumulators; each K element is converted
@@ -238,6 +408,135 @@ kv_score_kernel(const void* __restrict__ k, Geo g, const float* __restrict__ q_m
                 if (t + i < n * g.S) dst[t + i] = desc_key(acc[i][b]);
         }
     }
+}
+
+// Fast kv scoring for the product shape (bf16 K, D = 128): a register-tiled fp64 GEMM
+// S[pairs x keys] = q_mean[pairs x 128] . K^T per CTA tile of 64 (q head, segment) pairs x 128
+// keys (256 threads, 8 pairs x 4 keys each, d staged in chunks of 16 through double-buffered
+// shared memory as fp64). Each output accumulates d = 0..127 in order with DFMA, exactly
+// dot_f's sequence. CTA = (key block, pair batch); batches beyond a block's pair count exit.
+constexpr int kKS_Pairs = 64, kKS_Threads = 256, kKS_DC = 16;
+
+__global__ void __launch_bounds__(kKS_Threads, 2)
+kv_score128_kernel(const __nv_bfloat16* __restrict__ k, Geo g, const float* __restrict__ q_mean,
+                   uint64_t* __restrict__ kvkey, int max_batches) {
+    __shared__ __align__(16) double Ks[2][kKS_DC][kSK];        // 32 KB
+    __shared__ __align__(16) double Qs[2][kKS_DC][kKS_Pairs];  // 16 KB
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int64_t kb = blockIdx.x / max_batches;
+    const int batch = blockIdx.x % max_batches;
+    const int64_t zg = blockIdx.y;  // z * hkv + kvh
+    const int64_t z = zg / g.hkv, kvh = zg % g.hkv;
+    const int64_t t0 = kb * kSK;
+    const int64_t n_lo = t0 / g.S + 1;
+    const int64_t nsegs = (n_lo < g.N) ? g.N - n_lo : 0;
+    const int64_t pairs = g.group * nsegs;
+    const int64_t p0 = (int64_t)batch * kKS_Pairs;
+    if (p0 >= pairs) return;
+    const __nv_bfloat16* kbase = k + z * g.ks[0] + kvh * g.ks[1];
+    // staging roles: K row (tid >> 1), 8 d values at half (tid & 1); q pair (tid >> 2), 4 d at (tid & 3)
+    const int krow = tid >> 1, khalf = tid & 1;
+    const bool kvalid = t0 + krow < g.l;
+    const __nv_bfloat16* ksrc = kbase + (t0 + krow) * g.ks[2] + khalf * 8;
+    const int qp = tid >> 2, qq = tid & 3;
+    const int64_t pq = p0 + qp;
+    const float* qsrc = nullptr;
+    if (pq < pairs) {
+        const int64_t h = kvh * g.group + pq / nsegs;
+        const int64_t n = n_lo + pq % nsegs;
+        qsrc = q_mean + ((z * g.hq + h) * g.N + n) * 128 + qq * 4;
+    }
+    uint4 kreg;
+    float4 qreg;
+    auto fetch = [&](int dc) {
+        kreg = kvalid ? *reinterpret_cast<const uint4*>(ksrc + dc * kKS_DC) : make_uint4(0, 0, 0, 0);
+        qreg = qsrc ? *reinterpret_cast<const float4*>(qsrc + dc * kKS_DC) : make_float4(0.f, 0.f, 0.f, 0.f);
+    };
+    auto stash = [&](int buf) {
+        const uint32_t w[4] = {kreg.x, kreg.y, kreg.z, kreg.w};
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            Ks[buf][khalf * 8 + 2 * i][krow] = (double)__uint_as_float(w[i] << 16);
+            Ks[buf][khalf * 8 + 2 * i + 1][krow] = (double)__uint_as_float(w[i] & 0xffff0000u);
+        }
+        Qs[buf][qq * 4 + 0][qp] = (double)qreg.x;
+        Qs[buf][qq * 4 + 1][qp] = (double)qreg.y;
+        Qs[buf][qq * 4 + 2][qp] = (double)qreg.z;
+        Qs[buf][qq * 4 + 3][qp] = (double)qreg.w;
+    };
+    double acc[8][4];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
+    fetch(0);
+    stash(0);
+    __syncthreads();
+    constexpr int kChunks = 128 / kKS_DC;
+    for (int dc = 0; dc < kChunks; ++dc) {
+        const int buf = dc & 1;
+        if (dc + 1 < kChunks) fetch(dc + 1);
+#pragma unroll
+        for (int d = 0; d < kKS_DC; ++d) {
+            const double2 k01 = *reinterpret_cast<const double2*>(&Ks[buf][d][4 * lane]);
+            const double2 k23 = *reinterpret_cast<const double2*>(&Ks[buf][d][4 * lane + 2]);
+            const double kv[4] = {k01.x, k01.y, k23.x, k23.y};
+            double qv[8];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const double2 x = *reinterpret_cast<const double2*>(&Qs[buf][d][8 * warp + 2 * i]);
+                qv[2 * i] = x.x;
+                qv[2 * i + 1] = x.y;
+            }
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) acc[i][j] = fma(qv[i], kv[j], acc[i][j]);
+        }
+        if (dc + 1 < kChunks) stash(buf ^ 1);
+        __syncthreads();
+    }
+    const int64_t kvp = g.kv_per_head();
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const int64_t p = p0 + 8 * warp + i;
+        if (p >= pairs) break;
+        const int64_t h = kvh * g.group + p / nsegs;
+        const int64_t n = n_lo + p % nsegs;
+        uint64_t* dst = kvkey + (z * g.hq + h) * kvp + g.kv_off(n);
+        const int64_t t = t0 + 4 * lane;
+        if (t + 3 < n * g.S) {
+            ulonglong2* d2 = reinterpret_cast<ulonglong2*>(dst + t);
+            d2[0] = make_ulonglong2(desc_key(acc[i][0]), desc_key(acc[i][1]));
+            d2[1] = make_ulonglong2(desc_key(acc[i][2]), desc_key(acc[i][3]));
+        } else {
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+                if (t + j < n * g.S) dst[t + j] = desc_key(acc[i][j]);
+        }
+    }
+}
+
+bool kv_score128_ok(const Geo& g, const void* k) {
+    return g.in_bf16 && g.d == 128 && g.ks[0] % 8 == 0 && g.ks[1] % 8 == 0 && g.ks[2] % 8 == 0 &&
+           (reinterpret_cast<uintptr_t>(k) & 15) == 0 && g.S % 2 == 0;
+}
+
+cudaError_t launch_kv_score(const Geo& g, const void* k, const float* q_mean, uint64_t* kvkey, cudaStream_t st) {
+    const int64_t keys = (g.N - 1) * g.S;  // tokens that appear in some prefix
+    const int64_t blocks = (keys + kSK - 1) / kSK;
+    if (kv_score128_ok(g, k)) {
+        const int max_batches = (int)((g.group * (g.N - 1) + kKS_Pairs - 1) / kKS_Pairs);
+        dim3 grid((unsigned)(blocks * max_batches), (unsigned)(g.z * g.hkv));
+        kv_score128_kernel<<<grid, kKS_Threads, 0, st>>>(reinterpret_cast<const __nv_bfloat16*>(k), g, q_mean,
+                                                         kvkey, max_batches);
+        return cudaGetLastError();
+    }
+    const size_t smem = sizeof(double) * g.d * kSPairs + sizeof(float) * g.d * kSK;
+    cudaFuncSetAttribute(kv_score_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    dim3 grid((unsigned)blocks, (unsigned)(g.z * g.hkv));
+    kv_score_kernel<<<grid, kSKThreads, smem, st>>>(k, g, q_mean, kvkey);
+    return cudaGetLastError();
 }
 
 // ---------------------------------------------------------------- sort
@@ -465,21 +764,30 @@ select_topk_kernel(Geo g, const uint64_t* __restrict__ kvkey, int64_t topt, int3
             __syncthreads();
             const uint64_t theta = s_theta;
             const bool last_sample = (rank == kSelSample - 1);
-            // one pass: compact every key <= theta (ballot + per-warp atomic slot)
-            for (int64_t b0 = 0; b0 < len; b0 += blockDim.x) {
-                const int64_t i = b0 + threadIdx.x;
-                const bool take = i < len && keys[i] <= theta;
-                const unsigned m = __ballot_sync(0xffffffffu, take);
-                int base = 0;
-                if ((threadIdx.x & 31) == 0 && m) base = atomicAdd(&s_count, __popc(m));
-                base = __shfl_sync(0xffffffffu, base, 0);
-                if (take) {
-                    const int slot = base + __popc(m & ((1u << (threadIdx.x & 31)) - 1));
-                    if (slot < kSelCap) {
-                        // the sample area [0, kSelSample) is still needed for retries only
-                        // while attempts remain; collect above it, shift down later
-                        sk[slot] = keys[i];
-                        si[slot] = (uint32_t)i;
+            // one pass: compact every key <= theta (ballot + per-warp atomic slot); 8 coalesced
+            // loads per thread are in flight before any is used (the scan is latency-bound)
+            constexpr int kU = 8;
+            for (int64_t b0 = 0; b0 < len; b0 += (int64_t)blockDim.x * kU) {
+                uint64_t kk[kU];
+#pragma unroll
+                for (int u = 0; u < kU; ++u) {
+                    const int64_t i = b0 + (int64_t)u * blockDim.x + threadIdx.x;
+                    kk[u] = i < len ? keys[i] : ~0ull;
+                }
+#pragma unroll
+                for (int u = 0; u < kU; ++u) {
+                    const int64_t i = b0 + (int64_t)u * blockDim.x + threadIdx.x;
+                    const bool take = i < len && kk[u] <= theta;
+                    const unsigned m = __ballot_sync(0xffffffffu, take);
+                    int base = 0;
+                    if ((threadIdx.x & 31) == 0 && m) base = atomicAdd(&s_count, __popc(m));
+                    base = __shfl_sync(0xffffffffu, base, 0);
+                    if (take) {
+                        const int slot = base + __popc(m & ((1u << (threadIdx.x & 31)) - 1));
+                        if (slot < kSelCap) {
+                            sk[slot] = kk[u];
+                            si[slot] = (uint32_t)i;
+                        }
                     }
                 }
             }
@@ -620,21 +928,11 @@ cudaError_t launch_plan_topk(const Geo& g, const void* q, const void* k, int32_t
     cudaError_t err;
     if ((err = launch_segment_means(g, k, 1, 1, ws.guide, st)) != cudaSuccess) return err;
     {
-        const size_t smem = (2 * sizeof(uint64_t) + 2 * sizeof(uint32_t)) * kRun + sizeof(double) * g.d +
-                            sizeof(float) * kQRows * (g.d + 1);
-        cudaFuncSetAttribute(q_rank_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        q_rank_kernel<<<(unsigned)(g.z * g.hq * g.N), kQThreads, smem, st>>>(q, g, ws.guide, ws.q_mean,
-                                                                            ws.key0, q_perm);
-        if ((err = cudaGetLastError()) != cudaSuccess) return err;
+        if ((err = launch_q_rank(g, q, ws.guide, ws.q_mean, ws.key0, q_perm, st)) != cudaSuccess) return err;
         if (g.S > kRun && (err = sort_family(0, g, ws, q_perm, st)) != cudaSuccess) return err;
     }
     if (g.N > 1) {
-        const size_t smem = sizeof(double) * g.d * kSPairs + sizeof(float) * g.d * kSK;
-        cudaFuncSetAttribute(kv_score_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        const int64_t keys = (g.N - 1) * g.S;
-        dim3 grid((unsigned)((keys + kSK - 1) / kSK), (unsigned)(g.z * g.hkv));
-        kv_score_kernel<<<grid, kSKThreads, smem, st>>>(k, g, ws.q_mean, ws.key0);
-        if ((err = cudaGetLastError()) != cudaSuccess) return err;
+        if ((err = launch_kv_score(g, k, ws.q_mean, ws.key0, st)) != cudaSuccess) return err;
         const size_t ssm = (sizeof(uint64_t) + sizeof(uint32_t)) * kSelCap;
         cudaFuncSetAttribute(select_topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssm);
         select_topk_kernel<<<(unsigned)(g.z * g.hq * (g.N - 1)), kSelThreads, ssm, st>>>(g, ws.key0, topt,
@@ -649,6 +947,15 @@ cudaError_t launch_segment_means(const Geo& g, const void* x, int which_kv, int6
                                  float* out, cudaStream_t st) {
     const int64_t heads = which_kv ? g.hkv : g.hq;
     const int64_t* s = which_kv ? g.ks : g.qs;
+    if (g.in_bf16 && g.d == 128 && s[0] % 8 == 0 && s[1] % 8 == 0 && s[2] % 8 == 0 &&
+        (reinterpret_cast<uintptr_t>(x) & 15) == 0) {
+        const size_t smem = sizeof(uint32_t) * 2 * kQF_Rows * kQF_W;
+        cudaFuncSetAttribute(seg_mean128_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        dim3 grid((unsigned)(g.z * heads), (unsigned)nseg_out);
+        seg_mean128_kernel<<<grid, kQF_Threads, smem, st>>>(reinterpret_cast<const __nv_bfloat16*>(x), heads, s[0],
+                                                            s[1], s[2], g.S, g.N, g.last_len, nseg_out, out);
+        return cudaGetLastError();
+    }
     const int threads = (int)std::min<int64_t>(128, g.d);
     dim3 grid((unsigned)((g.d + threads - 1) / threads), (unsigned)(g.z * heads),
               (unsigned)nseg_out);
@@ -667,21 +974,11 @@ cudaError_t launch_plan_build(const Geo& g, const void* q, const void* k, int32_
     if ((err = launch_segment_means(g, k, 1, 1, ws.guide, st)) != cudaSuccess) return err;
     // q_mean + q keys (+ in-CTA sort when a segment fits one run)
     {
-        const size_t smem = (2 * sizeof(uint64_t) + 2 * sizeof(uint32_t)) * kRun + sizeof(double) * g.d +
-                            sizeof(float) * kQRows * (g.d + 1);
-        cudaFuncSetAttribute(q_rank_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        q_rank_kernel<<<(unsigned)(g.z * g.hq * g.N), kQThreads, smem, st>>>(q, g, ws.guide, ws.q_mean,
-                                                                            ws.key0, q_perm);
-        if ((err = cudaGetLastError()) != cudaSuccess) return err;
+        if ((err = launch_q_rank(g, q, ws.guide, ws.q_mean, ws.key0, q_perm, st)) != cudaSuccess) return err;
         if (g.S > kRun && (err = sort_family(0, g, ws, q_perm, st)) != cudaSuccess) return err;
     }
     if (g.N > 1) {
-        const size_t smem = sizeof(double) * g.d * kSPairs + sizeof(float) * g.d * kSK;
-        cudaFuncSetAttribute(kv_score_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        const int64_t keys = (g.N - 1) * g.S;  // tokens that appear in some prefix
-        dim3 grid((unsigned)((keys + kSK - 1) / kSK), (unsigned)(g.z * g.hkv));
-        kv_score_kernel<<<grid, kSKThreads, smem, st>>>(k, g, ws.q_mean, ws.key0);
-        if ((err = cudaGetLastError()) != cudaSuccess) return err;
+        if ((err = launch_kv_score(g, k, ws.q_mean, ws.key0, st)) != cudaSuccess) return err;
         if ((err = sort_family(1, g, ws, kv_perm, st)) != cudaSuccess) return err;
     }
     return cudaSuccess;
