@@ -24,6 +24,8 @@
 #include "internal.h"
 #include "sort.cuh"
 
+#include <cub/block/block_radix_sort.cuh>
+
 namespace s2o {
 
 namespace {
@@ -688,149 +690,179 @@ merge_pass_kernel(SortGeo sg, int64_t w, const uint64_t* __restrict__ ikeys,
 }
 
 // ---------------------------------------------------------------- top-T selection
-// For the fused operator only the leading chunks of each kv_perm segment are consumed
-// (the walk stops early), so instead of fully sorting the prefix the plan materialises its
-// exact top-T: a CTA per (zh, n >= 1) samples 2048 keys, picks a threshold key whose
-// expected rank is ~1.25 T, gathers every key <= threshold into shared memory (one pass over
-// the segment, warp-ballot compaction), sorts them by (key, index) and writes the first T
-// indices. The result equals the first T entries of argsort_desc_stable (a stable sort's top
-// T is a prefix of the full order). If the threshold catches fewer than T keys or more than
-// the capacity, the CTA retries with another sample rank; after the retries it falls back to
-// a plain capacity-sized best-so-far and flags the segment (never observed; checked by host).
+// For the fused operator only the leading chunks of each kv_perm segment are consumed (the walk
+// stops early), so instead of fully sorting the prefix the plan materialises its exact top-T.
+// A CTA per (zh, n >= 1): radix-sort a 2048-key sample, take a threshold key whose expected rank
+// is ~1.15 T, compact every key <= threshold in INDEX order (coalesced 8-key loads per thread +
+// a block scan), then a stable block radix sort of the candidates by key (ties keep index
+// order) and write the first T indices. The result equals the first T entries of
+// argsort_desc_stable (a stable sort's top T is a prefix of the full order). If the threshold
+// catches fewer than T keys or more than the capacity, the CTA retries with another sample
+// rank; after the retries it keeps a capacity-sized best-effort set and flags the segment (the
+// host then builds the full plan).
 constexpr int kSelThreads = 512;
-constexpr int kSelCap = 8192;      // keys held in smem for the final sort
+constexpr int kSelItems = 16;
+constexpr int kSelCap = kSelThreads * kSelItems;  // 8192 candidates
 constexpr int kSelSample = 2048;
+constexpr int kSelRadixBits = 6;
 
-__device__ __forceinline__ void bitonic_sort_smem(uint64_t* k, uint32_t* id, int n_pow2) {
-    for (int kk = 2; kk <= n_pow2; kk <<= 1) {
-        for (int jj = kk >> 1; jj > 0; jj >>= 1) {
-            for (int i = threadIdx.x; i < n_pow2 / 2; i += blockDim.x) {
-                // i-th compare-exchange pair of this stage
-                const int lo = ((i / jj) * (2 * jj)) + (i % jj);
-                const int hi = lo + jj;
-                const bool up = (lo & kk) == 0;
-                const uint64_t a = k[lo], b = k[hi];
-                const uint32_t ia = id[lo], ib = id[hi];
-                if (elt_less(b, ib, a, ia) == up) {
-                    k[lo] = b; k[hi] = a;
-                    id[lo] = ib; id[hi] = ia;
-                }
-            }
-            __syncthreads();
-        }
-    }
-}
+using SelSort = cub::BlockRadixSort<uint64_t, kSelThreads, kSelItems, uint32_t, kSelRadixBits>;
+using SampSort = cub::BlockRadixSort<uint64_t, kSelThreads, kSelSample / kSelThreads, cub::NullType, kSelRadixBits>;
+union SelSmem {
+    struct {
+        uint64_t k[kSelCap];
+        uint32_t i[kSelCap];
+    } cand;
+    typename SelSort::TempStorage sort;
+    typename SampSort::TempStorage samp;
+};
 
 __global__ void __launch_bounds__(kSelThreads)
 select_topk_kernel(Geo g, const uint64_t* __restrict__ kvkey, int64_t topt, int32_t* __restrict__ kvtop,
                    int32_t* __restrict__ flags) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    uint64_t* sk = reinterpret_cast<uint64_t*>(smem_raw);          // [kSelCap]
-    uint32_t* si = reinterpret_cast<uint32_t*>(sk + kSelCap);       // [kSelCap]
+    SelSmem& sm = *reinterpret_cast<SelSmem*>(smem_raw);
+    __shared__ int s_wsum[kSelThreads / 32];
     __shared__ int s_count;
     __shared__ uint64_t s_theta;
+    __shared__ unsigned long long s_or;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int64_t zh = blockIdx.x / (g.N - 1);
     const int64_t n = 1 + blockIdx.x % (g.N - 1);
     const int64_t len = n * g.S;
     const int64_t tt = min(topt, len);
     const uint64_t* keys = kvkey + zh * g.kv_per_head() + g.kv_off(n);
     int32_t* out = kvtop + (zh * g.N + n) * topt;
-    int count = 0;
+    uint64_t ck[kSelItems];
+    uint32_t ci[kSelItems];
     if (len <= kSelCap) {
-        for (int64_t i = threadIdx.x; i < len; i += blockDim.x) {
-            sk[i] = keys[i];
-            si[i] = (uint32_t)i;
+        // every key is a candidate, already in index order (blocked arrangement)
+#pragma unroll
+        for (int e = 0; e < kSelItems; ++e) {
+            const int64_t i = (int64_t)tid * kSelItems + e;
+            ck[e] = i < len ? keys[i] : ~0ull;
+            ci[e] = i < len ? (uint32_t)i : 0xffffffffu;
         }
-        count = (int)len;
     } else {
-        // sample: 128 runs of 16 consecutive keys spread over the segment
-        for (int e = threadIdx.x; e < kSelSample; e += blockDim.x) {
-            const int run = e / 16, off = e % 16;
-            const int64_t pos = (int64_t)run * (len / 128) + off;
-            sk[e] = keys[pos];
-            si[e] = (uint32_t)e;
+        // sample: 128 runs of 16 consecutive keys spread over the segment, radix-sorted
+        uint64_t smp[kSelSample / kSelThreads];
+#pragma unroll
+        for (int u = 0; u < kSelSample / kSelThreads; ++u) {
+            const int e = tid * (kSelSample / kSelThreads) + u;
+            smp[u] = keys[(int64_t)(e / 16) * (len / 128) + e % 16];
         }
-        __syncthreads();
-        bitonic_sort_smem(sk, si, kSelSample);
+        SampSort(sm.samp).Sort(smp);  // blocked: thread t holds ranks 4t .. 4t+3
         double want = 1.15 * (double)tt + 32.0;
         bool ok = false;
+        int count = 0;
         for (int attempt = 0; attempt < 6 && !ok; ++attempt) {
             int64_t rank = (int64_t)ceil(want * kSelSample / (double)len) + 4;
             if (rank > kSelSample - 1) rank = kSelSample - 1;
-            if (threadIdx.x == 0) {
-                s_theta = sk[rank];
-                s_count = 0;
-            }
+            __syncthreads();  // sample sort storage / previous candidates no longer read
+            if (tid == (int)(rank / (kSelSample / kSelThreads))) s_theta = smp[rank % (kSelSample / kSelThreads)];
+            if (tid == 0) s_count = 0;
             __syncthreads();
             const uint64_t theta = s_theta;
             const bool last_sample = (rank == kSelSample - 1);
-            // one pass: compact every key <= theta (ballot + per-warp atomic slot); 8 coalesced
-            // loads per thread are in flight before any is used (the scan is latency-bound)
+            // order-preserving compaction of every key <= theta
             constexpr int kU = 8;
-            for (int64_t b0 = 0; b0 < len; b0 += (int64_t)blockDim.x * kU) {
+            for (int64_t b0 = 0; b0 < len; b0 += (int64_t)kSelThreads * kU) {
+                const int64_t i0 = b0 + (int64_t)tid * kU;
                 uint64_t kk[kU];
+                if (i0 + kU <= len) {
+                    const ulonglong2* src = reinterpret_cast<const ulonglong2*>(keys + i0);
 #pragma unroll
-                for (int u = 0; u < kU; ++u) {
-                    const int64_t i = b0 + (int64_t)u * blockDim.x + threadIdx.x;
-                    kk[u] = i < len ? keys[i] : ~0ull;
+                    for (int u = 0; u < kU / 2; ++u) {
+                        const ulonglong2 x = src[u];
+                        kk[2 * u] = x.x;
+                        kk[2 * u + 1] = x.y;
+                    }
+                } else {
+#pragma unroll
+                    for (int u = 0; u < kU; ++u) kk[u] = (i0 + u < len) ? keys[i0 + u] : ~0ull;
                 }
+                int c = 0;
+#pragma unroll
+                for (int u = 0; u < kU; ++u) c += (kk[u] <= theta && i0 + u < len) ? 1 : 0;
+                int x = c;  // warp inclusive scan
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int y = __shfl_up_sync(0xffffffffu, x, o);
+                    if (lane >= o) x += y;
+                }
+                if (lane == 31) s_wsum[warp] = x;
+                __syncthreads();
+                int wbase = 0, total = 0;
+#pragma unroll
+                for (int w = 0; w < kSelThreads / 32; ++w) {
+                    const int v = s_wsum[w];
+                    wbase += (w < warp) ? v : 0;
+                    total += v;
+                }
+                int pos = s_count + wbase + x - c;
 #pragma unroll
                 for (int u = 0; u < kU; ++u) {
-                    const int64_t i = b0 + (int64_t)u * blockDim.x + threadIdx.x;
-                    const bool take = i < len && kk[u] <= theta;
-                    const unsigned m = __ballot_sync(0xffffffffu, take);
-                    int base = 0;
-                    if ((threadIdx.x & 31) == 0 && m) base = atomicAdd(&s_count, __popc(m));
-                    base = __shfl_sync(0xffffffffu, base, 0);
-                    if (take) {
-                        const int slot = base + __popc(m & ((1u << (threadIdx.x & 31)) - 1));
-                        if (slot < kSelCap) {
-                            sk[slot] = kk[u];
-                            si[slot] = (uint32_t)i;
+                    if (kk[u] <= theta && i0 + u < len) {
+                        if (pos < kSelCap) {
+                            sm.cand.k[pos] = kk[u];
+                            sm.cand.i[pos] = (uint32_t)(i0 + u);
                         }
+                        ++pos;
                     }
                 }
+                __syncthreads();  // s_wsum reusable, s_count read by all
+                if (tid == 0) s_count += total;
             }
             __syncthreads();
-            const int c = s_count;
-            __syncthreads();
-            if (c >= tt && c <= kSelCap) {
+            const int cnt = s_count;
+            if (cnt >= tt && cnt <= kSelCap) {
                 ok = true;
-                count = c;
-            } else if (c < tt) {
-                if (last_sample) { count = min(c, kSelCap); ok = true; if (threadIdx.x == 0) atomicExch(flags, 1); }
+                count = cnt;
+            } else if (cnt < tt) {
+                if (last_sample) {
+                    count = min(cnt, kSelCap);
+                    ok = true;
+                    if (tid == 0) atomicExch(flags, 1);
+                }
                 want *= 2.0;
             } else {
                 want = 0.5 * (want + (double)tt);
                 if (want < tt + 1) want = tt + 1;
             }
-            if (!ok) {
-                // the sample was overwritten by the collection: resample
-                for (int e = threadIdx.x; e < kSelSample; e += blockDim.x) {
-                    const int run = e / 16, off = e % 16;
-                    const int64_t pos = (int64_t)run * (len / 128) + off;
-                    sk[e] = keys[pos];
-                    si[e] = (uint32_t)e;
-                }
-                __syncthreads();
-                bitonic_sort_smem(sk, si, kSelSample);
-            }
         }
         if (!ok) {
             count = kSelCap;
-            if (threadIdx.x == 0) atomicExch(flags, 1);
+            if (tid == 0) atomicExch(flags, 1);
+        }
+#pragma unroll
+        for (int e = 0; e < kSelItems; ++e) {
+            const int i = tid * kSelItems + e;
+            ck[e] = i < count ? sm.cand.k[i] : ~0ull;
+            ci[e] = i < count ? sm.cand.i[i] : 0xffffffffu;
         }
     }
-    // sort the collected keys and emit the first tt indices
-    int np2 = 1;
-    while (np2 < count) np2 <<= 1;
-    for (int i = count + threadIdx.x; i < np2; i += blockDim.x) {
-        sk[i] = ~0ull;
-        si[i] = 0xffffffffu;
+    // radix sort restricted to the bits where candidates differ (pads ~0 stay last)
+    if (tid == 0) {
+        s_or = 0ull;
+        s_theta = ck[0];  // reference key: candidate 0
     }
     __syncthreads();
-    bitonic_sort_smem(sk, si, np2);
-    for (int64_t i = threadIdx.x; i < tt; i += blockDim.x) out[i] = (int32_t)si[i];
+    unsigned long long diff = 0ull;
+    const uint64_t ref = s_theta;
+#pragma unroll
+    for (int e = 0; e < kSelItems; ++e)
+        if (ci[e] != 0xffffffffu) diff |= (ck[e] ^ ref);
+    for (int o = 16; o > 0; o >>= 1) diff |= __shfl_xor_sync(0xffffffffu, diff, o);
+    if (lane == 0 && diff) atomicOr(&s_or, diff);
+    __syncthreads();  // also: candidate buffer fully read before the sort reuses it
+    const unsigned long long all = s_or;
+    const int end_bit = all ? 64 - __clzll((long long)all) : 1;
+    SelSort(sm.sort).Sort(ck, ci, 0, end_bit);
+#pragma unroll
+    for (int e = 0; e < kSelItems; ++e) {
+        const int64_t r = (int64_t)tid * kSelItems + e;
+        if (r < tt) out[r] = (int32_t)ci[e];
+    }
 }
 
 struct PlanWs {
@@ -933,7 +965,7 @@ cudaError_t launch_plan_topk(const Geo& g, const void* q, const void* k, int32_t
     }
     if (g.N > 1) {
         if ((err = launch_kv_score(g, k, ws.q_mean, ws.key0, st)) != cudaSuccess) return err;
-        const size_t ssm = (sizeof(uint64_t) + sizeof(uint32_t)) * kSelCap;
+        const size_t ssm = sizeof(SelSmem);
         cudaFuncSetAttribute(select_topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssm);
         select_topk_kernel<<<(unsigned)(g.z * g.hq * (g.N - 1)), kSelThreads, ssm, st>>>(g, ws.key0, topt,
                                                                                         kvtop, flags);
