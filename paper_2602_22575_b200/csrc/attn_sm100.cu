@@ -162,8 +162,13 @@ __device__ __forceinline__ PairInfo pair_info(const TcParams& p, int64_t idx) {
         else { P.n = g.N - 1; P.ti[0] = r - full; }
         P.ti[1] = -1;
     } else {
-        P.zh = idx / p.pairs_per_head;
-        const int64_t r = idx % p.pairs_per_head;
+        // The q heads of a GQA group share K/V: interleave them (head fastest) so the group's
+        // CTAs walk the same segment's K/V rows at the same time and hit L2 together.
+        const int64_t G = g.group;
+        const int64_t zg = idx / (p.pairs_per_head * G);
+        const int64_t rem = idx % (p.pairs_per_head * G);
+        P.zh = zg * G + rem % G;
+        const int64_t r = rem / G;
         const int64_t full = (g.N - 1) * p.pairs_full;
         int64_t pi, tcount;
         if (r < full) { P.n = r / p.pairs_full; pi = r % p.pairs_full; tcount = a.T; }

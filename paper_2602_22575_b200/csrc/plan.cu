@@ -158,19 +158,20 @@ q_rank_kernel(const void* __restrict__ q, Geo g, const float* __restrict__ guide
     for (int64_t i = threadIdx.x; i < len; i += blockDim.x) out[i] = (int32_t)res[i];
 }
 
-// Fast q ranking for the product shape (bf16, D = 128, 16-B aligned rows): 512 threads per
-// (zh, n). Rows stream through two shared buffers of 256 rows (odd 65-word row stride: the
-// per-row dot and the per-column sum both read conflict-free). Every thread prefetches 1/512
-// of chunk c+1 into registers (64 KB in flight per SM) while warps 0-7 score the 256 rows of
-// chunk c (one row per thread, fp64 sequential over d) and warps 8-11 extend the 128 column
-// sums (fp64 sequential over rows). Same arithmetic, same order as q_rank_kernel /
-// mean_pool_rows + dot_f.
-constexpr int kQF_Threads = 512;
-constexpr int kQF_Rows = 256;
+// Fast q ranking for the product shape (bf16, D = 128, 16-B aligned rows): 256 threads per
+// (zh, n), 3 CTAs per SM. Rows stream through two shared buffers of 128 rows (odd 65-word row
+// stride: the per-row dot and the per-column sum both read conflict-free). Every thread
+// prefetches 1/256 of chunk c+1 into registers while warps 0-3 score the 128 rows of chunk c
+// (one row per thread, fp64 sequential over d) and warps 4-7 extend the 128 column sums (fp64
+// sequential over rows). The sort buffers reuse the staging memory. Same arithmetic, same
+// order as q_rank_kernel / mean_pool_rows + dot_f.
+constexpr int kQF_Threads = 256;
+constexpr int kQF_Rows = 128;
 constexpr int kQF_W = 65;  // 32-bit words per staged row (64 used)
 constexpr int kQF_Per = kQF_Rows * 16 / kQF_Threads;  // 16-B pieces per thread per chunk (8)
-constexpr size_t kQF_Smem = sizeof(uint32_t) * 2 * kQF_Rows * kQF_W + (2 * sizeof(uint64_t) + 2 * sizeof(uint32_t)) * kRun +
-                            sizeof(double) * 128;
+constexpr size_t kQF_Stage = sizeof(uint32_t) * 2 * kQF_Rows * kQF_W;
+constexpr size_t kQF_Sort = (2 * sizeof(uint64_t) + 2 * sizeof(uint32_t)) * kRun;
+constexpr size_t kQF_Smem = sizeof(double) * 128 + (kQF_Stage > kQF_Sort ? kQF_Stage : kQF_Sort);
 
 // Register-prefetched staging of 256 bf16 rows of 128 columns (row stride `rs` elements).
 struct RowStager {
@@ -211,16 +212,16 @@ __device__ __forceinline__ double column_sum(const uint32_t* buf, int col, int c
     return acc;
 }
 
-__global__ void __launch_bounds__(kQF_Threads, 1)
+__global__ void __launch_bounds__(kQF_Threads, 3)
 q_rank128_kernel(const __nv_bfloat16* __restrict__ q, Geo g, const float* __restrict__ guide,
                  float* __restrict__ q_mean, uint64_t* __restrict__ qkey, int32_t* __restrict__ q_perm) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    uint32_t* stage = reinterpret_cast<uint32_t*>(smem_raw);                  // [2][256][65]
-    uint64_t* sk0 = reinterpret_cast<uint64_t*>(stage + 2 * kQF_Rows * kQF_W);  // [kRun]
-    uint64_t* sk1 = sk0 + kRun;
+    double* gd = reinterpret_cast<double*>(smem_raw);        // [128]
+    uint32_t* stage = reinterpret_cast<uint32_t*>(gd + 128);  // [2][128][65]; after the row loop:
+    uint64_t* sk0 = reinterpret_cast<uint64_t*>(gd + 128);    // sort buffers (keys round-trip
+    uint64_t* sk1 = sk0 + kRun;                               // through qkey, L2-resident)
     uint32_t* si0 = reinterpret_cast<uint32_t*>(sk1 + kRun);
     uint32_t* si1 = si0 + kRun;
-    double* gd = reinterpret_cast<double*>(si1 + kRun);                         // [128]
     const int tid = threadIdx.x;
     const int64_t zh = blockIdx.x / g.N;
     const int64_t n = blockIdx.x % g.N;
@@ -241,7 +242,7 @@ q_rank128_kernel(const __nv_bfloat16* __restrict__ q, Geo g, const float* __rest
         const int cn = min(kQF_Rows, len - r0);
         const uint32_t* buf = stage + (c & 1) * kQF_Rows * kQF_W;
         if (c + 1 < nchunks) rows.fetch(qseg, g.qs[2], r0 + kQF_Rows, len);
-        if (tid < 256) {
+        if (tid < 128) {
             if (tid < cn) {
                 const uint32_t* row = buf + tid * kQF_W;
                 double acc = 0.0;
@@ -251,26 +252,20 @@ q_rank128_kernel(const __nv_bfloat16* __restrict__ q, Geo g, const float* __rest
                     acc = fma((double)__uint_as_float(x << 16), gd[2 * w], acc);
                     acc = fma((double)__uint_as_float(x & 0xffff0000u), gd[2 * w + 1], acc);
                 }
-                const uint64_t key = desc_key(acc);
-                const int pos = r0 + tid;
-                if (local_sort) {
-                    sk0[pos] = key;
-                    si0[pos] = (uint32_t)pos;
-                } else {
-                    qkey[zh * g.N * g.S + n * g.S + pos] = key;
-                }
+                qkey[zh * g.N * g.S + n * g.S + r0 + tid] = desc_key(acc);
             }
-        } else if (tid < 384) {
-            col_acc = column_sum(buf, tid - 256, cn, col_acc);
+        } else {
+            col_acc = column_sum(buf, tid - 128, cn, col_acc);
         }
         if (c + 1 < nchunks) rows.stash(stage + ((c + 1) & 1) * kQF_Rows * kQF_W);
         __syncthreads();
     }
-    if (tid >= 256 && tid < 384) q_mean[(zh * g.N + n) * 128 + (tid - 256)] = (float)(col_acc * (1.0 / (double)len));
+    if (tid >= 128) q_mean[(zh * g.N + n) * 128 + (tid - 128)] = (float)(col_acc * (1.0 / (double)len));
     if (!local_sort) return;
-    for (int i = len + tid; i < kRun; i += kQF_Threads) {
-        sk0[i] = ~0ull;
-        si0[i] = 0xffffffffu;
+    const uint64_t* kseg = qkey + zh * g.N * g.S + n * g.S;
+    for (int i = tid; i < kRun; i += kQF_Threads) {
+        sk0[i] = i < len ? kseg[i] : ~0ull;
+        si0[i] = i < len ? (uint32_t)i : 0xffffffffu;
     }
     __syncthreads();
     const int which = block_merge_sort<kQF_Threads, kRun / kQF_Threads>(sk0, si0, sk1, si1);
