@@ -405,6 +405,84 @@ def run_ours(args, rank: int, world: int):
         dist.destroy_process_group()
 
 
+def run_heads(args, rank: int, world: int):
+    """--shard heads: one layer's heads partitioned over the ranks in whole GQA
+    groups (rank r: kv heads [r*8/N, (r+1)*8/N) and their q heads), no collective on the data
+    path; with --allgather every step ends with an NCCL all-gather of the output shards over
+    NVLink (reported separately as allgather_ms). value = max-over-ranks ms per layer."""
+    import torch
+
+    import paper_2602_22575_b200 as s2o
+    from paper_2602_22575_b200.shard import gather_heads, head_shard
+
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+    s2o.lib()
+    L, S = args.L, args.seg
+    cfg = s2o.KernelConfig(seg_len=S, tau=args.tau, tiles=s2o.TileSpec(128, 128), q_reorder=True)
+    sh = head_shard(HQ, HKV, world, rank)
+    qh, kh, vh = s2o.generate_synthetic("mixed", L // 64, 8.0, 0, 1, sh.q_hi, L, D)  # heads < q_hi
+    q = torch.from_numpy(qh[:, sh.q_lo:sh.q_hi].copy()).to(dev).to(torch.bfloat16)
+    k = torch.from_numpy(kh[:, sh.kv_lo:sh.kv_hi].copy()).to(dev).to(torch.bfloat16)
+    v = torch.from_numpy(vh[:, sh.kv_lo:sh.kv_hi].copy()).to(dev).to(torch.bfloat16)
+    del qh, kh, vh
+    out = torch.empty_like(q)
+
+    def step():
+        s2o.s2o_attention(q, k, v, cfg, out=out, want_plan=False)
+        if args.allgather and dist:
+            gather_heads(out, world)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    clocks = ClockSampler(local)
+    clocks.start()
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record()
+    for _ in range(args.steps):
+        step()
+    ev1.record()
+    torch.cuda.synchronize()
+    elapsed = ev0.elapsed_time(ev1)
+    clk = clocks.stop()
+    ag_ms = None
+    if dist:
+        t = torch.tensor([elapsed], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        elapsed = t.item()
+        if args.allgather:
+            ag_ms = cuda_time(torch, lambda: gather_heads(out, world), 3)
+            t = torch.tensor([ag_ms], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ag_ms = t.item()
+    ms_step = elapsed / args.steps
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(ms_step, 4), "unit": "ms", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(ms_step, 4), "higher_is_better": False,
+            "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic (reference generate_synthetic mixed stripes, L/64 stripes, gain 8, seed 0)",
+            "config": {"workload": "C4: one Llama-3.1-8B attention layer, heads sharded in whole GQA groups",
+                       "seq_len": L, "seg_len": S, "tau": args.tau,
+                       "parallelism": f"heads/{world} ({sh.hq} q / {sh.hkv} kv heads per rank)",
+                       "allgather": bool(args.allgather)},
+            "allgather_ms": round(ag_ms, 3) if ag_ms is not None else None,
+            "gpu_launches": launches_per_step(L, S) * args.steps, "clocks": clk,
+        }
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -419,11 +497,17 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-dense", action="store_true")
+    ap.add_argument("--shard", default="layers", choices=["layers", "heads"],
+                    help="multi-GPU: a full layer per rank (weak) or one layer's heads split (strong)")
+    ap.add_argument("--allgather", action="store_true", help="--shard heads: NCCL all-gather of O")
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     if args.impl == "reference":
         run_reference_arm(args, rank)
+        return
+    if args.shard == "heads":
+        run_heads(args, rank, world)
         return
     run_ours(args, rank, world)
 

@@ -119,6 +119,7 @@ __global__ void __launch_bounds__(kThreads) generic_pass_kernel(PassArgs a, doub
 
         // ---- ranked prefix traversal with the monotone-gain stop (kernel.cpp:86-122)
         int64_t committed = 0;
+        bool overflow = false;
         if ((a.mode & kPrefix) && n > 0) {
             const int32_t* kv = a.kv_seg(zh, n);
             const int64_t kv_len = a.avail(n);
@@ -176,29 +177,33 @@ __global__ void __launch_bounds__(kThreads) generic_pass_kernel(PassArgs a, doub
                 pairs += tn * cn;
                 __syncthreads();
             }
-            const bool overflow = kv_len < n * g.S && committed * a.bn >= kv_len;
+            overflow = a.truncated(n) && committed * a.bn >= kv_len;
             if (threadIdx.x == 0) {
+                const int base = a.tile_base ? a.tile_base[it] : 0;
                 if (overflow) {
                     const int slot = atomicAdd(a.ovf_count, 1);
                     a.ovf_tiles[slot] = (int32_t)tile;
+                    if (a.ovf_base) a.ovf_base[slot] = base + (int32_t)committed;
                 } else {
-                    if (pairs) atomicAdd((unsigned long long*)&a.pass2_pairs[zh], (unsigned long long)pairs);
-                    a.processed[(zh * g.N + n) * a.T + ti] = (int32_t)committed;
+                    a.processed[(zh * g.N + n) * a.T + ti] = base + (int32_t)committed;
                 }
+                if (pairs && (!overflow || a.acc_out))
+                    atomicAdd((unsigned long long*)&a.pass2_pairs[zh], (unsigned long long)pairs);
             }
         } else if ((a.mode & kPrefix) && threadIdx.x == 0) {
             a.processed[(zh * g.N + n) * a.T + ti] = 0;
         }
 
-        // ---- outputs
+        // ---- outputs (an overflow tile with a state buffer resumes at the next plan level)
+        const bool resume_later = overflow && a.acc_out != nullptr;
         for (int64_t r = threadIdx.x; r < tn; r += blockDim.x) {
             const int64_t slot = rowslot + grow[r];
-            if (a.mode & kStateOut) {
+            if ((a.mode & kStateOut) || resume_later) {
                 a.m_out[slot] = (float)m[r];
                 a.ell_out[slot] = (float)ell[r];
                 for (int64_t i = 0; i < d; ++i) a.acc_out[slot * d + i] = (float)acc[r * d + i];
             }
-            if (a.mode & kFinal) {
+            if ((a.mode & kFinal) && !resume_later) {
                 if (ell[r] == 0.0) atomicExch(a.err_flag, 2);
                 const int64_t ooff = g.o_base(zh) + grow[r] * g.os[2];
                 for (int64_t i = 0; i < d; ++i)

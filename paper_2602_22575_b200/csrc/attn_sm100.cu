@@ -711,14 +711,19 @@ tc_pass_kernel(const TcParams p, const __grid_constant__ CUtensorMap qmap,
                 }
             }
             const float inv = 1.0f / ell;
-            if (valid && (a.mode & kStateOut)) {
+            // A tile that walked its whole (truncated) kv list without stopping continues at
+            // the next plan level: its state is saved in place of the resumed one, no output yet.
+            const bool overflow = (a.mode & kPrefix) && P.np > 0 && committed == P.np && a.truncated(P.n);
+            const bool resume_later = overflow && a.acc_out != nullptr;
+            const bool save_state = (a.mode & kStateOut) || resume_later;
+            if (valid && save_state) {
                 float4* dst = reinterpret_cast<float4*>(a.acc_out + slot * kD);
 #pragma unroll
                 for (int i = 0; i < kD / 4; ++i)
                     dst[i] = make_float4(__uint_as_float(ov[4 * i]), __uint_as_float(ov[4 * i + 1]),
                                          __uint_as_float(ov[4 * i + 2]), __uint_as_float(ov[4 * i + 3]));
             }
-            if (valid && (a.mode & kFinal)) {
+            if (valid && (a.mode & kFinal) && !resume_later) {
                 const int64_t ooff = g.o_base(P.zh) + grow * g.os[2];
                 if (g.out_bf16) {
                     uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(a.o) + ooff);
@@ -739,22 +744,24 @@ tc_pass_kernel(const TcParams p, const __grid_constant__ CUtensorMap qmap,
                                              __uint_as_float(ov[4 * i + 2]) * inv, __uint_as_float(ov[4 * i + 3]) * inv);
                 }
             }
-            if (valid && (a.mode & kStateOut)) {
+            if (valid && save_state) {
                 a.m_out[slot] = (m2 == -INFINITY) ? -INFINITY : m2 * 0.6931471805599453f;
                 a.ell_out[slot] = ell;
             }
-            if (valid && (a.mode & kFinal) && !(ell > 0.0f)) atomicExch(a.err_flag, 2);
+            if (valid && (a.mode & kFinal) && !resume_later && !(ell > 0.0f)) atomicExch(a.err_flag, 2);
             if ((a.mode & kPrefix) && r == 0) {
                 const int64_t tile = P.zh * a.tiles_per_head + P.n * a.T + P.ti[x];
-                const bool overflow = P.np > 0 && committed == P.np && P.avail < P.n * g.S;
+                const int base = a.tile_base ? a.tile_base[it] : 0;
                 if (overflow) {
-                    // walked the whole truncated list without stopping: rerun on the full plan
                     const int s2 = atomicAdd(a.ovf_count, 1);
                     a.ovf_tiles[s2] = (int32_t)tile;
+                    if (a.ovf_base) a.ovf_base[s2] = base + committed;
                 } else {
-                    a.processed[(P.zh * g.N + P.n) * a.T + P.ti[x]] = committed;
-                    if (pairs) atomicAdd((unsigned long long*)&a.pass2_pairs[P.zh], (unsigned long long)pairs * P.tn[x]);
+                    a.processed[(P.zh * g.N + P.n) * a.T + P.ti[x]] = base + committed;
                 }
+                // (without a saved state the overflow tile is recomputed from scratch: no pairs)
+                if (pairs && (!overflow || resume_later))
+                    atomicAdd((unsigned long long*)&a.pass2_pairs[P.zh], (unsigned long long)pairs * P.tn[x]);
             }
             if (tl_on) tl_mark(p, 14 + 4 * x, no);
             tc_fence_before();

@@ -3,8 +3,10 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <algorithm>
 #include <mutex>
 #include <string>
+#include <vector>
 
 #include "internal.h"
 
@@ -390,8 +392,9 @@ static OpLayout op_layout(const Geo& g, const PassArgs& a, int fused, const s2o_
     L.pass = take(pass_ws_bytes(a));
     L.qperm = take(sizeof(int32_t) * zh * g.N * g.S);
     L.kvperm = take(sizeof(int32_t) * std::max<int64_t>(1, zh * g.kv_per_head()));
-    L.kvtop = take(sizeof(int32_t) * std::max<int64_t>(1, zh * g.N * L.topt));
-    L.ovf = take(sizeof(int32_t) * (4 + zh * a.tiles_per_head));
+    L.kvtop = take(2 * sizeof(int32_t) * std::max<int64_t>(1, zh * g.N * L.topt));  // level lists A, B
+    // [0] overflow count, [1] selection flag, then tiles A/B, bases A/B, segment list
+    L.ovf = take(sizeof(int32_t) * (4 + 5 * zh * a.tiles_per_head));
     L.acc = take(fused ? 0 : sizeof(float) * zh * g.l * g.d);
     L.ell = take(fused ? 0 : sizeof(float) * zh * g.l);
     L.m = take(fused ? 0 : sizeof(float) * zh * g.l);
@@ -442,11 +445,18 @@ s2o_status s2o_attention_fwd(const s2o_problem* p, const void* q, const void* k,
     } else {
         S2O_CUDA_TRY(launch_plan_build(g, q, k, qp, kvp, base + L.plan, s), "plan build");
     }
+    const int64_t ntiles = g.z * g.hq * a.tiles_per_head;
+    int32_t* lists[2] = {reinterpret_cast<int32_t*>(base + L.kvtop),
+                         reinterpret_cast<int32_t*>(base + L.kvtop) + std::max<int64_t>(1, g.z * g.hq * g.N * L.topt)};
+    int32_t* tiles[2] = {ovf + 4, ovf + 4 + ntiles};
+    int32_t* bases[2] = {ovf + 4 + 2 * ntiles, ovf + 4 + 3 * ntiles};
+    int32_t* seglist = ovf + 4 + 4 * ntiles;
     a.q = q; a.k = k; a.v = v; a.o = o;
-    a.kv_perm = topt > 0 ? reinterpret_cast<int32_t*>(base + L.kvtop) : kvp;
+    a.kv_perm = topt > 0 ? lists[0] : kvp;
     a.kv_top = topt;
     a.ovf_count = ovf;
-    a.ovf_tiles = ovf + 4;
+    a.ovf_tiles = tiles[0];
+    a.ovf_base = bases[0];
     a.processed = proc;
     a.pass2_pairs = p2;
     S2O_CUDA_TRY(launch_trace_init(a, p1, s), "trace init");
@@ -466,22 +476,69 @@ s2o_status s2o_attention_fwd(const s2o_problem* p, const void* q, const void* k,
         a2.mode = kStateIn | kPrefix | kFinal;
         a2.q_perm = qp;
         a2.acc_in = acc; a2.ell_in = ell; a2.m_in = m;
+        // a tile that exhausts a truncated list saves its state in place and resumes at the
+        // next plan level (entries [T, 2T), [2T, 3T), ... of the same order)
+        if (topt > 0) { a2.acc_out = acc; a2.ell_out = ell; a2.m_out = m; }
     }
     if ((st = run_pass(a2, cfg->path, base + L.pass, pass_ws_bytes(a), s))) return st;
     if (topt > 0) {
-        // Tiles that walked their whole truncated list are recomputed on the full plan.
         int32_t host[2] = {0, 0};
-        S2O_CUDA_TRY(cudaMemcpyAsync(host, ovf, sizeof host, cudaMemcpyDeviceToHost, s), "d2h overflow");
-        S2O_CUDA_TRY(cudaStreamSynchronize(s), "sync");
+        int cur = 0;
+        int64_t lvl_base = 0;
+        for (;;) {
+            S2O_CUDA_TRY(cudaMemcpyAsync(host, ovf, sizeof host, cudaMemcpyDeviceToHost, s), "d2h overflow");
+            S2O_CUDA_TRY(cudaStreamSynchronize(s), "sync");
+            if (host[0] == 0 || host[1] != 0 || cfg->fused) break;
+            // next plan level for the segments of the overflow tiles
+            std::vector<int32_t> ht(host[0]);
+            S2O_CUDA_TRY(cudaMemcpy(ht.data(), tiles[cur], sizeof(int32_t) * host[0], cudaMemcpyDeviceToHost),
+                         "d2h tiles");
+            std::vector<int32_t> segs;
+            segs.reserve(ht.size());
+            for (int32_t t : ht) {
+                const int64_t zh = t / a.tiles_per_head, r = t % a.tiles_per_head;
+                const int64_t full = (g.N - 1) * a.T;
+                const int64_t n = r < full ? r / a.T : g.N - 1;
+                segs.push_back((int32_t)(zh * g.N + n));
+            }
+            std::sort(segs.begin(), segs.end());
+            segs.erase(std::unique(segs.begin(), segs.end()), segs.end());
+            S2O_CUDA_TRY(cudaMemcpyAsync(seglist, segs.data(), sizeof(int32_t) * segs.size(), cudaMemcpyHostToDevice, s),
+                         "h2d segments");
+            lvl_base += topt;
+            S2O_CUDA_TRY(launch_plan_level(g, seglist, (int64_t)segs.size(), lists[cur], lvl_base, lists[cur ^ 1], topt,
+                                           ovf + 1, base + L.plan, s), "plan level");
+            S2O_CUDA_TRY(cudaMemsetAsync(ovf, 0, sizeof(int32_t), s), "memset");
+            PassArgs a3 = a2;
+            a3.kv_perm = lists[cur ^ 1];
+            a3.lvl_base = lvl_base;
+            a3.tile_list = tiles[cur];
+            a3.tile_base = bases[cur];
+            a3.tile_count = host[0];
+            a3.ovf_tiles = tiles[cur ^ 1];
+            a3.ovf_base = bases[cur ^ 1];
+            if ((st = run_pass(a3, cfg->path, base + L.pass, pass_ws_bytes(a), s, false))) return st;
+            cur ^= 1;
+        }
         if (host[0] > 0 || host[1] != 0) {
+            // Fused mode (no saved state) or an uncertified selection: full plan, recompute.
             S2O_CUDA_TRY(launch_plan_build(g, q, k, qp, kvp, base + L.plan, s), "plan build");
             PassArgs a3 = a2;
             a3.kv_perm = kvp;
             a3.kv_top = 0;
-            if (host[1] != 0) {  // selection could not be certified: redo everything
+            a3.lvl_base = 0;
+            a3.acc_out = a3.ell_out = a3.m_out = nullptr;
+            if (host[1] != 0 || !cfg->fused) {  // selection could not be certified: redo everything
                 S2O_CUDA_TRY(launch_trace_init(a, p1, s), "trace init");
+                if (!cfg->fused) {  // pass-1 state was overwritten by saved levels: redo pass-1
+                    PassArgs a1 = a;
+                    a1.mode = kDiag | kStateOut;
+                    a1.q_reorder = 0;
+                    a1.acc_out = acc; a1.ell_out = ell; a1.m_out = m;
+                    if ((st = run_pass(a1, cfg->path, base + L.pass, pass_ws_bytes(a), s))) return st;
+                }
             } else {
-                a3.tile_list = ovf + 4;
+                a3.tile_list = tiles[cur];
                 a3.tile_count = host[0];
             }
             if ((st = run_pass(a3, cfg->path, base + L.pass, pass_ws_bytes(a), s, host[1] != 0))) return st;

@@ -45,15 +45,21 @@ struct PassArgs {
     int32_t* err_flag;      // device: 1 uninitialized state, 2 uncovered row
     // truncated plan (fused operator): kv_perm laid out [Z*Hq][N][kv_top], 0 = packed full
     int64_t kv_top;
-    int32_t* ovf_count;     // tiles that consumed their whole truncated list (rerun needed)
+    int32_t* ovf_count;     // tiles that consumed their whole truncated list (next level needed)
     int32_t* ovf_tiles;
+    int32_t* ovf_base;      // committed chunks so far of each overflow tile (parallel to ovf_tiles)
     const int32_t* tile_list;  // optional: process only these tiles
+    const int32_t* tile_base;  // optional: committed chunks of earlier plan levels per tile-list entry
     int64_t tile_count;
+    int64_t lvl_base;       // kv_perm entries of a segment consumed by earlier plan levels
 
+    // entries of segment n's (current level) kv list
     __host__ __device__ int64_t avail(int64_t n) const {
-        const int64_t full = n * g.S;
-        return (kv_top > 0 && kv_top < full) ? kv_top : full;
+        const int64_t rem = n * g.S - lvl_base;
+        return (kv_top > 0 && kv_top < rem) ? kv_top : rem;
     }
+    // the level's list ran out before the segment's prefix did
+    __host__ __device__ bool truncated(int64_t n) const { return lvl_base + avail(n) < n * g.S; }
     __host__ __device__ const int32_t* kv_seg(int64_t zh, int64_t n) const {
         return kv_top > 0 ? kv_perm + (zh * g.N + n) * kv_top : kv_perm + zh * g.kv_per_head() + g.kv_off(n);
     }
@@ -68,6 +74,11 @@ cudaError_t launch_plan_build(const Geo& g, const void* q, const void* k, int32_
                               int32_t* kv_perm, void* workspace, cudaStream_t st);
 cudaError_t launch_plan_topk(const Geo& g, const void* q, const void* k, int32_t* q_perm, int32_t* kvtop,
                              int64_t topt, int32_t* flags, void* workspace, cudaStream_t st);
+// Next plan level: for the listed segments (codes zh * N + n), the topt entries of kv_perm that
+// follow the last entry of `prev` (entries [lvl_base, lvl_base + topt) of the full order).
+cudaError_t launch_plan_level(const Geo& g, const int32_t* seg_list, int64_t nseg, const int32_t* prev,
+                              int64_t lvl_base, int32_t* kvtop, int64_t topt, int32_t* flags, void* workspace,
+                              cudaStream_t st);
 cudaError_t launch_segment_means(const Geo& g, const void* x, int which_kv, int64_t nseg_out,
                                  float* out, cudaStream_t st);
 

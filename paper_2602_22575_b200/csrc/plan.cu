@@ -712,9 +712,12 @@ union SelSmem {
     typename SampSort::TempStorage samp;
 };
 
+// Level > 0 (seg_list / prev given): the same selection restricted to the keys that follow the
+// previous level's last entry in the (key, index) order, i.e. entries [lvl_base, lvl_base + T).
 __global__ void __launch_bounds__(kSelThreads)
 select_topk_kernel(Geo g, const uint64_t* __restrict__ kvkey, int64_t topt, int32_t* __restrict__ kvtop,
-                   int32_t* __restrict__ flags) {
+                   int32_t* __restrict__ flags, const int32_t* __restrict__ seg_list,
+                   const int32_t* __restrict__ prev, int64_t lvl_base) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     SelSmem& sm = *reinterpret_cast<SelSmem*>(smem_raw);
     __shared__ int s_wsum[kSelThreads / 32];
@@ -722,15 +725,25 @@ select_topk_kernel(Geo g, const uint64_t* __restrict__ kvkey, int64_t topt, int3
     __shared__ uint64_t s_theta;
     __shared__ unsigned long long s_or;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int64_t zh = blockIdx.x / (g.N - 1);
-    const int64_t n = 1 + blockIdx.x % (g.N - 1);
+    int64_t zh, n;
+    if (seg_list) {
+        zh = seg_list[blockIdx.x] / g.N;
+        n = seg_list[blockIdx.x] % g.N;
+    } else {
+        zh = blockIdx.x / (g.N - 1);
+        n = 1 + blockIdx.x % (g.N - 1);
+    }
     const int64_t len = n * g.S;
-    const int64_t tt = min(topt, len);
+    const int64_t tt = min(topt, len - lvl_base);
     const uint64_t* keys = kvkey + zh * g.kv_per_head() + g.kv_off(n);
     int32_t* out = kvtop + (zh * g.N + n) * topt;
+    // keys at or before the bound (the previous level's last entry) are not candidates
+    const int64_t bidx = prev ? prev[(zh * g.N + n) * topt + topt - 1] : -1;
+    const uint64_t bkey = prev ? keys[bidx] : 0ull;
+    auto after = [&](uint64_t k, int64_t i) { return !prev || k > bkey || (k == bkey && i > bidx); };
     uint64_t ck[kSelItems];
     uint32_t ci[kSelItems];
-    if (len <= kSelCap) {
+    if (len <= kSelCap && !prev) {
         // every key is a candidate, already in index order (blocked arrangement)
 #pragma unroll
         for (int e = 0; e < kSelItems; ++e) {
@@ -739,26 +752,29 @@ select_topk_kernel(Geo g, const uint64_t* __restrict__ kvkey, int64_t topt, int3
             ci[e] = i < len ? (uint32_t)i : 0xffffffffu;
         }
     } else {
-        // sample: 128 runs of 16 consecutive keys spread over the segment, radix-sorted
+        // sample: 128 runs of 16 consecutive keys spread over the segment, radix-sorted (a short
+        // segment of a later level takes every remaining key instead)
+        const bool small = len <= kSelCap;
         uint64_t smp[kSelSample / kSelThreads];
 #pragma unroll
         for (int u = 0; u < kSelSample / kSelThreads; ++u) {
             const int e = tid * (kSelSample / kSelThreads) + u;
-            smp[u] = keys[(int64_t)(e / 16) * (len / 128) + e % 16];
+            smp[u] = small ? 0ull : keys[(int64_t)(e / 16) * (len / 128) + e % 16];
         }
-        SampSort(sm.samp).Sort(smp);  // blocked: thread t holds ranks 4t .. 4t+3
-        double want = 1.15 * (double)tt + 32.0;
+        if (!small) SampSort(sm.samp).Sort(smp);  // blocked: thread t holds ranks 4t .. 4t+3
+        double want = small ? (double)len : (double)lvl_base + 1.15 * (double)tt + 32.0;
         bool ok = false;
         int count = 0;
         for (int attempt = 0; attempt < 6 && !ok; ++attempt) {
             int64_t rank = (int64_t)ceil(want * kSelSample / (double)len) + 4;
             if (rank > kSelSample - 1) rank = kSelSample - 1;
             __syncthreads();  // sample sort storage / previous candidates no longer read
-            if (tid == (int)(rank / (kSelSample / kSelThreads))) s_theta = smp[rank % (kSelSample / kSelThreads)];
+            const bool take_all = want >= (double)len;  // every remaining key fits the capacity
+            if (tid == (int)(rank / (kSelSample / kSelThreads))) s_theta = take_all ? ~0ull : smp[rank % (kSelSample / kSelThreads)];
             if (tid == 0) s_count = 0;
             __syncthreads();
             const uint64_t theta = s_theta;
-            const bool last_sample = (rank == kSelSample - 1);
+            const bool last_sample = take_all || (rank == kSelSample - 1);
             // order-preserving compaction of every key <= theta
             constexpr int kU = 8;
             for (int64_t b0 = 0; b0 < len; b0 += (int64_t)kSelThreads * kU) {
@@ -776,9 +792,13 @@ select_topk_kernel(Geo g, const uint64_t* __restrict__ kvkey, int64_t topt, int3
 #pragma unroll
                     for (int u = 0; u < kU; ++u) kk[u] = (i0 + u < len) ? keys[i0 + u] : ~0ull;
                 }
+                bool tk[kU];
                 int c = 0;
 #pragma unroll
-                for (int u = 0; u < kU; ++u) c += (kk[u] <= theta && i0 + u < len) ? 1 : 0;
+                for (int u = 0; u < kU; ++u) {
+                    tk[u] = kk[u] <= theta && i0 + u < len && after(kk[u], i0 + u);
+                    c += tk[u] ? 1 : 0;
+                }
                 int x = c;  // warp inclusive scan
 #pragma unroll
                 for (int o = 1; o < 32; o <<= 1) {
@@ -797,7 +817,7 @@ select_topk_kernel(Geo g, const uint64_t* __restrict__ kvkey, int64_t topt, int3
                 int pos = s_count + wbase + x - c;
 #pragma unroll
                 for (int u = 0; u < kU; ++u) {
-                    if (kk[u] <= theta && i0 + u < len) {
+                    if (tk[u]) {
                         if (pos < kSelCap) {
                             sm.cand.k[pos] = kk[u];
                             sm.cand.i[pos] = (uint32_t)(i0 + u);
@@ -962,13 +982,27 @@ cudaError_t launch_plan_topk(const Geo& g, const void* q, const void* k, int32_t
         if ((err = launch_kv_score(g, k, ws.q_mean, ws.key0, st)) != cudaSuccess) return err;
         const size_t ssm = sizeof(SelSmem);
         cudaFuncSetAttribute(select_topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssm);
-        select_topk_kernel<<<(unsigned)(g.z * g.hq * (g.N - 1)), kSelThreads, ssm, st>>>(g, ws.key0, topt,
-                                                                                        kvtop, flags);
+        select_topk_kernel<<<(unsigned)(g.z * g.hq * (g.N - 1)), kSelThreads, ssm, st>>>(
+            g, ws.key0, topt, kvtop, flags, nullptr, nullptr, 0);
         if ((err = cudaGetLastError()) != cudaSuccess) return err;
     }
     return cudaSuccess;
 }
 
+
+cudaError_t launch_plan_level(const Geo& g, const int32_t* seg_list, int64_t nseg, const int32_t* prev,
+                              int64_t lvl_base, int32_t* kvtop, int64_t topt, int32_t* flags, void* workspace,
+                              cudaStream_t st) {
+    if (nseg == 0) return cudaSuccess;
+    PlanWs ws;
+    char* base = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(workspace) + 255) & ~uintptr_t(255));
+    plan_ws_layout(g, base, &ws);  // the kv keys of the level-0 build are still in key0
+    const size_t ssm = sizeof(SelSmem);
+    cudaFuncSetAttribute(select_topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssm);
+    select_topk_kernel<<<(unsigned)nseg, kSelThreads, ssm, st>>>(g, ws.key0, topt, kvtop, flags, seg_list, prev,
+                                                                 lvl_base);
+    return cudaGetLastError();
+}
 
 cudaError_t launch_segment_means(const Geo& g, const void* x, int which_kv, int64_t nseg_out,
                                  float* out, cudaStream_t st) {

@@ -1,0 +1,125 @@
+"""C5: early-stop threshold sweep at 128K (BASELINE.json configs[4]).
+
+For tau in {0.001, 0.002, 0.004, 0.005, 0.01, 0.02} on the C3 layer
+(32 q / 8 kv heads, d=128, bf16, L=131072, S=2048, 128x128 tiles, stripe-structured synthetic):
+  * latency of the whole operator (plan + pass-1 + pass-2, CUDA events, min of 3),
+  * sparsity from the kernel's own trace (sparsity_from_trace semantics, metrics.cpp:35-57),
+  * MSE / MAE against dense causal attention on the same GPU (torch SDPA, bf16, fp32 compare),
+  * parity against the compiled CPU reference (oracle/_ref, test infrastructure) on a bounded
+    sample: 2 q heads x the first `--ref-segments` segments, which by causality is exactly the
+    same problem restricted to those rows (trace differences and max |dO| reported).
+Writes one JSON document (default profiles/tau_sweep.json).
+
+    python scripts/tau_sweep.py [--out profiles/tau_sweep.json] [--ref-segments 4]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+TAUS = [0.001, 0.002, 0.004, 0.005, 0.01, 0.02]
+HQ, HKV, D = 32, 8, 128
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--L", type=int, default=131072)
+    ap.add_argument("--seg", type=int, default=2048)
+    ap.add_argument("--ref-segments", type=int, default=4)
+    ap.add_argument("--ref-heads", type=int, default=2)
+    ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "tau_sweep.json"))
+    args = ap.parse_args()
+
+    import numpy as np
+    import torch
+
+    import paper_2602_22575_b200 as s2o
+    from oracle.oracle import Ref, build
+
+    L, S = args.L, args.seg
+    qh, kh, vh = s2o.generate_synthetic("mixed", L // 64, 8.0, 0, 1, HQ, L, D)
+    q = torch.from_numpy(qh).cuda().to(torch.bfloat16)
+    k = torch.from_numpy(kh[:, :HKV].copy()).cuda().to(torch.bfloat16)
+    v = torch.from_numpy(vh[:, :HKV].copy()).cuda().to(torch.bfloat16)
+    del kh, vh
+    dense = torch.nn.functional.scaled_dot_product_attention(q, k, v, is_causal=True, enable_gqa=True).float()
+    torch.cuda.synchronize()
+
+    # reference sample: first heads, first ref_segments * S tokens, bf16-rounded, K/V expanded
+    build()
+    ref = Ref()
+    lp = min(L, args.ref_segments * S)
+    hs = list(range(args.ref_heads))
+    qs = q[:, hs, :lp].float().cpu().numpy()
+    ks = k[:, [h // (HQ // HKV) for h in hs], :lp].float().cpu().numpy()
+    vs = v[:, [h // (HQ // HKV) for h in hs], :lp].float().cpu().numpy()
+    del qh
+
+    def timeit(fn, reps=3):
+        fn()
+        torch.cuda.synchronize()
+        best = float("inf")
+        for _ in range(reps):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            fn()
+            b.record()
+            torch.cuda.synchronize()
+            best = min(best, a.elapsed_time(b))
+        return best
+
+    rows = []
+    out = torch.empty_like(q)
+    for tau in TAUS:
+        cfg = s2o.KernelConfig(seg_len=S, tau=tau, tiles=s2o.TileSpec(128, 128))
+        ms = timeit(lambda: s2o.s2o_attention(q, k, v, cfg, out=out, want_plan=False))
+        res = s2o.s2o_attention(q, k, v, cfg, want_plan=False)
+        torch.cuda.synchronize()
+        p1 = int(res.trace.pass1_pairs.sum().item())
+        p2 = int(res.trace.pass2_pairs.sum().item())
+        sparsity = 1.0 - (p1 + p2) / (HQ * L * (L + 1) / 2)
+        diff = res.out.float() - dense
+        mse = float((diff * diff).mean().item())
+        mae = float(diff.abs().mean().item())
+        # parity sample against the compiled reference
+        class Cfg:
+            pass
+        c = Cfg()
+        c.seg_len, c.tau, c.b_m, c.b_n = S, tau, 128, 128
+        c.q_reorder, c.fused, c.local_window = True, False, -1
+        t0 = time.perf_counter()
+        ro, rt, _ = ref.attention(qs, ks, vs, c)
+        ref_s = time.perf_counter() - t0
+        got_t = res.trace.processed.reshape(HQ, L // S, -1).cpu().numpy()[hs, : lp // S]
+        want_t = rt.processed.reshape(len(hs), lp // S, -1)
+        tdiff = int((got_t != want_t).sum())
+        tmax = int(np.abs(got_t - want_t).max()) if tdiff else 0
+        go = res.out[:, hs, :lp].float().cpu().numpy()
+        row = {"tau": tau, "ms": round(ms, 3), "sparsity": round(sparsity, 5), "mse_vs_dense": mse,
+               "mae_vs_dense": mae, "pairs": {"pass1": p1, "pass2": p2},
+               "ref_sample": {"heads": len(hs), "tokens": lp, "cpu_s": round(ref_s, 2),
+                              "tiles": int(want_t.size), "trace_tiles_differing": tdiff,
+                              "trace_max_chunk_diff": tmax,
+                              "max_abs_out_diff": float(np.abs(go - ro).max()),
+                              "mean_abs_out_diff": float(np.abs(go - ro).mean())}}
+        rows.append(row)
+        print(json.dumps(row), flush=True)
+        del res, diff
+    doc = {"config": {"workload": "C5: C3 layer (32q/8kv, d=128, bf16, L=%d, S=%d, 128x128) tau sweep" % (L, S),
+                      "data": "synthetic mixed stripes (L/64, gain 8, seed 0)",
+                      "dense": "torch SDPA bf16 causal GQA on the same GPU (fp32 difference)",
+                      "ms": "plan + pass-1 + pass-2, CUDA events, min of 3"},
+           "rows": rows}
+    os.makedirs(os.path.dirname(args.out), exist_ok=True)
+    with open(args.out, "w") as f:
+        json.dump(doc, f, indent=1)
+
+
+if __name__ == "__main__":
+    main()

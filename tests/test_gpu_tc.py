@@ -152,8 +152,11 @@ def test_tc_generic_agree_at_scale(cuda):
 @pytest.mark.parametrize("path", [TC, GEN])
 def test_truncated_plan_matches_full_plan(cuda, path):
     """s2o_attention without a kv_perm output keeps only the exact top-T of each kv_perm
-    segment; tiles that exhaust it are recomputed on the full plan, so traces and outputs must
-    equal the full-plan run for any depth (tiny depths force the overflow fallback)."""
+    segment; a tile that exhausts it saves its state and resumes on the next level (entries
+    [T, 2T), ... of the same order), so traces equal the full-plan run for any depth (tiny
+    depths force many levels). Outputs agree to state-round-trip rounding (the fp32 state is
+    re-based at every level boundary): |dO| <= 1e-2 |O| + 1e-3 elementwise (one bf16 ulp is
+    2^-8 relative) and mean |dO| <= 1e-4."""
     import paper_2602_22575_b200 as s2o
     torch = cuda
     hq, hkv, l, s = 4, 2, 8192, 1024
@@ -168,12 +171,14 @@ def test_truncated_plan_matches_full_plan(cuda, path):
         torch.cuda.synchronize()
         assert torch.equal(res.trace.processed, full.trace.processed), depth
         assert torch.equal(res.trace.pass2_pairs, full.trace.pass2_pairs), depth
-        assert torch.equal(res.out, full.out), depth
+        d = (res.out.float() - full.out.float()).abs()
+        excess = (d - (1e-2 * full.out.float().abs() + 1e-3)).max().item()
+        assert excess <= 0 and d.mean().item() <= 1e-4, (depth, d.max().item(), d.mean().item())
 
 
 def test_truncated_plan_gaussian_fallback(cuda):
-    """Pure gaussian inputs never stop early: every tile exhausts its truncated list and the
-    whole pass-2 is recomputed on the full plan."""
+    """Pure gaussian inputs never stop early: every tile exhausts every truncated level and walks
+    the whole prefix level by level (fused mode instead recomputes on the full plan)."""
     import paper_2602_22575_b200 as s2o
     torch = cuda
     torch.manual_seed(0)
@@ -184,4 +189,13 @@ def test_truncated_plan_gaussian_fallback(cuda):
     res = s2o.s2o_attention(q, k, v, s2o.KernelConfig(seg_len=512, tau=0.005, plan_depth=256), want_plan=False)
     torch.cuda.synchronize()
     assert torch.equal(res.trace.processed, full.trace.processed)
-    assert torch.equal(res.out, full.out)
+    d = (res.out.float() - full.out.float()).abs()
+    excess = (d - (1e-2 * full.out.float().abs() + 1e-3)).max().item()
+    assert excess <= 0 and d.mean().item() <= 1e-4, (d.max().item(), d.mean().item())
+    fcfg = s2o.KernelConfig(seg_len=512, tau=0.005, q_reorder=False, fused=True)
+    ffull = s2o.s2o_attention(q, k, v, fcfg)
+    fcfg.plan_depth = 256
+    fres = s2o.s2o_attention(q, k, v, fcfg, want_plan=False)
+    torch.cuda.synchronize()
+    assert torch.equal(fres.trace.processed, ffull.trace.processed)
+    assert torch.equal(fres.out, ffull.out)
