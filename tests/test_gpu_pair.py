@@ -1,0 +1,59 @@
+"""The CTA-pair (tcgen05 cta_group::2) variant of the pass kernel, enabled with S2O_TC_CTAS=2
+(read once per process, so each case runs in a subprocess): traces equal to the single-CTA
+kernel and to the exact generic path, outputs within the tcgen05 tolerance (bf16 operands,
+fp32 accumulation): max |dO| <= 2.5e-2, mean <= 2e-3 against the generic fp64 path."""
+from __future__ import annotations
+
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+SCRIPT = r"""
+import json, sys
+sys.path.insert(0, sys.argv[1])
+import torch
+import paper_2602_22575_b200 as s2o
+out = []
+for (hq, hkv, l, s, reorder, fused, tau) in json.loads(sys.argv[2]):
+    q, k, v = s2o.generate_synthetic("mixed", max(1, l // 64), 8.0, 11, 1, hq, l, 128)
+    qd = torch.from_numpy(q).cuda().to(torch.bfloat16)
+    kd = torch.from_numpy(k[:, :hkv]).cuda().to(torch.bfloat16)
+    vd = torch.from_numpy(v[:, :hkv]).cuda().to(torch.bfloat16)
+    res = {}
+    for path in (s2o.PATH_TCGEN05, s2o.PATH_GENERIC):
+        cfg = s2o.KernelConfig(seg_len=s, tau=tau, q_reorder=reorder, fused=fused, path=path)
+        r = s2o.s2o_attention(qd, kd, vd, cfg, want_plan=False)
+        torch.cuda.synchronize()
+        res[path] = r
+    a, b = res[s2o.PATH_TCGEN05], res[s2o.PATH_GENERIC]
+    d = (a.out.float() - b.out.float()).abs()
+    out.append({"trace_diff": int((a.trace.processed != b.trace.processed).sum().item()),
+                "tiles": int(a.trace.processed.numel()),
+                "max": d.max().item(), "mean": d.mean().item(),
+                "p2": [int(a.trace.pass2_pairs.sum().item()), int(b.trace.pass2_pairs.sum().item())]})
+print(json.dumps(out))
+"""
+
+CASES = [(4, 2, 4096, 512, True, False, 0.005), (8, 2, 8192, 2048, True, False, 0.005),
+         (4, 1, 3000, 700, True, False, 0.01), (4, 2, 4096, 1024, False, True, 0.005),
+         (2, 1, 4096, 1024, True, False, 0.0)]
+
+
+def test_pair_kernel_matches_exact_path():
+    env = dict(os.environ, S2O_TC_CTAS="2")
+    r = subprocess.run([sys.executable, "-c", SCRIPT, ROOT, json.dumps(CASES)], env=env, capture_output=True,
+                       text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    rows = json.loads(r.stdout.strip().splitlines()[-1])
+    for case, row in zip(CASES, rows):
+        assert row["trace_diff"] <= max(1, row["tiles"] // 100), (case, row)
+        assert row["max"] <= 2.5e-2 and row["mean"] <= 2e-3, (case, row)
+        if row["trace_diff"] == 0:
+            assert row["p2"][0] == row["p2"][1], (case, row)
