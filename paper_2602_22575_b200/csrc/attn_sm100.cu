@@ -94,7 +94,7 @@ struct TcParams {
 };
 
 // Timeline events (profiling aid): tl[ev * kTlCap + seq] = clock64() in CTA 0.
-constexpr int kTlCap = 1024;
+[[maybe_unused]] constexpr int kTlCap = 1024;
 // Compiled in only with -DS2O_TIMELINE (S2O_NVCC_FLAGS=-DS2O_TIMELINE python -m ...build).
 __device__ __forceinline__ void tl_mark(const TcParams& p, int ev, uint32_t seq) {
 #ifdef S2O_TIMELINE
@@ -654,17 +654,20 @@ tc_pass_kernel(const TcParams p, const __grid_constant__ CUtensorMap qmap,
                 // red[] (double-buffered by block parity), then one arrive per warp on p_full; the
                 // MMA issuer and these warps both take the decision from the four warp maxima
                 // (gain >= tau  <=>  rowsum >= tau * prev; NaN rows never vote to continue)
+                bool my_vote = false;
                 if (!is_diag) {
                     const bool cont = valid && (rowsum >= (float)a.tau * (ell * alpha));
-                    const unsigned vote = __ballot_sync(0xffffffffu, cont);
-                    if (lane == 0) c.red[x][j & 1][warp % 4] = vote != 0u;
+                    my_vote = __ballot_sync(0xffffffffu, cont) != 0u;
+                    if (lane == 0) c.red[x][j & 1][warp % 4] = my_vote;
                 }
                 tmem_st_wait();
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(smem_u32(&c.p_full[x]));
+                // a warp that voted to continue already knows the chunk commits (the decision is
+                // an OR); only a warp that voted stop waits for the other three votes
                 bool commit = true;
-                if (!is_diag) {
+                if (!is_diag && !my_vote) {
                     mbar_wait(smem_u32(&c.p_full[x]), npf & 1, 3002);
                     commit = chunk_commit(c.red[x][j & 1]);
                 }

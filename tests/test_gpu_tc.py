@@ -199,3 +199,26 @@ def test_truncated_plan_gaussian_fallback(cuda):
     torch.cuda.synchronize()
     assert torch.equal(fres.trace.processed, ffull.trace.processed)
     assert torch.equal(fres.out, ffull.out)
+
+
+@pytest.mark.parametrize("z,hq,hkv,pinned", [(2, 4, 2, True), (1, 8, 4, False), (1, 2, 1, True)])
+def test_host_pipelined_equals_device(cuda, z, hq, hkv, pinned):
+    """s2o_attention_host pipelines (batch, kv head) chunks over copy-in / compute / copy-out
+    streams; the result must equal the one-shot device call bit for bit (same kernels, same
+    per-head work), for pinned and pageable host buffers and Z > 1."""
+    import paper_2602_22575_b200 as s2o
+    torch = cuda
+    l = 4096
+    q, k, v = s2o.generate_synthetic("mixed", l // 64, 8.0, 4, z, hq, l, 128)
+    qd = torch.from_numpy(q).cuda().to(torch.bfloat16)
+    kd = torch.from_numpy(k[:, :hkv].copy()).cuda().to(torch.bfloat16)
+    vd = torch.from_numpy(v[:, :hkv].copy()).cuda().to(torch.bfloat16)
+    cfg = s2o.KernelConfig(seg_len=512, tau=0.005)
+    want = s2o.s2o_attention(qd, kd, vd, cfg, want_plan=False).out
+    torch.cuda.synchronize()
+    qh, kh, vh = qd.cpu(), kd.cpu(), vd.cpu()
+    oh = torch.empty_like(qh)
+    if pinned:
+        qh, kh, vh, oh = qh.pin_memory(), kh.pin_memory(), vh.pin_memory(), oh.pin_memory()
+    s2o.attention_host_ptr(qh, kh, vh, oh, cfg)
+    assert torch.equal(oh, want.cpu())
