@@ -326,6 +326,18 @@ tc_pass_kernel(const TcParams p, const __grid_constant__ CUtensorMap qmap,
                         mbar_arrive(smem_u32(&c.q_full));
                     }
                 } else {
+#ifdef S2O_QGATHER_TMA
+                    // one gather4 op per lane: (slot, row group, column half) = lt >> 6, ...
+                    if (lt == 0) mbar_expect_tx(smem_u32(&c.q_full), (P.has[1] ? 2 : 1) * kTileBytes);
+                    else mbar_arrive(smem_u32(&c.q_full));
+                    const int x = lt >> 6, grp = (lt >> 1) & 31, h = lt & 1;
+                    if (P.has[x]) {
+                        int32_t rr[4];
+                        for (int i = 0; i < 4; ++i) rr[i] = (int32_t)(qb + q_row(a, P, x, grp * 4 + i) * qs);
+                        tma_gather4(sQ + x * kTileBytes + h * kHalf + grp * 512, &qmap, h * 64, rr[0], rr[1], rr[2],
+                                    rr[3], smem_u32(&c.q_full));
+                    }
+#else
                     for (int e = lt; e < 2 * kBM; e += nthr) {
                         const int x = e >> 7;
                         ring0[x * kBM + ring_pos(e & 127)] = P.has[x] ? (int32_t)(qb + q_row(a, P, x, e & 127) * qs) : 0;
@@ -335,6 +347,7 @@ tc_pass_kernel(const TcParams p, const __grid_constant__ CUtensorMap qmap,
                         if (P.has[x]) gather_tile(sQ + x * kTileBytes, qg, kD, ring0 + x * kBM);
                     cp_async_arrive_noinc(smem_u32(&c.q_full));
                     named_bar_sync(gbar, nthr);  // ring reusable
+#endif
                 }
                 if (lt == 0) tl_mark(p, 29, qcount);
                 ++qcount;
@@ -388,8 +401,31 @@ tc_pass_kernel(const TcParams p, const __grid_constant__ CUtensorMap qmap,
                         mbar_arrive(smem_u32(&xfull[st]));
                     }
                 } else {
+#ifndef S2O_GATHER_CPASYNC
+                    const bool use_tma = true;
+#else
+                    const bool use_tma = false;
+#endif
+                    if (use_tma) {
+                    // TMA tile::gather4 (A/B: 9 % faster pass-2 than 16-B cp.async here, which
+                    // competes with the tensor core for the LSU/shared-memory path): 64 ops (32 row
+                    // groups x 2 column halves) on lanes 0-15 (K) / 0-21 (V) of the group's warps
+                    if (lt == 0) mbar_expect_tx(smem_u32(&xfull[st]), kTileBytes);
+                    else mbar_arrive(smem_u32(&xfull[st]));
+                    const int wl = lt & 31, wi = lt >> 5;
+                    const int per = kgrp ? 16 : 22;
+                    const int opi = wl < per ? wi * per + wl : 64;
+                    if (opi < 64) {
+                        const int grp = opi >> 1, h = opi & 1;
+                        int32_t rr[4];
+                        for (int i = 0; i < 4; ++i) rr[i] = (int32_t)(xb + (int64_t)ring[ring_pos(4 * grp + i)] * xs);
+                        tma_gather4(dst + h * kHalf + grp * 512, kgrp ? &kmap : &vmap, h * 64, rr[0], rr[1], rr[2],
+                                    rr[3], smem_u32(&xfull[st]));
+                    }
+                    } else {
                     gather_tile(dst, xg + xb * kD, xs * kD, ring);
                     cp_async_arrive_noinc(smem_u32(&xfull[st]));
+                    }
                 }
                 if (kgrp && lt == 0) tl_mark(p, 10, gi);
                 ++nx;
