@@ -777,9 +777,9 @@ select_topk_kernel(Geo g, const uint64_t* __restrict__ kvkey, int64_t topt, int3
             const bool last_sample = take_all || (rank == kSelSample - 1);
             // order-preserving compaction of every key <= theta
             constexpr int kU = 8;
-            for (int64_t b0 = 0; b0 < len; b0 += (int64_t)kSelThreads * kU) {
-                const int64_t i0 = b0 + (int64_t)tid * kU;
-                uint64_t kk[kU];
+            // 8 consecutive keys per thread, the next iteration's keys loaded before this one's
+            // are used (the scan is latency-bound)
+            auto load8 = [&](int64_t i0, uint64_t (&kk)[kU]) {
                 if (i0 + kU <= len) {
                     const ulonglong2* src = reinterpret_cast<const ulonglong2*>(keys + i0);
 #pragma unroll
@@ -792,6 +792,15 @@ select_topk_kernel(Geo g, const uint64_t* __restrict__ kvkey, int64_t topt, int3
 #pragma unroll
                     for (int u = 0; u < kU; ++u) kk[u] = (i0 + u < len) ? keys[i0 + u] : ~0ull;
                 }
+            };
+            uint64_t nk[kU];
+            load8((int64_t)tid * kU, nk);
+            for (int64_t b0 = 0; b0 < len; b0 += (int64_t)kSelThreads * kU) {
+                const int64_t i0 = b0 + (int64_t)tid * kU;
+                uint64_t kk[kU];
+#pragma unroll
+                for (int u = 0; u < kU; ++u) kk[u] = nk[u];
+                if (b0 + (int64_t)kSelThreads * kU < len) load8(i0 + (int64_t)kSelThreads * kU, nk);
                 bool tk[kU];
                 int c = 0;
 #pragma unroll
