@@ -572,7 +572,8 @@ s2o_status s2o_dense_causal_fwd(const s2o_problem* p, const void* q, const void*
 // Host-buffer operator, pipelined over (batch, kv head) chunks -- heads are independent: chunk
 // c+1 moves host->device while chunk c computes and chunk c-1 moves device->host, on three
 // streams with double-buffered device chunk sets. Each chunk is the sub-problem
-// {Z=1, Hq=group, Hkv=1} through s2o_attention_fwd, so results equal the one-shot call.
+// {Z=1, Hq=group (or 1 for the split last group), Hkv=1} through s2o_attention_fwd, so results
+// equal the one-shot call.
 static s2o_status attention_host_pipelined(const s2o_problem* p, const Geo& g, const void* q, const void* k,
                                            const void* v, const s2o_kernel_config* cfg, void* o,
                                            int32_t* q_perm, int32_t* kv_perm, int32_t* processed,
@@ -599,7 +600,7 @@ static s2o_status attention_host_pipelined(const s2o_problem* p, const Geo& g, c
     const size_t off_qp = off_o + align256(ob), off_kvp = off_qp + align256(qpb);
     const size_t off_pr = off_kvp + align256(kvpb), off_p1 = off_pr + align256(prb), off_p2 = off_p1 + align256(pairb);
     const size_t set_bytes = off_p2 + align256(pairb);
-    const size_t need = 2 * set_bytes + SL.total + 256;
+    const size_t need = 2 * set_bytes + SL.total + 256 + 2 * align256(kb);  // + K/V of the split group
     std::lock_guard<std::mutex> lock(g_host.mu);
     if (!g_host.stream) S2O_CUDA_TRY(cudaStreamCreateWithFlags(&g_host.stream, cudaStreamNonBlocking), "stream");
     if (!g_host.s_in) {
@@ -618,28 +619,47 @@ static s2o_status attention_host_pipelined(const s2o_problem* p, const Geo& g, c
         S2O_CUDA_TRY(cudaMalloc(&g_host.dev, need), "arena alloc");
         g_host.bytes = need;
     }
-    if (g_host.nflags < nchunks) {
+    const int64_t max_chunks = nchunks + grp;
+    if (g_host.nflags < max_chunks) {
         if (g_host.flags) cudaFreeHost(g_host.flags);
         g_host.flags = nullptr;
         g_host.nflags = 0;
-        S2O_CUDA_TRY(cudaMallocHost(&g_host.flags, sizeof(int32_t) * nchunks), "pinned flags");
-        g_host.nflags = nchunks;
+        S2O_CUDA_TRY(cudaMallocHost(&g_host.flags, sizeof(int32_t) * max_chunks), "pinned flags");
+        g_host.nflags = max_chunks;
     }
     char* set[2] = {reinterpret_cast<char*>(g_host.dev), reinterpret_cast<char*>(g_host.dev) + set_bytes};
     char* ws = reinterpret_cast<char*>(g_host.dev) + 2 * set_bytes;
-    char* wbase = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(ws) + 255) & ~uintptr_t(255));
-    const int32_t* dflag = reinterpret_cast<const int32_t*>(wbase + SL.pass + align256(generic_scratch_bytes(sa)));
+    char* kvlast = ws + SL.total + 256;  // K/V of the last group when it is split per q head
     cudaStream_t sc = g_host.stream, si = g_host.s_in, so = g_host.s_out;
-    auto hq_off = [&](int64_t c) { return (c / p->hkv) * p->hq + (c % p->hkv) * grp; };  // first q head
+    // Chunks: whole GQA groups, except the last group, which goes half a group at a time (its K/V
+    // once, into kvlast) so the pipeline tail -- last compute + last D2H -- is shorter.
+    struct Chunk { int64_t zg, q0, nq; bool shared_kv; };
+    std::vector<Chunk> chunks;
+    for (int64_t zg = 0; zg < nchunks; ++zg) {
+        if (zg + 1 < nchunks || grp == 1) {
+            chunks.push_back({zg, 0, grp, false});
+        } else {  // halves: a 1-head problem computes slower than its copy, a half-group does not
+            const int64_t step = std::max<int64_t>(1, grp / 2);
+            for (int64_t h = 0; h < grp; h += step) chunks.push_back({zg, h, std::min(step, grp - h), true});
+        }
+    }
+    const int64_t ncs = (int64_t)chunks.size();
+    auto h0_of = [&](const Chunk& ch) { return (ch.zg / p->hkv) * p->hq + (ch.zg % p->hkv) * grp + ch.q0; };
     auto enqueue_in = [&](int64_t c) -> s2o_status {
+        const Chunk& ch = chunks[c];
         const int b = (int)(c & 1);
         if (c >= 2) S2O_CUDA_TRY(cudaStreamWaitEvent(si, g_host.ev_comp[b], 0), "wait");
-        const char* hq = reinterpret_cast<const char*>(q) + esz_in * row * hq_off(c);
-        const char* hk = reinterpret_cast<const char*>(k) + esz_in * row * c;
-        const char* hv = reinterpret_cast<const char*>(v) + esz_in * row * c;
-        S2O_CUDA_TRY(cudaMemcpyAsync(set[b] + off_q, hq, qb, cudaMemcpyHostToDevice, si), "h2d q");
-        S2O_CUDA_TRY(cudaMemcpyAsync(set[b] + off_k, hk, kb, cudaMemcpyHostToDevice, si), "h2d k");
-        S2O_CUDA_TRY(cudaMemcpyAsync(set[b] + off_v, hv, kb, cudaMemcpyHostToDevice, si), "h2d v");
+        const char* hq = reinterpret_cast<const char*>(q) + esz_in * row * h0_of(ch);
+        const char* hk = reinterpret_cast<const char*>(k) + esz_in * row * ch.zg;
+        const char* hv = reinterpret_cast<const char*>(v) + esz_in * row * ch.zg;
+        S2O_CUDA_TRY(cudaMemcpyAsync(set[b] + off_q, hq, esz_in * row * ch.nq, cudaMemcpyHostToDevice, si), "h2d q");
+        if (!ch.shared_kv) {
+            S2O_CUDA_TRY(cudaMemcpyAsync(set[b] + off_k, hk, kb, cudaMemcpyHostToDevice, si), "h2d k");
+            S2O_CUDA_TRY(cudaMemcpyAsync(set[b] + off_v, hv, kb, cudaMemcpyHostToDevice, si), "h2d v");
+        } else if (ch.q0 == 0) {  // stream order: later sub-chunks' events follow this copy
+            S2O_CUDA_TRY(cudaMemcpyAsync(kvlast, hk, kb, cudaMemcpyHostToDevice, si), "h2d k");
+            S2O_CUDA_TRY(cudaMemcpyAsync(kvlast + align256(kb), hv, kb, cudaMemcpyHostToDevice, si), "h2d v");
+        }
         S2O_CUDA_TRY(cudaEventRecord(g_host.ev_h2d[b], si), "record");
         return S2O_OK;
     };
@@ -649,42 +669,55 @@ static s2o_status attention_host_pipelined(const s2o_problem* p, const Geo& g, c
         cudaStreamSynchronize(so);
     };
     if ((st = enqueue_in(0))) return st;
-    for (int64_t c = 0; c < nchunks; ++c) {
+    for (int64_t c = 0; c < ncs; ++c) {
+        const Chunk& ch = chunks[c];
         const int b = (int)(c & 1);
-        if (c + 1 < nchunks && (st = enqueue_in(c + 1))) { drain(); return st; }
+        if (c + 1 < ncs && (st = enqueue_in(c + 1))) { drain(); return st; }
         S2O_CUDA_TRY(cudaStreamWaitEvent(sc, g_host.ev_h2d[b], 0), "wait");
         if (c >= 2) S2O_CUDA_TRY(cudaStreamWaitEvent(sc, g_host.ev_d2h[b], 0), "wait");
         char* cs = set[b];
-        st = s2o_attention_fwd(&sp, cs + off_q, cs + off_k, cs + off_v, cfg, cs + off_o,
+        s2o_problem cp;
+        s2o_problem_init(&cp, 1, ch.nq, 1, p->l, p->d, p->in_dtype, p->out_dtype);
+        Geo cg;
+        if ((st = make_geo(&cp, cfg->seg_len, &cg))) { drain(); return st; }
+        const PassArgs ca = base_args(cg, cfg);
+        const OpLayout CL = op_layout(cg, ca, cfg->fused, cfg);
+        const char* dk = ch.shared_kv ? kvlast : cs + off_k;
+        const char* dv = ch.shared_kv ? kvlast + align256(kb) : cs + off_v;
+        st = s2o_attention_fwd(&cp, cs + off_q, dk, dv, cfg, cs + off_o,
                                reinterpret_cast<int32_t*>(cs + off_qp),
                                kvpb ? reinterpret_cast<int32_t*>(cs + off_kvp) : nullptr,
                                reinterpret_cast<int32_t*>(cs + off_pr), reinterpret_cast<int64_t*>(cs + off_p1),
                                reinterpret_cast<int64_t*>(cs + off_p2), ws, SL.total + 256, sc);
         if (st) { drain(); return st; }
+        char* cwb = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(ws) + 255) & ~uintptr_t(255));
+        const int32_t* dflag = reinterpret_cast<const int32_t*>(cwb + CL.pass + align256(generic_scratch_bytes(ca)));
         S2O_CUDA_TRY(cudaMemcpyAsync(&g_host.flags[c], dflag, sizeof(int32_t), cudaMemcpyDeviceToHost, sc), "d2h flag");
         S2O_CUDA_TRY(cudaEventRecord(g_host.ev_comp[b], sc), "record");
         S2O_CUDA_TRY(cudaStreamWaitEvent(so, g_host.ev_comp[b], 0), "wait");
-        const int64_t h0 = hq_off(c);
-        S2O_CUDA_TRY(cudaMemcpyAsync(reinterpret_cast<char*>(o) + esz_out * row * h0, cs + off_o, ob,
+        const int64_t h0 = h0_of(ch), nq = ch.nq;
+        S2O_CUDA_TRY(cudaMemcpyAsync(reinterpret_cast<char*>(o) + esz_out * row * h0, cs + off_o, esz_out * row * nq,
                                      cudaMemcpyDeviceToHost, so), "d2h o");
         if (q_perm)
-            S2O_CUDA_TRY(cudaMemcpyAsync(q_perm + h0 * sg.N * sg.S, cs + off_qp, qpb, cudaMemcpyDeviceToHost, so),
-                         "d2h q_perm");
+            S2O_CUDA_TRY(cudaMemcpyAsync(q_perm + h0 * sg.N * sg.S, cs + off_qp, qpb / grp * nq, cudaMemcpyDeviceToHost,
+                                         so), "d2h q_perm");
         if (kvpb)
-            S2O_CUDA_TRY(cudaMemcpyAsync(kv_perm + h0 * sg.kv_per_head(), cs + off_kvp, kvpb,
+            S2O_CUDA_TRY(cudaMemcpyAsync(kv_perm + h0 * sg.kv_per_head(), cs + off_kvp, kvpb / grp * nq,
                                          cudaMemcpyDeviceToHost, so), "d2h kv_perm");
         if (processed)
-            S2O_CUDA_TRY(cudaMemcpyAsync(processed + h0 * sg.N * sa.T, cs + off_pr, prb, cudaMemcpyDeviceToHost, so),
-                         "d2h trace");
+            S2O_CUDA_TRY(cudaMemcpyAsync(processed + h0 * sg.N * sa.T, cs + off_pr, prb / grp * nq,
+                                         cudaMemcpyDeviceToHost, so), "d2h trace");
         if (pass1_pairs)
-            S2O_CUDA_TRY(cudaMemcpyAsync(pass1_pairs + h0, cs + off_p1, pairb, cudaMemcpyDeviceToHost, so), "d2h pairs");
+            S2O_CUDA_TRY(cudaMemcpyAsync(pass1_pairs + h0, cs + off_p1, pairb / grp * nq, cudaMemcpyDeviceToHost, so),
+                         "d2h pairs");
         if (pass2_pairs)
-            S2O_CUDA_TRY(cudaMemcpyAsync(pass2_pairs + h0, cs + off_p2, pairb, cudaMemcpyDeviceToHost, so), "d2h pairs");
+            S2O_CUDA_TRY(cudaMemcpyAsync(pass2_pairs + h0, cs + off_p2, pairb / grp * nq, cudaMemcpyDeviceToHost, so),
+                         "d2h pairs");
         S2O_CUDA_TRY(cudaEventRecord(g_host.ev_d2h[b], so), "record");
     }
     S2O_CUDA_TRY(cudaStreamSynchronize(so), "sync");
     S2O_CUDA_TRY(cudaStreamSynchronize(sc), "sync");
-    for (int64_t c = 0; c < nchunks; ++c) {
+    for (int64_t c = 0; c < ncs; ++c) {
         if (g_host.flags[c] == 1) return fail(S2O_ERR_UNINIT_STATE, "uninitialized state");
         if (g_host.flags[c] == 2) return fail(S2O_ERR_UNCOVERED_ROW, "uncovered query row");
     }
