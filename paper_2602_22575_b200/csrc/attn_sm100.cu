@@ -74,7 +74,8 @@ constexpr int kLaunchRegs = 65536 / kThreads / 8 * 8;  // 128: what __launch_bou
 // setmaxnreg.inc blocks until the pool has the registers: the decrements must cover it
 static_assert(kSoftmaxRegs - kLaunchRegs <= kLaunchRegs - kOtherRegs, "register pool overcommitted");
 static_assert(sizeof(uint64_t) * 19 + 4 + 64 + 8 <= 256, "Ctrl exceeds its 256 B");
-constexpr float kRescaleThresh = 8.0f;  // lazy max update, log2 units (factor 256)
+constexpr float kRescaleThresh = 8.0f;
+  // lazy max update, log2 units (factor 256)
 
 struct Ctrl {
     uint64_t q_full, q_empty;
@@ -221,6 +222,7 @@ __device__ __forceinline__ int64_t key_token(const PairInfo& P, const int32_t* k
     return (int64_t)kv[c0 + (i < cn ? i : 0)];
 }
 
+template <bool kPackedExp>
 __global__ void __launch_bounds__(kThreads, 1)
 tc_pass_kernel(const TcParams p, const __grid_constant__ CUtensorMap qmap,
                const __grid_constant__ CUtensorMap kmap, const __grid_constant__ CUtensorMap vmap,
@@ -378,7 +380,7 @@ tc_pass_kernel(const TcParams p, const __grid_constant__ CUtensorMap qmap,
                 const uint32_t gi = gx + j;
                 const int st = gi % nst;
                 mbar_wait(smem_u32(&xempty[st]), ((gi / nst) & 1) ^ 1, kgrp ? 1002 : 1003);
-                if (kgrp && lt == 0) tl_mark(p, 9, gi);
+                if (lt == 0) tl_mark(p, kgrp ? 9 : 1, gi);
                 // stage reuse certifies both slots' decisions on blocks <= j - lag
                 for (; known < j - lag;) {
                     ++known;
@@ -391,6 +393,11 @@ tc_pass_kernel(const TcParams p, const __grid_constant__ CUtensorMap qmap,
                 for (int x = 0; x < 2; ++x) need |= participates(P, x, j) && !(stop_at[x] <= j - lag);
                 if (!need) break;
                 const uint32_t dst = xbase + st * kTileBytes;
+#ifdef S2O_NOLOAD  // dev timing aid: no K/V data movement (results are garbage)
+                mbar_arrive(smem_u32(&xfull[st]));
+                ++nx;
+                continue;
+#endif
                 if (!gat) {
                     if (lt == 0) {
                         mbar_expect_tx(smem_u32(&xfull[st]), kTileBytes);
@@ -427,7 +434,7 @@ tc_pass_kernel(const TcParams p, const __grid_constant__ CUtensorMap qmap,
                     cp_async_arrive_noinc(smem_u32(&xfull[st]));
                     }
                 }
-                if (kgrp && lt == 0) tl_mark(p, 10, gi);
+                if (lt == 0) tl_mark(p, kgrp ? 10 : 2, gi);
                 ++nx;
             }
             gx += nx;
@@ -529,6 +536,7 @@ tc_pass_kernel(const TcParams p, const __grid_constant__ CUtensorMap qmap,
                                 kn_ready = true;
                             }
                             issue_s(x, (gki + 1) % kKStages);
+                            if (x == 0) tl_mark(p, 31, gki);
                         }
                     }
                     if (has_v && !v_ready) mbar_wait(smem_u32(&c.v_full[gvi % kVStages]), (gvi / kVStages) & 1, 2006);
@@ -643,17 +651,41 @@ tc_pass_kernel(const TcParams p, const __grid_constant__ CUtensorMap qmap,
                     // FMA-pipe polynomial for part of the row measured slower -- the softmax is
                     // latency- not MUFU-throughput-bound here, profiles/r01_summary.md.)
                     if (full) {
+                        if constexpr (kPackedExp) {
+                            // packed arguments and sums (FFMA2 / FADD2): A/B at C3 pass-2 -5.5 %, pass-1
+                            // +5 % (so pass-1 launches the scalar instance)
+                            const float2 sc2 = make_float2(sc, sc), nr2 = make_float2(neg_ref, neg_ref);
+                            float2 rs2[2] = {make_float2(0.0f, 0.0f), make_float2(0.0f, 0.0f)};
 #pragma unroll
-                        for (int c0 = 0; c0 < kBN; c0 += 32) {
-                            uint32_t pk[16];
+                            for (int c0 = 0; c0 < kBN; c0 += 32) {
+                                uint32_t pk[16];
 #pragma unroll
-                            for (int i = 0; i < 32; i += 2) {
-                                const float e0 = ex2(fmaf(__uint_as_float(sv[c0 + i]), sc, neg_ref));
-                                const float e1 = ex2(fmaf(__uint_as_float(sv[c0 + i + 1]), sc, neg_ref));
-                                rs[(i >> 1) & 3] += e0 + e1;
-                                pk[i >> 1] = pack_bf16(e0, e1);
+                                for (int i = 0; i < 32; i += 2) {
+                                    const float2 arg = ffma2(make_float2(__uint_as_float(sv[c0 + i]), __uint_as_float(sv[c0 + i + 1])),
+                                                             sc2, nr2);
+                                    const float2 e = make_float2(ex2(arg.x), ex2(arg.y));
+                                    rs2[(i >> 1) & 1] = fadd2(rs2[(i >> 1) & 1], e);
+                                    pk[i >> 1] = pack_bf16(e.x, e.y);
+                                }
+                                tmem_st16(tS + c0 / 2, pk);
                             }
-                            tmem_st16(tS + c0 / 2, pk);
+                            rs[0] = rs2[0].x;
+                            rs[1] = rs2[0].y;
+                            rs[2] = rs2[1].x;
+                            rs[3] = rs2[1].y;
+                        } else {
+#pragma unroll
+                            for (int c0 = 0; c0 < kBN; c0 += 32) {
+                                uint32_t pk[16];
+#pragma unroll
+                                for (int i = 0; i < 32; i += 2) {
+                                    const float e0 = ex2(fmaf(__uint_as_float(sv[c0 + i]), sc, neg_ref));
+                                    const float e1 = ex2(fmaf(__uint_as_float(sv[c0 + i + 1]), sc, neg_ref));
+                                    rs[(i >> 1) & 3] += e0 + e1;
+                                    pk[i >> 1] = pack_bf16(e0, e1);
+                                }
+                                tmem_st16(tS + c0 / 2, pk);
+                            }
                         }
                     } else {
 #pragma unroll
@@ -1540,8 +1572,10 @@ cudaError_t launch_tc_pass(const PassArgs& a, cudaStream_t st) {
     p.pairs_per_head = (g.N - 1) * p.pairs_full + (t_last + 1) / 2;
     static bool attr_done = false;
     if (!attr_done) {
-        cudaError_t e = cudaFuncSetAttribute(tc_pass_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
-        if (e != cudaSuccess) return e;
+        for (const void* f : {(const void*)tc_pass_kernel<false>, (const void*)tc_pass_kernel<true>}) {
+            cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
+            if (e != cudaSuccess) return e;
+        }
         attr_done = true;
     }
     int dev = 0, sms = 148;
@@ -1577,7 +1611,10 @@ cudaError_t launch_tc_pass(const PassArgs& a, cudaStream_t st) {
     const int64_t work = a.tile_list ? a.tile_count : g.z * g.hq * p.pairs_per_head;
     if (work == 0) return cudaSuccess;
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(work, sms));
-    tc_pass_kernel<<<grid, kThreads, kSmemBytes, st>>>(p, qmap, kmap, vmap, qtile, ktile, vtile);
+    if (a.mode & kPrefix)
+        tc_pass_kernel<true><<<grid, kThreads, kSmemBytes, st>>>(p, qmap, kmap, vmap, qtile, ktile, vtile);
+    else
+        tc_pass_kernel<false><<<grid, kThreads, kSmemBytes, st>>>(p, qmap, kmap, vmap, qtile, ktile, vtile);
     return cudaGetLastError();
 }
 

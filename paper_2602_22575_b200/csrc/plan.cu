@@ -408,17 +408,26 @@ kv_score_kernel(const void* __restrict__ k, Geo g, const float* __restrict__ q_m
 }
 
 // Fast kv scoring for the product shape (bf16 K, D = 128): a register-tiled fp64 GEMM
-// S[pairs x keys] = q_mean[pairs x 128] . K^T per CTA tile of 64 (q head, segment) pairs x 128
-// keys (256 threads, 8 pairs x 4 keys each, d staged in chunks of 16 through double-buffered
-// shared memory as fp64). Each output accumulates d = 0..127 in order with DFMA, exactly
-// dot_f's sequence. CTA = (key block, pair batch); batches beyond a block's pair count exit.
-constexpr int kKS_Pairs = 64, kKS_Threads = 256, kKS_DC = 16;
+// S[pairs x keys] = q_mean[pairs x 128] . K^T. CTA (128 threads, 2 per SM) = 64 (q head,
+// segment) pairs x 128 keys, the whole d = 128 staged once: K as raw bf16 rows (272-B stride,
+// conflict-free 16-B row reads), q_mean as fp64 [d][pair]. Warp tile 32 pairs x 64 keys; lane =
+// 4 pair groups x 8 key groups holds pairs {32wp + 8i + 2pg + e} x keys {64wk + kg + 8r}: 8 x 8
+// fp64 accumulators. Per d a warp reads 5 x 16 B per lane (K once per 8 d) for 64 DFMAs per
+// lane, so the FP64 pipe, not shared memory, is the bound. bf16 -> fp64 is exact. Each output
+// accumulates d = 0..127 in order with DFMA from 0.0, exactly dot_f's sequence (plan.cpp:14-20).
+// CTA = (key block, pair batch); batches beyond a block's pair count exit.
+constexpr int kKS_Pairs = 64, kKS_Threads = 128, kKS_KStride = 136;  // bf16 per staged K row
+constexpr size_t kKS_Smem = sizeof(double) * 128 * kKS_Pairs + sizeof(__nv_bfloat16) * kSK * kKS_KStride;
+
+__device__ __forceinline__ double bf16_lo_to_f64(uint32_t w) { return (double)__uint_as_float(w << 16); }
+__device__ __forceinline__ double bf16_hi_to_f64(uint32_t w) { return (double)__uint_as_float(w & 0xffff0000u); }
 
 __global__ void __launch_bounds__(kKS_Threads, 2)
 kv_score128_kernel(const __nv_bfloat16* __restrict__ k, Geo g, const float* __restrict__ q_mean,
                    uint64_t* __restrict__ kvkey, int max_batches) {
-    __shared__ __align__(16) double Ks[2][kKS_DC][kSK];        // 32 KB
-    __shared__ __align__(16) double Qs[2][kKS_DC][kKS_Pairs];  // 16 KB
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    double* Qd = reinterpret_cast<double*>(smem_raw);                                    // [128 d][64 pairs]
+    __nv_bfloat16* Kn = reinterpret_cast<__nv_bfloat16*>(Qd + 128 * kKS_Pairs);          // [128 keys][136]
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int64_t kb = blockIdx.x / max_batches;
     const int batch = blockIdx.x % max_batches;
@@ -430,86 +439,84 @@ kv_score128_kernel(const __nv_bfloat16* __restrict__ k, Geo g, const float* __re
     const int64_t pairs = g.group * nsegs;
     const int64_t p0 = (int64_t)batch * kKS_Pairs;
     if (p0 >= pairs) return;
-    const __nv_bfloat16* kbase = k + z * g.ks[0] + kvh * g.ks[1];
-    // staging roles: K row (tid >> 1), 8 d values at half (tid & 1); q pair (tid >> 2), 4 d at (tid & 3)
-    const int krow = tid >> 1, khalf = tid & 1;
-    const bool kvalid = t0 + krow < g.l;
-    const __nv_bfloat16* ksrc = kbase + (t0 + krow) * g.ks[2] + khalf * 8;
-    const int qp = tid >> 2, qq = tid & 3;
-    const int64_t pq = p0 + qp;
-    const float* qsrc = nullptr;
-    if (pq < pairs) {
-        const int64_t h = kvh * g.group + pq / nsegs;
-        const int64_t n = n_lo + pq % nsegs;
-        qsrc = q_mean + ((z * g.hq + h) * g.N + n) * 128 + qq * 4;
-    }
-    uint4 kreg;
-    float4 qreg;
-    auto fetch = [&](int dc) {
-        kreg = kvalid ? *reinterpret_cast<const uint4*>(ksrc + dc * kKS_DC) : make_uint4(0, 0, 0, 0);
-        qreg = qsrc ? *reinterpret_cast<const float4*>(qsrc + dc * kKS_DC) : make_float4(0.f, 0.f, 0.f, 0.f);
-    };
-    auto stash = [&](int buf) {
-        const uint32_t w[4] = {kreg.x, kreg.y, kreg.z, kreg.w};
+    {  // stage K rows (16-B chunks) and q_mean (fp32 -> fp64, transposed)
+        const __nv_bfloat16* kbase = k + z * g.ks[0] + kvh * g.ks[1];
+        uint4 kr[16];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            Ks[buf][khalf * 8 + 2 * i][krow] = (double)__uint_as_float(w[i] << 16);
-            Ks[buf][khalf * 8 + 2 * i + 1][krow] = (double)__uint_as_float(w[i] & 0xffff0000u);
+        for (int i = 0; i < 16; ++i) {
+            const int c = tid + i * kKS_Threads, row = c >> 4, col = c & 15;
+            kr[i] = (t0 + row < g.l) ? *reinterpret_cast<const uint4*>(kbase + (t0 + row) * g.ks[2] + col * 8)
+                                     : make_uint4(0, 0, 0, 0);
         }
-        Qs[buf][qq * 4 + 0][qp] = (double)qreg.x;
-        Qs[buf][qq * 4 + 1][qp] = (double)qreg.y;
-        Qs[buf][qq * 4 + 2][qp] = (double)qreg.z;
-        Qs[buf][qq * 4 + 3][qp] = (double)qreg.w;
-    };
-    double acc[8][4];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+            const int c = tid + i * kKS_Threads, row = c >> 4, col = c & 15;
+            *reinterpret_cast<uint4*>(Kn + row * kKS_KStride + col * 8) = kr[i];
+        }
+        const int qp = tid >> 1, qh = tid & 1;  // pair, d half
+        const int64_t pq = p0 + qp;
+        const float* qsrc = nullptr;
+        if (pq < pairs) {
+            const int64_t h = kvh * g.group + pq / nsegs;
+            const int64_t n = n_lo + pq % nsegs;
+            qsrc = q_mean + ((z * g.hq + h) * g.N + n) * 128 + qh * 64;
+        }
+#pragma unroll 4
+        for (int c = 0; c < 16; ++c) {
+            const float4 x = qsrc ? reinterpret_cast<const float4*>(qsrc)[c] : make_float4(0.f, 0.f, 0.f, 0.f);
+            const int d = qh * 64 + 4 * c;
+            Qd[(d + 0) * kKS_Pairs + qp] = (double)x.x;
+            Qd[(d + 1) * kKS_Pairs + qp] = (double)x.y;
+            Qd[(d + 2) * kKS_Pairs + qp] = (double)x.z;
+            Qd[(d + 3) * kKS_Pairs + qp] = (double)x.w;
+        }
+    }
+    __syncthreads();
+    const int wp = warp & 1, wk = warp >> 1, pg = lane >> 3, kg = lane & 7;
+    double acc[8][8];  // [pair 2i+e][key r]
 #pragma unroll
     for (int i = 0; i < 8; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
-    fetch(0);
-    stash(0);
-    __syncthreads();
-    constexpr int kChunks = 128 / kKS_DC;
-    for (int dc = 0; dc < kChunks; ++dc) {
-        const int buf = dc & 1;
-        if (dc + 1 < kChunks) fetch(dc + 1);
+        for (int r = 0; r < 8; ++r) acc[i][r] = 0.0;
+    const __nv_bfloat16* krow = Kn + (64 * wk + kg) * kKS_KStride;
+    const double* qcol = Qd + 32 * wp + 2 * pg;
+#pragma unroll 1
+    for (int dg = 0; dg < 16; ++dg) {
+        uint4 kr[8];
 #pragma unroll
-        for (int d = 0; d < kKS_DC; ++d) {
-            const double2 k01 = *reinterpret_cast<const double2*>(&Ks[buf][d][4 * lane]);
-            const double2 k23 = *reinterpret_cast<const double2*>(&Ks[buf][d][4 * lane + 2]);
-            const double kv[4] = {k01.x, k01.y, k23.x, k23.y};
+        for (int r = 0; r < 8; ++r) kr[r] = *reinterpret_cast<const uint4*>(krow + 8 * r * kKS_KStride + 8 * dg);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const int d = 8 * dg + j;
             double qv[8];
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
-                const double2 x = *reinterpret_cast<const double2*>(&Qs[buf][d][8 * warp + 2 * i]);
+                const double2 x = *reinterpret_cast<const double2*>(qcol + d * kKS_Pairs + 8 * i);
                 qv[2 * i] = x.x;
                 qv[2 * i + 1] = x.y;
             }
 #pragma unroll
-            for (int i = 0; i < 8; ++i)
+            for (int r = 0; r < 8; ++r) {
+                const uint32_t w = (j >> 1) == 0 ? kr[r].x : (j >> 1) == 1 ? kr[r].y : (j >> 1) == 2 ? kr[r].z : kr[r].w;
+                const double kd = (j & 1) ? bf16_hi_to_f64(w) : bf16_lo_to_f64(w);
 #pragma unroll
-                for (int j = 0; j < 4; ++j) acc[i][j] = fma(qv[i], kv[j], acc[i][j]);
+                for (int i = 0; i < 8; ++i) acc[i][r] = fma(qv[i], kd, acc[i][r]);
+            }
         }
-        if (dc + 1 < kChunks) stash(buf ^ 1);
-        __syncthreads();
     }
     const int64_t kvp = g.kv_per_head();
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
-        const int64_t p = p0 + 8 * warp + i;
-        if (p >= pairs) break;
+        const int64_t p = p0 + 32 * wp + 8 * (i >> 1) + 2 * pg + (i & 1);
+        if (p >= pairs) continue;
         const int64_t h = kvh * g.group + p / nsegs;
         const int64_t n = n_lo + p % nsegs;
         uint64_t* dst = kvkey + (z * g.hq + h) * kvp + g.kv_off(n);
-        const int64_t t = t0 + 4 * lane;
-        if (t + 3 < n * g.S) {
-            ulonglong2* d2 = reinterpret_cast<ulonglong2*>(dst + t);
-            d2[0] = make_ulonglong2(desc_key(acc[i][0]), desc_key(acc[i][1]));
-            d2[1] = make_ulonglong2(desc_key(acc[i][2]), desc_key(acc[i][3]));
-        } else {
+        const int64_t lim = n * g.S;
 #pragma unroll
-            for (int j = 0; j < 4; ++j)
-                if (t + j < n * g.S) dst[t + j] = desc_key(acc[i][j]);
+        for (int r = 0; r < 8; ++r) {
+            const int64_t t = t0 + 64 * wk + kg + 8 * r;
+            if (t < lim) dst[t] = desc_key(acc[i][r]);
         }
     }
 }
@@ -525,7 +532,8 @@ cudaError_t launch_kv_score(const Geo& g, const void* k, const float* q_mean, ui
     if (kv_score128_ok(g, k)) {
         const int max_batches = (int)((g.group * (g.N - 1) + kKS_Pairs - 1) / kKS_Pairs);
         dim3 grid((unsigned)(blocks * max_batches), (unsigned)(g.z * g.hkv));
-        kv_score128_kernel<<<grid, kKS_Threads, 0, st>>>(reinterpret_cast<const __nv_bfloat16*>(k), g, q_mean,
+        cudaFuncSetAttribute(kv_score128_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kKS_Smem);
+        kv_score128_kernel<<<grid, kKS_Threads, kKS_Smem, st>>>(reinterpret_cast<const __nv_bfloat16*>(k), g, q_mean,
                                                          kvkey, max_batches);
         return cudaGetLastError();
     }

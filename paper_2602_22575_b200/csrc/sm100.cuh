@@ -27,14 +27,21 @@ __device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
                  : "memory");
 }
+#ifndef S2O_MBAR_HINT_NS
+#define S2O_MBAR_HINT_NS 0x989680
+#endif
 __device__ __forceinline__ bool mbar_try_wait(uint32_t bar, uint32_t parity) {
     uint32_t ok;
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
+#ifdef S2O_MBAR_HINT
+        "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2, %3;\n\t"
+#else
         "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2;\n\t"
+#endif
         "selp.u32 %0, 1, 0, p;\n\t}"
         : "=r"(ok)
-        : "r"(bar), "r"(parity)
+        : "r"(bar), "r"(parity), "n"(S2O_MBAR_HINT_NS)
         : "memory");
     return ok != 0;
 }
@@ -56,6 +63,18 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity, int tag
     uint32_t spins = 0;
     while (!mbar_try_wait(bar, parity)) {
         if (tag != 0 && ++spins == (1u << 24)) {
+            printf("s2o watchdog: block %d thread %d tag %d parity %u\n", (int)blockIdx.x, (int)threadIdx.x,
+                   tag, parity);
+            __trap();
+        }
+    }
+}
+
+// Spin on test_wait (never suspends): for the latency-critical MMA issuer.
+__device__ __forceinline__ void mbar_spin(uint32_t bar, uint32_t parity, int tag = 0) {
+    uint32_t spins = 0;
+    while (!mbar_test(bar, parity)) {
+        if (tag != 0 && ++spins == (1u << 26)) {
             printf("s2o watchdog: block %d thread %d tag %d parity %u\n", (int)blockIdx.x, (int)threadIdx.x,
                    tag, parity);
             __trap();
@@ -279,6 +298,25 @@ __device__ __forceinline__ float ex2_poly(float x) {
     return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
 }
 
+// Packed fp32 pairs (FFMA2 / FADD2 / FMNMX3 on sm_100): one issue slot for two lanes' worth.
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
+    float2 d;
+    asm("{\n\t.reg .b64 ra, rb, rc, rd;\n\t"
+        "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\tmov.b64 rc, {%6, %7};\n\t"
+        "fma.rn.f32x2 rd, ra, rb, rc;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+        : "=f"(d.x), "=f"(d.y)
+        : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
+    return d;
+}
+__device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
+    float2 d;
+    asm("{\n\t.reg .b64 ra, rb, rd;\n\t"
+        "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\t"
+        "add.rn.f32x2 rd, ra, rb;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+        : "=f"(d.x), "=f"(d.y)
+        : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+    return d;
+}
 __device__ __forceinline__ float ex2(float x) {
     float y;
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));

@@ -23,7 +23,7 @@ NAMES = {5: "k_full", 6: "p0_seen", 7: "p1_seen", 8: "kv_empty", 9: "ld_acq", 10
          11: "s0_pair", 12: "s0_init", 13: "s0_odone", 14: "s0_epi", 15: "s1_pair", 16: "s1_init",
          17: "s1_odone", 18: "s1_epi", 19: "s0_sfull", 20: "s0_exps", 21: "s0_arrive",
          22: "s1_sfull", 23: "s1_exps", 24: "s1_arrive", 25: "s0_ldwait", 26: "mma_qfull", 27: "mma_s0iss",
-         28: "v_full", 29: "kq_issued", 30: "kq_start"}
+         28: "v_full", 29: "kq_issued", 30: "kq_start", 1: "v_acq", 2: "v_iss", 31: "s0_issued"}
 
 
 def dump(tag, buf):
@@ -32,7 +32,7 @@ def dump(tag, buf):
     rel = np.where(t > 0, t - t0, -1)
     np.save(os.path.join("gpurun_out", f"timeline_{tag}.npy"), rel)
     print(f"== {tag}: total span {rel.max()} clk")
-    for ev in (9, 10, 5, 28, 19, 25, 20, 21, 6, 22, 23, 24, 7, 8):
+    for ev in (9, 10, 1, 2, 5, 28, 31, 19, 25, 20, 21, 6, 22, 23, 24, 7, 8):
         row = rel[ev]
         n = int((row >= 0).sum())
         first = row[:24]
