@@ -104,6 +104,17 @@ __device__ __forceinline__ void tl_mark(const TcParams& p, int ev, uint32_t seq)
 #endif
 }
 
+// Per-CTA span in global-timer ns (timeline builds): tl[0][cta] = start, tl[3][cta] = end.
+__device__ __forceinline__ void tl_cta(const TcParams& p, int ev) {
+#ifdef S2O_TIMELINE
+    if (p.tl != nullptr && blockIdx.x < (uint32_t)kTlCap) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        p.tl[ev * kTlCap + blockIdx.x] = t;
+    }
+#endif
+}
+
 // Token rings: the loader thread owning rows r0, r0 + STEP, ... reads its tokens as int4 vectors,
 // so a ring stores row `row` at (row % STEP) * rows_per_thread + row / STEP.
 template <int STEP>
@@ -268,6 +279,7 @@ tc_pass_kernel(const TcParams p, const __grid_constant__ CUtensorMap qmap,
     __syncthreads();
     tc_fence_after();
     const uint32_t tbase = c.tmem_base;
+    if (threadIdx.x == 0) tl_cta(p, 0);
     const int64_t total = a.tile_list ? a.tile_count : g.z * g.hq * p.pairs_per_head;
     const int64_t rowu = g.d;  // row unit of the tensor maps = D elements
 
@@ -842,6 +854,7 @@ tc_pass_kernel(const TcParams p, const __grid_constant__ CUtensorMap qmap,
     }
     tc_fence_before();
     __syncthreads();
+    if (threadIdx.x == 0) tl_cta(p, 3);
     if (warp == 0) tmem_dealloc(tbase, kTmemCols);
 }
 

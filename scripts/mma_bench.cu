@@ -10,6 +10,8 @@
 //   mode 7: mode 4 while warps 1-3 stream ld.shared over the operand tiles
 //   mode 8: TS (A = TMEM cols 0-63) -> SS writing cols 0-127 (the P-aliased-in-S hazard), back to back
 //   mode 9: mode 8 for two slots interleaved (slot x at cols 256x): PV0 S0 PV1 S1
+// probe (after the modes): clocks from issuing 16 MMAs to (a) the last issue returning, (b) a
+// try_wait on an already-complete barrier returning, (c) the MMAs' commit completing
 // build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I paper_2602_22575_b200/csrc
 //        scripts/mma_bench.cu -o scripts/mma_bench
 #include <cuda_runtime.h>
@@ -115,6 +117,56 @@ __global__ void __launch_bounds__(128, 1) bench(int mode, long long* out) {
         }
         const long long t1 = clock64();
         if (leader) out[blockIdx.x] = t1 - t0;
+        if (mode == 0 && blockIdx.x == 0) {
+            // issue-blocking probe (one CTA): 16 MMAs, then a barrier check on a completed phase
+            __shared__ uint64_t bar2;
+            if (leader) { mbar_init(smem_u32(&bar2), 1); fence_mbar_init(); mbar_arrive(smem_u32(&bar2)); }
+            __syncwarp();
+            mbar_wait(smem_u32(&bar2), 0);
+            const long long a0 = clock64();
+            ss(tb, id128);
+            ss(tb + 256, id128);
+            const long long a1 = clock64();
+            mbar_wait(smem_u32(&bar2), 0);
+            const long long a2 = clock64();
+            if (leader) umma_commit(smem_u32(&bar));
+            __syncwarp();
+            mbar_wait(smem_u32(&bar), ph & 1);
+            const long long a3 = clock64();
+            if (leader) printf("probe: 16 MMAs issued after %lld clk, completed-barrier check returns at %lld, MMAs done at %lld\n",
+                               a1 - a0, a2 - a0, a3 - a0);
+            // same, with a commit between the MMAs and the check; then an ld.shared poll instead
+            ++ph;
+            __shared__ volatile uint32_t flag;
+            if (leader) flag = 7;
+            __syncwarp();
+            const long long b0 = clock64();
+            ss(tb, id128);
+            ss(tb + 256, id128);
+            if (leader) umma_commit(smem_u32(&bar));
+            const long long b1 = clock64();
+            mbar_wait(smem_u32(&bar2), 0);
+            const long long b2 = clock64();
+            uint32_t f = flag;
+            const long long b3 = clock64();
+            mbar_wait(smem_u32(&bar), ph & 1);
+            const long long b4 = clock64();
+            if (leader) printf("probe: MMAs+commit issued at %lld, completed-barrier check after the commit returns at %lld, "
+                               "ld.shared poll at %lld (f=%u), MMAs done at %lld\n", b1 - b0, b2 - b0, b3 - b0, f, b4 - b0);
+            // ld.shared poll first, then the barrier check
+            ++ph;
+            const long long c0 = clock64();
+            ss(tb, id128);
+            ss(tb + 256, id128);
+            if (leader) umma_commit(smem_u32(&bar));
+            const long long c1 = clock64();
+            f += flag;
+            const long long c2 = clock64();
+            mbar_wait(smem_u32(&bar), ph & 1);
+            const long long c3 = clock64();
+            if (leader) printf("probe: MMAs+commit issued at %lld, ld.shared right after at %lld (f=%u), MMAs done at %lld\n",
+                               c1 - c0, c2 - c0, f, c3 - c0);
+        }
         if (leader) done = 1;
     }
     tc_fence_before();

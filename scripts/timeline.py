@@ -31,6 +31,12 @@ def dump(tag, buf):
     t0 = t[t > 0].min()
     rel = np.where(t > 0, t - t0, -1)
     np.save(os.path.join("gpurun_out", f"timeline_{tag}.npy"), rel)
+    st, en = t[0][:148], t[3][:148]
+    if (st > 0).all() and (en > 0).all():  # per-CTA spans (global timer, ns)
+        d = (en - st) / 1e3
+        print(f"   CTA spans us: min {d.min():.0f} median {np.median(d):.0f} max {d.max():.0f}; "
+              f"starts spread {(st.max() - st.min()) / 1e3:.1f} us; kernel {(en.max() - st.min()) / 1e3:.0f} us; "
+              f"slowest CTAs {np.argsort(d)[-5:].tolist()}")
     print(f"== {tag}: total span {rel.max()} clk")
     for ev in (9, 10, 1, 2, 5, 28, 31, 19, 25, 20, 21, 6, 22, 23, 24, 7, 8):
         row = rel[ev]
