@@ -411,13 +411,18 @@ kv_score_kernel(const void* __restrict__ k, Geo g, const float* __restrict__ q_m
 // S[pairs x keys] = q_mean[pairs x 128] . K^T. CTA (128 threads, 2 per SM) = 64 (q head,
 // segment) pairs x 128 keys, the whole d = 128 staged once: K as raw bf16 rows (272-B stride,
 // conflict-free 16-B row reads), q_mean as fp64 [d][pair]. Warp tile 32 pairs x 64 keys; lane =
-// 4 pair groups x 8 key groups holds pairs {32wp + 8i + 2pg + e} x keys {64wk + kg + 8r}: 8 x 8
-// fp64 accumulators. Per d a warp reads 5 x 16 B per lane (K once per 8 d) for 64 DFMAs per
-// lane, so the FP64 pipe, not shared memory, is the bound. bf16 -> fp64 is exact. Each output
+// 4 pair groups x 8 key groups holds pairs {8i + 2pg + e} x keys {kg + 8r}: 8 x 8 fp64
+// accumulators. Per d a warp reads 5 x 16 B per lane (K once per 8 d) for 64 DFMAs per lane, so
+// the FP64 pipe, not shared memory, is the bound. bf16 -> fp64 is exact. Each output
 // accumulates d = 0..127 in order with DFMA from 0.0, exactly dot_f's sequence (plan.cpp:14-20).
-// CTA = (key block, pair batch); batches beyond a block's pair count exit.
+// CTA = (key block kb, pair batch). A block's pair count (group x later segments) is rarely a
+// multiple of 64: a remainder of <= 32 pairs is done by ONE "wide" CTA over the two key blocks
+// kb, kb + 1 of the same segment (32 pairs x 256 keys, same shared memory), so padded work drops
+// from 19 % to 10 %. CTAs without work exit.
 constexpr int kKS_Pairs = 64, kKS_Threads = 128, kKS_KStride = 136;  // bf16 per staged K row
-constexpr size_t kKS_Smem = sizeof(double) * 128 * kKS_Pairs + sizeof(__nv_bfloat16) * kSK * kKS_KStride;
+constexpr size_t kKS_SmemNarrow = sizeof(double) * 128 * kKS_Pairs + sizeof(__nv_bfloat16) * kSK * kKS_KStride;
+constexpr size_t kKS_SmemWide = sizeof(double) * 128 * (kKS_Pairs / 2) + sizeof(__nv_bfloat16) * 2 * kSK * kKS_KStride;
+constexpr size_t kKS_Smem = kKS_SmemNarrow > kKS_SmemWide ? kKS_SmemNarrow : kKS_SmemWide;  // 100 KB: 2 CTAs / SM
 
 __device__ __forceinline__ double bf16_lo_to_f64(uint32_t w) { return (double)__uint_as_float(w << 16); }
 __device__ __forceinline__ double bf16_hi_to_f64(uint32_t w) { return (double)__uint_as_float(w & 0xffff0000u); }
@@ -426,8 +431,6 @@ __global__ void __launch_bounds__(kKS_Threads, 2)
 kv_score128_kernel(const __nv_bfloat16* __restrict__ k, Geo g, const float* __restrict__ q_mean,
                    uint64_t* __restrict__ kvkey, int max_batches) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    double* Qd = reinterpret_cast<double*>(smem_raw);                                    // [128 d][64 pairs]
-    __nv_bfloat16* Kn = reinterpret_cast<__nv_bfloat16*>(Qd + 128 * kKS_Pairs);          // [128 keys][136]
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int64_t kb = blockIdx.x / max_batches;
     const int batch = blockIdx.x % max_batches;
@@ -439,47 +442,64 @@ kv_score128_kernel(const __nv_bfloat16* __restrict__ k, Geo g, const float* __re
     const int64_t pairs = g.group * nsegs;
     const int64_t p0 = (int64_t)batch * kKS_Pairs;
     if (p0 >= pairs) return;
+    const int64_t rem = pairs - p0;  // pairs from p0 on
+    const bool can_wide = g.S % (2 * kSK) == 0;  // kb, kb + 1 always share a segment
+    const bool wide = can_wide && rem <= kKS_Pairs / 2;
+    if (wide && (kb & 1)) return;  // the even block's wide CTA covers this block
+    const int np = wide ? kKS_Pairs / 2 : kKS_Pairs;  // pairs in the tile (Qd row length)
+    const int nrows = wide ? 2 * kSK : kSK;           // staged K rows
+    double* Qd = reinterpret_cast<double*>(smem_raw);                           // [128 d][np]
+    __nv_bfloat16* Kn = reinterpret_cast<__nv_bfloat16*>(Qd + 128 * np);       // [nrows][136]
     {  // stage K rows (16-B chunks) and q_mean (fp32 -> fp64, transposed)
         const __nv_bfloat16* kbase = k + z * g.ks[0] + kvh * g.ks[1];
-        uint4 kr[16];
+        for (int half = 0; half < nrows / kSK; ++half) {
+            const int64_t tb = t0 + half * kSK;
+            uint4 kr[16];
 #pragma unroll
-        for (int i = 0; i < 16; ++i) {
-            const int c = tid + i * kKS_Threads, row = c >> 4, col = c & 15;
-            kr[i] = (t0 + row < g.l) ? *reinterpret_cast<const uint4*>(kbase + (t0 + row) * g.ks[2] + col * 8)
-                                     : make_uint4(0, 0, 0, 0);
-        }
+            for (int i = 0; i < 16; ++i) {
+                const int c = tid + i * kKS_Threads, row = c >> 4, col = c & 15;
+                kr[i] = (tb + row < g.l) ? *reinterpret_cast<const uint4*>(kbase + (tb + row) * g.ks[2] + col * 8)
+                                         : make_uint4(0, 0, 0, 0);
+            }
 #pragma unroll
-        for (int i = 0; i < 16; ++i) {
-            const int c = tid + i * kKS_Threads, row = c >> 4, col = c & 15;
-            *reinterpret_cast<uint4*>(Kn + row * kKS_KStride + col * 8) = kr[i];
+            for (int i = 0; i < 16; ++i) {
+                const int c = tid + i * kKS_Threads, row = c >> 4, col = c & 15;
+                *reinterpret_cast<uint4*>(Kn + (half * kSK + row) * kKS_KStride + col * 8) = kr[i];
+            }
         }
-        const int qp = tid >> 1, qh = tid & 1;  // pair, d half
+        // q_mean: thread -> (pair qp, 64 / (128 / np) d values)
+        const int parts = kKS_Threads / np;  // threads per pair: 2 (64 pairs) or 4 (32 pairs)
+        const int qp = tid / parts, qh = tid % parts, dlen = 128 / parts;
         const int64_t pq = p0 + qp;
         const float* qsrc = nullptr;
         if (pq < pairs) {
             const int64_t h = kvh * g.group + pq / nsegs;
             const int64_t n = n_lo + pq % nsegs;
-            qsrc = q_mean + ((z * g.hq + h) * g.N + n) * 128 + qh * 64;
+            qsrc = q_mean + ((z * g.hq + h) * g.N + n) * 128 + qh * dlen;
         }
 #pragma unroll 4
-        for (int c = 0; c < 16; ++c) {
+        for (int c = 0; c < dlen / 4; ++c) {
             const float4 x = qsrc ? reinterpret_cast<const float4*>(qsrc)[c] : make_float4(0.f, 0.f, 0.f, 0.f);
-            const int d = qh * 64 + 4 * c;
-            Qd[(d + 0) * kKS_Pairs + qp] = (double)x.x;
-            Qd[(d + 1) * kKS_Pairs + qp] = (double)x.y;
-            Qd[(d + 2) * kKS_Pairs + qp] = (double)x.z;
-            Qd[(d + 3) * kKS_Pairs + qp] = (double)x.w;
+            const int d = qh * dlen + 4 * c;
+            Qd[(d + 0) * np + qp] = (double)x.x;
+            Qd[(d + 1) * np + qp] = (double)x.y;
+            Qd[(d + 2) * np + qp] = (double)x.z;
+            Qd[(d + 3) * np + qp] = (double)x.w;
         }
     }
     __syncthreads();
-    const int wp = warp & 1, wk = warp >> 1, pg = lane >> 3, kg = lane & 7;
+    // warp -> (pair half, 64-key quarter) of a 64 x 128 tile, or (key block, 64-key half) of a
+    // wide 32 x 256 tile: either way keys [64 wk_row, +64) of the staged rows and 32 pairs
+    const int pg = lane >> 3, kg = lane & 7;
+    const int wpair = wide ? 0 : (warp & 1);                      // 32-pair group
+    const int wrow = wide ? warp : (warp >> 1);                   // 64-row group of the staged K
     double acc[8][8];  // [pair 2i+e][key r]
 #pragma unroll
     for (int i = 0; i < 8; ++i)
 #pragma unroll
         for (int r = 0; r < 8; ++r) acc[i][r] = 0.0;
-    const __nv_bfloat16* krow = Kn + (64 * wk + kg) * kKS_KStride;
-    const double* qcol = Qd + 32 * wp + 2 * pg;
+    const __nv_bfloat16* krow = Kn + (64 * wrow + kg) * kKS_KStride;
+    const double* qcol = Qd + 32 * wpair + 2 * pg;
 #pragma unroll 1
     for (int dg = 0; dg < 16; ++dg) {
         uint4 kr[8];
@@ -491,7 +511,7 @@ kv_score128_kernel(const __nv_bfloat16* __restrict__ k, Geo g, const float* __re
             double qv[8];
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
-                const double2 x = *reinterpret_cast<const double2*>(qcol + d * kKS_Pairs + 8 * i);
+                const double2 x = *reinterpret_cast<const double2*>(qcol + d * np + 8 * i);
                 qv[2 * i] = x.x;
                 qv[2 * i + 1] = x.y;
             }
@@ -507,7 +527,7 @@ kv_score128_kernel(const __nv_bfloat16* __restrict__ k, Geo g, const float* __re
     const int64_t kvp = g.kv_per_head();
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
-        const int64_t p = p0 + 32 * wp + 8 * (i >> 1) + 2 * pg + (i & 1);
+        const int64_t p = p0 + 32 * wpair + 8 * (i >> 1) + 2 * pg + (i & 1);
         if (p >= pairs) continue;
         const int64_t h = kvh * g.group + p / nsegs;
         const int64_t n = n_lo + p % nsegs;
@@ -515,7 +535,7 @@ kv_score128_kernel(const __nv_bfloat16* __restrict__ k, Geo g, const float* __re
         const int64_t lim = n * g.S;
 #pragma unroll
         for (int r = 0; r < 8; ++r) {
-            const int64_t t = t0 + 64 * wk + kg + 8 * r;
+            const int64_t t = t0 + 64 * wrow + kg + 8 * r;
             if (t < lim) dst[t] = desc_key(acc[i][r]);
         }
     }
