@@ -714,206 +714,307 @@ merge_pass_kernel(SortGeo sg, int64_t w, const uint64_t* __restrict__ ikeys,
 
 // ---------------------------------------------------------------- top-T selection
 // For the fused operator only the leading chunks of each kv_perm segment are consumed (the walk
-// stops early), so instead of fully sorting the prefix the plan materialises its exact top-T.
-// A CTA per (zh, n >= 1): radix-sort a 2048-key sample, take a threshold key whose expected rank
-// is ~1.15 T, compact every key <= threshold in INDEX order (coalesced 8-key loads per thread +
-// a block scan), then a stable block radix sort of the candidates by key (ties keep index
-// order) and write the first T indices. The result equals the first T entries of
-// argsort_desc_stable (a stable sort's top T is a prefix of the full order). If the threshold
-// catches fewer than T keys or more than the capacity, the CTA retries with another sample
-// rank; after the retries it keeps a capacity-sized best-effort set and flags the segment (the
-// host then builds the full plan).
+// stops early), so instead of fully sorting the prefix the plan materialises its exact top-T,
+// per (zh, n >= 1), in two kernels:
+//  * sel_scan_kernel (256 threads, several CTAs/SM, HBM-latency bound): radix-sort a 2048-key
+//    sample, take a threshold key whose expected rank is ~1.15 T, compact every key <= threshold
+//    in INDEX order (coalesced 8-key loads per thread + a block scan) into the segment's own slot
+//    of the spare key1 / idx1 workspace. If the threshold catches fewer than T keys or more than
+//    the capacity it retries with another sample rank; after the retries it keeps a
+//    capacity-sized best-effort set and flags the segment (the host then builds the full plan).
+//    Segments with at most kSelCap keys skip the scan: all their keys are candidates.
+//  * sel_sort_kernel (512 threads, 1 CTA/SM, shared-memory bound): a stable block radix sort of
+//    the candidates by key over only the bits where they differ (ties keep index order), then
+//    the first T indices -- exactly the first T entries of argsort_desc_stable (a stable
+//    sort's top T is a prefix of the full order).
+// Split because the two phases want different occupancy: fused in one 512-thread CTA per SM
+// the scan's load latency and the sort's shared-memory traffic never overlapped.
 constexpr int kSelThreads = 512;
 constexpr int kSelItems = 16;
 constexpr int kSelCap = kSelThreads * kSelItems;  // 8192 candidates
 constexpr int kSelSample = 2048;
 constexpr int kSelRadixBits = 6;
+constexpr int kScanThreads = 256;
 
 using SelSort = cub::BlockRadixSort<uint64_t, kSelThreads, kSelItems, uint32_t, kSelRadixBits>;
-using SampSort = cub::BlockRadixSort<uint64_t, kSelThreads, kSelSample / kSelThreads, cub::NullType, kSelRadixBits>;
-union SelSmem {
-    struct {
-        uint64_t k[kSelCap];
-        uint32_t i[kSelCap];
-    } cand;
-    typename SelSort::TempStorage sort;
-    typename SampSort::TempStorage samp;
+using SampSort = cub::BlockRadixSort<uint64_t, kScanThreads, kSelSample / kScanThreads, cub::NullType, kSelRadixBits>;
+
+struct SelSeg {
+    int64_t zh, n, len, tt, off;  // off: the segment's first key in the [zh][kv_off] key layout
 };
+__device__ __forceinline__ SelSeg sel_seg(const Geo& g, const int32_t* seg_list, int64_t topt, int64_t lvl_base) {
+    SelSeg s;
+    if (seg_list) {
+        s.zh = seg_list[blockIdx.x] / g.N;
+        s.n = seg_list[blockIdx.x] % g.N;
+    } else {
+        s.zh = blockIdx.x / (g.N - 1);
+        s.n = 1 + blockIdx.x % (g.N - 1);
+    }
+    s.len = s.n * g.S;
+    s.tt = min(topt, s.len - lvl_base);
+    s.off = s.zh * g.kv_per_head() + g.kv_off(s.n);
+    return s;
+}
 
 // Level > 0 (seg_list / prev given): the same selection restricted to the keys that follow the
 // previous level's last entry in the (key, index) order, i.e. entries [lvl_base, lvl_base + T).
-__global__ void __launch_bounds__(kSelThreads)
-select_topk_kernel(Geo g, const uint64_t* __restrict__ kvkey, int64_t topt, int32_t* __restrict__ kvtop,
-                   int32_t* __restrict__ flags, const int32_t* __restrict__ seg_list,
-                   const int32_t* __restrict__ prev, int64_t lvl_base) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    SelSmem& sm = *reinterpret_cast<SelSmem*>(smem_raw);
-    __shared__ int s_wsum[kSelThreads / 32];
+__global__ void __launch_bounds__(kScanThreads, 3)
+sel_scan_kernel(Geo g, const uint64_t* __restrict__ kvkey, int64_t topt, uint64_t* __restrict__ ckey,
+                uint32_t* __restrict__ cidx, int32_t* __restrict__ ccount, int32_t* __restrict__ flags,
+                const int32_t* __restrict__ seg_list, const int32_t* __restrict__ prev, int64_t lvl_base) {
+    __shared__ typename SampSort::TempStorage samp;
+    __shared__ int s_wsum[kScanThreads / 32];
     __shared__ int s_count;
     __shared__ uint64_t s_theta;
-    __shared__ unsigned long long s_or;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    int64_t zh, n;
-    if (seg_list) {
-        zh = seg_list[blockIdx.x] / g.N;
-        n = seg_list[blockIdx.x] % g.N;
-    } else {
-        zh = blockIdx.x / (g.N - 1);
-        n = 1 + blockIdx.x % (g.N - 1);
-    }
-    const int64_t len = n * g.S;
-    const int64_t tt = min(topt, len - lvl_base);
-    const uint64_t* keys = kvkey + zh * g.kv_per_head() + g.kv_off(n);
-    int32_t* out = kvtop + (zh * g.N + n) * topt;
+    const SelSeg sg = sel_seg(g, seg_list, topt, lvl_base);
+    const int64_t len = sg.len, tt = sg.tt;
+    if (len <= kSelCap && !prev) return;  // every key is a candidate (sel_sort_kernel reads them)
+    const uint64_t* keys = kvkey + sg.off;
+    uint64_t* ck = ckey + sg.off;  // candidates <= min(cap, len) fit the segment's own slot
+    uint32_t* ci = cidx + sg.off;
     // keys at or before the bound (the previous level's last entry) are not candidates
-    const int64_t bidx = prev ? prev[(zh * g.N + n) * topt + topt - 1] : -1;
+    const int64_t bidx = prev ? prev[(sg.zh * g.N + sg.n) * topt + topt - 1] : -1;
     const uint64_t bkey = prev ? keys[bidx] : 0ull;
     auto after = [&](uint64_t k, int64_t i) { return !prev || k > bkey || (k == bkey && i > bidx); };
-    uint64_t ck[kSelItems];
-    uint32_t ci[kSelItems];
-    if (len <= kSelCap && !prev) {
-        // every key is a candidate, already in index order (blocked arrangement)
+    // sample: 128 runs of 16 consecutive keys spread over the segment, radix-sorted (a short
+    // segment of a later level takes every remaining key instead)
+    const bool small = len <= kSelCap;
+    constexpr int kPer = kSelSample / kScanThreads;
+    uint64_t smp[kPer];
 #pragma unroll
-        for (int e = 0; e < kSelItems; ++e) {
-            const int64_t i = (int64_t)tid * kSelItems + e;
-            ck[e] = i < len ? keys[i] : ~0ull;
-            ci[e] = i < len ? (uint32_t)i : 0xffffffffu;
-        }
-    } else {
-        // sample: 128 runs of 16 consecutive keys spread over the segment, radix-sorted (a short
-        // segment of a later level takes every remaining key instead)
-        const bool small = len <= kSelCap;
-        uint64_t smp[kSelSample / kSelThreads];
+    for (int u = 0; u < kPer; ++u) {
+        const int e = tid * kPer + u;
+        smp[u] = small ? 0ull : keys[(int64_t)(e / 16) * (len / 128) + e % 16];
+    }
+    if (!small) SampSort(samp).Sort(smp);  // blocked: thread t holds ranks kPer t .. kPer t + kPer - 1
+    double want = small ? (double)len : (double)lvl_base + 1.15 * (double)tt + 32.0;
+    bool ok = false;
+    int count = 0;
+    for (int attempt = 0; attempt < 6 && !ok; ++attempt) {
+        int64_t rank = (int64_t)ceil(want * kSelSample / (double)len) + 4;
+        if (rank > kSelSample - 1) rank = kSelSample - 1;
+        __syncthreads();  // previous attempt's s_count / s_theta reads are done
+        const bool take_all = want >= (double)len;  // every remaining key fits the capacity
+        if (tid == (int)(rank / kPer)) s_theta = take_all ? ~0ull : smp[rank % kPer];
+        if (tid == 0) s_count = 0;
+        __syncthreads();
+        const uint64_t theta = s_theta;
+        const bool last_sample = take_all || (rank == kSelSample - 1);
+        // order-preserving compaction of every key <= theta: 8 consecutive keys per thread, the
+        // next iteration's keys loaded before this one's are used (the scan is latency-bound)
+        constexpr int kU = 8;
+        auto load8 = [&](int64_t i0, uint64_t (&kk)[kU]) {
+            if (i0 + kU <= len) {
+                const ulonglong2* src = reinterpret_cast<const ulonglong2*>(keys + i0);
 #pragma unroll
-        for (int u = 0; u < kSelSample / kSelThreads; ++u) {
-            const int e = tid * (kSelSample / kSelThreads) + u;
-            smp[u] = small ? 0ull : keys[(int64_t)(e / 16) * (len / 128) + e % 16];
-        }
-        if (!small) SampSort(sm.samp).Sort(smp);  // blocked: thread t holds ranks 4t .. 4t+3
-        double want = small ? (double)len : (double)lvl_base + 1.15 * (double)tt + 32.0;
-        bool ok = false;
-        int count = 0;
-        for (int attempt = 0; attempt < 6 && !ok; ++attempt) {
-            int64_t rank = (int64_t)ceil(want * kSelSample / (double)len) + 4;
-            if (rank > kSelSample - 1) rank = kSelSample - 1;
-            __syncthreads();  // sample sort storage / previous candidates no longer read
-            const bool take_all = want >= (double)len;  // every remaining key fits the capacity
-            if (tid == (int)(rank / (kSelSample / kSelThreads))) s_theta = take_all ? ~0ull : smp[rank % (kSelSample / kSelThreads)];
-            if (tid == 0) s_count = 0;
+                for (int u = 0; u < kU / 2; ++u) {
+                    const ulonglong2 x = src[u];
+                    kk[2 * u] = x.x;
+                    kk[2 * u + 1] = x.y;
+                }
+            } else {
+#pragma unroll
+                for (int u = 0; u < kU; ++u) kk[u] = (i0 + u < len) ? keys[i0 + u] : ~0ull;
+            }
+        };
+        constexpr int64_t kStep = (int64_t)kScanThreads * kU;
+        uint64_t nk[kU];
+        load8((int64_t)tid * kU, nk);
+        for (int64_t b0 = 0; b0 < len; b0 += kStep) {
+            const int64_t i0 = b0 + (int64_t)tid * kU;
+            uint64_t kk[kU];
+#pragma unroll
+            for (int u = 0; u < kU; ++u) kk[u] = nk[u];
+            if (b0 + kStep < len) load8(i0 + kStep, nk);
+            uint32_t m = 0;  // taken keys of this thread, bit u
+            if (!prev) {  // level 0: a plain threshold; the tail past len is masked
+#pragma unroll
+                for (int u = 0; u < kU; ++u) m |= (kk[u] <= theta ? 1u : 0u) << u;
+                if (i0 + kU > len) m &= (i0 < len) ? (1u << (uint32_t)(len - i0)) - 1u : 0u;
+            } else {
+#pragma unroll
+                for (int u = 0; u < kU; ++u)
+                    m |= ((kk[u] <= theta && i0 + u < len && after(kk[u], i0 + u)) ? 1u : 0u) << u;
+            }
+            const int c = __popc(m);
+            int x = c;  // warp inclusive scan
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, x, o);
+                if (lane >= o) x += y;
+            }
+            if (lane == 31) s_wsum[warp] = x;
             __syncthreads();
-            const uint64_t theta = s_theta;
-            const bool last_sample = take_all || (rank == kSelSample - 1);
-            // order-preserving compaction of every key <= theta
-            constexpr int kU = 8;
-            // 8 consecutive keys per thread, the next iteration's keys loaded before this one's
-            // are used (the scan is latency-bound)
-            auto load8 = [&](int64_t i0, uint64_t (&kk)[kU]) {
-                if (i0 + kU <= len) {
-                    const ulonglong2* src = reinterpret_cast<const ulonglong2*>(keys + i0);
+            int wbase = 0, total = 0;
 #pragma unroll
-                    for (int u = 0; u < kU / 2; ++u) {
-                        const ulonglong2 x = src[u];
-                        kk[2 * u] = x.x;
-                        kk[2 * u + 1] = x.y;
-                    }
-                } else {
-#pragma unroll
-                    for (int u = 0; u < kU; ++u) kk[u] = (i0 + u < len) ? keys[i0 + u] : ~0ull;
-                }
-            };
-            uint64_t nk[kU];
-            load8((int64_t)tid * kU, nk);
-            for (int64_t b0 = 0; b0 < len; b0 += (int64_t)kSelThreads * kU) {
-                const int64_t i0 = b0 + (int64_t)tid * kU;
-                uint64_t kk[kU];
-#pragma unroll
-                for (int u = 0; u < kU; ++u) kk[u] = nk[u];
-                if (b0 + (int64_t)kSelThreads * kU < len) load8(i0 + (int64_t)kSelThreads * kU, nk);
-                bool tk[kU];
-                int c = 0;
+            for (int w = 0; w < kScanThreads / 32; ++w) {
+                const int v = s_wsum[w];
+                wbase += (w < warp) ? v : 0;
+                total += v;
+            }
+            int pos = s_count + wbase + x - c;
+            if (m != 0u) {
 #pragma unroll
                 for (int u = 0; u < kU; ++u) {
-                    tk[u] = kk[u] <= theta && i0 + u < len && after(kk[u], i0 + u);
-                    c += tk[u] ? 1 : 0;
-                }
-                int x = c;  // warp inclusive scan
-#pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    const int y = __shfl_up_sync(0xffffffffu, x, o);
-                    if (lane >= o) x += y;
-                }
-                if (lane == 31) s_wsum[warp] = x;
-                __syncthreads();
-                int wbase = 0, total = 0;
-#pragma unroll
-                for (int w = 0; w < kSelThreads / 32; ++w) {
-                    const int v = s_wsum[w];
-                    wbase += (w < warp) ? v : 0;
-                    total += v;
-                }
-                int pos = s_count + wbase + x - c;
-#pragma unroll
-                for (int u = 0; u < kU; ++u) {
-                    if (tk[u]) {
+                    if ((m >> u) & 1u) {
                         if (pos < kSelCap) {
-                            sm.cand.k[pos] = kk[u];
-                            sm.cand.i[pos] = (uint32_t)(i0 + u);
+                            ck[pos] = kk[u];
+                            ci[pos] = (uint32_t)(i0 + u);
                         }
                         ++pos;
                     }
                 }
-                __syncthreads();  // s_wsum reusable, s_count read by all
-                if (tid == 0) s_count += total;
             }
-            __syncthreads();
-            const int cnt = s_count;
-            if (cnt >= tt && cnt <= kSelCap) {
+            __syncthreads();  // s_wsum reusable, s_count read by all
+            if (tid == 0) s_count += total;
+        }
+        __syncthreads();
+        const int cnt = s_count;
+        if (cnt >= tt && cnt <= kSelCap) {
+            ok = true;
+            count = cnt;
+        } else if (cnt < tt) {
+            if (last_sample) {
+                count = min(cnt, kSelCap);
                 ok = true;
-                count = cnt;
-            } else if (cnt < tt) {
-                if (last_sample) {
-                    count = min(cnt, kSelCap);
-                    ok = true;
-                    if (tid == 0) atomicExch(flags, 1);
-                }
-                want *= 2.0;
-            } else {
-                want = 0.5 * (want + (double)tt);
-                if (want < tt + 1) want = tt + 1;
+                if (tid == 0) atomicExch(flags, 1);
             }
+            want *= 2.0;
+        } else {
+            want = 0.5 * (want + (double)tt);
+            if (want < tt + 1) want = tt + 1;
         }
-        if (!ok) {
-            count = kSelCap;
-            if (tid == 0) atomicExch(flags, 1);
+    }
+    if (!ok) {
+        count = kSelCap;
+        if (tid == 0) atomicExch(flags, 1);
+    }
+    if (tid == 0) ccount[sg.zh * g.N + sg.n] = count;
+}
+
+// Sort by a 32-bit coarse key -- the top 32 of the bits where candidates differ -- carrying the
+// candidate's position: 6 radix passes over 8-byte pairs instead of 10 over 12-byte ones. The
+// coarse sort is stable (index order within equal coarse keys); it is exact unless two coarse-
+// equal candidates have different full keys in the wrong order, which is checked and then (rarely)
+// settled by the full 64-bit sort.
+using SelSortC = cub::BlockRadixSort<uint32_t, kSelThreads, kSelItems, uint32_t, kSelRadixBits>;
+using SelXchg = cub::BlockExchange<uint32_t, kSelThreads, kSelItems>;
+struct SelSortSmem {  // ~170 KB: 1 CTA / SM
+    uint64_t key[kSelCap];  // candidates in index order (striped writes: conflict-free)
+    uint32_t idx[kSelCap];
+    uint32_t edge_c[kSelItems][kSelThreads / 32];  // each warp's last (coarse, pos) per rank row
+    uint32_t edge_p[kSelItems][kSelThreads / 32];
+    union {
+        typename SelXchg::TempStorage xchg;
+        typename SelSortC::TempStorage coarse;
+        typename SelSort::TempStorage full;
+    } t;
+};
+
+__global__ void __launch_bounds__(kSelThreads)
+sel_sort_kernel(Geo g, const uint64_t* __restrict__ kvkey, const uint64_t* __restrict__ ckey,
+                const uint32_t* __restrict__ cidx, const int32_t* __restrict__ ccount, int64_t topt,
+                int32_t* __restrict__ kvtop, const int32_t* __restrict__ seg_list, int level0, int64_t lvl_base) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    SelSortSmem& sm = *reinterpret_cast<SelSortSmem*>(smem_raw);
+    __shared__ unsigned long long s_or;
+    __shared__ uint64_t s_ref;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const SelSeg sg = sel_seg(g, seg_list, topt, lvl_base);
+    const int64_t tt = sg.tt;
+    int32_t* out = kvtop + (sg.zh * g.N + sg.n) * topt;
+    const bool direct = sg.len <= kSelCap && level0;  // every key, in index order
+    const int count = direct ? (int)sg.len : ccount[sg.zh * g.N + sg.n];
+    const uint64_t* kk = direct ? kvkey + sg.off : ckey + sg.off;
+    const uint32_t* ii = cidx + sg.off;
+    if (tid == 0) {
+        s_or = 0ull;
+        s_ref = count > 0 ? kk[0] : 0ull;  // reference key: candidate 0
+    }
+    __syncthreads();
+    const uint64_t ref = s_ref;
+    // striped (coalesced) load; bits where candidates differ
+    uint64_t ks[kSelItems];
+    unsigned long long diff = 0ull;
+#pragma unroll
+    for (int e = 0; e < kSelItems; ++e) {
+        const int i = e * kSelThreads + tid;
+        ks[e] = i < count ? kk[i] : ~0ull;
+        sm.key[i] = ks[e];
+        sm.idx[i] = i < count ? (direct ? (uint32_t)i : ii[i]) : 0xffffffffu;
+        if (i < count) diff |= ks[e] ^ ref;
+    }
+    for (int o = 16; o > 0; o >>= 1) diff |= __shfl_xor_sync(0xffffffffu, diff, o);
+    if (lane == 0 && diff) atomicOr(&s_or, diff);
+    __syncthreads();
+    const unsigned long long all = s_or;
+    const int end_bit = all ? 64 - __clzll((long long)all) : 1;
+    // coarse key = the top 32 of the differing bits, relative to the common top bits (real
+    // candidates share every bit above end_bit); pads (~0) get all ones and stay last: stable
+    const int shift = end_bit > 32 ? end_bit - 32 : 0;
+    const uint64_t base = ref & ~((end_bit >= 64) ? ~0ull : ((1ull << end_bit) - 1));
+    uint32_t cc[kSelItems], pos[kSelItems];
+#pragma unroll
+    for (int e = 0; e < kSelItems; ++e) {
+        const int i = e * kSelThreads + tid;
+        cc[e] = i < count ? (uint32_t)((ks[e] - base) >> shift) : 0xffffffffu;
+        pos[e] = (uint32_t)i;
+    }
+    SelXchg(sm.t.xchg).StripedToBlocked(cc, cc);  // index order == blocked order for the sort
+    __syncthreads();
+    SelXchg(sm.t.xchg).StripedToBlocked(pos, pos);
+    __syncthreads();
+    SelSortC(sm.t.coarse).SortBlockedToStriped(cc, pos, 0, end_bit - shift);  // rank e * 512 + tid
+    // exact unless coarse-equal neighbours are out of full-key order (stable sort: equal full
+    // keys keep index order)
+    auto out_of_order = [&](uint32_t ca, uint32_t pa, uint32_t cb, uint32_t pb) {  // a before b
+        return shift > 0 && ca == cb && sm.key[pb] < sm.key[pa];
+    };
+    bool bad = false;
+    if (lane == 31) {
+#pragma unroll
+        for (int e = 0; e < kSelItems; ++e) {
+            sm.edge_c[e][warp] = cc[e];
+            sm.edge_p[e][warp] = pos[e];
         }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int e = 0; e < kSelItems; ++e) {
+        const uint32_t pc = __shfl_up_sync(0xffffffffu, cc[e], 1), pp = __shfl_up_sync(0xffffffffu, pos[e], 1);
+        if (lane > 0) {
+            bad |= out_of_order(pc, pp, cc[e], pos[e]);
+        } else if (warp > 0) {
+            bad |= out_of_order(sm.edge_c[e][warp - 1], sm.edge_p[e][warp - 1], cc[e], pos[e]);
+        } else if (e > 0) {  // rank e*512 follows rank (e-1)*512 + 511
+            bad |= out_of_order(sm.edge_c[e - 1][kSelThreads / 32 - 1], sm.edge_p[e - 1][kSelThreads / 32 - 1], cc[e],
+                                pos[e]);
+        }
+    }
+    if (__syncthreads_or(bad)) {  // rare: full 64-bit sort
+        uint64_t ck[kSelItems];
+        uint32_t ci[kSelItems];
 #pragma unroll
         for (int e = 0; e < kSelItems; ++e) {
             const int i = tid * kSelItems + e;
-            ck[e] = i < count ? sm.cand.k[i] : ~0ull;
-            ci[e] = i < count ? sm.cand.i[i] : 0xffffffffu;
+            ck[e] = sm.key[i];
+            ci[e] = sm.idx[i];
         }
-    }
-    // radix sort restricted to the bits where candidates differ (pads ~0 stay last)
-    if (tid == 0) {
-        s_or = 0ull;
-        s_theta = ck[0];  // reference key: candidate 0
-    }
-    __syncthreads();
-    unsigned long long diff = 0ull;
-    const uint64_t ref = s_theta;
+        __syncthreads();
+        SelSort(sm.t.full).SortBlockedToStriped(ck, ci, 0, end_bit);
 #pragma unroll
-    for (int e = 0; e < kSelItems; ++e)
-        if (ci[e] != 0xffffffffu) diff |= (ck[e] ^ ref);
-    for (int o = 16; o > 0; o >>= 1) diff |= __shfl_xor_sync(0xffffffffu, diff, o);
-    if (lane == 0 && diff) atomicOr(&s_or, diff);
-    __syncthreads();  // also: candidate buffer fully read before the sort reuses it
-    const unsigned long long all = s_or;
-    const int end_bit = all ? 64 - __clzll((long long)all) : 1;
-    SelSort(sm.sort).Sort(ck, ci, 0, end_bit);
+        for (int e = 0; e < kSelItems; ++e) {
+            const int64_t r = (int64_t)e * kSelThreads + tid;
+            if (r < tt) out[r] = (int32_t)ci[e];
+        }
+        return;
+    }
 #pragma unroll
     for (int e = 0; e < kSelItems; ++e) {
-        const int64_t r = (int64_t)tid * kSelItems + e;
-        if (r < tt) out[r] = (int32_t)ci[e];
+        const int64_t r = (int64_t)e * kSelThreads + tid;
+        if (r < tt) out[r] = (int32_t)sm.idx[pos[e]];
     }
 }
 
@@ -926,6 +1027,7 @@ struct PlanWs {
     uint64_t* key1;
     uint32_t* idx0;
     uint32_t* idx1;
+    int32_t* ccount;   // [Z*Hq*N] top-T candidate counts (candidates live in key1 / idx1)
 };
 
 size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
@@ -948,6 +1050,7 @@ size_t plan_ws_layout(const Geo& g, char* base, PlanWs* out) {
     ws.key1 = reinterpret_cast<uint64_t*>(take(sizeof(uint64_t) * total));
     ws.idx0 = reinterpret_cast<uint32_t*>(take(sizeof(uint32_t) * total));
     ws.idx1 = reinterpret_cast<uint32_t*>(take(sizeof(uint32_t) * total));
+    ws.ccount = reinterpret_cast<int32_t*>(take(sizeof(int32_t) * zhq * g.N));
     if (out) *out = ws;
     return off;
 }
@@ -1001,6 +1104,23 @@ cudaError_t sort_family(int kind, const Geo& g, PlanWs& ws, int32_t* perm, cudaS
 
 size_t plan_workspace_bytes(const Geo& g) { return plan_ws_layout(g, nullptr, nullptr) + 256; }
 
+namespace {
+// Top-T selection of `nseg` segments (all of them, or seg_list) over the keys in ws.key0.
+cudaError_t launch_select(const Geo& g, const PlanWs& ws, int64_t nseg, const int32_t* seg_list,
+                          const int32_t* prev, int64_t lvl_base, int32_t* kvtop, int64_t topt, int32_t* flags,
+                          cudaStream_t st) {
+    sel_scan_kernel<<<(unsigned)nseg, kScanThreads, 0, st>>>(g, ws.key0, topt, ws.key1, ws.idx1, ws.ccount, flags,
+                                                             seg_list, prev, lvl_base);
+    const size_t ssm = sizeof(SelSortSmem);
+    cudaFuncSetAttribute(sel_sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssm);
+    sel_sort_kernel<<<(unsigned)nseg, kSelThreads, ssm, st>>>(g, ws.key0, ws.key1, ws.idx1, ws.ccount, topt, kvtop,
+                                                              seg_list, prev == nullptr ? 1 : 0, lvl_base);
+    return cudaGetLastError();
+}
+}  // namespace
+
+
+
 // Plan for the fused operator: q_perm in full, kv_perm truncated to its top `topt` entries
 // per segment, laid out [Z*Hq][N][topt] (segment 0 unused). flags[0] is set if a selection
 // could not certify its result (the caller then falls back to the full plan).
@@ -1017,11 +1137,9 @@ cudaError_t launch_plan_topk(const Geo& g, const void* q, const void* k, int32_t
     }
     if (g.N > 1) {
         if ((err = launch_kv_score(g, k, ws.q_mean, ws.key0, st)) != cudaSuccess) return err;
-        const size_t ssm = sizeof(SelSmem);
-        cudaFuncSetAttribute(select_topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssm);
-        select_topk_kernel<<<(unsigned)(g.z * g.hq * (g.N - 1)), kSelThreads, ssm, st>>>(
-            g, ws.key0, topt, kvtop, flags, nullptr, nullptr, 0);
-        if ((err = cudaGetLastError()) != cudaSuccess) return err;
+        if ((err = launch_select(g, ws, g.z * g.hq * (g.N - 1), nullptr, nullptr, 0, kvtop, topt, flags, st)) !=
+            cudaSuccess)
+            return err;
     }
     return cudaSuccess;
 }
@@ -1034,11 +1152,7 @@ cudaError_t launch_plan_level(const Geo& g, const int32_t* seg_list, int64_t nse
     PlanWs ws;
     char* base = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(workspace) + 255) & ~uintptr_t(255));
     plan_ws_layout(g, base, &ws);  // the kv keys of the level-0 build are still in key0
-    const size_t ssm = sizeof(SelSmem);
-    cudaFuncSetAttribute(select_topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssm);
-    select_topk_kernel<<<(unsigned)nseg, kSelThreads, ssm, st>>>(g, ws.key0, topt, kvtop, flags, seg_list, prev,
-                                                                 lvl_base);
-    return cudaGetLastError();
+    return launch_select(g, ws, nseg, seg_list, prev, lvl_base, kvtop, topt, flags, st);
 }
 
 cudaError_t launch_segment_means(const Geo& g, const void* x, int which_kv, int64_t nseg_out,
