@@ -233,6 +233,37 @@ class Ref(_Backend):
                    _f64(gain), C.c_uint64(seed), _i64(z), _i64(h), _i64(l), _i64(d), _p(q), _p(k), _p(v))
         return q, k, v
 
+    def save_tensor(self, path: str, x: np.ndarray) -> None:
+        x = self._t(x)
+        self._call("save_tensor", C.c_char_p(str(path).encode()), _p(x), *(_i64(v) for v in x.shape))
+
+    def load_tensor(self, path: str) -> np.ndarray:
+        dims = np.zeros(4, np.int64)
+        self._call("load_tensor", C.c_char_p(str(path).encode()), _p(dims), None)
+        out = np.zeros(tuple(int(v) for v in dims), np.float32)
+        self._call("load_tensor", C.c_char_p(str(path).encode()), _p(dims), _p(out))
+        return out
+
+    def block_topk(self, q, k, v, block_rows: int, block_cols: int, topk: int):
+        """block_topk_attention (baseline.cpp): (out fp32 [Z,H,L,D], computed pairs int64 [Z*H])."""
+        q, k, v = self._t(q), self._t(k), self._t(v)
+        out = np.zeros_like(q)
+        pairs = np.zeros(q.shape[0] * q.shape[1], np.int64)
+        self._call("block_topk", _p(q), _p(k), _p(v), *(_i64(x) for x in q.shape), _i64(block_rows),
+                   _i64(block_cols), _i64(topk), _p(out), _p(pairs))
+        return out, pairs
+
+    def run_sweep(self, pattern: str, stripe_count: int, gain: float, seed: int, dims, variants, seg_lens, taus,
+                  tiles, topk, block, dump_plan: bool, out_base: str) -> None:
+        """run_sweep (sweep.cpp) on a synthetic input: writes <out_base>.{json,csv}."""
+        seg = np.asarray(seg_lens, np.int64)
+        tau = np.asarray(taus, np.float64)
+        tk = np.asarray(topk if topk else [0], np.int64)
+        self._call("run_sweep", C.c_char_p(pattern.encode()), _i64(stripe_count), _f64(gain), C.c_uint64(seed),
+                   *(_i64(x) for x in dims), C.c_char_p(",".join(variants).encode()), _p(seg), _i64(len(seg)),
+                   _p(tau), _i64(len(tau)), _i64(tiles[0]), _i64(tiles[1]), _p(tk), _i64(len(topk)),
+                   _i64(block[0]), _i64(block[1]), C.c_int(1 if dump_plan else 0), C.c_char_p(out_base.encode()))
+
     def rng_normals(self, seed: int, n: int) -> np.ndarray:
         out = np.zeros(n, np.float64)
         self._call("rng_normals", C.c_uint64(seed), _i64(n), _p(out))

@@ -15,6 +15,9 @@
 //   segment_representatives proj/src/plan.cpp:46-67
 //   dense_causal_attention  proj/src/attention.cpp:90-125
 //   generate_synthetic  proj/src/synthetic.cpp:276-328
+//   save/load_tensor_file   proj/src/tensor_io.cpp:32-83 (S2OT)
+//   block_topk_attention    proj/src/baseline.cpp (block top-k baseline)
+//   run_sweep               proj/src/sweep.cpp:141-302 (report-format goldens)
 //
 // Flat layouts (shared with oracle/s2o_oracle.c and include/s2o_cuda.h):
 //   tensors      fp32 [Z,H,L,D] row-major
@@ -33,11 +36,14 @@
 #include <vector>
 
 #include "s2o/attention.hpp"
+#include "s2o/baseline.hpp"
 #include "s2o/kernel.hpp"
 #include "s2o/metrics.hpp"
 #include "s2o/plan.hpp"
+#include "s2o/sweep.hpp"
 #include "s2o/synthetic.hpp"
 #include "s2o/tensor.hpp"
+#include "s2o/tensor_io.hpp"
 
 using namespace s2o;
 
@@ -286,6 +292,83 @@ int ref_generate_synthetic(const char* pattern, int64_t stripe_count, double str
         store_tensor(data.k, k);
         store_tensor(data.v, v);
     });
+}
+
+int ref_save_tensor(const char* path, const float* x, int64_t z, int64_t h, int64_t l, int64_t d) {
+    return guarded([&] { save_tensor_file(make_tensor(x, z, h, l, d), path); });
+}
+
+// dims[4] = {z, h, l, d}; out (if non-null) receives the fp32 data
+int ref_load_tensor(const char* path, int64_t* dims, float* out) {
+    return guarded([&] {
+        const Tensor4 t = load_tensor_file(path);
+        dims[0] = t.z;
+        dims[1] = t.h;
+        dims[2] = t.l;
+        dims[3] = t.d;
+        if (out) store_tensor(t, out);
+    });
+}
+
+int ref_block_topk(const float* q, const float* k, const float* v, int64_t z, int64_t h, int64_t l,
+                   int64_t d, int64_t block_rows, int64_t block_cols, int64_t topk, float* out,
+                   int64_t* pair_count) {
+    return guarded([&] {
+        BlockBudget b;
+        b.block_rows = block_rows;
+        b.block_cols = block_cols;
+        b.k = topk;
+        const BlockTopkResult r = block_topk_attention(make_tensor(q, z, h, l, d), make_tensor(k, z, h, l, d),
+                                                       make_tensor(v, z, h, l, d), b);
+        store_tensor(r.out, out);
+        for (size_t i = 0; i < r.pair_count.size(); ++i) pair_count[i] = r.pair_count[i];
+    });
+}
+
+// run_sweep on a synthetic input; variants comma-separated; writes <out_base>.{json,csv}.
+// Returns 0, or 7 when the sweep itself recorded a failure (partial report).
+int ref_run_sweep(const char* pattern, int64_t stripe_count, double stripe_gain, uint64_t seed, int64_t z,
+                  int64_t h, int64_t l, int64_t d, const char* variants, const int64_t* seg_lens, int64_t n_seg,
+                  const double* taus, int64_t n_tau, int64_t b_m, int64_t b_n, const int64_t* topk, int64_t n_topk,
+                  int64_t block_rows, int64_t block_cols, int dump_plan, const char* out_base) {
+    int partial = 0;
+    std::string err;
+    const int rc = guarded([&] {
+        RunConfig cfg;
+        SyntheticSpec spec;
+        spec.pattern = parse_stripe_pattern(pattern);
+        spec.stripe_count = stripe_count;
+        spec.stripe_gain = stripe_gain;
+        spec.seed = seed;
+        cfg.synthetic = spec;
+        cfg.z = z;
+        cfg.h = h;
+        cfg.l = l;
+        cfg.d = d;
+        cfg.variants.clear();
+        std::string names(variants);
+        for (size_t a = 0; a <= names.size();) {
+            const size_t b = names.find(',', a);
+            const std::string one = names.substr(a, b == std::string::npos ? std::string::npos : b - a);
+            if (!one.empty()) cfg.variants.push_back(parse_variant(one));
+            if (b == std::string::npos) break;
+            a = b + 1;
+        }
+        cfg.seg_lens.assign(seg_lens, seg_lens + n_seg);
+        cfg.taus.assign(taus, taus + n_tau);
+        cfg.tiles = TileSpec{b_m, b_n};
+        cfg.topk.assign(topk, topk + n_topk);
+        cfg.block_shape = BlockBudget{block_rows, block_cols, 0};
+        cfg.dump_plan = dump_plan != 0;
+        cfg.out_base = out_base;
+        const SweepResult r = run_sweep(cfg);
+        if (r.partial) {
+            err = r.error;
+            partial = 1;
+        }
+    });
+    if (rc == 0 && partial) g_err = err;
+    return rc != 0 ? rc : (partial ? 7 : 0);
 }
 
 int ref_rng_normals(uint64_t seed, int64_t n, double* out) {

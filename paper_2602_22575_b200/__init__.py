@@ -2,7 +2,8 @@
 
 The product is libs2o_cuda.so (hand-written sm_100a kernels behind the C-ABI in
 include/s2o_cuda.h). This package holds its sources (csrc/), the in-tree build
-(build.py) and a Python mirror of the reference's entry points (s2o.py).
+(build.py), a Python mirror of the reference's entry points (s2o.py), head sharding (shard.py),
+S2OT tensor files (io.py) and the reference-format benchmark sweep (sweep.py).
 """
 from .s2o import (  # noqa: F401
     KernelConfig, TileSpec, SegmentConfig, PermutationPlan, PassBuffers, KernelTrace,
