@@ -57,7 +57,8 @@ typedef enum s2o_status {
     S2O_ERR_UNSUPPORTED = 15,     /* a shape no kernel of this build covers */
     S2O_ERR_WORKSPACE = 16,       /* workspace smaller than *_workspace_size() */
     S2O_ERR_CUDA = 17,            /* CUDA runtime error (text in s2o_last_error) */
-    S2O_ERR_NO_DEVICE = 18        /* no sm_100 device / kernels not loadable */
+    S2O_ERR_NO_DEVICE = 18,       /* no sm_100 device / kernels not loadable */
+    S2O_ERR_BLOCK_BUDGET = 19     /* "block budget must have positive shape and k >= 0" baseline.cpp:23 */
 } s2o_status;
 
 typedef enum s2o_dtype { S2O_F32 = 0, S2O_BF16 = 1 } s2o_dtype;
@@ -199,6 +200,19 @@ void s2o_host_release(void);
 s2o_status s2o_dense_causal_fwd(const s2o_problem* p, const void* q, const void* k,
                                 const void* v, int32_t path, void* o, void* workspace,
                                 size_t workspace_bytes, void* stream);
+
+/* --------------------------------------------------------------- block top-k baseline */
+/* block_topk_attention (baseline.hpp:28-36, baseline.cpp:106-185): per query block of
+ * block_rows rows, the self block plus the `topk` full prefix blocks of largest causal softmax
+ * mass (exact fp64 ranking, ties to the lower block) are kept and a masked softmax runs over
+ * them. Square blocks only (block_rows == block_cols). O in p->out_dtype; pair_count int64
+ * [Z, Hq] = computed causal pairs (BlockTopkResult::pair_count). path as s2o_select_path
+ * (tcgen05 for the masked attention when bf16, D = 128 and 128-token blocks). */
+s2o_status s2o_block_topk_workspace_size(const s2o_problem* p, int64_t block_rows, int64_t block_cols,
+                                         int64_t topk, size_t* bytes);
+s2o_status s2o_block_topk_fwd(const s2o_problem* p, const void* q, const void* k, const void* v,
+                              int64_t block_rows, int64_t block_cols, int64_t topk, int32_t path, void* o,
+                              int64_t* pair_count, void* workspace, size_t workspace_bytes, void* stream);
 
 /* --------------------------------------------------------------- synthetic inputs */
 /* generate_synthetic (synthetic.hpp:45, synthetic.cpp:276-328) on the host, bit-identical

@@ -9,6 +9,6 @@ from .s2o import (  # noqa: F401
     KernelConfig, TileSpec, SegmentConfig, PermutationPlan, PassBuffers, KernelTrace,
     RankingCost, Representatives, S2oResult, build_plan, build_plan_truncated, segment_representatives,
     pass1_dense_init, pass2_sparse, fused_single_pass, s2o_attention, early_stop_check,
-    dense_causal_attention, generate_synthetic, attention_host, attention_host_ptr, select_path, lib,
+    dense_causal_attention, block_topk_attention, generate_synthetic, attention_host, attention_host_ptr, select_path, lib,
     PATH_AUTO, PATH_GENERIC, PATH_TCGEN05, SCORE_EXACT, SCORE_FAST, S2O_F32, S2O_BF16,
 )

@@ -21,7 +21,7 @@ LIB_DIR = os.path.join(_VARIANT, "lib") if _VARIANT else os.path.join(PKG, "lib"
 LIB = os.path.join(LIB_DIR, "libs2o_cuda.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-CU_SRCS = ["capi.cu", "plan.cu", "attn_generic.cu", "attn_sm100.cu"]
+CU_SRCS = ["capi.cu", "plan.cu", "attn_generic.cu", "attn_sm100.cu", "baseline.cu"]
 CPP_SRCS = ["synthetic.cpp"]
 
 

@@ -127,6 +127,45 @@ struct HostArena {
     int64_t nflags = 0;
 } g_host;
 
+// Block top-k baseline: workspace = fp64 row stats and block masses, the selected token lists,
+// fp32 pass-1 state, trace and pass scratch.
+struct BtLayout {
+    size_t rmax, rden, mass, kvtop, acc, ell, m, proc, p2, pass, total;
+};
+
+s2o_status bt_setup(const s2o_problem* p, int64_t rows, int64_t cols, int64_t topk, Geo* g, PassArgs* a,
+                           BtLayout* L) {
+    if (rows < 1 || cols < 1 || topk < 0)
+        return fail(S2O_ERR_BLOCK_BUDGET, "block budget must have positive shape and k >= 0");
+    if (rows != cols) return fail(S2O_ERR_UNSUPPORTED, "block top-k baseline needs square blocks");
+    s2o_status st = make_geo(p, p ? std::min<int64_t>(rows, p->l) : 0, g);
+    if (st) return st;
+    s2o_kernel_config c;
+    s2o_kernel_config_init(&c);
+    c.seg_len = g->S;
+    c.tau = 0.0;  // never stops: every selected block is committed
+    c.b_m = rows;
+    c.b_n = cols;
+    c.q_reorder = 0;
+    *a = base_args(*g, &c);
+    const int64_t zh = g->z * g->hq, nqb = g->N, nkb = (g->l + cols - 1) / cols;
+    const int64_t topt = std::max<int64_t>(1, topk * cols);
+    size_t off = 0;
+    auto take = [&](size_t b) { size_t o = off; off += align256(b); return o; };
+    L->rmax = take(sizeof(double) * zh * g->l);
+    L->rden = take(sizeof(double) * zh * g->l);
+    L->mass = take(sizeof(double) * zh * nqb * nkb);
+    L->kvtop = take(sizeof(int32_t) * zh * g->N * topt);
+    L->acc = take(sizeof(float) * zh * g->l * g->d);
+    L->ell = take(sizeof(float) * zh * g->l);
+    L->m = take(sizeof(float) * zh * g->l);
+    L->proc = take(sizeof(int32_t) * zh * g->N * a->T);
+    L->p2 = take(sizeof(int64_t) * zh);
+    L->pass = take(pass_ws_bytes(*a));
+    L->total = off + 256;
+    return S2O_OK;
+}
+
 }  // namespace
 }  // namespace s2o
 
@@ -543,6 +582,62 @@ s2o_status s2o_attention_fwd(const s2o_problem* p, const void* q, const void* k,
             }
             if ((st = run_pass(a3, cfg->path, base + L.pass, pass_ws_bytes(a), s, host[1] != 0))) return st;
         }
+    }
+    g_err.clear();
+    return S2O_OK;
+}
+
+s2o_status s2o_block_topk_workspace_size(const s2o_problem* p, int64_t block_rows, int64_t block_cols,
+                                         int64_t topk, size_t* bytes) {
+    Geo g;
+    PassArgs a;
+    BtLayout L;
+    if (!bytes) return fail(S2O_ERR_INVALID_ARG, "null pointer");
+    s2o_status st = bt_setup(p, block_rows, block_cols, topk, &g, &a, &L);
+    if (st) return st;
+    *bytes = L.total;
+    return S2O_OK;
+}
+
+s2o_status s2o_block_topk_fwd(const s2o_problem* p, const void* q, const void* k, const void* v,
+                              int64_t block_rows, int64_t block_cols, int64_t topk, int32_t path, void* o,
+                              int64_t* pair_count, void* workspace, size_t workspace_bytes, void* stream) {
+    Geo g;
+    PassArgs a;
+    BtLayout L;
+    s2o_status st = bt_setup(p, block_rows, block_cols, topk, &g, &a, &L);
+    if (st) return st;
+    if (!q || !k || !v || !o || !pair_count) return fail(S2O_ERR_INVALID_ARG, "null pointer");
+    if (!workspace || workspace_bytes < L.total) return fail(S2O_ERR_WORKSPACE, "workspace too small");
+    char* base = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(workspace) + 255) & ~uintptr_t(255));
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    int32_t* kvtop = reinterpret_cast<int32_t*>(base + L.kvtop);
+    S2O_CUDA_TRY(launch_block_topk_select(g, q, k, block_rows, block_cols, topk, reinterpret_cast<double*>(base + L.rmax),
+                                          reinterpret_cast<double*>(base + L.rden),
+                                          reinterpret_cast<double*>(base + L.mass), kvtop, s),
+                 "block top-k selection");
+    a.q = q; a.k = k; a.v = v; a.o = o;
+    a.processed = reinterpret_cast<int32_t*>(base + L.proc);
+    a.pass2_pairs = reinterpret_cast<int64_t*>(base + L.p2);
+    a.kv_perm = kvtop;
+    a.kv_top = std::max<int64_t>(1, topk * block_cols);
+    a.no_overflow = 1;
+    // pass1_pairs = the self blocks' exact triangles (self_pair_count, baseline.cpp:95-104)
+    S2O_CUDA_TRY(launch_trace_init(a, pair_count, s), "trace init");
+    PassArgs a1 = a;
+    float* acc = reinterpret_cast<float*>(base + L.acc);
+    float* ell = reinterpret_cast<float*>(base + L.ell);
+    float* m = reinterpret_cast<float*>(base + L.m);
+    a1.mode = topk > 0 ? (kDiag | kStateOut) : (kDiag | kFinal);
+    a1.acc_out = acc; a1.ell_out = ell; a1.m_out = m;
+    if ((st = run_pass(a1, path, base + L.pass, pass_ws_bytes(a), s))) return st;
+    if (topk > 0) {
+        PassArgs a2 = a;
+        a2.mode = kStateIn | kPrefix | kFinal;
+        a2.acc_in = acc; a2.ell_in = ell; a2.m_in = m;
+        if ((st = run_pass(a2, path, base + L.pass, pass_ws_bytes(a), s))) return st;
+        // pair_count = self triangles + rows x committed tokens of the kept prefix blocks
+        S2O_CUDA_TRY(launch_add_pairs(pair_count, a.pass2_pairs, g.z * g.hq, s), "pair sum");
     }
     g_err.clear();
     return S2O_OK;

@@ -52,6 +52,7 @@ struct PassArgs {
     const int32_t* tile_base;  // optional: committed chunks of earlier plan levels per tile-list entry
     int64_t tile_count;
     int64_t lvl_base;       // kv_perm entries of a segment consumed by earlier plan levels
+    int no_overflow;        // a short kv list is the whole list (block top-k baseline), no next level
 
     // entries of segment n's (current level) kv list
     __host__ __device__ int64_t avail(int64_t n) const {
@@ -59,7 +60,7 @@ struct PassArgs {
         return (kv_top > 0 && kv_top < rem) ? kv_top : rem;
     }
     // the level's list ran out before the segment's prefix did
-    __host__ __device__ bool truncated(int64_t n) const { return lvl_base + avail(n) < n * g.S; }
+    __host__ __device__ bool truncated(int64_t n) const { return !no_overflow && lvl_base + avail(n) < n * g.S; }
     __host__ __device__ const int32_t* kv_seg(int64_t zh, int64_t n) const {
         return kv_top > 0 ? kv_perm + (zh * g.N + n) * kv_top : kv_perm + zh * g.kv_per_head() + g.kv_off(n);
     }
@@ -89,6 +90,12 @@ cudaError_t launch_generic_pass(const PassArgs& a, void* scratch, cudaStream_t s
 // tcgen05 path (bf16, D = 128, b_m = 128, b_n in {64, 128})
 bool tc_supported(const PassArgs& a);
 cudaError_t launch_tc_pass(const PassArgs& a, cudaStream_t st);
+
+// block top-k baseline selection (baseline.cu): row stats, block masses, kv token lists
+cudaError_t launch_block_topk_select(const Geo& g, const void* q, const void* k, int64_t rows, int64_t cols,
+                                     int64_t topk, double* rmax, double* rden, double* mass, int32_t* kvtop,
+                                     cudaStream_t st);
+cudaError_t launch_add_pairs(int64_t* dst, const int64_t* src, int64_t n, cudaStream_t st);
 
 // trace helpers
 cudaError_t launch_trace_init(const PassArgs& a, int64_t* pass1_pairs, cudaStream_t st);

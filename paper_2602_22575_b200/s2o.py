@@ -38,7 +38,7 @@ S2O_F32, S2O_BF16 = 0, 1
 PATH_AUTO, PATH_GENERIC, PATH_TCGEN05 = 0, 1, 2
 SCORE_EXACT, SCORE_FAST = 0, 1
 
-_ERR_VALUE = {1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 13, 14, 15, 16}
+_ERR_VALUE = {1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 13, 14, 15, 16, 19}
 _ERR_RUNTIME = {12, 17, 18}
 
 
@@ -467,6 +467,24 @@ def dense_causal_attention(q, k, v, out_dtype: int = S2O_F32, path: int = PATH_A
     _check(lib().s2o_dense_causal_fwd(C.byref(p), _ptr(q), _ptr(k), _ptr(v), C.c_int32(path),
                                       _ptr(o), _ptr(ws), C.c_size_t(ws.numel()), _stream()))
     return o
+
+
+def block_topk_attention(q, k, v, block_rows: int, block_cols: int, topk: int, out=None, path: int = PATH_AUTO):
+    """block_topk_attention (baseline.hpp:28-36): the self block plus the `topk` prefix blocks of
+    largest causal softmax mass per query block (exact fp64 ranking), masked softmax over them.
+    Returns (O, pair_count int64 [Z, Hq]) -- BlockTopkResult."""
+    torch = _torch()
+    o = out if out is not None else _out_like(q, _default_out_dtype(q))
+    p = _problem(q, k, v, o)
+    nbytes = C.c_size_t(0)
+    _check(lib().s2o_block_topk_workspace_size(C.byref(p), C.c_int64(block_rows), C.c_int64(block_cols),
+                                               C.c_int64(topk), C.byref(nbytes)))
+    ws = _workspace(nbytes.value, q.device)
+    pairs = torch.empty((p.z, p.hq), dtype=torch.int64, device=q.device)
+    _check(lib().s2o_block_topk_fwd(C.byref(p), _ptr(q), _ptr(k), _ptr(v), C.c_int64(block_rows),
+                                    C.c_int64(block_cols), C.c_int64(topk), C.c_int32(path), _ptr(o), _ptr(pairs),
+                                    _ptr(ws), C.c_size_t(ws.numel()), _stream()))
+    return o, pairs
 
 
 def select_path(q, k, v, cfg: KernelConfig) -> int:

@@ -268,7 +268,14 @@ class DeviceRunner:
         return out
 
     def baseline_point(self, k: int):
-        raise NotImplementedError("baseline-topk is not built on the device yet (SURVEY.md §8f rank 3)")
+        """One baseline-topk point (sweep.cpp:210-246): block_topk_attention, median of 3."""
+        ops, cfg = self.ops, self.cfg
+        rows, cols = cfg.block_shape
+        (out, pairs), secs = self._timed(lambda: ops.block_topk_attention(self.q, self.k, self.v, rows, cols, k))
+        total = self.l * (self.l + 1) // 2
+        pc = pairs.cpu().numpy().reshape(self.z, self.h)
+        sp = [(z, h, int(pc[z, h]), total) for z in range(self.z) for h in range(self.h)]
+        return make_sparsity_report(self._errors(out), sp, 0, 0), secs
 
 
 def run_sweep(cfg: RunConfig, runner_factory: Callable[[RunConfig], object] = DeviceRunner) -> SweepResult:

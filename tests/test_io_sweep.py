@@ -170,3 +170,77 @@ def test_device_sweep_matches_reference(tmp_path, ref):
     rows = open(ours + ".csv").read().splitlines()
     assert rows[0] == sw.CSV_HEADER and len(rows) == 13
     assert [r.split(",")[:3] for r in rows[1:]] == [r.split(",")[:3] for r in open(base + ".csv").read().splitlines()[1:]]
+
+
+# ------------------------------------------------------------------ block top-k baseline (§8f rank 3)
+def test_block_topk_budget_errors():
+    """The C-ABI validates the budget before touching device memory (no GPU needed)."""
+    import ctypes as C
+
+    from paper_2602_22575_b200 import s2o as ops
+
+    p = ops._Problem()
+    ops.lib().s2o_problem_init(C.byref(p), C.c_int64(1), C.c_int64(1), C.c_int64(1), C.c_int64(64),
+                               C.c_int64(16), C.c_int32(ops.S2O_F32), C.c_int32(ops.S2O_F32))
+    nbytes = C.c_size_t(0)
+    for rows, cols, k in ((16, 16, -1), (0, 16, 1), (16, 0, 1)):
+        rc = ops.lib().s2o_block_topk_workspace_size(C.byref(p), C.c_int64(rows), C.c_int64(cols), C.c_int64(k),
+                                                     C.byref(nbytes))
+        assert rc == 19
+        assert ops.lib().s2o_last_error().decode() == "block budget must have positive shape and k >= 0"
+    rc = ops.lib().s2o_block_topk_workspace_size(C.byref(p), C.c_int64(16), C.c_int64(8), C.c_int64(1),
+                                                 C.byref(nbytes))
+    assert rc == 15  # unsupported: square blocks only
+    assert ops.lib().s2o_block_topk_workspace_size(C.byref(p), C.c_int64(16), C.c_int64(16), C.c_int64(2),
+                                                   C.byref(nbytes)) == 0 and nbytes.value > 0
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("topk", [0, 1, 3, 100])
+def test_block_topk_matches_reference_fp32(ref, topk):
+    """fp32 inputs (exact fp64 generic path): identical pair counts, outputs to fp32 rounding."""
+    import torch
+
+    import paper_2602_22575_b200 as s2o
+
+    q, k, v = ref.generate_synthetic("mixed", 4, 8.0, 3, 1, 2, 256, 32)
+    want, want_pairs = ref.block_topk(q, k, v, 16, 16, topk)
+    dq, dk, dv = (torch.from_numpy(x).cuda() for x in (q, k, v))
+    got, pairs = s2o.block_topk_attention(dq, dk, dv, 16, 16, topk)
+    assert pairs.cpu().numpy().reshape(-1).tolist() == want_pairs.tolist()
+    np.testing.assert_allclose(got.cpu().numpy(), want, rtol=0, atol=2e-6)
+
+
+@pytest.mark.gpu
+def test_block_topk_tcgen05_matches_reference(ref):
+    """bf16, D = 128, 128-token blocks: the masked attention runs on the tcgen05 path; the
+    selection is still exact, so the kept sets (pair counts) equal the reference's on the same
+    bf16-rounded inputs; outputs within bf16 tolerance."""
+    import torch
+
+    import paper_2602_22575_b200 as s2o
+
+    q, k, v = ref.generate_synthetic("mixed", 16, 8.0, 1, 1, 2, 1024, 128)
+    dq, dk, dv = (torch.from_numpy(x).cuda().to(torch.bfloat16) for x in (q, k, v))
+    qr, kr, vr = (x.float().cpu().numpy() for x in (dq, dk, dv))
+    want, want_pairs = ref.block_topk(qr, kr, vr, 128, 128, 2)
+    got, pairs = s2o.block_topk_attention(dq, dk, dv, 128, 128, 2, path=s2o.PATH_TCGEN05)
+    assert pairs.cpu().numpy().reshape(-1).tolist() == want_pairs.tolist()
+    err = np.abs(got.float().cpu().numpy() - want)
+    assert err.max() <= 2e-2 and err.mean() <= 2e-3
+
+
+@pytest.mark.gpu
+def test_device_sweep_baseline_matches_reference(tmp_path, ref):
+    base = _ref_sweep(ref, tmp_path, variants=["baseline-topk"], topk=[0, 1, 3])
+    doc = json.load(open(base + ".json"))
+    ours = str(tmp_path / "devb")
+    res = sw.run_sweep(_cfg(ours, variants=["baseline-topk"], topk=[0, 1, 3]))
+    assert not res.partial, res.error
+    mine = json.load(open(ours + ".json"))
+    assert mine["config"] == doc["config"] and len(mine["points"]) == 3
+    for a, b in zip(mine["points"], doc["points"]):
+        assert a["k"] == b["k"] and a["report"]["ranking_cost"] == b["report"]["ranking_cost"]
+        for ha, hb in zip(a["report"]["per_head"], b["report"]["per_head"]):
+            assert ha["computed_pairs"] == hb["computed_pairs"] and ha["sparsity"] == hb["sparsity"]
+            assert ha["mse"] == pytest.approx(hb["mse"], rel=2e-3, abs=1e-12)
