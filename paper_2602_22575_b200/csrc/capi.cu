@@ -434,9 +434,12 @@ static OpLayout op_layout(const Geo& g, const PassArgs& a, int fused, const s2o_
     L.kvtop = take(2 * sizeof(int32_t) * std::max<int64_t>(1, zh * g.N * L.topt));  // level lists A, B
     // [0] overflow count, [1] selection flag, then tiles A/B, bases A/B, segment list
     L.ovf = take(sizeof(int32_t) * (4 + 5 * zh * a.tiles_per_head));
-    L.acc = take(fused ? 0 : sizeof(float) * zh * g.l * g.d);
-    L.ell = take(fused ? 0 : sizeof(float) * zh * g.l);
-    L.m = take(fused ? 0 : sizeof(float) * zh * g.l);
+    // pass state: pass-1 -> pass-2, and (also fused) the saved state of tiles that resume at the
+    // next plan level of a truncated plan
+    const bool state = !fused || L.topt > 0;
+    L.acc = take(state ? sizeof(float) * zh * g.l * g.d : 0);
+    L.ell = take(state ? sizeof(float) * zh * g.l : 0);
+    L.m = take(state ? sizeof(float) * zh * g.l : 0);
     L.proc = take(sizeof(int32_t) * zh * g.N * a.T);
     L.p1 = take(sizeof(int64_t) * zh);
     L.p2 = take(sizeof(int64_t) * zh);
@@ -506,6 +509,7 @@ s2o_status s2o_attention_fwd(const s2o_problem* p, const void* q, const void* k,
     if (cfg->fused) {
         a2.mode = kDiag | kPrefix | kFinal;
         a2.q_reorder = 0;
+        if (topt > 0) { a2.acc_out = acc; a2.ell_out = ell; a2.m_out = m; }  // resume state, as below
     } else {
         PassArgs a1 = a;
         a1.mode = kDiag | kStateOut;
@@ -527,7 +531,7 @@ s2o_status s2o_attention_fwd(const s2o_problem* p, const void* q, const void* k,
         for (;;) {
             S2O_CUDA_TRY(cudaMemcpyAsync(host, ovf, sizeof host, cudaMemcpyDeviceToHost, s), "d2h overflow");
             S2O_CUDA_TRY(cudaStreamSynchronize(s), "sync");
-            if (host[0] == 0 || host[1] != 0 || cfg->fused) break;
+            if (host[0] == 0 || host[1] != 0) break;
             // next plan level for the segments of the overflow tiles
             std::vector<int32_t> ht(host[0]);
             S2O_CUDA_TRY(cudaMemcpy(ht.data(), tiles[cur], sizeof(int32_t) * host[0], cudaMemcpyDeviceToHost),
@@ -549,6 +553,10 @@ s2o_status s2o_attention_fwd(const s2o_problem* p, const void* q, const void* k,
                                            ovf + 1, base + L.plan, s), "plan level");
             S2O_CUDA_TRY(cudaMemsetAsync(ovf, 0, sizeof(int32_t), s), "memset");
             PassArgs a3 = a2;
+            if (cfg->fused) {  // the diagonal part is done: resume the saved state, prefix only
+                a3.mode = kStateIn | kPrefix | kFinal;
+                a3.acc_in = acc; a3.ell_in = ell; a3.m_in = m;
+            }
             a3.kv_perm = lists[cur ^ 1];
             a3.lvl_base = lvl_base;
             a3.tile_list = tiles[cur];
@@ -559,28 +567,23 @@ s2o_status s2o_attention_fwd(const s2o_problem* p, const void* q, const void* k,
             if ((st = run_pass(a3, cfg->path, base + L.pass, pass_ws_bytes(a), s, false))) return st;
             cur ^= 1;
         }
-        if (host[0] > 0 || host[1] != 0) {
-            // Fused mode (no saved state) or an uncertified selection: full plan, recompute.
+        if (host[1] != 0) {
+            // A selection could not be certified: full plan, recompute everything.
             S2O_CUDA_TRY(launch_plan_build(g, q, k, qp, kvp, base + L.plan, s), "plan build");
             PassArgs a3 = a2;
             a3.kv_perm = kvp;
             a3.kv_top = 0;
             a3.lvl_base = 0;
             a3.acc_out = a3.ell_out = a3.m_out = nullptr;
-            if (host[1] != 0 || !cfg->fused) {  // selection could not be certified: redo everything
-                S2O_CUDA_TRY(launch_trace_init(a, p1, s), "trace init");
-                if (!cfg->fused) {  // pass-1 state was overwritten by saved levels: redo pass-1
-                    PassArgs a1 = a;
-                    a1.mode = kDiag | kStateOut;
-                    a1.q_reorder = 0;
-                    a1.acc_out = acc; a1.ell_out = ell; a1.m_out = m;
-                    if ((st = run_pass(a1, cfg->path, base + L.pass, pass_ws_bytes(a), s))) return st;
-                }
-            } else {
-                a3.tile_list = tiles[cur];
-                a3.tile_count = host[0];
+            S2O_CUDA_TRY(launch_trace_init(a, p1, s), "trace init");
+            if (!cfg->fused) {  // pass-1 state was overwritten by saved levels: redo pass-1
+                PassArgs a1 = a;
+                a1.mode = kDiag | kStateOut;
+                a1.q_reorder = 0;
+                a1.acc_out = acc; a1.ell_out = ell; a1.m_out = m;
+                if ((st = run_pass(a1, cfg->path, base + L.pass, pass_ws_bytes(a), s))) return st;
             }
-            if ((st = run_pass(a3, cfg->path, base + L.pass, pass_ws_bytes(a), s, host[1] != 0))) return st;
+            if ((st = run_pass(a3, cfg->path, base + L.pass, pass_ws_bytes(a), s))) return st;
         }
     }
     g_err.clear();

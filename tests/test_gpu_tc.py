@@ -149,8 +149,8 @@ def test_tc_generic_agree_at_scale(cuda):
     assert err.max().item() <= 2.5e-2 and err.mean().item() <= 2e-3
 
 
-@pytest.mark.parametrize("path", [TC, GEN])
-def test_truncated_plan_matches_full_plan(cuda, path):
+@pytest.mark.parametrize("path,fused", [(TC, False), (GEN, False), (TC, True)])
+def test_truncated_plan_matches_full_plan(cuda, path, fused):
     """s2o_attention without a kv_perm output keeps only the exact top-T of each kv_perm
     segment; a tile that exhausts it saves its state and resumes on the next level (entries
     [T, 2T), ... of the same order), so traces equal the full-plan run for any depth (tiny
@@ -162,11 +162,11 @@ def test_truncated_plan_matches_full_plan(cuda, path):
     hq, hkv, l, s = 4, 2, 8192, 1024
     q, k, v = inputs(s2o, hq, hkv, l, seed=5)
     qd, kd, vd = dev_bf16(torch, q), dev_bf16(torch, k), dev_bf16(torch, v)
-    base = s2o.KernelConfig(seg_len=s, tau=0.005, path=path)
+    base = s2o.KernelConfig(seg_len=s, tau=0.005, path=path, q_reorder=not fused, fused=fused)
     full = s2o.s2o_attention(qd, kd, vd, base)  # kv_perm requested -> full plan
     torch.cuda.synchronize()
     for depth in (0, 128, 512, 2048):
-        cfg = s2o.KernelConfig(seg_len=s, tau=0.005, path=path, plan_depth=depth)
+        cfg = s2o.KernelConfig(seg_len=s, tau=0.005, path=path, plan_depth=depth, q_reorder=not fused, fused=fused)
         res = s2o.s2o_attention(qd, kd, vd, cfg, want_plan=False)
         torch.cuda.synchronize()
         assert torch.equal(res.trace.processed, full.trace.processed), depth
@@ -178,7 +178,8 @@ def test_truncated_plan_matches_full_plan(cuda, path):
 
 def test_truncated_plan_gaussian_fallback(cuda):
     """Pure gaussian inputs never stop early: every tile exhausts every truncated level and walks
-    the whole prefix level by level (fused mode instead recomputes on the full plan)."""
+    the whole prefix level by level, in the two-pass and the fused variant (whose tiles save
+    their state at a level boundary like pass-2's)."""
     import paper_2602_22575_b200 as s2o
     torch = cuda
     torch.manual_seed(0)
@@ -198,7 +199,10 @@ def test_truncated_plan_gaussian_fallback(cuda):
     fres = s2o.s2o_attention(q, k, v, fcfg, want_plan=False)
     torch.cuda.synchronize()
     assert torch.equal(fres.trace.processed, ffull.trace.processed)
-    assert torch.equal(fres.out, ffull.out)
+    assert torch.equal(fres.trace.pass2_pairs, ffull.trace.pass2_pairs)
+    d = (fres.out.float() - ffull.out.float()).abs()
+    excess = (d - (1e-2 * ffull.out.float().abs() + 1e-3)).max().item()
+    assert excess <= 0 and d.mean().item() <= 1e-4, (d.max().item(), d.mean().item())
 
 
 @pytest.mark.parametrize("z,hq,hkv,pinned", [(2, 4, 2, True), (1, 8, 4, False), (1, 2, 1, True)])
