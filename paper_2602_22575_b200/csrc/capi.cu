@@ -549,8 +549,17 @@ s2o_status s2o_attention_fwd(const s2o_problem* p, const void* q, const void* k,
             S2O_CUDA_TRY(cudaMemcpyAsync(seglist, segs.data(), sizeof(int32_t) * segs.size(), cudaMemcpyHostToDevice, s),
                          "h2d segments");
             lvl_base += topt;
+            if (std::getenv("S2O_LEVEL_LOG"))
+                std::fprintf(stderr, "s2o plan level %lld: %d overflow tiles in %zu segments\n",
+                             (long long)(lvl_base / topt), host[0], segs.size());
+            const bool lvl_log = std::getenv("S2O_LEVEL_LOG") != nullptr;
+            cudaEvent_t lev[3];
+            if (lvl_log)
+                for (auto& e : lev) { cudaEventCreate(&e); }
+            if (lvl_log) cudaEventRecord(lev[0], s);
             S2O_CUDA_TRY(launch_plan_level(g, seglist, (int64_t)segs.size(), lists[cur], lvl_base, lists[cur ^ 1], topt,
                                            ovf + 1, base + L.plan, s), "plan level");
+            if (lvl_log) cudaEventRecord(lev[1], s);
             S2O_CUDA_TRY(cudaMemsetAsync(ovf, 0, sizeof(int32_t), s), "memset");
             PassArgs a3 = a2;
             if (cfg->fused) {  // the diagonal part is done: resume the saved state, prefix only
@@ -565,8 +574,20 @@ s2o_status s2o_attention_fwd(const s2o_problem* p, const void* q, const void* k,
             a3.ovf_tiles = tiles[cur ^ 1];
             a3.ovf_base = bases[cur ^ 1];
             if ((st = run_pass(a3, cfg->path, base + L.pass, pass_ws_bytes(a), s, false))) return st;
+            if (lvl_log) {
+                cudaEventRecord(lev[2], s);
+                cudaEventSynchronize(lev[2]);
+                float t01 = 0.f, t12 = 0.f;
+                cudaEventElapsedTime(&t01, lev[0], lev[1]);
+                cudaEventElapsedTime(&t12, lev[1], lev[2]);
+                std::fprintf(stderr, "   level selection %.3f ms, tile rerun %.3f ms\n", t01, t12);
+                for (auto& e : lev) cudaEventDestroy(e);
+            }
             cur ^= 1;
         }
+        if (host[1] != 0 && std::getenv("S2O_LEVEL_LOG"))
+            std::fprintf(stderr, "s2o plan: a selection was not certified at level %lld -> full plan\n",
+                         (long long)(lvl_base / topt));
         if (host[1] != 0) {
             // A selection could not be certified: full plan, recompute everything.
             S2O_CUDA_TRY(launch_plan_build(g, q, k, qp, kvp, base + L.plan, s), "plan build");

@@ -789,19 +789,31 @@ sel_scan_kernel(Geo g, const uint64_t* __restrict__ kvkey, int64_t topt, uint64_
         smp[u] = small ? 0ull : keys[(int64_t)(e / 16) * (len / 128) + e % 16];
     }
     if (!small) SampSort(samp).Sort(smp);  // blocked: thread t holds ranks kPer t .. kPer t + kPer - 1
-    double want = small ? (double)len : (double)lvl_base + 1.15 * (double)tt + 32.0;
+    // Threshold: first the sample key of the rank expected to hold ~1.15 T of the level's keys;
+    // retries step the sample rank by the observed count's distance to the middle of the
+    // [T, capacity] window until the window is bracketed, then bisect between the bracketing
+    // keys (the count is monotone in the key, so this converges however dense the keys are).
+    const double dens = (double)kSelSample / (double)len;  // sample ranks per key
+    const double mid = (double)tt + 0.5 * (double)(kSelCap - tt);
+    const double want = small ? (double)len : (double)lvl_base + 1.15 * (double)tt + 32.0;
+    bool take_all = want >= (double)len;  // every remaining key fits the capacity
+    int64_t rank = min((int64_t)ceil(want * dens) + 4, (int64_t)(kSelSample - 1));
+    bool have_lo = false, have_hi = false;  // a threshold known to take too few / too many
+    uint64_t t_lo = 0ull, t_hi = ~0ull;
     bool ok = false;
     int count = 0;
-    for (int attempt = 0; attempt < 6 && !ok; ++attempt) {
-        int64_t rank = (int64_t)ceil(want * kSelSample / (double)len) + 4;
-        if (rank > kSelSample - 1) rank = kSelSample - 1;
+    for (int attempt = 0; attempt < 8 && !ok; ++attempt) {
         __syncthreads();  // previous attempt's s_count / s_theta reads are done
-        const bool take_all = want >= (double)len;  // every remaining key fits the capacity
-        if (tid == (int)(rank / kPer)) s_theta = take_all ? ~0ull : smp[rank % kPer];
+        const bool bisect = have_lo && have_hi;
+        if (bisect) {
+            if (tid == 0) s_theta = t_lo + (t_hi - t_lo) / 2;
+        } else if (tid == (int)(rank / kPer)) {
+            s_theta = take_all ? ~0ull : smp[rank % kPer];
+        }
         if (tid == 0) s_count = 0;
         __syncthreads();
         const uint64_t theta = s_theta;
-        const bool last_sample = take_all || (rank == kSelSample - 1);
+        const bool last_sample = theta == ~0ull;
         // order-preserving compaction of every key <= theta: 8 consecutive keys per thread, the
         // next iteration's keys loaded before this one's are used (the scan is latency-bound)
         constexpr int kU = 8;
@@ -872,20 +884,44 @@ sel_scan_kernel(Geo g, const uint64_t* __restrict__ kvkey, int64_t topt, uint64_
         }
         __syncthreads();
         const int cnt = s_count;
+#ifdef S2O_SEL_DEBUG
+        if (tid == 0 && (attempt > 0 || cnt < tt || cnt > kSelCap))
+            printf("sel zh %lld n %lld len %lld tt %lld lvl %lld attempt %d rank %lld all %d cnt %d\n", (long long)sg.zh,
+                   (long long)sg.n, (long long)len, (long long)tt, (long long)lvl_base, attempt, (long long)rank,
+                   (int)take_all, cnt);
+#endif
         if (cnt >= tt && cnt <= kSelCap) {
             ok = true;
             count = cnt;
         } else if (cnt < tt) {
-            if (last_sample) {
+            if (last_sample) {  // every remaining key is a candidate and still fewer than T
                 count = min(cnt, kSelCap);
                 ok = true;
                 if (tid == 0) atomicExch(flags, 1);
             }
-            want *= 2.0;
+            have_lo = true;
+            t_lo = theta;
+            if (!have_hi) {
+                rank += max((int64_t)1, (int64_t)ceil((mid - cnt) * dens));
+                if (rank >= kSelSample - 1) {
+                    rank = kSelSample - 1;
+                    take_all = true;
+                }
+            }
         } else {
-            want = 0.5 * (want + (double)tt);
-            if (want < tt + 1) want = tt + 1;
+            have_hi = true;
+            t_hi = theta;
+            if (!have_lo) {
+                if (rank == 0) {  // below the smallest sample key: bisect from key 0
+                    have_lo = true;
+                    t_lo = 0ull;
+                }
+                rank = take_all ? (int64_t)(kSelSample - 1)
+                                : max((int64_t)0, rank - max((int64_t)1, (int64_t)ceil((cnt - mid) * dens)));
+                take_all = false;
+            }
         }
+        if (!ok && have_lo && have_hi && t_hi - t_lo <= 1) break;  // equal keys straddle the window
     }
     if (!ok) {
         count = kSelCap;
