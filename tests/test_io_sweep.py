@@ -244,3 +244,40 @@ def test_device_sweep_baseline_matches_reference(tmp_path, ref):
         for ha, hb in zip(a["report"]["per_head"], b["report"]["per_head"]):
             assert ha["computed_pairs"] == hb["computed_pairs"] and ha["sparsity"] == hb["sparsity"]
             assert ha["mse"] == pytest.approx(hb["mse"], rel=2e-3, abs=1e-12)
+
+
+@pytest.mark.gpu
+def test_block_topk_ragged_gqa(ref):
+    """L not a multiple of the block (ragged last block) and GQA (K/V expanded for the reference)."""
+    import torch
+
+    import paper_2602_22575_b200 as s2o
+
+    q, k, v = ref.generate_synthetic("mixed", 3, 8.0, 7, 2, 4, 200, 16)
+    kk, vv = k[:, ::2].copy(), v[:, ::2].copy()  # hkv = 2: q head h reads kv head h // 2
+    want, want_pairs = ref.block_topk(q, np.repeat(kk, 2, axis=1), np.repeat(vv, 2, axis=1), 16, 16, 2)
+    dq, dk, dv = (torch.from_numpy(np.ascontiguousarray(x)).cuda() for x in (q, kk, vv))
+    got, pairs = s2o.block_topk_attention(dq, dk, dv, 16, 16, 2)
+    assert pairs.cpu().numpy().reshape(-1).tolist() == want_pairs.tolist()
+    np.testing.assert_allclose(got.cpu().numpy(), want, rtol=0, atol=2e-6)
+
+
+@pytest.mark.gpu
+def test_sweep_from_s2ot_trio_equals_synthetic(tmp_path):
+    """The file input source (<base>.{q,k,v}.s2ot) gives the same report as the generator."""
+    import paper_2602_22575_b200 as s2o
+
+    q, k, v = s2o.generate_synthetic("mixed", 4, 8.0, 0, 1, 2, 256, 32)
+    base = str(tmp_path / "in")
+    for name, x in (("q", q), ("k", k), ("v", v)):
+        save_tensor_file(x, f"{base}.{name}.s2ot")
+    grid = dict(variants=["two-pass", "baseline-topk"], taus=[0.02], seg_lens=[64], topk=[2])
+    syn = sw.run_sweep(_cfg(str(tmp_path / "syn"), **grid))
+    cfg = _cfg(str(tmp_path / "file"), **grid)
+    cfg.synthetic, cfg.input_base = None, base
+    fil = sw.run_sweep(cfg)
+    assert not syn.partial and not fil.partial, (syn.error, fil.error)
+    a, b = json.load(open(syn.json_path)), json.load(open(fil.json_path))
+    assert b["config"]["input"] == base
+    for pa, pb in zip(a["points"], b["points"]):
+        assert pa["report"] == pb["report"]
