@@ -90,6 +90,7 @@ struct TcParams {
     PassArgs a;
     float scale_log2;  // (1/sqrt(D)) * log2(e)
     int q_contig, kv_contig;
+    int vec_acc, vec_o;  // 256-bit epilogue accesses (32-B aligned state / output rows)
     int64_t pairs_per_head, pairs_full;  // pairs per head; pairs in a full segment
     unsigned long long* tl;              // optional timeline (CTA 0), see s2o_debug_timeline
 };
@@ -495,6 +496,7 @@ tc_pass_kernel(const TcParams p, const __grid_constant__ CUtensorMap qmap,
                 ++qcount;
                 int stop_at[2] = {1 << 30, 1 << 30};
                 bool pv_any[2] = {false, false};  // first P V of a slot overwrites O (accumulate = 0)
+                bool q_released = false;
                 auto need = [&](int j, int lag) {
                     bool n = false;
                     for (int x = 0; x < 2; ++x) n |= participates(P, x, j) && !(stop_at[x] <= j - lag);
@@ -563,7 +565,7 @@ tc_pass_kernel(const TcParams p, const __grid_constant__ CUtensorMap qmap,
                     if (!has_kn) break;
                     if (!kn_ready) wait_k(gki + 1);
                 }
-                if (leader) umma_commit(smem_u32(&c.q_empty));
+                if (leader && !q_released) umma_commit(smem_u32(&c.q_empty));
                 gk += nk;
                 gv += nv;
             }
@@ -644,16 +646,19 @@ tc_pass_kernel(const TcParams p, const __grid_constant__ CUtensorMap qmap,
                     float mxa[8];
 #pragma unroll
                     for (int i = 0; i < 8; ++i) mxa[i] = -INFINITY;
+                    // three-input max (FMNMX3): 64 instructions for the 128 scores
                     if (full) {
 #pragma unroll
-                        for (int i = 0; i < kBN; ++i) mxa[i & 7] = fmaxf(mxa[i & 7], __uint_as_float(sv[i]));
+                        for (int i = 0; i < kBN; i += 2)
+                            mxa[(i >> 1) & 7] = fmax3(mxa[(i >> 1) & 7], __uint_as_float(sv[i]), __uint_as_float(sv[i + 1]));
                     } else {
 #pragma unroll
-                        for (int i = 0; i < kBN; ++i)
-                            mxa[i & 7] = fmaxf(mxa[i & 7], i < lim ? __uint_as_float(sv[i]) : -INFINITY);
+                        for (int i = 0; i < kBN; i += 2)
+                            mxa[(i >> 1) & 7] = fmax3(mxa[(i >> 1) & 7], i < lim ? __uint_as_float(sv[i]) : -INFINITY,
+                                                      i + 1 < lim ? __uint_as_float(sv[i + 1]) : -INFINITY);
                     }
-                    const float mx = fmaxf(fmaxf(fmaxf(mxa[0], mxa[1]), fmaxf(mxa[2], mxa[3])),
-                                           fmaxf(fmaxf(mxa[4], mxa[5]), fmaxf(mxa[6], mxa[7]))) * sc;
+                    const float mx = fmax3(fmax3(mxa[0], mxa[1], mxa[2]), fmax3(mxa[3], mxa[4], mxa[5]),
+                                           fmaxf(mxa[6], mxa[7])) * sc;
                     const float m_new = fmaxf(m2, mx);
                     rescale = (m_new > m2 + kRescaleThresh) || (m2 == -INFINITY);
                     m_use = rescale ? m_new : m2;
@@ -784,14 +789,30 @@ tc_pass_kernel(const TcParams p, const __grid_constant__ CUtensorMap qmap,
                 for (int i = 0; i < kD; ++i) ov[i] = 0u;
             }
             if (a.mode & kStateIn) {
-                const float4* src = reinterpret_cast<const float4*>(a.acc_in + slot * kD);
+                if (p.vec_acc) {
+                    const float* src = a.acc_in + slot * kD;
 #pragma unroll
-                for (int i = 0; i < kD / 4; ++i) {
-                    const float4 y = src[i];
-                    ov[4 * i] = __float_as_uint(fmaf(y.x, sacc, __uint_as_float(ov[4 * i])));
-                    ov[4 * i + 1] = __float_as_uint(fmaf(y.y, sacc, __uint_as_float(ov[4 * i + 1])));
-                    ov[4 * i + 2] = __float_as_uint(fmaf(y.z, sacc, __uint_as_float(ov[4 * i + 2])));
-                    ov[4 * i + 3] = __float_as_uint(fmaf(y.w, sacc, __uint_as_float(ov[4 * i + 3])));
+                    for (int i0 = 0; i0 < kD; i0 += 32) {  // 4 x 256-bit loads in flight per round
+                        uint32_t y[4][8];
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) ldg256(src + i0 + 8 * u, y[u]);
+#pragma unroll
+                        for (int u = 0; u < 4; ++u)
+#pragma unroll
+                            for (int e = 0; e < 8; ++e)
+                                ov[i0 + 8 * u + e] = __float_as_uint(
+                                    fmaf(__uint_as_float(y[u][e]), sacc, __uint_as_float(ov[i0 + 8 * u + e])));
+                    }
+                } else {
+                    const float4* src = reinterpret_cast<const float4*>(a.acc_in + slot * kD);
+#pragma unroll
+                    for (int i = 0; i < kD / 4; ++i) {
+                        const float4 y = src[i];
+                        ov[4 * i] = __float_as_uint(fmaf(y.x, sacc, __uint_as_float(ov[4 * i])));
+                        ov[4 * i + 1] = __float_as_uint(fmaf(y.y, sacc, __uint_as_float(ov[4 * i + 1])));
+                        ov[4 * i + 2] = __float_as_uint(fmaf(y.z, sacc, __uint_as_float(ov[4 * i + 2])));
+                        ov[4 * i + 3] = __float_as_uint(fmaf(y.w, sacc, __uint_as_float(ov[4 * i + 3])));
+                    }
                 }
             }
             const float inv = 1.0f / ell;
@@ -801,15 +822,31 @@ tc_pass_kernel(const TcParams p, const __grid_constant__ CUtensorMap qmap,
             const bool resume_later = overflow && a.acc_out != nullptr;
             const bool save_state = (a.mode & kStateOut) || resume_later;
             if (valid && save_state) {
-                float4* dst = reinterpret_cast<float4*>(a.acc_out + slot * kD);
+                if (p.vec_acc) {
+                    float* dst = a.acc_out + slot * kD;
 #pragma unroll
-                for (int i = 0; i < kD / 4; ++i)
-                    dst[i] = make_float4(__uint_as_float(ov[4 * i]), __uint_as_float(ov[4 * i + 1]),
-                                         __uint_as_float(ov[4 * i + 2]), __uint_as_float(ov[4 * i + 3]));
+                    for (int i = 0; i < kD; i += 8) stg256(dst + i, &ov[i]);
+                } else {
+                    float4* dst = reinterpret_cast<float4*>(a.acc_out + slot * kD);
+#pragma unroll
+                    for (int i = 0; i < kD / 4; ++i)
+                        dst[i] = make_float4(__uint_as_float(ov[4 * i]), __uint_as_float(ov[4 * i + 1]),
+                                             __uint_as_float(ov[4 * i + 2]), __uint_as_float(ov[4 * i + 3]));
+                }
             }
             if (valid && (a.mode & kFinal) && !resume_later) {
                 const int64_t ooff = g.o_base(P.zh) + grow * g.os[2];
-                if (g.out_bf16) {
+                if (g.out_bf16 && p.vec_o) {
+                    __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(a.o) + ooff;
+#pragma unroll
+                    for (int i = 0; i < kD; i += 16) {
+                        uint32_t w[8];
+#pragma unroll
+                        for (int e = 0; e < 8; ++e)
+                            w[e] = pack_bf16(__uint_as_float(ov[i + 2 * e]) * inv, __uint_as_float(ov[i + 2 * e + 1]) * inv);
+                        stg256(dst + i, w);
+                    }
+                } else if (g.out_bf16) {
                     uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(a.o) + ooff);
 #pragma unroll
                     for (int i = 0; i < kD / 8; ++i) {
@@ -1326,16 +1363,19 @@ tc_pass2cta_kernel(const TcParams p, const __grid_constant__ CUtensorMap qmap,
                     float mxa[8];
 #pragma unroll
                     for (int i = 0; i < 8; ++i) mxa[i] = -INFINITY;
+                    // three-input max (FMNMX3): 64 instructions for the 128 scores
                     if (full) {
 #pragma unroll
-                        for (int i = 0; i < kBN; ++i) mxa[i & 7] = fmaxf(mxa[i & 7], __uint_as_float(sv[i]));
+                        for (int i = 0; i < kBN; i += 2)
+                            mxa[(i >> 1) & 7] = fmax3(mxa[(i >> 1) & 7], __uint_as_float(sv[i]), __uint_as_float(sv[i + 1]));
                     } else {
 #pragma unroll
-                        for (int i = 0; i < kBN; ++i)
-                            mxa[i & 7] = fmaxf(mxa[i & 7], i < lim ? __uint_as_float(sv[i]) : -INFINITY);
+                        for (int i = 0; i < kBN; i += 2)
+                            mxa[(i >> 1) & 7] = fmax3(mxa[(i >> 1) & 7], i < lim ? __uint_as_float(sv[i]) : -INFINITY,
+                                                      i + 1 < lim ? __uint_as_float(sv[i + 1]) : -INFINITY);
                     }
-                    const float mx = fmaxf(fmaxf(fmaxf(mxa[0], mxa[1]), fmaxf(mxa[2], mxa[3])),
-                                           fmaxf(fmaxf(mxa[4], mxa[5]), fmaxf(mxa[6], mxa[7]))) * sc;
+                    const float mx = fmax3(fmax3(mxa[0], mxa[1], mxa[2]), fmax3(mxa[3], mxa[4], mxa[5]),
+                                           fmaxf(mxa[6], mxa[7])) * sc;
                     const float m_new = fmaxf(m2, mx);
                     rescale = (m_new > m2 + kRescaleThresh) || (m2 == -INFINITY);
                     m_use = rescale ? m_new : m2;
@@ -1579,6 +1619,10 @@ cudaError_t launch_tc_pass(const PassArgs& a, cudaStream_t st) {
     p.scale_log2 = (float)(a.scale * 1.4426950408889634);
     p.q_contig = g.qs[2] == kD;
     p.kv_contig = g.ks[2] == kD && g.vs[2] == kD;
+    // 256-bit epilogue accesses need 32-B aligned rows
+    const auto al32 = [](const void* ptr) { return (reinterpret_cast<uintptr_t>(ptr) & 31) == 0; };
+    p.vec_acc = al32(a.acc_in) && al32(a.acc_out);
+    p.vec_o = g.out_bf16 && al32(a.o) && g.os[0] % 16 == 0 && g.os[1] % 16 == 0 && g.os[2] % 16 == 0;
     p.pairs_full = (a.T + 1) / 2;
     p.tl = g_timeline;
     const int64_t t_last = (g.last_len + kBM - 1) / kBM;
