@@ -75,6 +75,9 @@ constexpr int kLaunchRegs = 65536 / kThreads / 8 * 8;  // 128: what __launch_bou
 static_assert(kSoftmaxRegs - kLaunchRegs <= kLaunchRegs - kOtherRegs, "register pool overcommitted");
 static_assert(sizeof(uint64_t) * 19 + 4 + 64 + 8 <= 256, "Ctrl exceeds its 256 B");
 constexpr float kRescaleThresh = 8.0f;
+#ifndef S2O_POLY_MOD
+#define S2O_POLY_MOD 0  // pass-2 softmax: every n-th exponential pair on the FMA pipe (0 = all MUFU)
+#endif
   // lazy max update, log2 units (factor 256)
 
 struct Ctrl {
@@ -680,7 +683,14 @@ tc_pass_kernel(const TcParams p, const __grid_constant__ CUtensorMap qmap,
                                 for (int i = 0; i < 32; i += 2) {
                                     const float2 arg = ffma2(make_float2(__uint_as_float(sv[c0 + i]), __uint_as_float(sv[c0 + i + 1])),
                                                              sc2, nr2);
+#if S2O_POLY_MOD > 0
+                                    // every S2O_POLY_MOD-th pair on the FMA pipe (MUFU offload)
+                                    const float2 e = ((i >> 1) % S2O_POLY_MOD == S2O_POLY_MOD - 1)
+                                                         ? ex2_poly3x2(arg)
+                                                         : make_float2(ex2(arg.x), ex2(arg.y));
+#else
                                     const float2 e = make_float2(ex2(arg.x), ex2(arg.y));
+#endif
                                     rs2[(i >> 1) & 1] = fadd2(rs2[(i >> 1) & 1], e);
                                     pk[i >> 1] = pack_bf16(e.x, e.y);
                                 }

@@ -345,6 +345,21 @@ __device__ __forceinline__ void stg256(void* dst, const uint32_t* r) {
                  "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
                  : "memory");
 }
+// 2^x for a pair of arguments on the FMA pipe (FADD2 / FFMA2 + two integer adds per value):
+// x = j + f with j = round(x), f in [-0.5, 0.5], degree-3 fit of 2^f (max rel. error 7.5e-5,
+// below the bf16 rounding of P), j added to the exponent field. x is clamped to >= -126.
+__device__ __forceinline__ float2 ex2_poly3x2(float2 x) {
+    const float2 xc = make_float2(fmaxf(x.x, -126.0f), fmaxf(x.y, -126.0f));
+    const float2 t = fadd2(xc, make_float2(12582912.0f, 12582912.0f));  // low mantissa bits = round(xc)
+    const float2 j = fadd2(t, make_float2(-12582912.0f, -12582912.0f));  // exact
+    const float2 f = ffma2(j, make_float2(-1.0f, -1.0f), xc);               // xc - j, exact
+    float2 p = ffma2(make_float2(0.05517115443944931f, 0.05517115443944931f), f,
+                     make_float2(0.2426098734140396f, 0.2426098734140396f));
+    p = ffma2(p, f, make_float2(0.6932609677314758f, 0.6932609677314758f));
+    p = ffma2(p, f, make_float2(0.9999281764030457f, 0.9999281764030457f));
+    return make_float2(__int_as_float(__float_as_int(p.x) + (__float_as_int(t.x) << 23)),
+                       __int_as_float(__float_as_int(p.y) + (__float_as_int(t.y) << 23)));
+}
 __device__ __forceinline__ float fmax3(float a, float b, float c) {  // FMNMX3 (sm_100)
     float d;
     asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
