@@ -905,6 +905,375 @@ tc_pass_kernel(const TcParams p, const __grid_constant__ CUtensorMap qmap,
     if (warp == 0) tmem_dealloc(tbase, kTmemCols);
 }
 
+// ============================================================== single-tile diagonal kernel
+// Pass-1 (and any diagonal-only pass: the dense reference with S = L) on ONE 128-row query tile
+// per work item, with the score buffer double-buffered in TMEM: S(j+1) = Q K(j+1)^T is computed
+// while the softmax of block j runs, so the softmax warps run block after block without waiting
+// on P V(j) + S(j+1) (the pair kernel's per-slot chain: softmax -> P V -> S -> softmax). The pair
+// kernel shares a K/V block between two tiles, which matters for gathered prefix chunks; the
+// diagonal blocks are contiguous 2-D TMA tiles served from L2, so one tile per item costs little.
+//
+//   warps 0-3  softmax + epilogue (thread r owns row r = TMEM lane 32 * warp + lane)
+//   warp 4     MMA issuer (one elected lane)
+//   warp 5     Q + K loader (lane 0, 2-D TMA tiles), warp 6 V loader (lane 0)
+//
+// TMEM: S buffers at columns [0, 128) and [128, 256) (P in bf16 over the first 64 columns of its
+// buffer), O at [256, 384). Blocks are numbered globally per CTA (gb); block gb uses S buffer
+// gb & 1. MMA order: S(0), S(1), then per block j: P V(j), S(j+2) (into the buffer P(j) held;
+// the tensor pipe executes in order, so S(j+2) overwrites P(j) only after P V(j) read it).
+// pv_bar completes once per P V: a softmax that must rescale O at block gb (lazy max update,
+// rare) first waits for completion gb, i.e. all earlier P V of the tile.
+constexpr int kDThreads = 224;
+constexpr int kDSoftWarps = 4, kDMmaWarp = 4, kDKWarp = 5, kDVWarp = 6;
+constexpr int kDKStages = 3, kDVStages = 3;
+constexpr uint32_t kDOffQ = 0;
+constexpr uint32_t kDOffK = kTileBytes;
+constexpr uint32_t kDOffV = kDOffK + kDKStages * kTileBytes;
+constexpr uint32_t kDOffCtrl = kDOffV + kDVStages * kTileBytes;
+constexpr uint32_t kDSmemBytes = kDOffCtrl + 256;  // 224.25 KB
+
+struct CtrlD {
+    uint64_t q_full, q_empty;
+    uint64_t k_full[kDKStages], k_empty[kDKStages], v_full[kDVStages], v_empty[kDVStages];
+    uint64_t s_full[2], p_full[2], pv_bar, o_done;
+    uint32_t tmem_base;
+};
+static_assert(sizeof(CtrlD) <= 256, "CtrlD exceeds its 256 B");
+
+struct TileInfo {
+    int64_t zh, n, sb, t0;
+    int tn, segr, nd;
+};
+
+// Work item idx -> (head, segment, tile). The q heads of a GQA group are interleaved (they read
+// the same K/V rows, which then hit L2 together); within a head the longest tiles come first.
+__device__ __forceinline__ TileInfo diag_tile(const TcParams& p, int64_t idx) {
+    const Geo& g = p.a.g;
+    const int64_t T = p.a.T, G = g.group;
+    const int64_t tiles_head = p.pairs_per_head;  // tiles per head (launcher)
+    const int64_t zg = idx / (tiles_head * G);
+    const int64_t rem = idx % (tiles_head * G);
+    TileInfo t;
+    t.zh = zg * G + rem % G;
+    int64_t r = rem / G;
+    const int64_t t_last = (g.last_len + kBM - 1) / kBM;
+    const int64_t full = (g.N - 1) * T;
+    // longest first: reverse the tile order inside a segment
+    if (r < full) { t.n = r / T; r = T - 1 - r % T; }
+    else { t.n = g.N - 1; r = t_last - 1 - (r - full); }
+    t.sb = t.n * g.S;
+    t.segr = (int)g.seg_rows(t.n);
+    t.t0 = r * kBM;
+    t.tn = (int)min((int64_t)kBM, (int64_t)t.segr - t.t0);
+    t.nd = (int)((t.t0 + t.tn - 1) / kBN + 1);
+    return t;
+}
+
+__global__ void __launch_bounds__(kDThreads, 1)
+tc_diag_kernel(const TcParams p, const __grid_constant__ CUtensorMap qtile,
+               const __grid_constant__ CUtensorMap ktile, const __grid_constant__ CUtensorMap vtile) {
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    unsigned char* smem = smem_raw;
+    if ((smem_u32(smem) & 1023u) != 0) __trap();
+    CtrlD& c = *reinterpret_cast<CtrlD*>(smem + kDOffCtrl);
+    const PassArgs& a = p.a;
+    const Geo& g = a.g;
+    const int warp = threadIdx.x / 32;
+    const int lane = threadIdx.x % 32;
+    const uint32_t sQ = smem_u32(smem + kDOffQ);
+    const uint32_t sK = smem_u32(smem + kDOffK);
+    const uint32_t sV = smem_u32(smem + kDOffV);
+    if (threadIdx.x == 0) {
+        mbar_init(smem_u32(&c.q_full), 1);
+        mbar_init(smem_u32(&c.q_empty), 1);
+        for (int s = 0; s < kDKStages; ++s) {
+            mbar_init(smem_u32(&c.k_full[s]), 1);
+            mbar_init(smem_u32(&c.k_empty[s]), 1);
+        }
+        for (int s = 0; s < kDVStages; ++s) {
+            mbar_init(smem_u32(&c.v_full[s]), 1);
+            mbar_init(smem_u32(&c.v_empty[s]), 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(smem_u32(&c.s_full[b]), 1);
+            mbar_init(smem_u32(&c.p_full[b]), kDSoftWarps);
+        }
+        mbar_init(smem_u32(&c.pv_bar), 1);
+        mbar_init(smem_u32(&c.o_done), 1);
+        fence_mbar_init();
+    }
+    if (warp == 0) {
+        tmem_alloc(smem_u32(&c.tmem_base), kTmemCols);
+        tmem_relinquish();
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tbase = c.tmem_base;
+    const int64_t total = g.z * g.hq * p.pairs_per_head;
+    const int64_t rowu = g.d;
+
+    if (warp == kDKWarp || warp == kDVWarp) {
+        // ============================== loaders (one lane each) ==============================
+        if (lane != 0) return;
+        const bool kl = warp == kDKWarp;
+        const CUtensorMap* xtile = kl ? &ktile : &vtile;
+        const uint32_t xbase = kl ? sK : sV;
+        const int nst = kl ? kDKStages : kDVStages;
+        uint64_t* xfull = kl ? c.k_full : c.v_full;
+        uint64_t* xempty = kl ? c.k_empty : c.v_empty;
+        uint32_t gi = 0, qc = 0;
+        for (int64_t it = blockIdx.x; it < total; it += gridDim.x) {
+            const TileInfo t = diag_tile(p, it);
+            if (kl) {
+                mbar_wait(smem_u32(&c.q_empty), (qc & 1) ^ 1, 4001);
+                mbar_expect_tx(smem_u32(&c.q_full), kTileBytes);
+                const int64_t qb = g.q_base(t.zh) / rowu;
+                for (int h = 0; h < 2; ++h)
+                    tma_load2d(sQ + h * kHalf, &qtile, h * 64, (int32_t)(qb + t.sb + t.t0), smem_u32(&c.q_full));
+                ++qc;
+            }
+            const int64_t xb = (kl ? g.k_base(t.zh) : g.v_base(t.zh)) / rowu;
+            for (int j = 0; j < t.nd; ++j, ++gi) {
+                const int st = gi % nst;
+                mbar_wait(smem_u32(&xempty[st]), ((gi / nst) & 1) ^ 1, kl ? 4002 : 4003);
+                mbar_expect_tx(smem_u32(&xfull[st]), kTileBytes);
+                const uint32_t dst = xbase + st * kTileBytes;
+                for (int h = 0; h < 2; ++h)
+                    tma_load2d(dst + h * kHalf, xtile, h * 64, (int32_t)(xb + t.sb + (int64_t)j * kBN),
+                               smem_u32(&xfull[st]));
+            }
+        }
+        return;
+    }
+    if (warp == kDMmaWarp) {
+        // ============================== MMA issuer ==============================
+        const bool leader = elect_one();
+        const uint32_t idesc_s = umma_idesc_bf16(kBM, kBN, false, false);
+        const uint32_t idesc_o = umma_idesc_bf16(kBM, kD, false, true);
+        const uint64_t dq = umma_desc_sw128(sQ, 16, 1024);
+        const uint64_t dk0 = umma_desc_sw128(sK, 16, 1024);
+        const uint64_t dv0 = umma_desc_sw128(sV, kHalf, 1024);
+        uint32_t gb = 0, qc = 0;
+        auto issue_s = [&](uint32_t blk) {  // S(blk) into buffer blk & 1; K(blk) from stage blk % 3
+            const uint32_t st = blk % kDKStages;
+            mbar_wait(smem_u32(&c.k_full[st]), (blk / kDKStages) & 1, 4101);
+            tc_fence_after();
+            const uint64_t dk = dk0 + ((st * kTileBytes) >> 4);
+#pragma unroll
+            for (int kk = 0; kk < kD / 16; ++kk) {
+                const uint32_t off = ((kk / 4) * kHalf + (kk % 4) * 32) >> 4;
+                if (leader) umma_bf16(tbase + (blk & 1) * 128, dq + off, dk + off, idesc_s, kk > 0);
+            }
+            if (leader) {
+                umma_commit(smem_u32(&c.s_full[blk & 1]));
+                umma_commit(smem_u32(&c.k_empty[st]));
+            }
+            __syncwarp();
+        };
+        for (int64_t it = blockIdx.x; it < total; it += gridDim.x) {
+            const TileInfo t = diag_tile(p, it);
+            const uint32_t g0 = gb;
+            mbar_wait(smem_u32(&c.q_full), qc & 1, 4102);
+            ++qc;
+            issue_s(g0);
+            if (t.nd > 1) issue_s(g0 + 1);
+            if (t.nd <= 2 && leader) umma_commit(smem_u32(&c.q_empty));
+            for (int j = 0; j < t.nd; ++j) {
+                const uint32_t blk = g0 + j;
+                mbar_wait(smem_u32(&c.p_full[blk & 1]), (blk >> 1) & 1, 4103);
+                const uint32_t vst = blk % kDVStages;
+                mbar_wait(smem_u32(&c.v_full[vst]), (blk / kDVStages) & 1, 4104);
+                tc_fence_after();
+                const uint64_t dv = dv0 + ((vst * kTileBytes) >> 4);
+#pragma unroll
+                for (int kk = 0; kk < kBN / 16; ++kk)
+                    if (leader)
+                        umma_bf16_ts(tbase + 256, tbase + (blk & 1) * 128 + kk * 8, dv + ((kk * 16 * 128) >> 4),
+                                     idesc_o, (kk > 0 || j > 0) ? 1 : 0);
+                if (leader) {
+                    umma_commit(smem_u32(&c.pv_bar));
+                    umma_commit(smem_u32(&c.v_empty[vst]));
+                    if (j == t.nd - 1) umma_commit(smem_u32(&c.o_done));
+                }
+                __syncwarp();
+                if (j + 2 < t.nd) {
+                    issue_s(blk + 2);
+                    if (j + 2 == t.nd - 1 && leader) umma_commit(smem_u32(&c.q_empty));
+                }
+            }
+            gb += t.nd;
+        }
+        __syncwarp();
+    } else if (warp < kDSoftWarps) {
+        // ============================== softmax / epilogue ==============================
+        const int r = threadIdx.x;  // TMEM lane
+        const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
+        const uint32_t tS0 = tbase + lane_off;
+        const uint32_t tO = tS0 + 256;
+        const float sc = p.scale_log2;
+        uint32_t gb = 0, no = 0;
+        for (int64_t it = blockIdx.x; it < total; it += gridDim.x) {
+            const TileInfo t = diag_tile(p, it);
+            const bool valid = r < t.tn;
+            const int rr = valid ? r : 0;
+            float m2 = -INFINITY, ell = 0.0f;
+            const int t0x = (int)t.t0;
+            for (int j = 0; j < t.nd; ++j, ++gb) {
+                const uint32_t tS = tS0 + (gb & 1) * 128;
+                mbar_wait(smem_u32(&c.s_full[gb & 1]), (gb >> 1) & 1, 4201);
+                tc_fence_after();
+                uint32_t sv[kBN];
+#pragma unroll
+                for (int c0 = 0; c0 < kBN; c0 += 32) tmem_ld32(tS + c0, *reinterpret_cast<uint32_t(*)[32]>(&sv[c0]));
+                tmem_ld_wait();
+                // visible keys of this row in block j (causal on segment positions, kernel.cpp:58-69)
+                const int k0 = j * kBN;
+                const int kn = min(kBN, t.segr - k0);
+                const int vis = (k0 + kn - 1 <= t0x) ? kn : min(kn, t0x + rr - k0 + 1);
+                const int lim = max(0, vis);
+                const bool full = __all_sync(0xffffffffu, lim >= kBN);
+                float mxa[8];
+#pragma unroll
+                for (int i = 0; i < 8; ++i) mxa[i] = -INFINITY;
+                if (full) {
+#pragma unroll
+                    for (int i = 0; i < kBN; i += 2)
+                        mxa[(i >> 1) & 7] = fmax3(mxa[(i >> 1) & 7], __uint_as_float(sv[i]), __uint_as_float(sv[i + 1]));
+                } else {
+#pragma unroll
+                    for (int i = 0; i < kBN; i += 2)
+                        mxa[(i >> 1) & 7] = fmax3(mxa[(i >> 1) & 7], i < lim ? __uint_as_float(sv[i]) : -INFINITY,
+                                                  i + 1 < lim ? __uint_as_float(sv[i + 1]) : -INFINITY);
+                }
+                const float mx = fmax3(fmax3(mxa[0], mxa[1], mxa[2]), fmax3(mxa[3], mxa[4], mxa[5]),
+                                       fmaxf(mxa[6], mxa[7])) * sc;
+                const float m_new = fmaxf(m2, mx);
+                const bool rescale = (m_new > m2 + kRescaleThresh) || (m2 == -INFINITY);
+                const float m_use = rescale ? m_new : m2;
+                const float neg_ref = (m_use == -INFINITY) ? 0.0f : -m_use;
+                const float alpha = (m2 == -INFINITY) ? 0.0f : ex2(m2 + neg_ref);
+                float rs[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+                if (full) {
+#pragma unroll
+                    for (int c0 = 0; c0 < kBN; c0 += 32) {
+                        uint32_t pk[16];
+#pragma unroll
+                        for (int i = 0; i < 32; i += 2) {
+                            const float e0 = ex2(fmaf(__uint_as_float(sv[c0 + i]), sc, neg_ref));
+                            const float e1 = ex2(fmaf(__uint_as_float(sv[c0 + i + 1]), sc, neg_ref));
+                            rs[(i >> 1) & 3] += e0 + e1;
+                            pk[i >> 1] = pack_bf16(e0, e1);
+                        }
+                        tmem_st16(tS + c0 / 2, pk);
+                    }
+                } else {
+#pragma unroll
+                    for (int c0 = 0; c0 < kBN; c0 += 32) {
+                        uint32_t pk[16];
+#pragma unroll
+                        for (int i = 0; i < 32; i += 2) {
+                            const float e0 = c0 + i < lim ? ex2(fmaf(__uint_as_float(sv[c0 + i]), sc, neg_ref)) : 0.0f;
+                            const float e1 =
+                                c0 + i + 1 < lim ? ex2(fmaf(__uint_as_float(sv[c0 + i + 1]), sc, neg_ref)) : 0.0f;
+                            rs[(i >> 1) & 3] += e0 + e1;
+                            pk[i >> 1] = pack_bf16(e0, e1);
+                        }
+                        tmem_st16(tS + c0 / 2, pk);
+                    }
+                }
+                const float rowsum = (rs[0] + rs[1]) + (rs[2] + rs[3]);
+                // O rescale (lazy, rare): all earlier P V of this tile must have completed
+                if (__any_sync(0xffffffffu, j > 0 && rescale && m2 != -INFINITY)) {
+                    mbar_wait(smem_u32(&c.pv_bar), (gb - 1) & 1, 4202);
+                    tc_fence_after();
+#pragma unroll
+                    for (int c0 = 0; c0 < kD; c0 += 32) {
+                        uint32_t v[32];
+                        tmem_ld32(tO + c0, v);
+                        tmem_ld_wait();
+#pragma unroll
+                        for (int i = 0; i < 32; ++i) v[i] = __float_as_uint(__uint_as_float(v[i]) * alpha);
+                        tmem_st32(tO + c0, v);
+                    }
+                }
+                tmem_st_wait();
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(smem_u32(&c.p_full[gb & 1]));
+                ell = ell * alpha + rowsum;
+                m2 = m_use;
+            }
+            // ---- epilogue: read O after the tile's last P V, persist state / finalize
+            mbar_wait(smem_u32(&c.o_done), no & 1, 4203);
+            ++no;
+            tc_fence_after();
+            uint32_t ov[kD];
+#pragma unroll
+            for (int c0 = 0; c0 < kD; c0 += 32) tmem_ld32(tO + c0, *reinterpret_cast<uint32_t(*)[32]>(&ov[c0]));
+            tmem_ld_wait();
+            tc_fence_before();
+            const int64_t grow = t.sb + t.t0 + rr;
+            const int64_t slot = t.zh * g.l + grow;
+            if (valid && (a.mode & kStateOut)) {
+                if (p.vec_acc) {
+                    float* dst = a.acc_out + slot * kD;
+#pragma unroll
+                    for (int i = 0; i < kD; i += 8) stg256(dst + i, &ov[i]);
+                } else {
+                    float4* dst = reinterpret_cast<float4*>(a.acc_out + slot * kD);
+#pragma unroll
+                    for (int i = 0; i < kD / 4; ++i)
+                        dst[i] = make_float4(__uint_as_float(ov[4 * i]), __uint_as_float(ov[4 * i + 1]),
+                                             __uint_as_float(ov[4 * i + 2]), __uint_as_float(ov[4 * i + 3]));
+                }
+                a.m_out[slot] = (m2 == -INFINITY) ? -INFINITY : m2 * 0.6931471805599453f;
+                a.ell_out[slot] = ell;
+            }
+            if (valid && (a.mode & kFinal)) {
+                const float inv = 1.0f / ell;
+                const int64_t ooff = g.o_base(t.zh) + grow * g.os[2];
+                if (g.out_bf16 && p.vec_o) {
+                    __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(a.o) + ooff;
+#pragma unroll
+                    for (int i = 0; i < kD; i += 16) {
+                        uint32_t w[8];
+#pragma unroll
+                        for (int e = 0; e < 8; ++e)
+                            w[e] = pack_bf16(__uint_as_float(ov[i + 2 * e]) * inv, __uint_as_float(ov[i + 2 * e + 1]) * inv);
+                        stg256(dst + i, w);
+                    }
+                } else if (g.out_bf16) {
+                    uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(a.o) + ooff);
+#pragma unroll
+                    for (int i = 0; i < kD / 8; ++i) {
+                        uint4 w;
+                        w.x = pack_bf16(__uint_as_float(ov[8 * i]) * inv, __uint_as_float(ov[8 * i + 1]) * inv);
+                        w.y = pack_bf16(__uint_as_float(ov[8 * i + 2]) * inv, __uint_as_float(ov[8 * i + 3]) * inv);
+                        w.z = pack_bf16(__uint_as_float(ov[8 * i + 4]) * inv, __uint_as_float(ov[8 * i + 5]) * inv);
+                        w.w = pack_bf16(__uint_as_float(ov[8 * i + 6]) * inv, __uint_as_float(ov[8 * i + 7]) * inv);
+                        dst[i] = w;
+                    }
+                } else {
+                    float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(a.o) + ooff);
+#pragma unroll
+                    for (int i = 0; i < kD / 4; ++i)
+                        dst[i] = make_float4(__uint_as_float(ov[4 * i]) * inv, __uint_as_float(ov[4 * i + 1]) * inv,
+                                             __uint_as_float(ov[4 * i + 2]) * inv, __uint_as_float(ov[4 * i + 3]) * inv);
+                }
+                if (!(ell > 0.0f)) atomicExch(a.err_flag, 2);
+            }
+        }
+    }
+    // (warp 7 does not exist: kDThreads = 7 warps)
+    tc_fence_before();
+    if (warp <= kDMmaWarp) named_bar_sync(5, 32 * (kDMmaWarp + 1));
+    if (warp == 0) {
+        tc_fence_after();
+        tmem_dealloc(tbase, kTmemCols);
+    }
+}
+
 // ============================================================== CTA-pair kernel
 // The same operator on CTA pairs (cluster of 2, tcgen05 cta_group::2). The work unit is a QUAD
 // of 128-row query tiles of one (head, segment): slot x of the pair is the 256-row M tile made
@@ -1637,6 +2006,32 @@ cudaError_t launch_tc_pass(const PassArgs& a, cudaStream_t st) {
     p.tl = g_timeline;
     const int64_t t_last = (g.last_len + kBM - 1) / kBM;
     p.pairs_per_head = (g.N - 1) * p.pairs_full + (t_last + 1) / 2;
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    // Diagonal-only passes (pass-1, the dense reference) on contiguous rows: the single-tile
+    // kernel with double-buffered S (S2O_DIAG_KERNEL=0 selects the pair kernel instead).
+    static const bool diag_on = [] {
+        const char* e = std::getenv("S2O_DIAG_KERNEL");
+        return !(e && std::strcmp(e, "0") == 0);
+    }();
+    if (diag_on && (a.mode & kDiag) && !(a.mode & (kPrefix | kStateIn)) && !a.tile_list && p.q_contig &&
+        p.kv_contig) {
+        TcParams pd = p;
+        pd.pairs_per_head = (g.N - 1) * a.T + t_last;  // tiles per head (diag_tile)
+        static bool attrd_done = false;
+        if (!attrd_done) {
+            cudaError_t e = cudaFuncSetAttribute(tc_diag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 (int)kDSmemBytes);
+            if (e != cudaSuccess) return e;
+            attrd_done = true;
+        }
+        const int64_t work = g.z * g.hq * pd.pairs_per_head;
+        if (work == 0) return cudaSuccess;
+        const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(work, sms));
+        tc_diag_kernel<<<grid, kDThreads, kDSmemBytes, st>>>(pd, qtile, ktile, vtile);
+        return cudaGetLastError();
+    }
     static bool attr_done = false;
     if (!attr_done) {
         for (const void* f : {(const void*)tc_pass_kernel<false>, (const void*)tc_pass_kernel<true>}) {
@@ -1645,9 +2040,6 @@ cudaError_t launch_tc_pass(const PassArgs& a, cudaStream_t st) {
         }
         attr_done = true;
     }
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     // CTA-pair variant (cta_group::2, quads of tiles) only on request (S2O_TC_CTAS=2): it halves
     // the gathered bytes per SM but its per-block cross-SM handshakes (4 remote p_full arrivals,
     // remote decision publication) cost more than they save at C3 (pass-2 8.9 vs 7.4 ms,
