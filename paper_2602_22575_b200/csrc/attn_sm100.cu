@@ -913,29 +913,38 @@ tc_pass_kernel(const TcParams p, const __grid_constant__ CUtensorMap qmap,
 // kernel shares a K/V block between two tiles, which matters for gathered prefix chunks; the
 // diagonal blocks are contiguous 2-D TMA tiles served from L2, so one tile per item costs little.
 //
-//   warps 0-3  softmax + epilogue (thread r owns row r = TMEM lane 32 * warp + lane)
-//   warp 4     MMA issuer (one elected lane)
-//   warp 5     Q + K loader (lane 0, 2-D TMA tiles), warp 6 V loader (lane 0)
+//   warps 0-3  softmax (thread r owns row r = TMEM lane 32 * warp + lane)
+//   warps 4-7  epilogue: read O of a finished tile from TMEM, persist state / write O, so the
+//              softmax warps go straight on to the next tile
+//   warp 8     MMA issuer (one elected lane)
+//   warp 9     Q + K loader (lane 0, 2-D TMA tiles), warp 10 V loader (lane 0), warp 11 idle
 //
 // TMEM: S buffers at columns [0, 128) and [128, 256) (P in bf16 over the first 64 columns of its
-// buffer), O at [256, 384). Blocks are numbered globally per CTA (gb); block gb uses S buffer
+// buffer), O double-buffered by tile parity at [256, 384) and [384, 512): the epilogue of tile k
+// overlaps tile k+1. Blocks are numbered globally per CTA (gb); block gb uses S buffer
 // gb & 1. MMA order: S(0), S(1), then per block j: P V(j), S(j+2) (into the buffer P(j) held;
 // the tensor pipe executes in order, so S(j+2) overwrites P(j) only after P V(j) read it).
 // pv_bar completes once per P V: a softmax that must rescale O at block gb (lazy max update,
 // rare) first waits for completion gb, i.e. all earlier P V of the tile.
-constexpr int kDThreads = 224;
-constexpr int kDSoftWarps = 4, kDMmaWarp = 4, kDKWarp = 5, kDVWarp = 6;
+#ifndef S2O_DIAG_PACKED
+#define S2O_DIAG_PACKED 0  // packed FFMA2/FADD2 softmax arguments and sums in the diagonal kernel
+#endif
+constexpr int kDThreads = 384;
+constexpr int kDSoftWarps = 4, kDEpiWarp0 = 4, kDMmaWarp = 8, kDKWarp = 9, kDVWarp = 10;
+constexpr int kDSoftRegs = 208, kDEpiRegs = 160, kDOtherRegs = 56;  // setmaxnreg per warpgroup
 constexpr int kDKStages = 3, kDVStages = 3;
 constexpr uint32_t kDOffQ = 0;
 constexpr uint32_t kDOffK = kTileBytes;
 constexpr uint32_t kDOffV = kDOffK + kDKStages * kTileBytes;
 constexpr uint32_t kDOffCtrl = kDOffV + kDVStages * kTileBytes;
-constexpr uint32_t kDSmemBytes = kDOffCtrl + 256;  // 224.25 KB
+constexpr uint32_t kDOffML = kDOffCtrl + 256;        // float [2 tile parity][2 (m, ell)][128 rows]
+constexpr uint32_t kDSmemBytes = kDOffML + 2 * 2 * 128 * 4;  // 226.25 KB
 
 struct CtrlD {
     uint64_t q_full, q_empty;
     uint64_t k_full[kDKStages], k_empty[kDKStages], v_full[kDVStages], v_empty[kDVStages];
-    uint64_t s_full[2], p_full[2], pv_bar, o_done;
+    uint64_t s_full[2], p_full[2], pv_bar;
+    uint64_t o_done[2], o_free[2], ml_full[2];  // per O buffer (tile parity)
     uint32_t tmem_base;
 };
 static_assert(sizeof(CtrlD) <= 256, "CtrlD exceeds its 256 B");
@@ -999,7 +1008,11 @@ tc_diag_kernel(const TcParams p, const __grid_constant__ CUtensorMap qtile,
             mbar_init(smem_u32(&c.p_full[b]), kDSoftWarps);
         }
         mbar_init(smem_u32(&c.pv_bar), 1);
-        mbar_init(smem_u32(&c.o_done), 1);
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(smem_u32(&c.o_done[b]), 1);
+            mbar_init(smem_u32(&c.o_free[b]), 4);   // epilogue warps
+            mbar_init(smem_u32(&c.ml_full[b]), kDSoftWarps);
+        }
         fence_mbar_init();
     }
     if (warp == 0) {
@@ -1012,10 +1025,12 @@ tc_diag_kernel(const TcParams p, const __grid_constant__ CUtensorMap qtile,
     const uint32_t tbase = c.tmem_base;
     const int64_t total = g.z * g.hq * p.pairs_per_head;
     const int64_t rowu = g.d;
-
-    if (warp == kDKWarp || warp == kDVWarp) {
+    float* ml = reinterpret_cast<float*>(smem + kDOffML);
+    // (setmaxnreg inside each role branch, so the softmax code is dominated by its increase)
+    if (warp == kDKWarp || warp == kDVWarp || warp > kDVWarp) {
+        setmaxnreg_dec<kDOtherRegs>();
         // ============================== loaders (one lane each) ==============================
-        if (lane != 0) return;
+        if (lane != 0 || warp > kDVWarp) return;
         const bool kl = warp == kDKWarp;
         const CUtensorMap* xtile = kl ? &ktile : &vtile;
         const uint32_t xbase = kl ? sK : sV;
@@ -1048,13 +1063,14 @@ tc_diag_kernel(const TcParams p, const __grid_constant__ CUtensorMap qtile,
     }
     if (warp == kDMmaWarp) {
         // ============================== MMA issuer ==============================
+        setmaxnreg_dec<kDOtherRegs>();
         const bool leader = elect_one();
         const uint32_t idesc_s = umma_idesc_bf16(kBM, kBN, false, false);
         const uint32_t idesc_o = umma_idesc_bf16(kBM, kD, false, true);
         const uint64_t dq = umma_desc_sw128(sQ, 16, 1024);
         const uint64_t dk0 = umma_desc_sw128(sK, 16, 1024);
         const uint64_t dv0 = umma_desc_sw128(sV, kHalf, 1024);
-        uint32_t gb = 0, qc = 0;
+        uint32_t gb = 0, qc = 0, tk = 0;
         auto issue_s = [&](uint32_t blk) {  // S(blk) into buffer blk & 1; K(blk) from stage blk % 3
             const uint32_t st = blk % kDKStages;
             mbar_wait(smem_u32(&c.k_full[st]), (blk / kDKStages) & 1, 4101);
@@ -1079,9 +1095,11 @@ tc_diag_kernel(const TcParams p, const __grid_constant__ CUtensorMap qtile,
             issue_s(g0);
             if (t.nd > 1) issue_s(g0 + 1);
             if (t.nd <= 2 && leader) umma_commit(smem_u32(&c.q_empty));
+            const uint32_t ob = tk & 1;
             for (int j = 0; j < t.nd; ++j) {
                 const uint32_t blk = g0 + j;
                 mbar_wait(smem_u32(&c.p_full[blk & 1]), (blk >> 1) & 1, 4103);
+                if (j == 0) mbar_wait(smem_u32(&c.o_free[ob]), ((tk >> 1) & 1) ^ 1, 4105);  // epilogue of tile tk-2 done
                 const uint32_t vst = blk % kDVStages;
                 mbar_wait(smem_u32(&c.v_full[vst]), (blk / kDVStages) & 1, 4104);
                 tc_fence_after();
@@ -1089,12 +1107,12 @@ tc_diag_kernel(const TcParams p, const __grid_constant__ CUtensorMap qtile,
 #pragma unroll
                 for (int kk = 0; kk < kBN / 16; ++kk)
                     if (leader)
-                        umma_bf16_ts(tbase + 256, tbase + (blk & 1) * 128 + kk * 8, dv + ((kk * 16 * 128) >> 4),
+                        umma_bf16_ts(tbase + 256 + ob * 128, tbase + (blk & 1) * 128 + kk * 8, dv + ((kk * 16 * 128) >> 4),
                                      idesc_o, (kk > 0 || j > 0) ? 1 : 0);
                 if (leader) {
                     umma_commit(smem_u32(&c.pv_bar));
                     umma_commit(smem_u32(&c.v_empty[vst]));
-                    if (j == t.nd - 1) umma_commit(smem_u32(&c.o_done));
+                    if (j == t.nd - 1) umma_commit(smem_u32(&c.o_done[ob]));
                 }
                 __syncwarp();
                 if (j + 2 < t.nd) {
@@ -1103,20 +1121,22 @@ tc_diag_kernel(const TcParams p, const __grid_constant__ CUtensorMap qtile,
                 }
             }
             gb += t.nd;
+            ++tk;
         }
         __syncwarp();
     } else if (warp < kDSoftWarps) {
-        // ============================== softmax / epilogue ==============================
+        // ============================== softmax ==============================
+        setmaxnreg_inc<kDSoftRegs>();
         const int r = threadIdx.x;  // TMEM lane
         const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
         const uint32_t tS0 = tbase + lane_off;
-        const uint32_t tO = tS0 + 256;
         const float sc = p.scale_log2;
-        uint32_t gb = 0, no = 0;
-        for (int64_t it = blockIdx.x; it < total; it += gridDim.x) {
+        uint32_t gb = 0, tk = 0;
+        for (int64_t it = blockIdx.x; it < total; it += gridDim.x, ++tk) {
             const TileInfo t = diag_tile(p, it);
             const bool valid = r < t.tn;
             const int rr = valid ? r : 0;
+            const uint32_t tO = tS0 + 256 + (tk & 1) * 128;
             float m2 = -INFINITY, ell = 0.0f;
             const int t0x = (int)t.t0;
             for (int j = 0; j < t.nd; ++j, ++gb) {
@@ -1155,6 +1175,27 @@ tc_diag_kernel(const TcParams p, const __grid_constant__ CUtensorMap qtile,
                 const float alpha = (m2 == -INFINITY) ? 0.0f : ex2(m2 + neg_ref);
                 float rs[4] = {0.0f, 0.0f, 0.0f, 0.0f};
                 if (full) {
+#if S2O_DIAG_PACKED
+                    const float2 sc2 = make_float2(sc, sc), nr2 = make_float2(neg_ref, neg_ref);
+                    float2 rs2[2] = {make_float2(0.0f, 0.0f), make_float2(0.0f, 0.0f)};
+#pragma unroll
+                    for (int c0 = 0; c0 < kBN; c0 += 32) {
+                        uint32_t pk[16];
+#pragma unroll
+                        for (int i = 0; i < 32; i += 2) {
+                            const float2 arg = ffma2(make_float2(__uint_as_float(sv[c0 + i]), __uint_as_float(sv[c0 + i + 1])),
+                                                     sc2, nr2);
+                            const float2 e = make_float2(ex2(arg.x), ex2(arg.y));
+                            rs2[(i >> 1) & 1] = fadd2(rs2[(i >> 1) & 1], e);
+                            pk[i >> 1] = pack_bf16(e.x, e.y);
+                        }
+                        tmem_st16(tS + c0 / 2, pk);
+                    }
+                    rs[0] = rs2[0].x;
+                    rs[1] = rs2[0].y;
+                    rs[2] = rs2[1].x;
+                    rs[3] = rs2[1].y;
+#else
 #pragma unroll
                     for (int c0 = 0; c0 < kBN; c0 += 32) {
                         uint32_t pk[16];
@@ -1167,6 +1208,7 @@ tc_diag_kernel(const TcParams p, const __grid_constant__ CUtensorMap qtile,
                         }
                         tmem_st16(tS + c0 / 2, pk);
                     }
+#endif
                 } else {
 #pragma unroll
                     for (int c0 = 0; c0 < kBN; c0 += 32) {
@@ -1204,15 +1246,38 @@ tc_diag_kernel(const TcParams p, const __grid_constant__ CUtensorMap qtile,
                 ell = ell * alpha + rowsum;
                 m2 = m_use;
             }
-            // ---- epilogue: read O after the tile's last P V, persist state / finalize
-            mbar_wait(smem_u32(&c.o_done), no & 1, 4203);
-            ++no;
+            // ---- hand the tile to the epilogue warps: final (m, ell) of the row through smem
+            {
+                float* mlb = ml + (tk & 1) * 256;
+                mlb[r] = m2;
+                mlb[128 + r] = ell;
+                __syncwarp();
+                if (lane == 0) mbar_arrive(smem_u32(&c.ml_full[tk & 1]));
+            }
+        }
+    } else if (warp < kDEpiWarp0 + 4) {
+        // ============================== epilogue ==============================
+        setmaxnreg_dec<kDEpiRegs>();
+        const int r = (warp - kDEpiWarp0) * 32 + lane;  // TMEM lane quarter = warp % 4
+        const uint32_t lane_off = (uint32_t)((warp % 4) * 32) << 16;
+        uint32_t tk = 0;
+        for (int64_t it = blockIdx.x; it < total; it += gridDim.x, ++tk) {
+            const TileInfo t = diag_tile(p, it);
+            const bool valid = r < t.tn;
+            const int rr = valid ? r : 0;
+            const uint32_t ob = tk & 1;
+            mbar_wait(smem_u32(&c.ml_full[ob]), (tk >> 1) & 1, 4203);
+            mbar_wait(smem_u32(&c.o_done[ob]), (tk >> 1) & 1, 4204);
             tc_fence_after();
             uint32_t ov[kD];
 #pragma unroll
-            for (int c0 = 0; c0 < kD; c0 += 32) tmem_ld32(tO + c0, *reinterpret_cast<uint32_t(*)[32]>(&ov[c0]));
+            for (int c0 = 0; c0 < kD; c0 += 32)
+                tmem_ld32(tbase + lane_off + 256 + ob * 128 + c0, *reinterpret_cast<uint32_t(*)[32]>(&ov[c0]));
             tmem_ld_wait();
+            const float m2 = ml[ob * 256 + r], ell = ml[ob * 256 + 128 + r];
             tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(smem_u32(&c.o_free[ob]));  // O buffer and (m, ell) slot reusable
             const int64_t grow = t.sb + t.t0 + rr;
             const int64_t slot = t.zh * g.l + grow;
             if (valid && (a.mode & kStateOut)) {
@@ -1265,9 +1330,8 @@ tc_diag_kernel(const TcParams p, const __grid_constant__ CUtensorMap qtile,
             }
         }
     }
-    // (warp 7 does not exist: kDThreads = 7 warps)
     tc_fence_before();
-    if (warp <= kDMmaWarp) named_bar_sync(5, 32 * (kDMmaWarp + 1));
+    if (warp <= kDMmaWarp) named_bar_sync(5, 32 * (kDMmaWarp + 1));  // softmax, epilogue, MMA warps
     if (warp == 0) {
         tc_fence_after();
         tmem_dealloc(tbase, kTmemCols);
