@@ -929,16 +929,17 @@ tc_pass_kernel(const TcParams p, const __grid_constant__ CUtensorMap qmap,
 #ifndef S2O_DIAG_PACKED
 #define S2O_DIAG_PACKED 0  // packed FFMA2/FADD2 softmax arguments and sums in the diagonal kernel
 #endif
-constexpr int kDThreads = 384;
-constexpr int kDSoftWarps = 4, kDEpiWarp0 = 4, kDMmaWarp = 8, kDKWarp = 9, kDVWarp = 10;
-constexpr int kDSoftRegs = 208, kDEpiRegs = 160, kDOtherRegs = 56;  // setmaxnreg per warpgroup
-constexpr int kDKStages = 3, kDVStages = 3;
+constexpr int kDThreads = 512;
+constexpr int kDSoftWarps = 8, kDEpiWarp0 = 8, kDMmaWarp = 12, kDKWarp = 13, kDVWarp = 14;
+constexpr int kDEpiRegs = 160, kDOtherRegs = 56;  // setmaxnreg (softmax warpgroups keep 128)
+constexpr int kDKStages = 3, kDVStages = 2;
 constexpr uint32_t kDOffQ = 0;
 constexpr uint32_t kDOffK = kTileBytes;
 constexpr uint32_t kDOffV = kDOffK + kDKStages * kTileBytes;
 constexpr uint32_t kDOffCtrl = kDOffV + kDVStages * kTileBytes;
-constexpr uint32_t kDOffML = kDOffCtrl + 256;        // float [2 tile parity][2 (m, ell)][128 rows]
-constexpr uint32_t kDSmemBytes = kDOffML + 2 * 2 * 128 * 4;  // 226.25 KB
+constexpr uint32_t kDOffML = kDOffCtrl + 256;  // float [2 tile parity][m, ell half 0, ell half 1][128 rows]
+constexpr uint32_t kDOffX = kDOffML + 2 * 3 * 128 * 4;  // float [2 block parity][2 halves][128 rows]: row max
+constexpr uint32_t kDSmemBytes = kDOffX + 2 * 2 * 128 * 4;  // 197.25 KB
 
 struct CtrlD {
     uint64_t q_full, q_empty;
@@ -1005,7 +1006,7 @@ tc_diag_kernel(const TcParams p, const __grid_constant__ CUtensorMap qtile,
         }
         for (int b = 0; b < 2; ++b) {
             mbar_init(smem_u32(&c.s_full[b]), 1);
-            mbar_init(smem_u32(&c.p_full[b]), kDSoftWarps);
+            mbar_init(smem_u32(&c.p_full[b]), kDSoftWarps);  // both row halves
         }
         mbar_init(smem_u32(&c.pv_bar), 1);
         for (int b = 0; b < 2; ++b) {
@@ -1026,6 +1027,7 @@ tc_diag_kernel(const TcParams p, const __grid_constant__ CUtensorMap qtile,
     const int64_t total = g.z * g.hq * p.pairs_per_head;
     const int64_t rowu = g.d;
     float* ml = reinterpret_cast<float*>(smem + kDOffML);
+    float* xch = reinterpret_cast<float*>(smem + kDOffX);
     // (setmaxnreg inside each role branch, so the softmax code is dominated by its increase)
     if (warp == kDKWarp || warp == kDVWarp || warp > kDVWarp) {
         setmaxnreg_dec<kDOtherRegs>();
@@ -1126,9 +1128,13 @@ tc_diag_kernel(const TcParams p, const __grid_constant__ CUtensorMap qtile,
         __syncwarp();
     } else if (warp < kDSoftWarps) {
         // ============================== softmax ==============================
-        setmaxnreg_inc<kDSoftRegs>();
-        const int r = threadIdx.x;  // TMEM lane
-        const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
+        // Two warps per row quarter: warp w (w < 4) takes key columns [0, 64) of rows 32w.., warp
+        // w + 4 columns [64, 128), so every SMSP runs two softmax warps. The row max is exchanged
+        // through shared memory (named barrier per warp pair); both halves then use the same
+        // reference, so each keeps a partial ell and the epilogue adds them.
+        const int h = warp >> 2, q = warp & 3;
+        const int r = q * 32 + lane;  // TMEM lane = row
+        const uint32_t lane_off = (uint32_t)(q * 32) << 16;
         const uint32_t tS0 = tbase + lane_off;
         const float sc = p.scale_log2;
         uint32_t gb = 0, tk = 0;
@@ -1136,38 +1142,44 @@ tc_diag_kernel(const TcParams p, const __grid_constant__ CUtensorMap qtile,
             const TileInfo t = diag_tile(p, it);
             const bool valid = r < t.tn;
             const int rr = valid ? r : 0;
-            const uint32_t tO = tS0 + 256 + (tk & 1) * 128;
+            const uint32_t tO = tS0 + 256 + (tk & 1) * 128 + h * 64;
             float m2 = -INFINITY, ell = 0.0f;
             const int t0x = (int)t.t0;
             for (int j = 0; j < t.nd; ++j, ++gb) {
                 const uint32_t tS = tS0 + (gb & 1) * 128;
                 mbar_wait(smem_u32(&c.s_full[gb & 1]), (gb >> 1) & 1, 4201);
                 tc_fence_after();
-                uint32_t sv[kBN];
-#pragma unroll
-                for (int c0 = 0; c0 < kBN; c0 += 32) tmem_ld32(tS + c0, *reinterpret_cast<uint32_t(*)[32]>(&sv[c0]));
+                uint32_t sv[64];
+                tmem_ld32(tS + h * 64, *reinterpret_cast<uint32_t(*)[32]>(&sv[0]));
+                tmem_ld32(tS + h * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(&sv[32]));
                 tmem_ld_wait();
-                // visible keys of this row in block j (causal on segment positions, kernel.cpp:58-69)
+                // visible keys of this row in block j (causal on segment positions, kernel.cpp:58-69),
+                // relative to this half's first key
                 const int k0 = j * kBN;
                 const int kn = min(kBN, t.segr - k0);
                 const int vis = (k0 + kn - 1 <= t0x) ? kn : min(kn, t0x + rr - k0 + 1);
-                const int lim = max(0, vis);
-                const bool full = __all_sync(0xffffffffu, lim >= kBN);
+                const int lim = max(0, vis) - h * 64;
+                const bool full = __all_sync(0xffffffffu, lim >= 64);
                 float mxa[8];
 #pragma unroll
                 for (int i = 0; i < 8; ++i) mxa[i] = -INFINITY;
                 if (full) {
 #pragma unroll
-                    for (int i = 0; i < kBN; i += 2)
+                    for (int i = 0; i < 64; i += 2)
                         mxa[(i >> 1) & 7] = fmax3(mxa[(i >> 1) & 7], __uint_as_float(sv[i]), __uint_as_float(sv[i + 1]));
                 } else {
 #pragma unroll
-                    for (int i = 0; i < kBN; i += 2)
+                    for (int i = 0; i < 64; i += 2)
                         mxa[(i >> 1) & 7] = fmax3(mxa[(i >> 1) & 7], i < lim ? __uint_as_float(sv[i]) : -INFINITY,
                                                   i + 1 < lim ? __uint_as_float(sv[i + 1]) : -INFINITY);
                 }
-                const float mx = fmax3(fmax3(mxa[0], mxa[1], mxa[2]), fmax3(mxa[3], mxa[4], mxa[5]),
-                                       fmaxf(mxa[6], mxa[7])) * sc;
+                float mx = fmax3(fmax3(mxa[0], mxa[1], mxa[2]), fmax3(mxa[3], mxa[4], mxa[5]), fmaxf(mxa[6], mxa[7]));
+                // exchange with the other half (double-buffered by block parity): after this barrier
+                // both halves have also finished reading S, so P may overwrite it
+                float* xb = xch + (gb & 1) * 256;
+                xb[h * 128 + r] = mx;
+                named_bar_sync(1 + q, 64);
+                mx = fmaxf(mx, xb[(1 - h) * 128 + r]) * sc;
                 const float m_new = fmaxf(m2, mx);
                 const bool rescale = (m_new > m2 + kRescaleThresh) || (m2 == -INFINITY);
                 const float m_use = rescale ? m_new : m2;
@@ -1175,29 +1187,8 @@ tc_diag_kernel(const TcParams p, const __grid_constant__ CUtensorMap qtile,
                 const float alpha = (m2 == -INFINITY) ? 0.0f : ex2(m2 + neg_ref);
                 float rs[4] = {0.0f, 0.0f, 0.0f, 0.0f};
                 if (full) {
-#if S2O_DIAG_PACKED
-                    const float2 sc2 = make_float2(sc, sc), nr2 = make_float2(neg_ref, neg_ref);
-                    float2 rs2[2] = {make_float2(0.0f, 0.0f), make_float2(0.0f, 0.0f)};
 #pragma unroll
-                    for (int c0 = 0; c0 < kBN; c0 += 32) {
-                        uint32_t pk[16];
-#pragma unroll
-                        for (int i = 0; i < 32; i += 2) {
-                            const float2 arg = ffma2(make_float2(__uint_as_float(sv[c0 + i]), __uint_as_float(sv[c0 + i + 1])),
-                                                     sc2, nr2);
-                            const float2 e = make_float2(ex2(arg.x), ex2(arg.y));
-                            rs2[(i >> 1) & 1] = fadd2(rs2[(i >> 1) & 1], e);
-                            pk[i >> 1] = pack_bf16(e.x, e.y);
-                        }
-                        tmem_st16(tS + c0 / 2, pk);
-                    }
-                    rs[0] = rs2[0].x;
-                    rs[1] = rs2[0].y;
-                    rs[2] = rs2[1].x;
-                    rs[3] = rs2[1].y;
-#else
-#pragma unroll
-                    for (int c0 = 0; c0 < kBN; c0 += 32) {
+                    for (int c0 = 0; c0 < 64; c0 += 32) {
                         uint32_t pk[16];
 #pragma unroll
                         for (int i = 0; i < 32; i += 2) {
@@ -1206,12 +1197,11 @@ tc_diag_kernel(const TcParams p, const __grid_constant__ CUtensorMap qtile,
                             rs[(i >> 1) & 3] += e0 + e1;
                             pk[i >> 1] = pack_bf16(e0, e1);
                         }
-                        tmem_st16(tS + c0 / 2, pk);
+                        tmem_st16(tS + h * 32 + c0 / 2, pk);
                     }
-#endif
                 } else {
 #pragma unroll
-                    for (int c0 = 0; c0 < kBN; c0 += 32) {
+                    for (int c0 = 0; c0 < 64; c0 += 32) {
                         uint32_t pk[16];
 #pragma unroll
                         for (int i = 0; i < 32; i += 2) {
@@ -1221,16 +1211,16 @@ tc_diag_kernel(const TcParams p, const __grid_constant__ CUtensorMap qtile,
                             rs[(i >> 1) & 3] += e0 + e1;
                             pk[i >> 1] = pack_bf16(e0, e1);
                         }
-                        tmem_st16(tS + c0 / 2, pk);
+                        tmem_st16(tS + h * 32 + c0 / 2, pk);
                     }
                 }
                 const float rowsum = (rs[0] + rs[1]) + (rs[2] + rs[3]);
-                // O rescale (lazy, rare): all earlier P V of this tile must have completed
+                // O rescale (lazy, rare; this half's 64 columns): all earlier P V of the tile done
                 if (__any_sync(0xffffffffu, j > 0 && rescale && m2 != -INFINITY)) {
                     mbar_wait(smem_u32(&c.pv_bar), (gb - 1) & 1, 4202);
                     tc_fence_after();
 #pragma unroll
-                    for (int c0 = 0; c0 < kD; c0 += 32) {
+                    for (int c0 = 0; c0 < 64; c0 += 32) {
                         uint32_t v[32];
                         tmem_ld32(tO + c0, v);
                         tmem_ld_wait();
@@ -1246,18 +1236,18 @@ tc_diag_kernel(const TcParams p, const __grid_constant__ CUtensorMap qtile,
                 ell = ell * alpha + rowsum;
                 m2 = m_use;
             }
-            // ---- hand the tile to the epilogue warps: final (m, ell) of the row through smem
+            // ---- hand the tile to the epilogue warps: (m, this half's ell) through smem
             {
-                float* mlb = ml + (tk & 1) * 256;
-                mlb[r] = m2;
-                mlb[128 + r] = ell;
+                float* mlb = ml + (tk & 1) * 384;
+                if (h == 0) mlb[r] = m2;
+                mlb[128 + h * 128 + r] = ell;
                 __syncwarp();
                 if (lane == 0) mbar_arrive(smem_u32(&c.ml_full[tk & 1]));
             }
         }
     } else if (warp < kDEpiWarp0 + 4) {
         // ============================== epilogue ==============================
-        setmaxnreg_dec<kDEpiRegs>();
+        setmaxnreg_inc<kDEpiRegs>();
         const int r = (warp - kDEpiWarp0) * 32 + lane;  // TMEM lane quarter = warp % 4
         const uint32_t lane_off = (uint32_t)((warp % 4) * 32) << 16;
         uint32_t tk = 0;
@@ -1274,7 +1264,7 @@ tc_diag_kernel(const TcParams p, const __grid_constant__ CUtensorMap qtile,
             for (int c0 = 0; c0 < kD; c0 += 32)
                 tmem_ld32(tbase + lane_off + 256 + ob * 128 + c0, *reinterpret_cast<uint32_t(*)[32]>(&ov[c0]));
             tmem_ld_wait();
-            const float m2 = ml[ob * 256 + r], ell = ml[ob * 256 + 128 + r];
+            const float m2 = ml[ob * 384 + r], ell = ml[ob * 384 + 128 + r] + ml[ob * 384 + 256 + r];
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(smem_u32(&c.o_free[ob]));  // O buffer and (m, ell) slot reusable
