@@ -926,6 +926,9 @@ tc_pass_kernel(const TcParams p, const __grid_constant__ CUtensorMap qmap,
 // the tensor pipe executes in order, so S(j+2) overwrites P(j) only after P V(j) read it).
 // pv_bar completes once per P V: a softmax that must rescale O at block gb (lazy max update,
 // rare) first waits for completion gb, i.e. all earlier P V of the tile.
+#ifndef S2O_DIAG_POLY
+#define S2O_DIAG_POLY 8  // diagonal kernel: every n-th exponential pair on the FMA pipe (0 = all MUFU; A/B: 8 -3 %, 4 even)
+#endif
 #ifndef S2O_DIAG_PACKED
 #define S2O_DIAG_PACKED 0  // packed FFMA2/FADD2 softmax arguments and sums in the diagonal kernel
 #endif
@@ -1192,8 +1195,19 @@ tc_diag_kernel(const TcParams p, const __grid_constant__ CUtensorMap qtile,
                         uint32_t pk[16];
 #pragma unroll
                         for (int i = 0; i < 32; i += 2) {
-                            const float e0 = ex2(fmaf(__uint_as_float(sv[c0 + i]), sc, neg_ref));
-                            const float e1 = ex2(fmaf(__uint_as_float(sv[c0 + i + 1]), sc, neg_ref));
+                            float e0, e1;
+#if S2O_DIAG_POLY > 0
+                            if ((i >> 1) % S2O_DIAG_POLY == S2O_DIAG_POLY - 1) {  // FMA-pipe exp2 (MUFU offload)
+                                const float2 e = ex2_poly3x2(make_float2(fmaf(__uint_as_float(sv[c0 + i]), sc, neg_ref),
+                                                                         fmaf(__uint_as_float(sv[c0 + i + 1]), sc, neg_ref)));
+                                e0 = e.x;
+                                e1 = e.y;
+                            } else
+#endif
+                            {
+                                e0 = ex2(fmaf(__uint_as_float(sv[c0 + i]), sc, neg_ref));
+                                e1 = ex2(fmaf(__uint_as_float(sv[c0 + i + 1]), sc, neg_ref));
+                            }
                             rs[(i >> 1) & 3] += e0 + e1;
                             pk[i >> 1] = pack_bf16(e0, e1);
                         }
