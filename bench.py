@@ -52,13 +52,23 @@ def peaks():
 
 
 class ClockSampler:
-    """SM clocks + throttle reasons sampled every 20 ms (NVML) during the timed region."""
+    """SM clocks + throttle reasons sampled every 5 ms (NVML); started before the warm-up so the
+    first (slow) NVML queries are done, and only the samples taken inside the timed region
+    (mark_start .. mark_end) are reported."""
 
     def __init__(self, index: int):
         self.index = index
-        self.samples: list[tuple[float, float, int]] = []
+        self.samples: list[tuple[float, float, int, float]] = []
         self._stop = threading.Event()
         self.ok = False
+        self.t0 = None
+        self.t1 = None
+
+    def mark_start(self):
+        self.t0 = time.perf_counter()
+
+    def mark_end(self):
+        self.t1 = time.perf_counter()
 
     def start(self):
         try:
@@ -80,10 +90,10 @@ class ClockSampler:
                 sm = float(n.nvmlDeviceGetClockInfo(self.h, n.NVML_CLOCK_SM))
                 pw = n.nvmlDeviceGetPowerUsage(self.h) / 1000.0
                 rs = n.nvmlDeviceGetCurrentClocksEventReasons(self.h)
-                self.samples.append((sm, pw, rs))
+                self.samples.append((sm, pw, rs, time.perf_counter()))
             except Exception:  # noqa: BLE001
                 pass
-            time.sleep(0.02)
+            time.sleep(0.005)
 
     def stop(self) -> dict:
         if not self.ok:
@@ -97,8 +107,11 @@ class ClockSampler:
             "hw_thermal_slowdown": getattr(n, "nvmlClocksEventReasonHwThermalSlowdown", 0x40),
             "sw_power_cap": getattr(n, "nvmlClocksEventReasonSwPowerCap", 0x4),
         }
+        if self.t0 is not None and self.t1 is not None:
+            inside = [x for x in self.samples if self.t0 <= x[3] <= self.t1]
+            self.samples = inside or sorted(self.samples, key=lambda x: abs(x[3] - self.t1))[:1]
         reasons = set()
-        for _, _, rs in self.samples:
+        for _, _, rs, _ in self.samples:
             for name, bit in names.items():
                 if rs & bit:
                     reasons.add(name)
@@ -266,20 +279,22 @@ def run_ours(args, rank: int, world: int):
     def step():
         s2o.s2o_attention(q, k, v, cfg, out=out, want_plan=False)
 
+    clocks = ClockSampler(local)
+    clocks.start()
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
     if dist:
         dist.barrier()
-    clocks = ClockSampler(local)
-    clocks.start()
     torch.cuda.synchronize()
+    clocks.mark_start()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ev0.record()
     for _ in range(args.steps):
         step()
     ev1.record()
     torch.cuda.synchronize()
+    clocks.mark_end()
     elapsed = ev0.elapsed_time(ev1)
     clk = clocks.stop()
     if dist:
@@ -438,20 +453,22 @@ def run_heads(args, rank: int, world: int):
         if args.allgather and dist:
             gather_heads(out, world)
 
+    clocks = ClockSampler(local)
+    clocks.start()
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
     if dist:
         dist.barrier()
-    clocks = ClockSampler(local)
-    clocks.start()
     torch.cuda.synchronize()
+    clocks.mark_start()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ev0.record()
     for _ in range(args.steps):
         step()
     ev1.record()
     torch.cuda.synchronize()
+    clocks.mark_end()
     elapsed = ev0.elapsed_time(ev1)
     clk = clocks.stop()
     ag_ms = None
