@@ -907,31 +907,38 @@ tc_pass_kernel(const TcParams p, const __grid_constant__ CUtensorMap qmap,
 
 // ============================================================== single-tile diagonal kernel
 // Pass-1 (and any diagonal-only pass: the dense reference with S = L) on ONE 128-row query tile
-// per work item, with the score buffer double-buffered in TMEM: S(j+1) = Q K(j+1)^T is computed
-// while the softmax of block j runs, so the softmax warps run block after block without waiting
-// on P V(j) + S(j+1) (the pair kernel's per-slot chain: softmax -> P V -> S -> softmax). The pair
+// per work item, with the score buffer triple-buffered in TMEM: S(j+1), S(j+2) are computed while
+// the softmax of block j runs, so the softmax warps run block after block without waiting on
+// P V(j) + S(j+1) (the pair kernel's per-slot chain: softmax -> P V -> S -> softmax). The pair
 // kernel shares a K/V block between two tiles, which matters for gathered prefix chunks; the
 // diagonal blocks are contiguous 2-D TMA tiles served from L2, so one tile per item costs little.
 //
-//   warps 0-3  softmax (thread r owns row r = TMEM lane 32 * warp + lane)
-//   warps 4-7  epilogue: read O of a finished tile from TMEM, persist state / write O, so the
-//              softmax warps go straight on to the next tile
-//   warp 8     MMA issuer (one elected lane)
-//   warp 9     Q + K loader (lane 0, 2-D TMA tiles), warp 10 V loader (lane 0), warp 11 idle
+//   warps 0-7   softmax: warp w < 4 takes key columns [0, 64) of rows 32w.. (TMEM lanes), warp
+//               w + 4 columns [64, 128) of the same rows; the row max is exchanged in smem
+//   warps 8-11  epilogue: read O of a finished tile from TMEM, persist state / write O, so the
+//               softmax warps go straight on to the next tile
+//   warp 12     MMA issuer (one elected lane)
+//   warp 13     Q + K loader (lane 0, 2-D TMA tiles), warp 14 V loader (lane 0), warp 15 idle
 //
-// TMEM: S buffers at columns [0, 128) and [128, 256) (P in bf16 over the first 64 columns of its
-// buffer), O double-buffered by tile parity at [256, 384) and [384, 512): the epilogue of tile k
-// overlaps tile k+1. Blocks are numbered globally per CTA (gb); block gb uses S buffer
-// gb & 1. MMA order: S(0), S(1), then per block j: P V(j), S(j+2) (into the buffer P(j) held;
-// the tensor pipe executes in order, so S(j+2) overwrites P(j) only after P V(j) read it).
-// pv_bar completes once per P V: a softmax that must rescale O at block gb (lazy max update,
-// rare) first waits for completion gb, i.e. all earlier P V of the tile.
+// TMEM: S buffers at columns [0, 128), [128, 256), [256, 384) (P in bf16 over the first 64
+// columns of its buffer), O at [384, 512) (kDSBuf = 2: two S buffers, O double-buffered by
+// tile). Blocks are numbered globally per CTA (gb); block gb uses S buffer gb % kDSBuf. MMA
+// order: S(0..kDSBuf-1), then per block j: P V(j), S(j+kDSBuf) (into the buffer P(j) held; the
+// tensor pipe executes in order, so the new S overwrites P(j) only after P V(j) read it).
+// pv_done[b] completes once per P V on buffer b: a softmax that must rescale O at block gb (lazy
+// max update, rare) first waits for P V(gb-1), i.e. all earlier P V of the tile.
 #ifndef S2O_DIAG_POLY
 #define S2O_DIAG_POLY 8  // diagonal kernel: every n-th exponential pair on the FMA pipe (0 = all MUFU; A/B: 8 -3 %, 4 even)
 #endif
 #ifndef S2O_DIAG_PACKED
 #define S2O_DIAG_PACKED 0  // packed FFMA2/FADD2 softmax arguments and sums in the diagonal kernel
 #endif
+#ifndef S2O_DIAG_SBUF
+#define S2O_DIAG_SBUF 3  // S buffers in TMEM (3: single O buffer; 2: O double-buffered by tile)
+#endif
+constexpr int kDSBuf = S2O_DIAG_SBUF;
+constexpr int kDOBuf = kDSBuf == 3 ? 1 : 2;
+static_assert(kDSBuf * 128 + kDOBuf * 128 <= 512, "TMEM columns");
 constexpr int kDThreads = 512;
 constexpr int kDSoftWarps = 8, kDEpiWarp0 = 8, kDMmaWarp = 12, kDKWarp = 13, kDVWarp = 14;
 constexpr int kDEpiRegs = 160, kDOtherRegs = 56;  // setmaxnreg (softmax warpgroups keep 128)
@@ -947,8 +954,9 @@ constexpr uint32_t kDSmemBytes = kDOffX + 2 * 2 * 128 * 4;  // 197.25 KB
 struct CtrlD {
     uint64_t q_full, q_empty;
     uint64_t k_full[kDKStages], k_empty[kDKStages], v_full[kDVStages], v_empty[kDVStages];
-    uint64_t s_full[2], p_full[2], pv_bar;
-    uint64_t o_done[2], o_free[2], ml_full[2];  // per O buffer (tile parity)
+    uint64_t s_full[kDSBuf], p_full[kDSBuf], pv_done[kDSBuf];  // per S buffer
+    uint64_t o_done[kDOBuf], o_free[kDOBuf];                    // per O buffer
+    uint64_t ml_full[2], ml_free[2];                            // (m, ell) hand-off slots (tile parity)
     uint32_t tmem_base;
 };
 static_assert(sizeof(CtrlD) <= 256, "CtrlD exceeds its 256 B");
@@ -1007,15 +1015,18 @@ tc_diag_kernel(const TcParams p, const __grid_constant__ CUtensorMap qtile,
             mbar_init(smem_u32(&c.v_full[s]), 1);
             mbar_init(smem_u32(&c.v_empty[s]), 1);
         }
-        for (int b = 0; b < 2; ++b) {
+        for (int b = 0; b < kDSBuf; ++b) {
             mbar_init(smem_u32(&c.s_full[b]), 1);
             mbar_init(smem_u32(&c.p_full[b]), kDSoftWarps);  // both row halves
+            mbar_init(smem_u32(&c.pv_done[b]), 1);
         }
-        mbar_init(smem_u32(&c.pv_bar), 1);
-        for (int b = 0; b < 2; ++b) {
+        for (int b = 0; b < kDOBuf; ++b) {
             mbar_init(smem_u32(&c.o_done[b]), 1);
             mbar_init(smem_u32(&c.o_free[b]), 4);   // epilogue warps
+        }
+        for (int b = 0; b < 2; ++b) {
             mbar_init(smem_u32(&c.ml_full[b]), kDSoftWarps);
+            mbar_init(smem_u32(&c.ml_free[b]), 4);  // epilogue warps
         }
         fence_mbar_init();
     }
@@ -1084,10 +1095,10 @@ tc_diag_kernel(const TcParams p, const __grid_constant__ CUtensorMap qtile,
 #pragma unroll
             for (int kk = 0; kk < kD / 16; ++kk) {
                 const uint32_t off = ((kk / 4) * kHalf + (kk % 4) * 32) >> 4;
-                if (leader) umma_bf16(tbase + (blk & 1) * 128, dq + off, dk + off, idesc_s, kk > 0);
+                if (leader) umma_bf16(tbase + (blk % kDSBuf) * 128, dq + off, dk + off, idesc_s, kk > 0);
             }
             if (leader) {
-                umma_commit(smem_u32(&c.s_full[blk & 1]));
+                umma_commit(smem_u32(&c.s_full[blk % kDSBuf]));
                 umma_commit(smem_u32(&c.k_empty[st]));
             }
             __syncwarp();
@@ -1097,14 +1108,14 @@ tc_diag_kernel(const TcParams p, const __grid_constant__ CUtensorMap qtile,
             const uint32_t g0 = gb;
             mbar_wait(smem_u32(&c.q_full), qc & 1, 4102);
             ++qc;
-            issue_s(g0);
-            if (t.nd > 1) issue_s(g0 + 1);
-            if (t.nd <= 2 && leader) umma_commit(smem_u32(&c.q_empty));
-            const uint32_t ob = tk & 1;
+            for (int j = 0; j < t.nd && j < kDSBuf; ++j) issue_s(g0 + j);
+            if (t.nd <= kDSBuf && leader) umma_commit(smem_u32(&c.q_empty));
+            const uint32_t ob = tk % kDOBuf;
             for (int j = 0; j < t.nd; ++j) {
                 const uint32_t blk = g0 + j;
-                mbar_wait(smem_u32(&c.p_full[blk & 1]), (blk >> 1) & 1, 4103);
-                if (j == 0) mbar_wait(smem_u32(&c.o_free[ob]), ((tk >> 1) & 1) ^ 1, 4105);  // epilogue of tile tk-2 done
+                mbar_wait(smem_u32(&c.p_full[blk % kDSBuf]), (blk / kDSBuf) & 1, 4103);
+                // the epilogue of the tile that used this O buffer last (tk - kDOBuf) read it
+                if (j == 0) mbar_wait(smem_u32(&c.o_free[ob]), ((tk / kDOBuf) & 1) ^ 1, 4105);
                 const uint32_t vst = blk % kDVStages;
                 mbar_wait(smem_u32(&c.v_full[vst]), (blk / kDVStages) & 1, 4104);
                 tc_fence_after();
@@ -1112,17 +1123,17 @@ tc_diag_kernel(const TcParams p, const __grid_constant__ CUtensorMap qtile,
 #pragma unroll
                 for (int kk = 0; kk < kBN / 16; ++kk)
                     if (leader)
-                        umma_bf16_ts(tbase + 256 + ob * 128, tbase + (blk & 1) * 128 + kk * 8, dv + ((kk * 16 * 128) >> 4),
-                                     idesc_o, (kk > 0 || j > 0) ? 1 : 0);
+                        umma_bf16_ts(tbase + (kDSBuf + ob) * 128, tbase + (blk % kDSBuf) * 128 + kk * 8,
+                                     dv + ((kk * 16 * 128) >> 4), idesc_o, (kk > 0 || j > 0) ? 1 : 0);
                 if (leader) {
-                    umma_commit(smem_u32(&c.pv_bar));
+                    umma_commit(smem_u32(&c.pv_done[blk % kDSBuf]));
                     umma_commit(smem_u32(&c.v_empty[vst]));
                     if (j == t.nd - 1) umma_commit(smem_u32(&c.o_done[ob]));
                 }
                 __syncwarp();
-                if (j + 2 < t.nd) {
-                    issue_s(blk + 2);
-                    if (j + 2 == t.nd - 1 && leader) umma_commit(smem_u32(&c.q_empty));
+                if (j + kDSBuf < t.nd) {
+                    issue_s(blk + kDSBuf);  // into the buffer P(j) held: the pipe runs P V(j) first
+                    if (j + kDSBuf == t.nd - 1 && leader) umma_commit(smem_u32(&c.q_empty));
                 }
             }
             gb += t.nd;
@@ -1145,12 +1156,12 @@ tc_diag_kernel(const TcParams p, const __grid_constant__ CUtensorMap qtile,
             const TileInfo t = diag_tile(p, it);
             const bool valid = r < t.tn;
             const int rr = valid ? r : 0;
-            const uint32_t tO = tS0 + 256 + (tk & 1) * 128 + h * 64;
+            const uint32_t tO = tS0 + (kDSBuf + tk % kDOBuf) * 128 + h * 64;
             float m2 = -INFINITY, ell = 0.0f;
             const int t0x = (int)t.t0;
             for (int j = 0; j < t.nd; ++j, ++gb) {
-                const uint32_t tS = tS0 + (gb & 1) * 128;
-                mbar_wait(smem_u32(&c.s_full[gb & 1]), (gb >> 1) & 1, 4201);
+                const uint32_t tS = tS0 + (gb % kDSBuf) * 128;
+                mbar_wait(smem_u32(&c.s_full[gb % kDSBuf]), (gb / kDSBuf) & 1, 4201);
                 tc_fence_after();
                 uint32_t sv[64];
                 tmem_ld32(tS + h * 64, *reinterpret_cast<uint32_t(*)[32]>(&sv[0]));
@@ -1231,7 +1242,9 @@ tc_diag_kernel(const TcParams p, const __grid_constant__ CUtensorMap qtile,
                 const float rowsum = (rs[0] + rs[1]) + (rs[2] + rs[3]);
                 // O rescale (lazy, rare; this half's 64 columns): all earlier P V of the tile done
                 if (__any_sync(0xffffffffu, j > 0 && rescale && m2 != -INFINITY)) {
-                    mbar_wait(smem_u32(&c.pv_bar), (gb - 1) & 1, 4202);
+                    // P V(gb-1) done (then all earlier ones are): its buffer's barrier is at most one
+                    // phase behind, since S(gb) completing implies P V(gb - kDSBuf) completed
+                    mbar_wait(smem_u32(&c.pv_done[(gb - 1) % kDSBuf]), ((gb - 1) / kDSBuf) & 1, 4202);
                     tc_fence_after();
 #pragma unroll
                     for (int c0 = 0; c0 < 64; c0 += 32) {
@@ -1246,12 +1259,15 @@ tc_diag_kernel(const TcParams p, const __grid_constant__ CUtensorMap qtile,
                 tmem_st_wait();
                 tc_fence_before();
                 __syncwarp();
-                if (lane == 0) mbar_arrive(smem_u32(&c.p_full[gb & 1]));
+                if (lane == 0) mbar_arrive(smem_u32(&c.p_full[gb % kDSBuf]));
                 ell = ell * alpha + rowsum;
                 m2 = m_use;
             }
             // ---- hand the tile to the epilogue warps: (m, this half's ell) through smem
             {
+                // the epilogue of tile tk-2 has read this slot (a tile short enough to need no
+                // P V before its last S does not order this write otherwise)
+                mbar_wait(smem_u32(&c.ml_free[tk & 1]), ((tk >> 1) & 1) ^ 1, 4206);
                 float* mlb = ml + (tk & 1) * 384;
                 if (h == 0) mlb[r] = m2;
                 mlb[128 + h * 128 + r] = ell;
@@ -1269,19 +1285,22 @@ tc_diag_kernel(const TcParams p, const __grid_constant__ CUtensorMap qtile,
             const TileInfo t = diag_tile(p, it);
             const bool valid = r < t.tn;
             const int rr = valid ? r : 0;
-            const uint32_t ob = tk & 1;
-            mbar_wait(smem_u32(&c.ml_full[ob]), (tk >> 1) & 1, 4203);
-            mbar_wait(smem_u32(&c.o_done[ob]), (tk >> 1) & 1, 4204);
+            const uint32_t ob = tk % kDOBuf, mb = tk & 1;
+            mbar_wait(smem_u32(&c.ml_full[mb]), (tk >> 1) & 1, 4203);
+            mbar_wait(smem_u32(&c.o_done[ob]), (tk / kDOBuf) & 1, 4204);
             tc_fence_after();
             uint32_t ov[kD];
 #pragma unroll
             for (int c0 = 0; c0 < kD; c0 += 32)
-                tmem_ld32(tbase + lane_off + 256 + ob * 128 + c0, *reinterpret_cast<uint32_t(*)[32]>(&ov[c0]));
+                tmem_ld32(tbase + lane_off + (kDSBuf + ob) * 128 + c0, *reinterpret_cast<uint32_t(*)[32]>(&ov[c0]));
             tmem_ld_wait();
-            const float m2 = ml[ob * 384 + r], ell = ml[ob * 384 + 128 + r] + ml[ob * 384 + 256 + r];
+            const float m2 = ml[mb * 384 + r], ell = ml[mb * 384 + 128 + r] + ml[mb * 384 + 256 + r];
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(smem_u32(&c.o_free[ob]));  // O buffer and (m, ell) slot reusable
+            if (lane == 0) {
+                mbar_arrive(smem_u32(&c.o_free[ob]));   // O buffer reusable
+                mbar_arrive(smem_u32(&c.ml_free[mb]));  // (m, ell) slot reusable
+            }
             const int64_t grow = t.sb + t.t0 + rr;
             const int64_t slot = t.zh * g.l + grow;
             if (valid && (a.mode & kStateOut)) {
