@@ -274,3 +274,20 @@ def test_diag_dense_ragged_gqa_vs_sdpa(cuda):
     ref = torch.nn.functional.scaled_dot_product_attention(
         q.float(), k.float().repeat_interleave(4, 1), v.float().repeat_interleave(4, 1), is_causal=True)
     assert (o.float() - ref).abs().max().item() <= 2e-2
+
+
+def test_tc_pass1_states_short_tiles(cuda, port):
+    """Segments of one tile (S = 128: every tile has a single block), many heads: the diagonal
+    kernel's softmax finishes tiles back to back, ahead of the epilogue; the per-row (m, ell)
+    hand-off must still reach the right tile (ml_free ordering)."""
+    import paper_2602_22575_b200 as s2o
+    torch = cuda
+    q, k, v = inputs(s2o, 8, 8, 4096, seed=7)
+    c = Cfg(128, 0.005, 128, 128)
+    bufs = s2o.pass1_dense_init(dev_bf16(torch, q), dev_bf16(torch, k), dev_bf16(torch, v), kcfg(s2o, c, TC))
+    acc, ell, m = port.pass1(q, k, v, c)
+    got = (bufs.acc / bufs.ell[..., None]).cpu().numpy()
+    assert np.abs(got - acc / ell[..., None]).max() <= 2e-2
+    mg = bufs.m.cpu().numpy().astype(np.float64)
+    assert (mg <= m + 1e-3).all() and (mg >= m - 8.0 * np.log(2.0) - 1e-3).all()
+    np.testing.assert_allclose(bufs.ell.cpu().numpy() * np.exp(mg - m), ell, rtol=2e-3)
