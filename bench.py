@@ -162,14 +162,14 @@ def plan_sort_passes(l: int, s: int) -> int:
 
 def launches_per_step(l: int, s: int) -> int:
     """Our kernels per s2o_attention_fwd call with the truncated plan (no overflow rerun):
-    guide means, q ranking (+ q sort when S > 2048), kv scoring, top-T selection, trace init,
-    pass-1, pass-2."""
+    guide means, q ranking (+ q sort when S > 2048), kv scoring, top-T selection (scan + sort
+    kernels), trace init, pass-1 (tc_diag_kernel), pass-2 (tc_pass_kernel)."""
     n = -(-l // s)
     count = 2
     if s > 2048:
         count += 2 + plan_sort_passes(l, s)
     if n > 1:
-        count += 2
+        count += 3
     return count + 3
 
 
