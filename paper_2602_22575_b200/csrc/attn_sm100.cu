@@ -65,15 +65,15 @@ constexpr uint32_t kOffQ = 0;               // slot X at X * kTileBytes
 constexpr uint32_t kOffK = 2 * kTileBytes;
 constexpr uint32_t kOffV = kOffK + kKStages * kTileBytes;
 constexpr uint32_t kOffCtrl = kOffV + kVStages * kTileBytes;
-constexpr uint32_t kOffTok = kOffCtrl + 256;  // token rings: K group int32 [2][128], V group [2][144]
-constexpr uint32_t kSmemBytes = kOffTok + 2304;  // 226.5 KB (base must be 1024-B aligned)
+constexpr uint32_t kOffTok = kOffCtrl + 512;  // token rings: K group int32 [2][128], V group [2][144]
+constexpr uint32_t kSmemBytes = kOffTok + 2304;  // 226.75 KB (base must be 1024-B aligned)
 constexpr uint32_t kTmemCols = 512;
 constexpr int kSoftmaxRegs = 192;   // setmaxnreg: softmax warpgroups (0, 1)
 constexpr int kOtherRegs = 64;      // MMA + loader warpgroups (2, 3)
 constexpr int kLaunchRegs = 65536 / kThreads / 8 * 8;  // 128: what __launch_bounds__(512, 1) allots
 // setmaxnreg.inc blocks until the pool has the registers: the decrements must cover it
 static_assert(kSoftmaxRegs - kLaunchRegs <= kLaunchRegs - kOtherRegs, "register pool overcommitted");
-static_assert(sizeof(uint64_t) * 19 + 4 + 64 + 8 <= 256, "Ctrl exceeds its 256 B");
+static_assert(sizeof(uint64_t) * 31 + 4 + 64 + 8 <= 512, "Ctrl exceeds its 512 B");
 constexpr float kRescaleThresh = 8.0f;
 #ifndef S2O_POLY_MOD
 #define S2O_POLY_MOD 0  // pass-2 softmax: every n-th exponential pair on the FMA pipe (0 = all MUFU)
@@ -87,7 +87,22 @@ struct Ctrl {
     uint32_t tmem_base;
     uint32_t red[2][2][4];  // continue votes [slot][block parity][warp]
     uint8_t dec[2][4];  // per slot decision ring (block j -> j & 3): 1 = commit, 2 = stop
+    // dynamic work ring: the K loader group fetches pair indices from a global counter
+    // (work_ctr) and every warp of the CTA takes them in order (item k in slot k & 3)
+    uint64_t w_full[4], w_empty[4];
+    int64_t wq[4];
 };
+
+constexpr int kWarps = kThreads / 32;
+
+// Item k of the work ring (all lanes of the calling warp): the pair index, or -1 when done.
+__device__ __forceinline__ int64_t ring_get(Ctrl& c, uint32_t k, int lane) {
+    mbar_wait(smem_u32(&c.w_full[k & 3]), (k >> 2) & 1, 5001);
+    const int64_t it = *reinterpret_cast<volatile int64_t*>(&c.wq[k & 3]);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(smem_u32(&c.w_empty[k & 3]));
+    return it;
+}
 
 struct TcParams {
     PassArgs a;
@@ -273,6 +288,10 @@ tc_pass_kernel(const TcParams p, const __grid_constant__ CUtensorMap qmap,
             mbar_init(smem_u32(&c.p_full[x]), 4);
             mbar_init(smem_u32(&c.o_done[x]), 1);
         }
+        for (int w = 0; w < 4; ++w) {
+            mbar_init(smem_u32(&c.w_full[w]), 1);
+            mbar_init(smem_u32(&c.w_empty[w]), kWarps);
+        }
         fence_mbar_init();
     }
     if (warp == 0) {
@@ -320,7 +339,15 @@ tc_pass_kernel(const TcParams p, const __grid_constant__ CUtensorMap qmap,
         uint64_t* xfull = kgrp ? c.k_full : c.v_full;
         uint64_t* xempty = kgrp ? c.k_empty : c.v_empty;
         uint32_t gx = 0, qcount = 0;
-        for (int64_t it = blockIdx.x; it < total; it += gridDim.x) {
+        for (uint32_t wk = 0;; ++wk) {
+            if (kgrp && lt == 0) {  // producer: the next pair index (or -1) into ring slot wk & 3
+                mbar_wait(smem_u32(&c.w_empty[wk & 3]), ((wk >> 2) & 1) ^ 1, 5002);
+                const int64_t v = (int64_t)atomicAdd(a.work_ctr, 1);
+                *reinterpret_cast<volatile int64_t*>(&c.wq[wk & 3]) = v < total ? v : -1;
+                mbar_arrive(smem_u32(&c.w_full[wk & 3]));
+            }
+            const int64_t it = ring_get(c, wk, lane);
+            if (it < 0) break;
             const PairInfo P = pair_info(p, it);
             if (P.nb == 0) continue;
             const int32_t* kv = (P.np > 0) ? a.kv_seg(P.zh, P.n) : nullptr;
@@ -491,7 +518,9 @@ tc_pass_kernel(const TcParams p, const __grid_constant__ CUtensorMap qmap,
                 fence_proxy_async_smem();  // cp.async (generic proxy) writes -> UMMA reads
                 tc_fence_after();
             };
-            for (int64_t it = blockIdx.x; it < total; it += gridDim.x) {
+            for (uint32_t wk = 0;; ++wk) {
+                const int64_t it = ring_get(c, wk, lane);
+                if (it < 0) break;
                 const PairInfo P = pair_info(p, it);
                 if (P.nb == 0) continue;
                 mbar_wait(smem_u32(&c.q_full), qcount & 1, 2001);
@@ -585,7 +614,9 @@ tc_pass_kernel(const TcParams p, const __grid_constant__ CUtensorMap qmap,
         const uint32_t bar_id = 1 + x;
         const float sc = p.scale_log2;
         uint32_t ns = 0, no = 0, npf = 0;
-        for (int64_t it = blockIdx.x; it < total; it += gridDim.x) {
+        for (uint32_t wk = 0;; ++wk) {
+            const int64_t it = ring_get(c, wk, lane);
+            if (it < 0) break;
             float m2, ell;
             float sacc = 1.0f;    // scale of the resumed accumulator (kStateIn)
             bool pv_any = false;  // a P V has been issued into O_x for this pair

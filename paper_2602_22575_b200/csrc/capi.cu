@@ -103,7 +103,9 @@ s2o_status run_pass(PassArgs a, int32_t path, void* ws, size_t ws_bytes, cudaStr
     char* base = reinterpret_cast<char*>(ws);
     if (!ws || ws_bytes < pass_ws_bytes(a)) return fail(S2O_ERR_WORKSPACE, "workspace too small");
     a.err_flag = reinterpret_cast<int32_t*>(base + align256(generic_scratch_bytes(a)));
-    if (clear_flag) S2O_CUDA_TRY(cudaMemsetAsync(a.err_flag, 0, sizeof(int32_t), st), "memset");
+    a.work_ctr = a.err_flag + 4;  // same 256-B slot
+    if (clear_flag) S2O_CUDA_TRY(cudaMemsetAsync(a.err_flag, 0, 8 * sizeof(int32_t), st), "memset");
+    else S2O_CUDA_TRY(cudaMemsetAsync(a.work_ctr, 0, sizeof(int32_t), st), "memset");
     if (path == S2O_PATH_TCGEN05 && !tc_supported(a))
         return fail(S2O_ERR_UNSUPPORTED,
                     "tcgen05 path needs bf16 inputs, D=128, b_m=128, b_n in {64,128}");

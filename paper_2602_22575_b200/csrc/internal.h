@@ -53,6 +53,7 @@ struct PassArgs {
     int64_t tile_count;
     int64_t lvl_base;       // kv_perm entries of a segment consumed by earlier plan levels
     int no_overflow;        // a short kv list is the whole list (block top-k baseline), no next level
+    int32_t* work_ctr;      // pass scratch: dynamic work counter of the tcgen05 pass kernel (zeroed per pass)
 
     // entries of segment n's (current level) kv list
     __host__ __device__ int64_t avail(int64_t n) const {
