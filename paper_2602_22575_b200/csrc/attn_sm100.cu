@@ -958,6 +958,11 @@ tc_pass_kernel(const TcParams p, const __grid_constant__ CUtensorMap qmap,
 // tensor pipe executes in order, so the new S overwrites P(j) only after P V(j) read it).
 // pv_done[b] completes once per P V on buffer b: a softmax that must rescale O at block gb (lazy
 // max update, rare) first waits for P V(gb-1), i.e. all earlier P V of the tile.
+#ifdef S2O_DIAG_NOEXP  // dev timing aid: exponentials replaced by a multiply (results are garbage)
+#define DX2(x) ((x) * 0.5f)
+#else
+#define DX2(x) ex2(x)
+#endif
 #ifndef S2O_DIAG_POLY
 #define S2O_DIAG_POLY 8  // diagonal kernel: every n-th exponential pair on the FMA pipe (0 = all MUFU; A/B: 8 -3 %, 4 even)
 #endif
@@ -1247,8 +1252,8 @@ tc_diag_kernel(const TcParams p, const __grid_constant__ CUtensorMap qtile,
                             } else
 #endif
                             {
-                                e0 = ex2(fmaf(__uint_as_float(sv[c0 + i]), sc, neg_ref));
-                                e1 = ex2(fmaf(__uint_as_float(sv[c0 + i + 1]), sc, neg_ref));
+                                e0 = DX2(fmaf(__uint_as_float(sv[c0 + i]), sc, neg_ref));
+                                e1 = DX2(fmaf(__uint_as_float(sv[c0 + i + 1]), sc, neg_ref));
                             }
                             rs[(i >> 1) & 3] += e0 + e1;
                             pk[i >> 1] = pack_bf16(e0, e1);
@@ -1261,9 +1266,9 @@ tc_diag_kernel(const TcParams p, const __grid_constant__ CUtensorMap qtile,
                         uint32_t pk[16];
 #pragma unroll
                         for (int i = 0; i < 32; i += 2) {
-                            const float e0 = c0 + i < lim ? ex2(fmaf(__uint_as_float(sv[c0 + i]), sc, neg_ref)) : 0.0f;
+                            const float e0 = c0 + i < lim ? DX2(fmaf(__uint_as_float(sv[c0 + i]), sc, neg_ref)) : 0.0f;
                             const float e1 =
-                                c0 + i + 1 < lim ? ex2(fmaf(__uint_as_float(sv[c0 + i + 1]), sc, neg_ref)) : 0.0f;
+                                c0 + i + 1 < lim ? DX2(fmaf(__uint_as_float(sv[c0 + i + 1]), sc, neg_ref)) : 0.0f;
                             rs[(i >> 1) & 3] += e0 + e1;
                             pk[i >> 1] = pack_bf16(e0, e1);
                         }
