@@ -966,9 +966,6 @@ tc_pass_kernel(const TcParams p, const __grid_constant__ CUtensorMap qmap,
 #ifndef S2O_DIAG_POLY
 #define S2O_DIAG_POLY 8  // diagonal kernel: every n-th exponential pair on the FMA pipe (0 = all MUFU; A/B: 8 -3 %, 4 even)
 #endif
-#ifndef S2O_DIAG_PACKED
-#define S2O_DIAG_PACKED 0  // packed FFMA2/FADD2 softmax arguments and sums in the diagonal kernel
-#endif
 #ifndef S2O_DIAG_SBUF
 #define S2O_DIAG_SBUF 3  // S buffers in TMEM (3: single O buffer; 2: O double-buffered by tile)
 #endif
