@@ -1101,6 +1101,10 @@ tc_diag_kernel(const TcParams p, const __grid_constant__ CUtensorMap qtile,
             for (int j = 0; j < t.nd; ++j, ++gi) {
                 const int st = gi % nst;
                 mbar_wait(smem_u32(&xempty[st]), ((gi / nst) & 1) ^ 1, kl ? 4002 : 4003);
+#ifdef S2O_DIAG_NOLOAD  // dev timing aid: no K/V data movement (results are garbage)
+                mbar_arrive(smem_u32(&xfull[st]));
+                continue;
+#endif
                 mbar_expect_tx(smem_u32(&xfull[st]), kTileBytes);
                 const uint32_t dst = xbase + st * kTileBytes;
                 for (int h = 0; h < 2; ++h)
