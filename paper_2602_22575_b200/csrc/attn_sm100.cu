@@ -1151,6 +1151,7 @@ tc_diag_kernel(const TcParams p, const __grid_constant__ CUtensorMap qtile,
             for (int j = 0; j < t.nd; ++j) {
                 const uint32_t blk = g0 + j;
                 mbar_wait(smem_u32(&c.p_full[blk % kDSBuf]), (blk / kDSBuf) & 1, 4103);
+                tl_mark(p, 6, blk);
                 // the epilogue of the tile that used this O buffer last (tk - kDOBuf) read it
                 if (j == 0) mbar_wait(smem_u32(&c.o_free[ob]), ((tk / kDOBuf) & 1) ^ 1, 4105);
                 const uint32_t vst = blk % kDVStages;
@@ -1168,8 +1169,10 @@ tc_diag_kernel(const TcParams p, const __grid_constant__ CUtensorMap qtile,
                     if (j == t.nd - 1) umma_commit(smem_u32(&c.o_done[ob]));
                 }
                 __syncwarp();
+                tl_mark(p, 7, blk);
                 if (j + kDSBuf < t.nd) {
                     issue_s(blk + kDSBuf);  // into the buffer P(j) held: the pipe runs P V(j) first
+                    tl_mark(p, 31, blk + kDSBuf);
                     if (j + kDSBuf == t.nd - 1 && leader) umma_commit(smem_u32(&c.q_empty));
                 }
             }
@@ -1199,6 +1202,7 @@ tc_diag_kernel(const TcParams p, const __grid_constant__ CUtensorMap qtile,
             for (int j = 0; j < t.nd; ++j, ++gb) {
                 const uint32_t tS = tS0 + (gb % kDSBuf) * 128;
                 mbar_wait(smem_u32(&c.s_full[gb % kDSBuf]), (gb / kDSBuf) & 1, 4201);
+                if (threadIdx.x == 0) tl_mark(p, 19, gb);  // timeline (S2O_TIMELINE builds only)
                 tc_fence_after();
                 uint32_t sv[64];
                 tmem_ld32(tS + h * 64, *reinterpret_cast<uint32_t(*)[32]>(&sv[0]));
@@ -1231,6 +1235,7 @@ tc_diag_kernel(const TcParams p, const __grid_constant__ CUtensorMap qtile,
                 xb[h * 128 + r] = mx;
                 named_bar_sync(1 + q, 64);
                 mx = fmaxf(mx, xb[(1 - h) * 128 + r]) * sc;
+                if (threadIdx.x == 0) tl_mark(p, 25, gb);
                 const float m_new = fmaxf(m2, mx);
                 const bool rescale = (m_new > m2 + kRescaleThresh) || (m2 == -INFINITY);
                 const float m_use = rescale ? m_new : m2;
@@ -1297,6 +1302,7 @@ tc_diag_kernel(const TcParams p, const __grid_constant__ CUtensorMap qtile,
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(smem_u32(&c.p_full[gb % kDSBuf]));
+                if (threadIdx.x == 0) tl_mark(p, 21, gb);
                 ell = ell * alpha + rowsum;
                 m2 = m_use;
             }
