@@ -975,9 +975,10 @@ static_assert(kDSBuf * 128 + kDOBuf * 128 <= 512, "TMEM columns");
 constexpr int kDThreads = 512;
 constexpr int kDSoftWarps = 8, kDEpiWarp0 = 8, kDMmaWarp = 12, kDKWarp = 13, kDVWarp = 14;
 constexpr int kDEpiRegs = 160, kDOtherRegs = 56;  // setmaxnreg (softmax warpgroups keep 128)
-constexpr int kDKStages = 3, kDVStages = 2;
+constexpr int kDKStages = 2, kDVStages = 2;
+constexpr int kDQBuf = 2;  // Q double-buffered by tile parity: the next tile's Q lands during this one
 constexpr uint32_t kDOffQ = 0;
-constexpr uint32_t kDOffK = kTileBytes;
+constexpr uint32_t kDOffK = kDQBuf * kTileBytes;
 constexpr uint32_t kDOffV = kDOffK + kDKStages * kTileBytes;
 constexpr uint32_t kDOffCtrl = kDOffV + kDVStages * kTileBytes;
 constexpr uint32_t kDOffML = kDOffCtrl + 256;  // float [2 tile parity][m, ell half 0, ell half 1][128 rows]
@@ -985,7 +986,7 @@ constexpr uint32_t kDOffX = kDOffML + 2 * 3 * 128 * 4;  // float [2 block parity
 constexpr uint32_t kDSmemBytes = kDOffX + 2 * 2 * 128 * 4;  // 197.25 KB
 
 struct CtrlD {
-    uint64_t q_full, q_empty;
+    uint64_t q_full[kDQBuf], q_empty[kDQBuf];
     uint64_t k_full[kDKStages], k_empty[kDKStages], v_full[kDVStages], v_empty[kDVStages];
     uint64_t s_full[kDSBuf], p_full[kDSBuf], pv_done[kDSBuf];  // per S buffer
     uint64_t o_done[kDOBuf], o_free[kDOBuf];                    // per O buffer
@@ -1038,8 +1039,10 @@ tc_diag_kernel(const TcParams p, const __grid_constant__ CUtensorMap qtile,
     const uint32_t sK = smem_u32(smem + kDOffK);
     const uint32_t sV = smem_u32(smem + kDOffV);
     if (threadIdx.x == 0) {
-        mbar_init(smem_u32(&c.q_full), 1);
-        mbar_init(smem_u32(&c.q_empty), 1);
+        for (int b = 0; b < kDQBuf; ++b) {
+            mbar_init(smem_u32(&c.q_full[b]), 1);
+            mbar_init(smem_u32(&c.q_empty[b]), 1);
+        }
         for (int s = 0; s < kDKStages; ++s) {
             mbar_init(smem_u32(&c.k_full[s]), 1);
             mbar_init(smem_u32(&c.k_empty[s]), 1);
@@ -1090,11 +1093,13 @@ tc_diag_kernel(const TcParams p, const __grid_constant__ CUtensorMap qtile,
         for (int64_t it = blockIdx.x; it < total; it += gridDim.x) {
             const TileInfo t = diag_tile(p, it);
             if (kl) {
-                mbar_wait(smem_u32(&c.q_empty), (qc & 1) ^ 1, 4001);
-                mbar_expect_tx(smem_u32(&c.q_full), kTileBytes);
+                const uint32_t qb_i = qc % kDQBuf;
+                mbar_wait(smem_u32(&c.q_empty[qb_i]), ((qc / kDQBuf) & 1) ^ 1, 4001);
+                mbar_expect_tx(smem_u32(&c.q_full[qb_i]), kTileBytes);
                 const int64_t qb = g.q_base(t.zh) / rowu;
                 for (int h = 0; h < 2; ++h)
-                    tma_load2d(sQ + h * kHalf, &qtile, h * 64, (int32_t)(qb + t.sb + t.t0), smem_u32(&c.q_full));
+                    tma_load2d(sQ + qb_i * kTileBytes + h * kHalf, &qtile, h * 64, (int32_t)(qb + t.sb + t.t0),
+                               smem_u32(&c.q_full[qb_i]));
                 ++qc;
             }
             const int64_t xb = (kl ? g.k_base(t.zh) : g.v_base(t.zh)) / rowu;
@@ -1120,7 +1125,8 @@ tc_diag_kernel(const TcParams p, const __grid_constant__ CUtensorMap qtile,
         const bool leader = elect_one();
         const uint32_t idesc_s = umma_idesc_bf16(kBM, kBN, false, false);
         const uint32_t idesc_o = umma_idesc_bf16(kBM, kD, false, true);
-        const uint64_t dq = umma_desc_sw128(sQ, 16, 1024);
+        const uint64_t dq0 = umma_desc_sw128(sQ, 16, 1024);
+        uint64_t dq = dq0;
         const uint64_t dk0 = umma_desc_sw128(sK, 16, 1024);
         const uint64_t dv0 = umma_desc_sw128(sV, kHalf, 1024);
         uint32_t gb = 0, qc = 0, tk = 0;
@@ -1143,10 +1149,12 @@ tc_diag_kernel(const TcParams p, const __grid_constant__ CUtensorMap qtile,
         for (int64_t it = blockIdx.x; it < total; it += gridDim.x) {
             const TileInfo t = diag_tile(p, it);
             const uint32_t g0 = gb;
-            mbar_wait(smem_u32(&c.q_full), qc & 1, 4102);
+            const uint32_t qb_i = qc % kDQBuf;
+            mbar_wait(smem_u32(&c.q_full[qb_i]), (qc / kDQBuf) & 1, 4102);
+            dq = dq0 + ((qb_i * kTileBytes) >> 4);
             ++qc;
             for (int j = 0; j < t.nd && j < kDSBuf; ++j) issue_s(g0 + j);
-            if (t.nd <= kDSBuf && leader) umma_commit(smem_u32(&c.q_empty));
+            if (t.nd <= kDSBuf && leader) umma_commit(smem_u32(&c.q_empty[qb_i]));
             const uint32_t ob = tk % kDOBuf;
             for (int j = 0; j < t.nd; ++j) {
                 const uint32_t blk = g0 + j;
@@ -1173,7 +1181,7 @@ tc_diag_kernel(const TcParams p, const __grid_constant__ CUtensorMap qtile,
                 if (j + kDSBuf < t.nd) {
                     issue_s(blk + kDSBuf);  // into the buffer P(j) held: the pipe runs P V(j) first
                     tl_mark(p, 31, blk + kDSBuf);
-                    if (j + kDSBuf == t.nd - 1 && leader) umma_commit(smem_u32(&c.q_empty));
+                    if (j + kDSBuf == t.nd - 1 && leader) umma_commit(smem_u32(&c.q_empty[qb_i]));
                 }
             }
             gb += t.nd;
