@@ -371,7 +371,7 @@ tc_pass_kernel(const TcParams p, const __grid_constant__ CUtensorMap qmap,
                         mbar_arrive(smem_u32(&c.q_full));
                     }
                 } else {
-#ifdef S2O_QGATHER_TMA
+#ifndef S2O_QGATHER_CPASYNC  // A/B: TMA gather4 for permuted Q rows, pass-2 6.03 -> 5.90 ms
                     // one gather4 op per lane: (slot, row group, column half) = lt >> 6, ...
                     if (lt == 0) mbar_expect_tx(smem_u32(&c.q_full), (P.has[1] ? 2 : 1) * kTileBytes);
                     else mbar_arrive(smem_u32(&c.q_full));
