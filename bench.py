@@ -160,6 +160,16 @@ def plan_sort_passes(l: int, s: int) -> int:
     return passes
 
 
+def plan_hbm(l: int, s: int, t_ms: float, pk: dict) -> dict:
+    """SURVEY.md §8(d) algorithmic preprocessing bytes and the achieved fraction of HBM."""
+    n = -(-l // s)
+    b_alg = HQ * l * D * 2 + HKV * l * D * 2 + HQ * s * n * (n - 1) // 2 * 4 + HQ * l * 4
+    gbs = b_alg / (t_ms * 1e-3) / 1e9
+    peak = float(pk.get("hbm_gbs", PEAKS_FALLBACK["hbm_gbs"]))
+    return {"alg_bytes": b_alg, "achieved_gbs": round(gbs, 1), "peak_gbs": peak, "frac": round(gbs / peak, 4),
+            "bound": "fp64 (exact scoring) and sort, not HBM"}
+
+
 def launches_per_step(l: int, s: int) -> int:
     """Our kernels per s2o_attention_fwd call with the truncated plan (no overflow rerun):
     guide means, q ranking (+ q sort when S > 2048), kv scoring, top-T selection (scan + sort
@@ -407,6 +417,9 @@ def run_ours(args, rank: int, world: int):
                        "l2": "inputs 1.6 GB > 126 MB L2 (no flush needed)", "path": {1: "generic", 2: "tcgen05"}[path]},
             "breakdown_ms": {"plan_truncated": round(t_plan, 3), "pass1": round(t_p1, 3), "pass2": round(t_p2, 3),
                              "plan_full_permutation": round(t_plan_full, 3)},
+            # preprocessing against HBM (SURVEY.md §8(d) B_alg: Q + K read, full kv_perm + q_perm
+            # written; the truncated plan writes only the top-T lists, so this overstates its bytes)
+            "plan_hbm": plan_hbm(L, S, t_plan, peaks()),
             "sparsity": round(sparsity, 5), "pairs": {"pass1": p1, "pass2": p2},
             "dense_ms": round(dense_ms, 3) if isinstance(dense_ms, float) else dense_ms,
             "speedup_vs_dense": round(dense_ms / ms_step, 2) if isinstance(dense_ms, float) else None,
