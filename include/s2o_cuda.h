@@ -64,12 +64,13 @@ typedef enum s2o_status {
 typedef enum s2o_dtype { S2O_F32 = 0, S2O_BF16 = 1 } s2o_dtype;
 
 /* Which kernels run the attention passes. AUTO picks the tcgen05 path when the shape is
- * covered (bf16, D=128, b_m=128, b_n in {64,128}), the generic SIMT fp64 path otherwise. */
+ * covered (bf16, D=128, b_m=128, b_n=128, strides multiples of D), the generic SIMT fp64 path
+ * otherwise. */
 typedef enum s2o_path { S2O_PATH_AUTO = 0, S2O_PATH_GENERIC = 1, S2O_PATH_TCGEN05 = 2 } s2o_path;
 
 /* How prefix keys / queries are scored for the permutation.
  * EXACT: fp64, sequential over d, identical to dot_f (plan.cpp:14-20) -> bit-identical plans.
- * FAST : fp32 scores; plans are bit-identical to argsort_desc_stable of those scores. */
+ * FAST : reserved; every entry point rejects it with S2O_ERR_UNSUPPORTED. */
 typedef enum s2o_score_mode { S2O_SCORE_EXACT = 0, S2O_SCORE_FAST = 1 } s2o_score_mode;
 
 /* Problem geometry. Strides are in elements. */
@@ -93,8 +94,11 @@ typedef struct s2o_kernel_config {
     int32_t plan_depth;   /* kv_perm entries per segment s2o_attention_fwd materialises when the
                              caller does not ask for kv_perm: 0 = auto (6144), -1 = the full
                              permutation, > 0 = that many (rounded up to b_n). A tile that walks
-                             its whole truncated list without stopping is recomputed on the full
-                             plan, so results never depend on this knob. */
+                             its whole truncated list without stopping saves its state (fp32
+                             acc, ell, m) and resumes on the next level (the following entries
+                             of the same order). Traces and pair counts do not depend on this
+                             knob; outputs agree to the fp32 state re-basing at level
+                             boundaries (about one bf16 ulp). */
 } s2o_kernel_config;
 
 /* ------------------------------------------------------------------ utilities */
@@ -167,17 +171,28 @@ s2o_status s2o_fused(const s2o_problem* p, const void* q, const void* k, const v
 s2o_status s2o_pass_workspace_size(const s2o_problem* p, const s2o_kernel_config* cfg,
                                    size_t* bytes);
 
+/* Device-side errors of the last s2o_pass1/s2o_pass2/s2o_fused on `workspace`, which the
+ * asynchronous entry points cannot return: reads the workspace's status word on `stream`
+ * (synchronises it) and returns S2O_ERR_UNINIT_STATE ("uninitialized state", kernel.cpp:228),
+ * S2O_ERR_UNCOVERED_ROW ("uncovered query row", kernel.cpp:155) or S2O_OK. */
+s2o_status s2o_pass_status(const s2o_problem* p, const s2o_kernel_config* cfg, const void* workspace,
+                           size_t workspace_bytes, void* stream);
+
 /* ------------------------------------------------------------- whole operator */
 /* Workspace for s2o_attention_fwd: plan + pass buffers + scratch. */
 s2o_status s2o_attention_workspace_size(const s2o_problem* p, const s2o_kernel_config* cfg,
                                         size_t* bytes);
 
+/* Same as s2o_pass_status for the workspace of the last s2o_attention_fwd. */
+s2o_status s2o_attention_status(const s2o_problem* p, const s2o_kernel_config* cfg, const void* workspace,
+                                size_t workspace_bytes, void* stream);
+
 /* s2o_attention (kernel.hpp:106-107, kernel.cpp:351-369): validate -> build_plan ->
  * (fused ? fused : pass1 + pass2). q_perm / kv_perm / processed / pair outputs are optional
  * (NULL -> kept in the workspace). When kv_perm is NULL the plan keeps only the exact top
  * plan_depth entries of each kv_perm segment (selection instead of a full sort); tiles that
- * exhaust them are recomputed on the full plan. That check reads one counter back, so in this
- * mode the call synchronises `stream` once before returning. */
+ * exhaust them resume on the next plan level (see plan_depth). Device errors are reported by
+ * s2o_attention_status. */
 s2o_status s2o_attention_fwd(const s2o_problem* p, const void* q, const void* k, const void* v,
                              const s2o_kernel_config* cfg, void* o, int32_t* q_perm,
                              int32_t* kv_perm, int32_t* processed, int64_t* pass1_pairs,

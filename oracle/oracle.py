@@ -211,6 +211,23 @@ class _Backend:
         return out, tr, plan
 
 
+    def tile_gains(self, qh, kh, vh, seg_len: int, b_n: int, rows, n: int, kv_seg, nchunks: int) -> np.ndarray:
+        """Max relative normaliser gain of each of the first `nchunks` kv_perm chunks of one query
+        tile, every chunk committed (SURVEY.md §8c P2 evidence). qh/kh/vh: one head [L, D];
+        rows: the tile's segment-local query rows; kv_seg: kv_perm[n] (absolute token ids)."""
+        qh = np.ascontiguousarray(qh, np.float32)
+        kh = np.ascontiguousarray(kh, np.float32)
+        vh = np.ascontiguousarray(vh, np.float32)
+        rows = np.ascontiguousarray(rows, np.int64)
+        kv = np.ascontiguousarray(kv_seg, np.int64)
+        if kv.size == 0:
+            kv = np.zeros(1, np.int64)
+        out = np.zeros(max(nchunks, 1), np.float64)
+        self._call("tile_gains", _p(qh), _p(kh), _p(vh), _i64(qh.shape[0]), _i64(qh.shape[1]), _i64(seg_len),
+                   _i64(b_n), _p(rows), _i64(len(rows)), _i64(n), _p(kv), _i64(nchunks), _p(out))
+        return out[:nchunks]
+
+
 class Ref(_Backend):
     """The compiled reference (oracle/_ref/libs2o_ref.so)."""
     prefix = "ref_"
@@ -322,3 +339,42 @@ def visible_sets(plan: Plan, trace: Trace, cfg, l: int, zh: int) -> list[list[in
                 vis = list(range(begin, row + 1)) + [int(x) for x in kv[:take]]
                 sets[row] = sorted(vis)
     return sets
+
+
+TIE_RTOL = 1e-4  # a trace difference must sit at a threshold tie |gain - tau| / tau <= 1e-4
+
+
+def trace_ties(backend: _Backend, q, k, v, cfg, q_perm, kv_perm, got, want, zh_list=None) -> list[dict]:
+    """Explain every (head, segment, tile) whose committed chunk count differs between `got` (the
+    device trace) and `want` (the reference's): replay the tile in the reference arithmetic
+    (Backend.tile_gains), take the gain of the first chunk the two decided differently
+    (k = min(got, want); both committed chunks 0..k-1), and report it with its distance to tau.
+
+    q/k/v: fp32 [Z, H, L, D] as the reference saw them (K/V already expanded to H heads);
+    q_perm int [ZH, N, S] / kv_perm int [ZH, S*N*(N-1)/2] (the reference's plan, identical to the
+    device plan); got/want int [ZH, N, T]. Returns one dict per differing tile with 'tie' = whether
+    |gain - tau| / tau <= TIE_RTOL."""
+    q = np.asarray(q)
+    z, h, l, d = q.shape
+    seg = SegCfg.of(l, cfg.seg_len)
+    got = np.asarray(got).reshape(z * h, seg.seg_count, -1)
+    want = np.asarray(want).reshape(z * h, seg.seg_count, -1)
+    out = []
+    for zh, n, t in zip(*np.nonzero(got != want)):
+        if zh_list is not None and zh not in zh_list:
+            continue
+        zi, hi = divmod(int(zh), h)
+        ln = seg.len(int(n))
+        t0 = int(t) * cfg.b_m
+        tn = min(cfg.b_m, ln - t0)
+        rows = (np.asarray(q_perm)[zh, n, t0:t0 + tn] if cfg.q_reorder else np.arange(t0, t0 + tn))
+        off = seg.kv_offset(int(n))
+        kv = np.asarray(kv_perm)[zh, off: off + int(n) * seg.seg_len]
+        kc = int(min(got[zh, n, t], want[zh, n, t]))
+        gains = backend.tile_gains(q[zi, hi], np.asarray(k)[zi, hi], np.asarray(v)[zi, hi], cfg.seg_len, cfg.b_n,
+                                   rows, int(n), kv, kc + 1)
+        g = float(gains[kc])
+        rel = abs(g - cfg.tau) / cfg.tau if cfg.tau > 0 else float("inf")
+        out.append({"zh": int(zh), "segment": int(n), "tile": int(t), "got": int(got[zh, n, t]),
+                    "want": int(want[zh, n, t]), "gain": g, "rel_to_tau": rel, "tie": bool(rel <= TIE_RTOL)})
+    return out

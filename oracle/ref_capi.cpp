@@ -28,9 +28,12 @@
 // Every entry point returns 0 on success, otherwise a nonzero code with the
 // exception text available from ref_last_error().
 
+#include <cmath>
 #include <cstdint>
 #include <cstring>
 #include <exception>
+#include <limits>
+#include <span>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -369,6 +372,77 @@ int ref_run_sweep(const char* pattern, int64_t stripe_count, double stripe_gain,
     });
     if (rc == 0 && partial) g_err = err;
     return rc != 0 ? rc : (partial ? 7 : 0);
+}
+
+// Stop-decision evidence: the relative normaliser gain max_r (new-prev)/prev of
+// each of the first `nchunks` kv_perm chunks of ONE query tile, with every chunk committed, built
+// from the reference's own os_update (attention.cpp:31-88) exactly as traverse_prefix
+// (kernel.cpp:86-122) would see it up to its stop chunk. rows: segment-local query rows of the tile
+// (q_perm order for pass-2, t0.. for fused); each row's pass-1 state is the reference's per-row
+// result of segment_causal_tile (kernel.cpp:36-71: b_n key chunks of the segment, masked by original
+// position; rows are independent inside os_update). qh/kh/vh: one head [L, D] fp32; kv_seg: the nS
+// absolute token ids of kv_perm[n]. gains[c] = NaN for a chunk past the list.
+int ref_tile_gains(const float* qh, const float* kh, const float* vh, int64_t l, int64_t d, int64_t seg_len,
+                   int64_t b_n, const int64_t* rows, int64_t tn, int64_t n, const int64_t* kv_seg,
+                   int64_t nchunks, double* gains) {
+    return guarded([&] {
+        const int64_t sb = n * seg_len;
+        const int64_t kv_len = n * seg_len;
+        std::vector<OnlineSoftmaxState> st(static_cast<std::size_t>(tn), OnlineSoftmaxState(d));
+        RowMatrix qt(tn, d), kt, vt;
+        for (int64_t r = 0; r < tn; ++r) std::memcpy(qt.row(r), qh + (sb + rows[r]) * d, sizeof(float) * d);
+        auto load = [&](RowMatrix& dst, const float* src, const int64_t* ids, int64_t cnt) {
+            dst = RowMatrix(cnt, d);
+            for (int64_t j = 0; j < cnt; ++j) std::memcpy(dst.row(j), src + ids[j] * d, sizeof(float) * d);
+        };
+        // pass-1 state, one row at a time (identical to the tile-wide scan: os_update is per row)
+        std::vector<int64_t> ids;
+        for (int64_t r = 0; r < tn; ++r) {
+            RowMatrix q1(1, d);
+            std::memcpy(q1.row(0), qt.row(r), sizeof(float) * d);
+            std::span<OnlineSoftmaxState> one(&st[static_cast<std::size_t>(r)], 1);
+            const int64_t rr = rows[r];
+            const int64_t seg_rows = std::min(seg_len, l - sb);
+            for (int64_t k0 = 0; k0 <= rr && k0 < seg_rows; k0 += b_n) {
+                const int64_t kn = std::min(b_n, seg_rows - k0);
+                ids.resize(static_cast<std::size_t>(kn));
+                for (int64_t j = 0; j < kn; ++j) ids[static_cast<std::size_t>(j)] = sb + k0 + j;
+                load(kt, kh, ids.data(), kn);
+                load(vt, vh, ids.data(), kn);
+                if (k0 + kn - 1 <= rr) {
+                    os_update(one, q1, kt, vt);
+                } else {
+                    std::vector<std::uint8_t> mask(static_cast<std::size_t>(kn));
+                    for (int64_t j = 0; j < kn; ++j) mask[static_cast<std::size_t>(j)] = (k0 + j <= rr) ? 1 : 0;
+                    os_update(one, q1, kt, vt, mask);
+                }
+            }
+        }
+        std::vector<OnlineSoftmaxState> cand(st.size(), OnlineSoftmaxState(d));
+        for (int64_t c = 0; c < nchunks; ++c) {
+            const int64_t c0 = c * b_n;
+            if (c0 >= kv_len) {
+                gains[c] = std::numeric_limits<double>::quiet_NaN();
+                continue;
+            }
+            const int64_t cn = std::min(b_n, kv_len - c0);
+            load(kt, kh, kv_seg + c0, cn);
+            load(vt, vh, kv_seg + c0, cn);
+            for (std::size_t r = 0; r < st.size(); ++r) {
+                cand[r].m = st[r].m;
+                cand[r].ell = st[r].ell;
+                cand[r].acc = st[r].acc;
+            }
+            os_update(std::span<OnlineSoftmaxState>(cand), qt, kt, vt);
+            double max_gain = -std::numeric_limits<double>::infinity();
+            for (std::size_t r = 0; r < st.size(); ++r) {
+                const double prev = st[r].ell * std::exp(st[r].m - cand[r].m);
+                max_gain = std::max(max_gain, (cand[r].ell - prev) / prev);  // kernel.cpp:226-232
+            }
+            gains[c] = max_gain;
+            st.swap(cand);  // commit
+        }
+    });
 }
 
 int ref_rng_normals(uint64_t seed, int64_t n, double* out) {

@@ -537,3 +537,60 @@ int orc_masked_softmax_row(const float* q_row, const float* k, const float* v, i
     free(s);
     return 0;
 }
+
+/* Stop-decision evidence, the restatement of ref_tile_gains (ref_capi.cpp):
+ * max_r (new - prev) / prev for each of the first nchunks kv_perm chunks of ONE query tile with
+ * every chunk committed (traverse_prefix proj/src/kernel.cpp:86-122 without the break); each
+ * row's pass-1 state is its own segment_causal_tile scan (kernel.cpp:36-71). rows: segment-local
+ * rows of the tile; qh/kh/vh one head [L, D]; kv_seg: kv_perm[n] (n*S absolute ids). */
+int orc_tile_gains(const float* qh, const float* kh, const float* vh, int64_t l, int64_t d, int64_t seg_len,
+                   int64_t b_n, const int64_t* rows, int64_t tn, int64_t n, const int64_t* kv_seg,
+                   int64_t nchunks, double* gains) {
+    tile_ws w;
+    ws_init(&w, tn, b_n, d);
+    ws_reset_state(&w, tn);
+    const int64_t sb = n * seg_len, kv_len = n * seg_len;
+    const int64_t seg_rows = (seg_len < l - sb) ? seg_len : l - sb;
+    for (int64_t r = 0; r < tn; ++r) {
+        const int64_t rr = rows[r];
+        const float* qr[1] = {qh + (sb + rr) * d};
+        for (int64_t k0 = 0; k0 <= rr && k0 < seg_rows; k0 += b_n) {
+            const int64_t kn = (b_n < seg_rows - k0) ? b_n : seg_rows - k0;
+            for (int64_t j = 0; j < kn; ++j) {
+                w.kr[j] = kh + (sb + k0 + j) * d;
+                w.vr[j] = vh + (sb + k0 + j) * d;
+                w.mask[j] = (k0 + j <= rr);
+            }
+            os_update(1, kn, d, w.m + r, w.ell + r, w.acc + r * d, qr, w.kr, w.vr,
+                      (k0 + kn - 1 <= rr) ? NULL : w.mask, w.scratch);
+        }
+        w.qr[r] = qh + (sb + rr) * d;
+    }
+    for (int64_t c = 0; c < nchunks; ++c) {
+        const int64_t c0 = c * b_n;
+        if (c0 >= kv_len) {
+            gains[c] = NAN;
+            continue;
+        }
+        const int64_t cn = (b_n < kv_len - c0) ? b_n : kv_len - c0;
+        for (int64_t j = 0; j < cn; ++j) {
+            w.kr[j] = kh + kv_seg[c0 + j] * d;
+            w.vr[j] = vh + kv_seg[c0 + j] * d;
+        }
+        memcpy(w.cm, w.m, (size_t)tn * sizeof(double));
+        memcpy(w.cell, w.ell, (size_t)tn * sizeof(double));
+        memcpy(w.cacc, w.acc, (size_t)(tn * d) * sizeof(double));
+        os_update(tn, cn, d, w.cm, w.cell, w.cacc, w.qr, w.kr, w.vr, NULL, w.scratch);
+        double max_gain = -INFINITY;
+        for (int64_t r = 0; r < tn; ++r) {
+            const double prev = w.ell[r] * exp(w.m[r] - w.cm[r]);
+            max_gain = std_max(max_gain, (w.cell[r] - prev) / prev);
+        }
+        gains[c] = max_gain;
+        memcpy(w.m, w.cm, (size_t)tn * sizeof(double));
+        memcpy(w.ell, w.cell, (size_t)tn * sizeof(double));
+        memcpy(w.acc, w.cacc, (size_t)(tn * d) * sizeof(double));
+    }
+    ws_free(&w);
+    return 0;
+}

@@ -38,6 +38,8 @@
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <utility>
+#include <vector>
 
 #include "internal.h"
 #include "sm100.cuh"
@@ -694,6 +696,10 @@ tc_pass_kernel(const TcParams p, const __grid_constant__ CUtensorMap qmap,
                     const float mx = fmax3(fmax3(mxa[0], mxa[1], mxa[2]), fmax3(mxa[3], mxa[4], mxa[5]),
                                            fmaxf(mxa[6], mxa[7])) * sc;
                     const float m_new = fmaxf(m2, mx);
+                    // early_stop_check's "uninitialized state" (kernel.cpp:228): the reference's
+                    // fp64 prev = ell * e^(m - m') is <= 0 iff ell <= 0 or e^(m - m') underflows
+                    // fp64 (a max jump beyond 1075 log2 units)
+                    if (!is_diag && valid && (ell <= 0.0f || m_new - m2 > 1075.0f)) atomicExch(a.err_flag, 1);
                     rescale = (m_new > m2 + kRescaleThresh) || (m2 == -INFINITY);
                     m_use = rescale ? m_new : m2;
                     const float neg_ref = (m_use == -INFINITY) ? 0.0f : -m_use;
@@ -717,7 +723,7 @@ tc_pass_kernel(const TcParams p, const __grid_constant__ CUtensorMap qmap,
 #if S2O_POLY_MOD > 0
                                     // every S2O_POLY_MOD-th pair on the FMA pipe (MUFU offload)
                                     const float2 e = ((i >> 1) % S2O_POLY_MOD == S2O_POLY_MOD - 1)
-                                                         ? ex2_poly3x2(arg)
+                                                         ? ex2_poly4x2(arg)
                                                          : make_float2(ex2(arg.x), ex2(arg.y));
 #else
                                     const float2 e = make_float2(ex2(arg.x), ex2(arg.y));
@@ -910,7 +916,7 @@ tc_pass_kernel(const TcParams p, const __grid_constant__ CUtensorMap qmap,
                 a.m_out[slot] = (m2 == -INFINITY) ? -INFINITY : m2 * 0.6931471805599453f;
                 a.ell_out[slot] = ell;
             }
-            if (valid && (a.mode & kFinal) && !resume_later && !(ell > 0.0f)) atomicExch(a.err_flag, 2);
+            if (valid && (a.mode & kFinal) && !resume_later && ell == 0.0f) atomicExch(a.err_flag, 2);
             if ((a.mode & kPrefix) && r == 0) {
                 const int64_t tile = P.zh * a.tiles_per_head + P.n * a.T + P.ti[x];
                 const int base = a.tile_base ? a.tile_base[it] : 0;
@@ -1259,7 +1265,7 @@ tc_diag_kernel(const TcParams p, const __grid_constant__ CUtensorMap qtile,
                             float e0, e1;
 #if S2O_DIAG_POLY > 0
                             if ((i >> 1) % S2O_DIAG_POLY == S2O_DIAG_POLY - 1) {  // FMA-pipe exp2 (MUFU offload)
-                                const float2 e = ex2_poly3x2(make_float2(fmaf(__uint_as_float(sv[c0 + i]), sc, neg_ref),
+                                const float2 e = ex2_poly4x2(make_float2(fmaf(__uint_as_float(sv[c0 + i]), sc, neg_ref),
                                                                          fmaf(__uint_as_float(sv[c0 + i + 1]), sc, neg_ref)));
                                 e0 = e.x;
                                 e1 = e.y;
@@ -1400,7 +1406,7 @@ tc_diag_kernel(const TcParams p, const __grid_constant__ CUtensorMap qtile,
                         dst[i] = make_float4(__uint_as_float(ov[4 * i]) * inv, __uint_as_float(ov[4 * i + 1]) * inv,
                                              __uint_as_float(ov[4 * i + 2]) * inv, __uint_as_float(ov[4 * i + 3]) * inv);
                 }
-                if (!(ell > 0.0f)) atomicExch(a.err_flag, 2);
+                if (ell == 0.0f) atomicExch(a.err_flag, 2);
             }
         }
     }
@@ -2048,7 +2054,7 @@ tc_pass2cta_kernel(const TcParams p, const __grid_constant__ CUtensorMap qmap,
                     a.m_out[slot] = (m2 == -INFINITY) ? -INFINITY : m2 * 0.6931471805599453f;
                     a.ell_out[slot] = ell;
                 }
-                if (valid && (a.mode & kFinal) && !resume_later && !(ell > 0.0f)) atomicExch(a.err_flag, 2);
+                if (valid && (a.mode & kFinal) && !resume_later && ell == 0.0f) atomicExch(a.err_flag, 2);
                 if ((a.mode & kPrefix) && r == 0) {
                     const int64_t tile = Q.zh * a.tiles_per_head + Q.n * a.T + Q.ti[x];
                     if (overflow) {
@@ -2107,6 +2113,21 @@ unsigned long long* g_timeline = nullptr;
 
 bool strides_ok(const int64_t* st) { return st[0] % kD == 0 && st[1] % kD == 0 && st[2] % kD == 0; }
 
+// Max dynamic shared memory is a per-device function attribute: set it once per (kernel, device).
+cudaError_t smem_attr(const void* fn, uint32_t bytes) {
+    static std::mutex mu;
+    static std::vector<std::pair<const void*, int>> done;
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    std::lock_guard<std::mutex> lock(mu);
+    for (const auto& d : done)
+        if (d.first == fn && d.second == dev) return cudaSuccess;
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    if (e == cudaSuccess) done.emplace_back(fn, dev);
+    return e;
+}
+
 }  // namespace
 
 bool tc_supported(const PassArgs& a) {
@@ -2157,27 +2178,15 @@ cudaError_t launch_tc_pass(const PassArgs& a, cudaStream_t st) {
         p.kv_contig) {
         TcParams pd = p;
         pd.pairs_per_head = (g.N - 1) * a.T + t_last;  // tiles per head (diag_tile)
-        static bool attrd_done = false;
-        if (!attrd_done) {
-            cudaError_t e = cudaFuncSetAttribute(tc_diag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                 (int)kDSmemBytes);
-            if (e != cudaSuccess) return e;
-            attrd_done = true;
-        }
+        if (cudaError_t e = smem_attr((const void*)tc_diag_kernel, kDSmemBytes)) return e;
         const int64_t work = g.z * g.hq * pd.pairs_per_head;
         if (work == 0) return cudaSuccess;
         const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(work, sms));
         tc_diag_kernel<<<grid, kDThreads, kDSmemBytes, st>>>(pd, qtile, ktile, vtile);
         return cudaGetLastError();
     }
-    static bool attr_done = false;
-    if (!attr_done) {
-        for (const void* f : {(const void*)tc_pass_kernel<false>, (const void*)tc_pass_kernel<true>}) {
-            cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
-            if (e != cudaSuccess) return e;
-        }
-        attr_done = true;
-    }
+    for (const void* f : {(const void*)tc_pass_kernel<false>, (const void*)tc_pass_kernel<true>})
+        if (cudaError_t e = smem_attr(f, kSmemBytes)) return e;
     // CTA-pair variant (cta_group::2, quads of tiles) only on request (S2O_TC_CTAS=2): it halves
     // the gathered bytes per SM but its per-block cross-SM handshakes (4 remote p_full arrivals,
     // remote decision publication) cost more than they save at C3 (pass-2 8.9 vs 7.4 ms,
@@ -2192,13 +2201,7 @@ cudaError_t launch_tc_pass(const PassArgs& a, cudaStream_t st) {
         TcParams p2 = p;
         p2.pairs_full = (a.T + 3) / 4;  // quads per full segment
         p2.pairs_per_head = (g.N - 1) * p2.pairs_full + (t_last + 3) / 4;
-        static bool attr2_done = false;
-        if (!attr2_done) {
-            cudaError_t e = cudaFuncSetAttribute(tc_pass2cta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                 (int)k2SmemBytes);
-            if (e != cudaSuccess) return e;
-            attr2_done = true;
-        }
+        if (cudaError_t e = smem_attr((const void*)tc_pass2cta_kernel, k2SmemBytes)) return e;
         const int64_t work2 = g.z * g.hq * p2.pairs_per_head;
         if (work2 == 0) return cudaSuccess;
         const int clusters = (int)std::max<int64_t>(1, std::min<int64_t>(work2, sms / 2));

@@ -72,6 +72,8 @@ s2o_status validate_cfg(const s2o_kernel_config* c, int64_t l) {
         return fail(S2O_ERR_LOCAL_WINDOW, "local window must satisfy W <= S");
     if (c->fused && c->q_reorder)
         return fail(S2O_ERR_FUSED_REORDER, "fused variant requires q_reorder = false");
+    if (c->score_mode != S2O_SCORE_EXACT)
+        return fail(S2O_ERR_UNSUPPORTED, "only exact (fp64 sequential) scoring is implemented");
     return S2O_OK;
 }
 
@@ -107,8 +109,7 @@ s2o_status run_pass(PassArgs a, int32_t path, void* ws, size_t ws_bytes, cudaStr
     if (clear_flag) S2O_CUDA_TRY(cudaMemsetAsync(a.err_flag, 0, 8 * sizeof(int32_t), st), "memset");
     else S2O_CUDA_TRY(cudaMemsetAsync(a.work_ctr, 0, sizeof(int32_t), st), "memset");
     if (path == S2O_PATH_TCGEN05 && !tc_supported(a))
-        return fail(S2O_ERR_UNSUPPORTED,
-                    "tcgen05 path needs bf16 inputs, D=128, b_m=128, b_n in {64,128}");
+        return fail(S2O_ERR_UNSUPPORTED, "tcgen05 path needs bf16 inputs, D=128, b_m=128, b_n=128");
     if (path_is_tc(a, path)) {
         S2O_CUDA_TRY(launch_tc_pass(a, st), "tcgen05 pass launch");
     } else {
@@ -292,8 +293,8 @@ s2o_status s2o_plan_build(const s2o_problem* p, const void* q, const void* k,
     if (!q || !k || !q_perm || (g.N > 1 && !kv_perm)) return fail(S2O_ERR_INVALID_ARG, "null pointer");
     if (!workspace || workspace_bytes < plan_workspace_bytes(g))
         return fail(S2O_ERR_WORKSPACE, "workspace too small");
-    if (cfg->score_mode != S2O_SCORE_EXACT && cfg->score_mode != S2O_SCORE_FAST)
-        return fail(S2O_ERR_INVALID_ARG, "unknown score mode");
+    if (cfg->score_mode != S2O_SCORE_EXACT)
+        return fail(S2O_ERR_UNSUPPORTED, "only exact (fp64 sequential) scoring is implemented");
     void* ws = reinterpret_cast<void*>((reinterpret_cast<uintptr_t>(workspace) + 255) & ~uintptr_t(255));
     S2O_CUDA_TRY(launch_plan_build(g, q, k, q_perm, kv_perm, ws, reinterpret_cast<cudaStream_t>(stream)),
                  "plan build");
@@ -336,6 +337,31 @@ s2o_status s2o_pass_workspace_size(const s2o_problem* p, const s2o_kernel_config
     if ((st = validate_cfg(cfg, p->l))) return st;
     *bytes = pass_ws_bytes(base_args(g, cfg));
     return S2O_OK;
+}
+
+// Device status word of the last pass on this workspace: 0 ok, 1 uninitialized state
+// (kernel.cpp:228), 2 uncovered query row (kernel.cpp:155). One D2H read; synchronises `stream`.
+static s2o_status read_status(const int32_t* dflag, cudaStream_t s) {
+    int32_t flag = 0;
+    S2O_CUDA_TRY(cudaMemcpyAsync(&flag, dflag, sizeof flag, cudaMemcpyDeviceToHost, s), "d2h status");
+    S2O_CUDA_TRY(cudaStreamSynchronize(s), "sync");
+    if (flag == 1) return fail(S2O_ERR_UNINIT_STATE, "uninitialized state");
+    if (flag == 2) return fail(S2O_ERR_UNCOVERED_ROW, "uncovered query row");
+    g_err.clear();
+    return S2O_OK;
+}
+
+s2o_status s2o_pass_status(const s2o_problem* p, const s2o_kernel_config* cfg, const void* workspace,
+                           size_t workspace_bytes, void* stream) {
+    Geo g;
+    s2o_status st = make_geo(p, cfg ? cfg->seg_len : 0, &g);
+    if (st) return st;
+    if ((st = validate_cfg(cfg, p->l))) return st;
+    const PassArgs a = base_args(g, cfg);
+    if (!workspace || workspace_bytes < pass_ws_bytes(a)) return fail(S2O_ERR_WORKSPACE, "workspace too small");
+    const char* base = reinterpret_cast<const char*>(workspace);
+    return read_status(reinterpret_cast<const int32_t*>(base + align256(generic_scratch_bytes(a))),
+                       reinterpret_cast<cudaStream_t>(stream));
 }
 
 s2o_status s2o_pass1(const s2o_problem* p, const void* q, const void* k, const void* v,
@@ -459,6 +485,20 @@ s2o_status s2o_attention_workspace_size(const s2o_problem* p, const s2o_kernel_c
     return S2O_OK;
 }
 
+s2o_status s2o_attention_status(const s2o_problem* p, const s2o_kernel_config* cfg, const void* workspace,
+                                size_t workspace_bytes, void* stream) {
+    Geo g;
+    s2o_status st = make_geo(p, cfg ? cfg->seg_len : 0, &g);
+    if (st) return st;
+    if ((st = validate_cfg(cfg, p->l))) return st;
+    const PassArgs a = base_args(g, cfg);
+    const OpLayout L = op_layout(g, a, cfg->fused, cfg);
+    if (!workspace || workspace_bytes < L.total) return fail(S2O_ERR_WORKSPACE, "workspace too small");
+    const char* base = reinterpret_cast<const char*>((reinterpret_cast<uintptr_t>(workspace) + 255) & ~uintptr_t(255));
+    return read_status(reinterpret_cast<const int32_t*>(base + L.pass + align256(generic_scratch_bytes(a))),
+                       reinterpret_cast<cudaStream_t>(stream));
+}
+
 s2o_status s2o_attention_fwd(const s2o_problem* p, const void* q, const void* k, const void* v,
                              const s2o_kernel_config* cfg, void* o, int32_t* q_perm,
                              int32_t* kv_perm, int32_t* processed, int64_t* pass1_pairs,
@@ -536,8 +576,9 @@ s2o_status s2o_attention_fwd(const s2o_problem* p, const void* q, const void* k,
             if (host[0] == 0 || host[1] != 0) break;
             // next plan level for the segments of the overflow tiles
             std::vector<int32_t> ht(host[0]);
-            S2O_CUDA_TRY(cudaMemcpy(ht.data(), tiles[cur], sizeof(int32_t) * host[0], cudaMemcpyDeviceToHost),
+            S2O_CUDA_TRY(cudaMemcpyAsync(ht.data(), tiles[cur], sizeof(int32_t) * host[0], cudaMemcpyDeviceToHost, s),
                          "d2h tiles");
+            S2O_CUDA_TRY(cudaStreamSynchronize(s), "sync");
             std::vector<int32_t> segs;
             segs.reserve(ht.size());
             for (int32_t t : ht) {

@@ -360,6 +360,22 @@ __device__ __forceinline__ float2 ex2_poly3x2(float2 x) {
     return make_float2(__int_as_float(__float_as_int(p.x) + (__float_as_int(t.x) << 23)),
                        __int_as_float(__float_as_int(p.y) + (__float_as_int(t.y) << 23)));
 }
+// Degree-4 variant (one more FFMA2): max rel. error 2.7e-6 in fp32, so the normaliser ell that
+// pass-2's stop test divides by stays within the SURVEY §7.3-1 bound (<~1e-5) even if every
+// polynomial exponential erred the same way.
+__device__ __forceinline__ float2 ex2_poly4x2(float2 x) {
+    const float2 xc = make_float2(fmaxf(x.x, -126.0f), fmaxf(x.y, -126.0f));
+    const float2 t = fadd2(xc, make_float2(12582912.0f, 12582912.0f));
+    const float2 j = fadd2(t, make_float2(-12582912.0f, -12582912.0f));
+    const float2 f = ffma2(j, make_float2(-1.0f, -1.0f), xc);
+    float2 p = ffma2(make_float2(0.009570068679749966f, 0.009570068679749966f), f,
+                     make_float2(0.055917806923389435f, 0.055917806923389435f));
+    p = ffma2(p, f, make_float2(0.240247443318367f, 0.240247443318367f));
+    p = ffma2(p, f, make_float2(0.6931218504905701f, 0.6931218504905701f));
+    p = ffma2(p, f, make_float2(0.9999992847442627f, 0.9999992847442627f));
+    return make_float2(__int_as_float(__float_as_int(p.x) + (__float_as_int(t.x) << 23)),
+                       __int_as_float(__float_as_int(p.y) + (__float_as_int(t.y) << 23)));
+}
 __device__ __forceinline__ float fmax3(float a, float b, float c) {  // FMNMX3 (sm_100)
     float d;
     asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));

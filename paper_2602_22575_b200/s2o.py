@@ -23,6 +23,7 @@ IndexError, std::runtime_error -> RuntimeError (message text identical).
 from __future__ import annotations
 
 import ctypes as C
+import functools
 import math
 import os
 from dataclasses import dataclass, field
@@ -268,8 +269,15 @@ def _problem(q, k, v=None, o=None, out_dtype=None) -> _Problem:
     return p
 
 
-def _stream() -> C.c_void_p:
-    return C.c_void_p(_torch().cuda.current_stream().cuda_stream)
+def _stream(device=None) -> C.c_void_p:
+    """The current stream of `device` (the tensors' device, not the current device)."""
+    return C.c_void_p(_torch().cuda.current_stream(device).cuda_stream)
+
+
+def _on(t):
+    """Context that makes the tensors' device current for the C-ABI call (the library launches
+    on the current device; smem attributes and TMEM are per device)."""
+    return _torch().cuda.device(t.device)
 
 
 def _ptr(t) -> C.c_void_p:
@@ -280,14 +288,38 @@ _WS: dict = {}
 
 
 def _workspace(nbytes: int, device):
-    """Per-device cached workspace (grown on demand)."""
+    """Cached workspace per (device, current stream), grown on demand. The C-ABI is only safe
+    for distinct workspaces across streams, so each stream gets its own; a buffer replaced by
+    a larger one is freed through the caching allocator, which orders the free after the work
+    already queued on that stream."""
     torch = _torch()
-    key = (device.index if hasattr(device, "index") else device)
+    stream = torch.cuda.current_stream(device)
+    key = (device.index if hasattr(device, "index") else device, stream.cuda_stream)
     buf = _WS.get(key)
     if buf is None or buf.numel() < nbytes:
         buf = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=device)
         _WS[key] = buf
     return buf
+
+
+def _pass_status(p: _Problem, c: _Config, ws, whole_op: bool) -> None:
+    """Device-side errors of the last call ('uninitialized state' kernel.cpp:228, 'uncovered query
+    row' kernel.cpp:155): one read of the workspace status word (synchronises the stream)."""
+    fn = lib().s2o_attention_status if whole_op else lib().s2o_pass_status
+    _check(fn(C.byref(p), C.byref(c), _ptr(ws), C.c_size_t(ws.numel()), _stream()))
+
+
+def _device_guard(fn):
+    """Run a C-ABI wrapper with the device of its first CUDA tensor argument current, so the
+    kernels launch on that device and on its current stream."""
+    @functools.wraps(fn)
+    def wrapped(*args, **kwargs):
+        t = next((a for a in args if hasattr(a, "is_cuda") and a.is_cuda), None)
+        if t is None:
+            return fn(*args, **kwargs)
+        with _torch().cuda.device(t.device):
+            return fn(*args, **kwargs)
+    return wrapped
 
 
 def _out_like(q, out_dtype):
@@ -301,6 +333,7 @@ def _default_out_dtype(q) -> int:
 
 
 # ----------------------------------------------------------------------------- Step 1
+@_device_guard
 def segment_representatives(q, k, seg: SegmentConfig) -> Representatives:
     torch = _torch()
     p = _problem(q, k)
@@ -311,6 +344,7 @@ def segment_representatives(q, k, seg: SegmentConfig) -> Representatives:
     return Representatives(qm, km)
 
 
+@_device_guard
 def build_plan(q, k, seg_len: int, score_mode: int = SCORE_EXACT):
     """build_plan (plan.cpp:140-162) on the device. Returns (PermutationPlan, RankingCost)."""
     torch = _torch()
@@ -329,6 +363,7 @@ def build_plan(q, k, seg_len: int, score_mode: int = SCORE_EXACT):
     return plan, RankingCost(int(cost[0]), int(cost[1]))
 
 
+@_device_guard
 def build_plan_truncated(q, k, seg_len: int, depth: int = 6144):
     """Truncated plan (s2o_plan_build_truncated): (q_perm [Z,Hq,N,S], kv_top [Z,Hq,N,depth],
     flag). kv_top[..., n, :min(nS, depth)] == the first entries of the full kv_perm segment."""
@@ -365,6 +400,7 @@ def _trace(p: _Problem, cfg: KernelConfig, device) -> KernelTrace:
                        torch.empty((p.z, p.hq), dtype=torch.int64, device=device))
 
 
+@_device_guard
 def pass1_dense_init(q, k, v, cfg: KernelConfig) -> PassBuffers:
     torch = _torch()
     p = _problem(q, k, v)
@@ -385,8 +421,9 @@ def _check_plan(plan: PermutationPlan, p: _Problem, cfg: KernelConfig) -> None:
         raise ValueError("plan/config mismatch: segment layout differs")
 
 
+@_device_guard
 def pass2_sparse(q, k, v, bufs: PassBuffers, plan: PermutationPlan, cfg: KernelConfig,
-                 out=None):
+                 out=None, check: bool = True):
     o = out if out is not None else _out_like(q, _default_out_dtype(q))
     p = _problem(q, k, v, o)
     c = cfg._c()
@@ -402,10 +439,13 @@ def pass2_sparse(q, k, v, bufs: PassBuffers, plan: PermutationPlan, cfg: KernelC
                            _ptr(kv) if kv.numel() else _ptr(plan.q_perm), _ptr(o), _ptr(tr.processed),
                            _ptr(tr.pass1_pairs), _ptr(tr.pass2_pairs), _ptr(ws),
                            C.c_size_t(ws.numel()), _stream()))
+    if check:
+        _pass_status(p, c, ws, False)
     return o, tr
 
 
-def fused_single_pass(q, k, v, plan: PermutationPlan, cfg: KernelConfig, out=None):
+@_device_guard
+def fused_single_pass(q, k, v, plan: PermutationPlan, cfg: KernelConfig, out=None, check: bool = True):
     if not cfg.fused or cfg.q_reorder:
         raise ValueError("fused variant requires fused = true, q_reorder = false")
     o = out if out is not None else _out_like(q, _default_out_dtype(q))
@@ -420,9 +460,12 @@ def fused_single_pass(q, k, v, plan: PermutationPlan, cfg: KernelConfig, out=Non
                            _ptr(kv) if kv.numel() else _ptr(plan.q_perm), _ptr(o), _ptr(tr.processed),
                            _ptr(tr.pass1_pairs), _ptr(tr.pass2_pairs), _ptr(ws),
                            C.c_size_t(ws.numel()), _stream()))
+    if check:
+        _pass_status(p, c, ws, False)
     return o, tr
 
 
+@_device_guard
 def attention_workspace_bytes(q, k, v, cfg: KernelConfig) -> int:
     p = _problem(q, k, v)
     c = cfg._c()
@@ -431,8 +474,12 @@ def attention_workspace_bytes(q, k, v, cfg: KernelConfig) -> int:
     return nbytes.value
 
 
-def s2o_attention(q, k, v, cfg: KernelConfig, out=None, want_plan: bool = True) -> S2oResult:
-    """s2o_attention (kernel.cpp:351-369): one C-ABI call (plan + passes) on the current stream."""
+@_device_guard
+def s2o_attention(q, k, v, cfg: KernelConfig, out=None, want_plan: bool = True, check: bool = True) -> S2oResult:
+    """s2o_attention (kernel.cpp:351-369): one C-ABI call (plan + passes) on the current stream of
+    q's device. check=True reads the device status word afterwards (one stream synchronisation)
+    and raises the reference's exception for an uninitialized state / uncovered row; check=False
+    keeps the call fully asynchronous (CUDA-graph capturable)."""
     torch = _torch()
     o = out if out is not None else _out_like(q, _default_out_dtype(q))
     p = _problem(q, k, v, o)
@@ -450,11 +497,14 @@ def s2o_attention(q, k, v, cfg: KernelConfig, out=None, want_plan: bool = True) 
     _check(lib().s2o_attention_fwd(C.byref(p), _ptr(q), _ptr(k), _ptr(v), C.byref(c), _ptr(o),
                                    _ptr(qp), _ptr(kv), _ptr(tr.processed), _ptr(tr.pass1_pairs),
                                    _ptr(tr.pass2_pairs), _ptr(ws), C.c_size_t(ws.numel()), _stream()))
+    if check:
+        _pass_status(p, c, ws, True)
     dots = p.l + seg.kv_per_head
     plan = PermutationPlan(p.z, p.hq, seg, qp, kv[:, :, : seg.kv_per_head] if kv is not None else None)
     return S2oResult(o, tr, plan, RankingCost(dots, dots))
 
 
+@_device_guard
 def dense_causal_attention(q, k, v, out_dtype: int = S2O_F32, path: int = PATH_AUTO):
     """Dense causal attention through the same pass-1 kernels with S = L."""
     torch = _torch()
@@ -469,6 +519,7 @@ def dense_causal_attention(q, k, v, out_dtype: int = S2O_F32, path: int = PATH_A
     return o
 
 
+@_device_guard
 def block_topk_attention(q, k, v, block_rows: int, block_cols: int, topk: int, out=None, path: int = PATH_AUTO):
     """block_topk_attention (baseline.hpp:28-36): the self block plus the `topk` prefix blocks of
     largest causal softmax mass per query block (exact fp64 ranking), masked softmax over them.
@@ -487,6 +538,7 @@ def block_topk_attention(q, k, v, block_rows: int, block_cols: int, topk: int, o
     return o, pairs
 
 
+@_device_guard
 def select_path(q, k, v, cfg: KernelConfig) -> int:
     p = _problem(q, k, v)
     c = cfg._c()

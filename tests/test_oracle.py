@@ -191,3 +191,38 @@ def test_visible_set_semantics(port):
             assert all(key <= i for key in sets[i])
             want = port.masked_softmax_row(q[0, 0, i], k[0, 0], v[0, 0], sets[i])
             np.testing.assert_allclose(out[0, 0, i], want, rtol=1e-5, atol=1e-6)
+
+
+@pytest.mark.parametrize("q_reorder,fused", [(True, False), (False, True)])
+def test_tile_gains_pin_the_stop_decision(oracles, q_reorder, fused):
+    """The P2 tie evidence (ref_tile_gains / orc_tile_gains): both backends give bit-identical gain
+    curves, and the curve reproduces the reference's own trace -- every committed chunk has gain
+    >= tau and the stop chunk has gain < tau (kernel.cpp:106-119, 220-234)."""
+    ref, port = oracles
+    if ref is None:
+        pytest.skip("reference .so unavailable")
+    from oracle.oracle import SegCfg, trace_ties
+    l, d, s, tau = 2048, 64, 512, 0.005
+    q, k, v = ref.generate_synthetic("mixed", l // 64, 8.0, 3, 1, 1, l, d)
+    cfg = Cfg(s, tau, 64, 64, q_reorder=q_reorder, fused=fused)
+    _, tr, plan = ref.attention(q, k, v, cfg)
+    seg = SegCfg.of(l, s)
+    stops = 0
+    for n in range(1, seg.seg_count):
+        kv = plan.kv_perm[0, seg.kv_offset(n): seg.kv_offset(n) + n * s]
+        for t in range(s // 64):
+            rows = plan.q_perm[0, n, t * 64:(t + 1) * 64] if q_reorder else np.arange(t * 64, (t + 1) * 64)
+            c = int(tr.processed[0, n, t])
+            g_ref = ref.tile_gains(q[0, 0], k[0, 0], v[0, 0], s, 64, rows, n, kv, c + 1)
+            g_port = port.tile_gains(q[0, 0], k[0, 0], v[0, 0], s, 64, rows, n, kv, c + 1)
+            np.testing.assert_array_equal(g_ref, g_port)
+            assert (g_ref[:c] >= tau).all()
+            if c < n * s // 64:
+                assert g_ref[c] < tau
+                stops += 1
+    assert stops > 0, "fixture never stops early"
+    # a perturbed trace is explained only by a real tie: here none is
+    bad = tr.processed.copy()
+    bad[0, 2, 1] += 1
+    ties = trace_ties(ref, q, k, v, cfg, plan.q_perm, plan.kv_perm, bad, tr.processed)
+    assert len(ties) == 1 and not ties[0]["tie"]
