@@ -37,6 +37,17 @@ def to_dev(torch, x):
 def check_outputs(got, want):
     err = np.abs(got - want)
     assert err.max() <= 2.5e-2 and err.mean() <= 2e-3, (float(err.max()), float(err.mean()))
+    return {"max_abs": float(err.max()), "mean_abs": float(err.mean())}
+
+
+def record(name: str, rec: dict) -> None:
+    """Evidence for profiles/ (set S2O_PARITY_OUT=dir): one JSON file per config."""
+    out = os.environ.get("S2O_PARITY_OUT")
+    if out:
+        import json
+        os.makedirs(out, exist_ok=True)
+        with open(os.path.join(out, f"parity_{name}.json"), "w") as f:
+            json.dump(rec, f, indent=1)
 
 
 def test_c2_full_plan_all_heads_and_one_group(cuda, port, ref):
@@ -62,7 +73,12 @@ def test_c2_full_plan_all_heads_and_one_group(cuda, port, ref):
     if not ties:
         np.testing.assert_array_equal(res.trace.pass2_pairs[0, :g].cpu().numpy(), want_t.pass2_pairs)
     np.testing.assert_array_equal(res.trace.pass1_pairs[0, :g].cpu().numpy(), want_t.pass1_pairs)
-    check_outputs(res.out[0, :g].float().cpu().numpy(), want_o[0])
+    errs = check_outputs(res.out[0, :g].float().cpu().numpy(), want_o[0])
+    record("c2", {"config": "C2 L=32768 32q/8kv S=2048 128x128 tau=0.005", "plan_heads_bit_identical": HQ,
+                  "trace_heads_vs_compiled_reference": list(range(g)), "trace_tiles": int(got_t.size),
+                  "trace_tiles_differing": len(ties), "ties": ties, "outputs": errs,
+                  "pass2_pairs": {"device": res.trace.pass2_pairs[0, :g].tolist(),
+                                  "reference": want_t.pass2_pairs.tolist()}})
     # the production entry (truncated top-T plan with levels) gives the same trace and outputs
     fast = s2o.s2o_attention(qd, kd, vd, cfg, want_plan=False)
     torch.cuda.synchronize()
@@ -97,8 +113,14 @@ def test_c3_full_depth_two_heads_vs_reference(cuda, port, ref):
     c = Cfg(S, 0.005, 128, 128)
     os.environ["S2O_THREADS"] = str(len(heads))
     want_o, want_t, want_p = ref.attention(qs, ks, vs, c)
-    assert_trace_ties(ref, qs, ks, vs, c, want_p.q_perm, want_p.kv_perm, got_t[heads], want_t.processed)
+    ties = assert_trace_ties(ref, qs, ks, vs, c, want_p.q_perm, want_p.kv_perm, got_t[heads], want_t.processed)
     np.testing.assert_array_equal(res.trace.pass1_pairs[0, heads].cpu().numpy(), want_t.pass1_pairs)
     if np.array_equal(got_t[heads], want_t.processed):
         np.testing.assert_array_equal(res.trace.pass2_pairs[0, heads].cpu().numpy(), want_t.pass2_pairs)
-    check_outputs(out[0, heads, ::8].cpu().numpy(), want_o[0, :, ::8])
+    errs = check_outputs(out[0, heads, ::8].cpu().numpy(), want_o[0, :, ::8])
+    record("c3", {"config": "C3 L=131072 32q/8kv S=2048 128x128 tau=0.005 (bench path: truncated plan + levels)",
+                  "plan_heads_bit_identical": [0, 1, 2, 3], "trace_heads_vs_compiled_reference": heads,
+                  "trace_tiles": int(got_t[heads].size), "trace_tiles_differing": len(ties), "ties": ties,
+                  "outputs_every_8th_row": errs,
+                  "pass2_pairs": {"device": res.trace.pass2_pairs[0, heads].tolist(),
+                                  "reference": want_t.pass2_pairs.tolist()}})
