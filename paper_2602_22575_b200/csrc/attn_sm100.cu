@@ -93,6 +93,10 @@ struct Ctrl {
     // (work_ctr) and every warp of the CTA takes them in order (item k in slot k & 3)
     uint64_t w_full[4], w_empty[4];
     int64_t wq[4];
+    // 2-CTA clusters: the PEER's stop decisions, written by the peer's MMA warp into this CTA
+    // (st.shared::cluster), indexed [pair sequence & 1][peer slot]: bits 31-17 sequence, bit 16
+    // stopped, bits 15-0 the stop block (stopped) or the number of blocks decided so far.
+    uint32_t pdec[2][2];
 };
 
 constexpr int kWarps = kThreads / 32;
@@ -145,30 +149,6 @@ struct TokRing {
     __device__ static int pos(int row) { return (row % STEP) * kRpt + row / STEP; }
 };
 
-// cp.async of one 16-B column chunk `ch` of rows r0, r0 + STEP, ... (< 128) of a 128-row tile into
-// the SWIZZLE_128B layout; byte offset tok * rbytes from bch.
-template <int STEP>
-__device__ __forceinline__ void gather_rows(uint32_t dst, const char* bch, uint32_t rbytes, const int32_t* ring,
-                                            int r0, uint32_t ch) {
-    using R = TokRing<STEP>;
-    const uint32_t xr = ch & 7u;
-    const int4* tv = reinterpret_cast<const int4*>(ring + r0 * R::kRpt);
-#pragma unroll
-    for (int q = 0; q < R::kRpt / 4; ++q) {
-        const int4 t4 = tv[q];
-        const int tt[4] = {t4.x, t4.y, t4.z, t4.w};
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-            const int i = 4 * q + e;
-            const int row = r0 + STEP * i;
-            if (STEP * (i + 1) <= kBM || row < kBM) {
-                const char* src = bch + (uint64_t)(uint32_t)tt[e] * rbytes;
-                sm100::cp_async16(dst + row * 128 + ((xr ^ ((uint32_t)row & 7u)) << 4), src, 16);
-            }
-        }
-    }
-}
-
 // Early-stop decision from the four per-warp votes (early_stop_check kernel.cpp:220-234: stop iff
 // max gain < tau, strictly, NaN gains dropped <=> continue iff some row has gain >= tau).
 __device__ __forceinline__ bool chunk_commit(const uint32_t* red) {
@@ -181,13 +161,36 @@ struct PairInfo {
     int64_t ti[2], t0[2], tn[2];
     int has[2];
     int nd[2], ndmax, np, nb;
+    int phas[2], pnd[2];  // the peer CTA's two tiles (2-CTA clusters; phas = 0 otherwise)
 };
 
-__device__ __forceinline__ PairInfo pair_info(const TcParams& p, int64_t idx) {
+// Work item `idx`: a pair of tiles (kCl = 1), or a quad of 4 tiles on a 2-CTA cluster (kCl = 2:
+// CTA `rank` owns tiles 4q + 2 rank + {0, 1}, the peer the other two; the K/V block stream is
+// the quad's).
+template <int kCl>
+__device__ __forceinline__ PairInfo pair_info(const TcParams& p, int64_t idx, uint32_t rank) {
     const PassArgs& a = p.a;
     const Geo& g = a.g;
     PairInfo P;
-    if (a.tile_list) {
+    P.phas[0] = P.phas[1] = 0;
+    P.pnd[0] = P.pnd[1] = 0;
+    int64_t pti[2] = {-1, -1};
+    if (kCl == 2) {
+        const int64_t G = g.group;
+        const int64_t zg = idx / (p.pairs_per_head * G);
+        const int64_t rem = idx % (p.pairs_per_head * G);
+        P.zh = zg * G + rem % G;
+        const int64_t r = rem / G;
+        const int64_t full = (g.N - 1) * p.pairs_full;
+        int64_t qi, tcount;
+        if (r < full) { P.n = r / p.pairs_full; qi = r % p.pairs_full; tcount = a.T; }
+        else { P.n = g.N - 1; qi = r - full; tcount = (g.last_len + kBM - 1) / kBM; }
+        for (int x = 0; x < 2; ++x) {
+            const int64_t mine = 4 * qi + 2 * rank + x, peer = 4 * qi + 2 * (1 - rank) + x;
+            P.ti[x] = mine < tcount ? mine : -1;
+            pti[x] = peer < tcount ? peer : -1;
+        }
+    } else if (a.tile_list) {
         const int64_t tile = a.tile_list[idx];
         P.zh = tile / a.tiles_per_head;
         const int64_t r = tile % a.tiles_per_head;
@@ -221,9 +224,20 @@ __device__ __forceinline__ PairInfo pair_info(const TcParams& p, int64_t idx) {
         P.nd[x] = (P.has[x] && (a.mode & kDiag)) ? (int)((P.t0[x] + P.tn[x] - 1) / kBN + 1) : 0;
         P.ndmax = max(P.ndmax, P.nd[x]);
     }
+    for (int x = 0; x < 2; ++x) {  // peer tiles (kCl = 2): participation in the shared stream
+        P.phas[x] = pti[x] >= 0;
+        if (P.phas[x] && (a.mode & kDiag)) {
+            const int64_t t0 = pti[x] * kBM, tn = min((int64_t)kBM, P.seg_rows - t0);
+            P.pnd[x] = (int)((t0 + tn - 1) / kBN + 1);
+            P.ndmax = max(P.ndmax, P.pnd[x]);
+        }
+    }
     P.np = ((a.mode & kPrefix) && P.n > 0) ? (int)((P.avail + kBN - 1) / kBN) : 0;
     P.nb = P.ndmax + P.np;
     return P;
+}
+__device__ __forceinline__ bool peer_participates(const PairInfo& P, int x, int j) {
+    return P.phas[x] && (j < P.ndmax ? j < P.pnd[x] : true);
 }
 
 __device__ __forceinline__ bool participates(const PairInfo& P, int x, int j) {
@@ -254,7 +268,39 @@ __device__ __forceinline__ int64_t key_token(const PairInfo& P, const int32_t* k
     return (int64_t)kv[c0 + (i < cn ? i : 0)];
 }
 
-template <bool kPackedExp>
+// Peer decision word (Ctrl::pdec) for one slot after block j of pair `seq` (kCl = 2).
+__device__ __forceinline__ uint32_t dec_word(uint32_t seq, bool stopped, int v) {
+    return ((seq & 0x7fffu) << 17) | (stopped ? 0x10000u : 0u) | ((uint32_t)v & 0xffffu);
+}
+// Has the peer's slot x stopped at a block <= b? Spins until the peer's MMA warp has published
+// decisions through block b (it publishes after every block; it is never more than a few blocks
+// behind, since both CTAs consume the same multicast K/V stages).
+__device__ __forceinline__ bool peer_stopped_by(const Ctrl& c, const PairInfo& P, uint32_t seq, int x, int b) {
+    if (b < P.ndmax) return false;  // diagonal blocks always commit
+    const uint32_t addr = smem_u32(&c.pdec[seq & 1][x]);
+    uint32_t spins = 0;
+    for (;;) {
+        const uint32_t w = ld_volatile_u32(addr);
+        if ((w >> 17) == (seq & 0x7fffu)) {
+            const int v = (int)(w & 0xffffu);
+            if (w & 0x10000u) return v <= b;
+            if (v > b) return false;
+        }
+        if (++spins == (1u << 26)) {
+            printf("s2o watchdog: block %d thread %d peer decision seq %u slot %d block %d word %08x\n",
+                   (int)blockIdx.x, (int)threadIdx.x, seq, x, b, w);
+            __trap();
+        }
+    }
+}
+
+// kCl = 1: one CTA per pair of tiles. kCl = 2: 2-CTA clusters, one CTA per half of a quad of tiles
+// of the same (head, segment); each CTA gathers one 64-column half of every K/V block and
+// multicasts it to both, so every gathered block is fetched once for four tiles (half the TMA
+// ops and L2 reads per SM of kCl = 1). A stage is released when BOTH MMA warps are done with it
+// (multicast commits, empty barriers of count 2); the block stream runs while any of the four
+// tiles needs it, so each MMA warp publishes its slots' stop decisions into the peer (pdec).
+template <bool kPackedExp, int kCl>
 __global__ void __launch_bounds__(kThreads, 1)
 tc_pass_kernel(const TcParams p, const __grid_constant__ CUtensorMap qmap,
                const __grid_constant__ CUtensorMap kmap, const __grid_constant__ CUtensorMap vmap,
@@ -279,12 +325,13 @@ tc_pass_kernel(const TcParams p, const __grid_constant__ CUtensorMap qmap,
         mbar_init(smem_u32(&c.q_empty), 1);
         for (int s = 0; s < kKStages; ++s) {
             mbar_init(smem_u32(&c.k_full[s]), kKThreads);
-            mbar_init(smem_u32(&c.k_empty[s]), 1);
+            mbar_init(smem_u32(&c.k_empty[s]), kCl);  // one release per CTA of the cluster
         }
         for (int s = 0; s < kVStages; ++s) {
             mbar_init(smem_u32(&c.v_full[s]), kVThreads);
-            mbar_init(smem_u32(&c.v_empty[s]), 1);
+            mbar_init(smem_u32(&c.v_empty[s]), kCl);
         }
+        for (int i = 0; i < 4; ++i) (&c.pdec[0][0])[i] = 0xffffffffu;
         for (int x = 0; x < 2; ++x) {
             mbar_init(smem_u32(&c.s_full[x]), 1);
             mbar_init(smem_u32(&c.p_full[x]), 4);
@@ -302,20 +349,33 @@ tc_pass_kernel(const TcParams p, const __grid_constant__ CUtensorMap qmap,
     }
     tc_fence_before();
     __syncthreads();
+    if (kCl == 2) cluster_sync();  // the peer's barriers are initialised before any multicast
     tc_fence_after();
     const uint32_t tbase = c.tmem_base;
     if (threadIdx.x == 0) tl_cta(p, 0);
     const int64_t total = a.tile_list ? a.tile_count : g.z * g.hq * p.pairs_per_head;
+    const uint32_t rank = kCl == 2 ? cluster_rank() : 0u;
+    const uint32_t peer = rank ^ 1u;
+    // kCl = 2: clusters take quads statically (cluster c: c, c + #clusters, ...); every warp of
+    // both CTAs walks the same sequence
+    const int64_t ncl = gridDim.x / kCl, cid = blockIdx.x / kCl;
+    auto next_item = [&](uint32_t wk) -> int64_t {
+        if (kCl == 2) {
+            const int64_t it = cid + (int64_t)wk * ncl;
+            return it < total ? it : -1;
+        }
+        return ring_get(c, wk, lane);
+    };
     const int64_t rowu = g.d;  // row unit of the tensor maps = D elements
 
     if (warp >= kMmaWarp) setmaxnreg_dec<kOtherRegs>();  // warpgroups 2-3
     if (warp >= kKWarp0) {
         // ============================== loaders ==============================
         // Two independent groups: K (+ Q) and V, so K(j+1) never waits behind V(j)'s gating.
-        // Gathered rows (permuted Q rows, ranked prefix keys) move with 16-byte cp.async into
-        // the SWIZZLE_128B layout: a thread owns one 16-B column chunk and a fixed row stride,
-        // so a warp instruction moves 2 rows x 256 B with no per-lane TMA issue loop.
-        // Contiguous 128-row blocks move with one 2-D TMA tile per 64-column half.
+        // Gathered rows (permuted Q rows, ranked prefix keys) move with TMA tile::gather4 (4 rows
+        // x one 64-column half per op) into the SWIZZLE_128B layout; contiguous 128-row blocks
+        // with one 2-D TMA tile per 64-column half. Tokens of the next block wait in a shared
+        // ring, one block ahead.
         const bool kgrp = warp < kVWarp0;
         const int nthr = kgrp ? kKThreads : kVThreads;
         const int lt = (warp - (kgrp ? kKWarp0 : kVWarp0)) * 32 + lane;
@@ -324,16 +384,6 @@ tc_pass_kernel(const TcParams p, const __grid_constant__ CUtensorMap qmap,
         const int ring_sz = kgrp ? TokRing<kKStep>::kSize : TokRing<kVStep>::kSize;
         int32_t* ring0 = reinterpret_cast<int32_t*>(smem + kOffTok) + (kgrp ? 0 : 2 * TokRing<kKStep>::kSize);
         auto ring_pos = [&](int row) { return kgrp ? TokRing<kKStep>::pos(row) : TokRing<kVStep>::pos(row); };
-        const int ch = lt & 15, r0 = lt >> 4;  // rows r0, r0 + nthr/16, ...
-        const uint32_t ch_off = (uint32_t)(ch >> 3) * kHalf;
-        auto gather_tile = [&](uint32_t dst, const __nv_bfloat16* base, int64_t rstride, const int32_t* tok) {
-            const char* bch = reinterpret_cast<const char*>(base) + ch * 16;
-            const uint32_t rbytes = (uint32_t)(rstride * 2);
-            if (kgrp) gather_rows<kKStep>(dst + ch_off, bch, rbytes, tok, r0, (uint32_t)ch);
-            else gather_rows<kVStep>(dst + ch_off, bch, rbytes, tok, r0, (uint32_t)ch);
-        };
-        const __nv_bfloat16* qg = reinterpret_cast<const __nv_bfloat16*>(a.q);
-        const __nv_bfloat16* xg = reinterpret_cast<const __nv_bfloat16*>(kgrp ? a.k : a.v);
         const CUtensorMap* xtile = kgrp ? &ktile : &vtile;
         const uint32_t xbase = kgrp ? sK : sV;
         const int nst = kgrp ? kKStages : kVStages;
@@ -342,41 +392,42 @@ tc_pass_kernel(const TcParams p, const __grid_constant__ CUtensorMap qmap,
         uint64_t* xempty = kgrp ? c.k_empty : c.v_empty;
         uint32_t gx = 0, qcount = 0;
         for (uint32_t wk = 0;; ++wk) {
-            if (kgrp && lt == 0) {  // producer: the next pair index (or -1) into ring slot wk & 3
+            if (kCl == 1 && kgrp && lt == 0) {  // producer: the next pair index (or -1) into ring slot wk & 3
                 mbar_wait(smem_u32(&c.w_empty[wk & 3]), ((wk >> 2) & 1) ^ 1, 5002);
                 const int64_t v = (int64_t)atomicAdd(a.work_ctr, 1);
                 *reinterpret_cast<volatile int64_t*>(&c.wq[wk & 3]) = v < total ? v : -1;
                 mbar_arrive(smem_u32(&c.w_full[wk & 3]));
             }
-            const int64_t it = ring_get(c, wk, lane);
+            const int64_t it = next_item(wk);
             if (it < 0) break;
-            const PairInfo P = pair_info(p, it);
+            const PairInfo P = pair_info<kCl>(p, it, rank);
             if (P.nb == 0) continue;
             const int32_t* kv = (P.np > 0) ? a.kv_seg(P.zh, P.n) : nullptr;
             named_bar_sync(gbar, nthr);  // every thread of the group is done with its ring
             if (kgrp && lt == 0) tl_mark(p, 30, qcount);
             if (kgrp) {
-                // ---- Q (both slots)
+                // ---- Q (this CTA's slots; no multicast)
                 mbar_wait(smem_u32(&c.q_empty), (qcount & 1) ^ 1, 1001);
                 const int64_t qb = g.q_base(P.zh) / rowu, qs = g.qs[2] / rowu;
-                const bool q_tile = p.q_contig && !((a.mode & kStateIn) && a.q_reorder) && P.tn[0] == kBM &&
-                                    (!P.has[1] || P.tn[1] == kBM);
+                const uint32_t qbytes = (uint32_t)(P.has[0] + P.has[1]) * kTileBytes;
+                const bool q_tile = p.q_contig && !((a.mode & kStateIn) && a.q_reorder) &&
+                                    (!P.has[0] || P.tn[0] == kBM) && (!P.has[1] || P.tn[1] == kBM);
+                if (lt == 0) {
+                    if (qbytes) mbar_expect_tx(smem_u32(&c.q_full), qbytes);
+                    else mbar_arrive(smem_u32(&c.q_full));
+                } else {
+                    mbar_arrive(smem_u32(&c.q_full));
+                }
                 if (q_tile) {
-                    if (lt == 0) {
-                        mbar_expect_tx(smem_u32(&c.q_full), (P.has[1] ? 2 : 1) * kTileBytes);
+                    if (lt == 0)
                         for (int x = 0; x < 2; ++x)
                             if (P.has[x])
                                 for (int h = 0; h < 2; ++h)
                                     tma_load2d(sQ + x * kTileBytes + h * kHalf, &qtile, h * 64,
                                                (int32_t)(qb + (P.sb + P.t0[x]) * qs), smem_u32(&c.q_full));
-                    } else {
-                        mbar_arrive(smem_u32(&c.q_full));
-                    }
                 } else {
-#ifndef S2O_QGATHER_CPASYNC  // A/B: TMA gather4 for permuted Q rows, pass-2 6.03 -> 5.90 ms
-                    // one gather4 op per lane: (slot, row group, column half) = lt >> 6, ...
-                    if (lt == 0) mbar_expect_tx(smem_u32(&c.q_full), (P.has[1] ? 2 : 1) * kTileBytes);
-                    else mbar_arrive(smem_u32(&c.q_full));
+                    // permuted Q rows: one TMA gather4 op per lane, (slot, row group, column half)
+                    // (A/B against 16-B cp.async: pass-2 6.03 -> 5.90 ms)
                     const int x = lt >> 6, grp = (lt >> 1) & 31, h = lt & 1;
                     if (P.has[x]) {
                         int32_t rr[4];
@@ -384,17 +435,6 @@ tc_pass_kernel(const TcParams p, const __grid_constant__ CUtensorMap qmap,
                         tma_gather4(sQ + x * kTileBytes + h * kHalf + grp * 512, &qmap, h * 64, rr[0], rr[1], rr[2],
                                     rr[3], smem_u32(&c.q_full));
                     }
-#else
-                    for (int e = lt; e < 2 * kBM; e += nthr) {
-                        const int x = e >> 7;
-                        ring0[x * kBM + ring_pos(e & 127)] = P.has[x] ? (int32_t)(qb + q_row(a, P, x, e & 127) * qs) : 0;
-                    }
-                    named_bar_sync(gbar, nthr);
-                    for (int x = 0; x < 2; ++x)
-                        if (P.has[x]) gather_tile(sQ + x * kTileBytes, qg, kD, ring0 + x * kBM);
-                    cp_async_arrive_noinc(smem_u32(&c.q_full));
-                    named_bar_sync(gbar, nthr);  // ring reusable
-#endif
                 }
                 if (lt == 0) tl_mark(p, 29, qcount);
                 ++qcount;
@@ -436,34 +476,42 @@ tc_pass_kernel(const TcParams p, const __grid_constant__ CUtensorMap qmap,
                 }
                 bool need = false;
                 for (int x = 0; x < 2; ++x) need |= participates(P, x, j) && !(stop_at[x] <= j - lag);
+                if (kCl == 2)  // the quad's stream: the peer's tiles count too (same answer in both CTAs)
+                    for (int x = 0; x < 2 && !need; ++x)
+                        need |= peer_participates(P, x, j) && !peer_stopped_by(c, P, wk, x, j - lag);
                 if (!need) break;
                 const uint32_t dst = xbase + st * kTileBytes;
-#ifdef S2O_NOLOAD  // dev timing aid: no K/V data movement (results are garbage)
-                mbar_arrive(smem_u32(&xfull[st]));
-                ++nx;
-                continue;
-#endif
-                if (!gat) {
+                if (lt == 0) mbar_expect_tx(smem_u32(&xfull[st]), kTileBytes);
+                else mbar_arrive(smem_u32(&xfull[st]));
+                if (kCl == 2) {
+                    // this CTA's 64-column half of the block, multicast to both CTAs
+                    const int h = (int)rank;
+                    if (!gat) {
+                        if (lt == 0)
+                            tma_load2d_mc(dst + h * kHalf, xtile, h * 64,
+                                          (int32_t)(xb + (P.sb + (int64_t)j * kBN) * xs), smem_u32(&xfull[st]), 3);
+                    } else {
+                        // 32 gather4 ops (row groups) on lanes 0-7 (K) / 0-10 (V) of the group's warps
+                        const int wl = lt & 31, wi = lt >> 5;
+                        const int per = kgrp ? 8 : 11;
+                        const int grp = wl < per ? wi * per + wl : 32;
+                        if (grp < 32) {
+                            int32_t rr[4];
+                            for (int i = 0; i < 4; ++i) rr[i] = (int32_t)(xb + (int64_t)ring[ring_pos(4 * grp + i)] * xs);
+                            tma_gather4_mc(dst + h * kHalf + grp * 512, kgrp ? &kmap : &vmap, h * 64, rr[0], rr[1], rr[2],
+                                           rr[3], smem_u32(&xfull[st]), 3);
+                        }
+                    }
+                } else if (!gat) {
                     if (lt == 0) {
-                        mbar_expect_tx(smem_u32(&xfull[st]), kTileBytes);
                         const int64_t tok = P.sb + (int64_t)j * kBN;
                         for (int h = 0; h < 2; ++h)
                             tma_load2d(dst + h * kHalf, xtile, h * 64, (int32_t)(xb + tok * xs), smem_u32(&xfull[st]));
-                    } else {
-                        mbar_arrive(smem_u32(&xfull[st]));
                     }
                 } else {
-#ifndef S2O_GATHER_CPASYNC
-                    const bool use_tma = true;
-#else
-                    const bool use_tma = false;
-#endif
-                    if (use_tma) {
-                    // TMA tile::gather4 (A/B: 9 % faster pass-2 than 16-B cp.async here, which
-                    // competes with the tensor core for the LSU/shared-memory path): 64 ops (32 row
-                    // groups x 2 column halves) on lanes 0-15 (K) / 0-21 (V) of the group's warps
-                    if (lt == 0) mbar_expect_tx(smem_u32(&xfull[st]), kTileBytes);
-                    else mbar_arrive(smem_u32(&xfull[st]));
+                    // TMA tile::gather4 (A/B: 9 % faster pass-2 than 16-B cp.async, which competes with
+                    // the tensor core for the LSU/shared-memory path): 64 ops (32 row groups x 2 column
+                    // halves) on lanes 0-15 (K) / 0-21 (V) of the group's warps
                     const int wl = lt & 31, wi = lt >> 5;
                     const int per = kgrp ? 16 : 22;
                     const int opi = wl < per ? wi * per + wl : 64;
@@ -473,10 +521,6 @@ tc_pass_kernel(const TcParams p, const __grid_constant__ CUtensorMap qmap,
                         for (int i = 0; i < 4; ++i) rr[i] = (int32_t)(xb + (int64_t)ring[ring_pos(4 * grp + i)] * xs);
                         tma_gather4(dst + h * kHalf + grp * 512, kgrp ? &kmap : &vmap, h * 64, rr[0], rr[1], rr[2],
                                     rr[3], smem_u32(&xfull[st]));
-                    }
-                    } else {
-                    gather_tile(dst, xg + xb * kD, xs * kD, ring);
-                    cp_async_arrive_noinc(smem_u32(&xfull[st]));
                     }
                 }
                 if (lt == 0) tl_mark(p, kgrp ? 10 : 2, gi);
@@ -520,10 +564,11 @@ tc_pass_kernel(const TcParams p, const __grid_constant__ CUtensorMap qmap,
                 fence_proxy_async_smem();  // cp.async (generic proxy) writes -> UMMA reads
                 tc_fence_after();
             };
+            const uint32_t pdec_peer = kCl == 2 ? mapa(smem_u32(&c.pdec[0][0]), peer) : 0u;
             for (uint32_t wk = 0;; ++wk) {
-                const int64_t it = ring_get(c, wk, lane);
+                const int64_t it = next_item(wk);
                 if (it < 0) break;
-                const PairInfo P = pair_info(p, it);
+                const PairInfo P = pair_info<kCl>(p, it, rank);
                 if (P.nb == 0) continue;
                 mbar_wait(smem_u32(&c.q_full), qcount & 1, 2001);
                 tl_mark(p, 26, qcount);
@@ -534,6 +579,9 @@ tc_pass_kernel(const TcParams p, const __grid_constant__ CUtensorMap qmap,
                 auto need = [&](int j, int lag) {
                     bool n = false;
                     for (int x = 0; x < 2; ++x) n |= participates(P, x, j) && !(stop_at[x] <= j - lag);
+                    if (kCl == 2)  // the quad's stream (the loaders evaluate the same union)
+                        for (int x = 0; x < 2 && !n; ++x)
+                            n |= peer_participates(P, x, j) && !peer_stopped_by(c, P, wk, x, j - lag);
                     return n;
                 };
                 wait_k(gk);
@@ -588,10 +636,20 @@ tc_pass_kernel(const TcParams p, const __grid_constant__ CUtensorMap qmap,
                         }
                     }
                     if (has_v && !v_ready) mbar_wait(smem_u32(&c.v_full[gvi % kVStages]), (gvi / kVStages) & 1, 2006);
+                    if (kCl == 2 && leader)  // this CTA's decisions through block j, into the peer
+                        for (int x = 0; x < 2; ++x)
+                            st_cluster_u32(pdec_peer + (uint32_t)(((wk & 1) * 2 + x) * 4),
+                                           stop_at[x] <= j ? dec_word(wk, true, stop_at[x]) : dec_word(wk, false, j + 1));
                     // both slots' decisions on block j are read: the loader may reuse its stages
+                    // (kCl = 2: in both CTAs -- each stage holds halves loaded by both)
                     if (leader) {
-                        umma_commit(smem_u32(&c.k_empty[gki % kKStages]));
-                        if (has_v) umma_commit(smem_u32(&c.v_empty[gvi % kVStages]));
+                        if (kCl == 2) {
+                            umma_commit_mc(smem_u32(&c.k_empty[gki % kKStages]), 3);
+                            if (has_v) umma_commit_mc(smem_u32(&c.v_empty[gvi % kVStages]), 3);
+                        } else {
+                            umma_commit(smem_u32(&c.k_empty[gki % kKStages]));
+                            if (has_v) umma_commit(smem_u32(&c.v_empty[gvi % kVStages]));
+                        }
                     }
                     tl_mark(p, 8, gki);
                     ++nk;
@@ -617,7 +675,7 @@ tc_pass_kernel(const TcParams p, const __grid_constant__ CUtensorMap qmap,
         const float sc = p.scale_log2;
         uint32_t ns = 0, no = 0, npf = 0;
         for (uint32_t wk = 0;; ++wk) {
-            const int64_t it = ring_get(c, wk, lane);
+            const int64_t it = next_item(wk);
             if (it < 0) break;
             float m2, ell;
             float sacc = 1.0f;    // scale of the resumed accumulator (kStateIn)
@@ -627,7 +685,7 @@ tc_pass_kernel(const TcParams p, const __grid_constant__ CUtensorMap qmap,
             const bool tl_on = r == 0;
             {
             // 32-bit copies of what the block loop needs (keeps the 128 scores in registers)
-            const PairInfo P = pair_info(p, it);
+            const PairInfo P = pair_info<kCl>(p, it, rank);
             if (!P.has[x]) continue;
             if (tl_on) tl_mark(p, 11 + 4 * x, no);
             const int nd_x = P.nd[x], ndmax = P.ndmax, nb = P.nb;
@@ -816,7 +874,7 @@ tc_pass_kernel(const TcParams p, const __grid_constant__ CUtensorMap qmap,
                 if (!commit) break;
             }
             }  // block loop scope
-            const PairInfo P = pair_info(p, it);
+            const PairInfo P = pair_info<kCl>(p, it, rank);
             const bool valid = r < P.tn[x];
             const int64_t grow = q_row(a, P, x, r);
             const int64_t slot = P.zh * g.l + grow;
@@ -938,6 +996,7 @@ tc_pass_kernel(const TcParams p, const __grid_constant__ CUtensorMap qmap,
     }
     tc_fence_before();
     __syncthreads();
+    if (kCl == 2) cluster_sync();  // no CTA leaves while its peer may still multicast into it
     if (threadIdx.x == 0) tl_cta(p, 3);
     if (warp == 0) tmem_dealloc(tbase, kTmemCols);
 }
@@ -1418,665 +1477,6 @@ tc_diag_kernel(const TcParams p, const __grid_constant__ CUtensorMap qtile,
     }
 }
 
-// ============================================================== CTA-pair kernel
-// The same operator on CTA pairs (cluster of 2, tcgen05 cta_group::2). The work unit is a QUAD
-// of 128-row query tiles of one (head, segment): slot x of the pair is the 256-row M tile made
-// of tile 4q+2x (CTA 0) and tile 4q+2x+1 (CTA 1). Each CTA keeps its own 128 rows of Q, S, P
-// and O; the K/V operand of a 128-key block is split across the pair (S = Q K^T: CTA r holds
-// keys [64r, 64r+64); O += P V: CTA r holds head dims [64r, 64r+64)), so every SM gathers half
-// of each block and four tiles share it. Loads are TMA (tile / tile::gather4) with cta_group::2
-// completion on the leader's barriers; only the leader's MMA warp issues MMAs; commits
-// multicast to both CTAs. Each tile still stops on its own (reference semantics per 128-row
-// tile): a stopped tile writes P = 0 for the rest of its slot's stream (its O and state stay
-// frozen) until the slot's other tile stops too.
-constexpr int kK2Stages = 4;                 // K: block j loads once decisions <= j-4 are known
-constexpr int kV2Stages = 3;                 // V: decisions <= j-3
-constexpr uint32_t kKHalf2 = 64u * 128u;     // 8 KB: 64 keys x one 64-column half
-constexpr uint32_t kKStage2 = 2 * kKHalf2;   // 16 KB: this CTA's 64 keys x 128 dims
-constexpr uint32_t kVStage2 = kHalf;         // 16 KB: 128 keys x this CTA's 64 dims
-constexpr uint32_t k2OffK = 2 * kTileBytes;
-constexpr uint32_t k2OffV = k2OffK + kK2Stages * kKStage2;
-constexpr uint32_t k2OffCtrl = k2OffV + kV2Stages * kVStage2;
-constexpr uint32_t k2SmemBytes = k2OffCtrl + 512;
-
-struct Ctrl2 {
-    uint64_t q_full, q_empty;
-    uint64_t k_full[kK2Stages], k_empty[kK2Stages], v_full[kV2Stages], v_empty[kV2Stages];
-    uint64_t s_full[2], p_full[2], o_done[2], d_full[2];
-    uint32_t tmem_base;
-    uint32_t red[2][2][8];  // continue votes [slot][block parity][cta * 4 + warp]
-    uint8_t dec[2][4];      // slot decision ring (block j -> j & 3): 1 = commit, 2 = stop
-};
-static_assert(sizeof(Ctrl2) <= 512, "Ctrl2 exceeds its 512 B");
-
-// Timeline for the pair kernel: CTA 0 (leader) events ev, CTA 1 (peer) events ev + 16.
-__device__ __forceinline__ void tl2_mark(const TcParams& p, int ev, uint32_t seq) {
-#ifdef S2O_TIMELINE
-    if (p.tl != nullptr && blockIdx.x < 2 && seq < (uint32_t)kTlCap)
-        p.tl[(ev + 16 * blockIdx.x) * kTlCap + seq] = clock64();
-#endif
-}
-
-struct QuadInfo {
-    int64_t zh, n, sb, seg_rows, avail;
-    int64_t ti[2], t0[2], tn[2];  // this CTA's tile of slot x
-    int has[2];                   // this CTA has a tile in slot x
-    int slot_has[2];              // slot x has a tile (CTA 0's always exists first)
-    int ndt[2];                   // causal blocks of this CTA's tile
-    int nds[2];                   // causal blocks of slot x (its larger tile)
-    int ndmax, np, nb;
-};
-
-__device__ __forceinline__ QuadInfo quad_info(const TcParams& p, int64_t idx, int rank) {
-    const PassArgs& a = p.a;
-    const Geo& g = a.g;
-    QuadInfo Q;
-    const int64_t G = g.group;  // q heads of a GQA group interleaved (as pair_info)
-    const int64_t zg = idx / (p.pairs_per_head * G);
-    const int64_t rem = idx % (p.pairs_per_head * G);
-    Q.zh = zg * G + rem % G;
-    const int64_t r = rem / G;
-    const int64_t full = (g.N - 1) * p.pairs_full;
-    int64_t qi, tcount;
-    if (r < full) { Q.n = r / p.pairs_full; qi = r % p.pairs_full; tcount = a.T; }
-    else { Q.n = g.N - 1; qi = r - full; tcount = (g.last_len + kBM - 1) / kBM; }
-    Q.sb = Q.n * g.S;
-    Q.seg_rows = g.seg_rows(Q.n);
-    Q.avail = a.avail(Q.n);
-    auto nd_of = [&](int64_t t) -> int {
-        if (t >= tcount || !(a.mode & kDiag)) return 0;
-        const int64_t t0 = t * kBM, tn = min((int64_t)kBM, Q.seg_rows - t0);
-        return (int)((t0 + tn - 1) / kBN + 1);
-    };
-    Q.ndmax = 0;
-    for (int x = 0; x < 2; ++x) {
-        const int64_t base = 4 * qi + 2 * x;
-        Q.slot_has[x] = base < tcount;
-        const int64_t t = base + rank;
-        Q.has[x] = t < tcount;
-        Q.ti[x] = Q.has[x] ? t : -1;
-        Q.t0[x] = Q.has[x] ? t * kBM : 0;
-        Q.tn[x] = Q.has[x] ? min((int64_t)kBM, Q.seg_rows - Q.t0[x]) : 0;
-        Q.ndt[x] = nd_of(t);
-        Q.nds[x] = max(nd_of(base), nd_of(base + 1));
-        Q.ndmax = max(Q.ndmax, Q.nds[x]);
-    }
-    Q.np = ((a.mode & kPrefix) && Q.n > 0) ? (int)((Q.avail + kBN - 1) / kBN) : 0;
-    Q.nb = Q.ndmax + Q.np;
-    return Q;
-}
-__device__ __forceinline__ bool participates2(const QuadInfo& Q, int x, int j) {
-    return Q.slot_has[x] && (j < Q.ndmax ? j < Q.nds[x] : true);
-}
-__device__ __forceinline__ int last_block2(const QuadInfo& Q, int x) {
-    return Q.np > 0 ? Q.nb - 1 : Q.nds[x] - 1;
-}
-__device__ __forceinline__ int64_t q_row2(const PassArgs& a, const QuadInfo& Q, int x, int64_t r) {
-    if (r >= Q.tn[x]) r = 0;
-    const int64_t local = ((a.mode & kStateIn) && a.q_reorder)
-                              ? (int64_t)a.q_perm[(Q.zh * a.g.N + Q.n) * a.g.S + Q.t0[x] + r]
-                              : Q.t0[x] + r;
-    return Q.sb + local;
-}
-__device__ __forceinline__ int64_t key_token2(const QuadInfo& Q, const int32_t* kv, int j, int i) {
-    if (j < Q.ndmax) {
-        const int64_t k0 = (int64_t)j * kBN;
-        const int64_t kn = min((int64_t)kBN, Q.seg_rows - k0);
-        return Q.sb + k0 + (i < kn ? i : 0);
-    }
-    const int64_t c0 = (int64_t)(j - Q.ndmax) * kBN;
-    const int64_t cn = min((int64_t)kBN, Q.avail - c0);
-    return (int64_t)kv[c0 + (i < cn ? i : 0)];
-}
-
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
-tc_pass2cta_kernel(const TcParams p, const __grid_constant__ CUtensorMap qmap,
-                   const __grid_constant__ CUtensorMap kmap, const __grid_constant__ CUtensorMap vmap,
-                   const __grid_constant__ CUtensorMap qtile, const __grid_constant__ CUtensorMap ktile64,
-                   const __grid_constant__ CUtensorMap vtile) {
-    extern __shared__ __align__(1024) unsigned char smem_raw[];
-    unsigned char* smem = smem_raw;
-    if ((smem_u32(smem) & 1023u) != 0) __trap();
-    Ctrl2& c = *reinterpret_cast<Ctrl2*>(smem + k2OffCtrl);
-    const PassArgs& a = p.a;
-    const Geo& g = a.g;
-    const int warp = threadIdx.x / 32;
-    const int lane = threadIdx.x % 32;
-    const int rank = (int)cluster_rank();
-    const uint32_t sQ = smem_u32(smem + kOffQ);
-    const uint32_t sK = smem_u32(smem + k2OffK);
-    const uint32_t sV = smem_u32(smem + k2OffV);
-    auto lead = [&](const void* obj) { return mapa(smem_u32(obj), 0); };  // leader CTA's copy
-    auto peer = [&](const void* obj) { return mapa(smem_u32(obj), 1); };
-
-    if (threadIdx.x == 0) {
-        mbar_init(smem_u32(&c.q_full), 2);  // one expect_tx arrive per CTA (+ bytes)
-        mbar_init(smem_u32(&c.q_empty), 1);
-        for (int s = 0; s < kK2Stages; ++s) {
-            mbar_init(smem_u32(&c.k_full[s]), 2);
-            mbar_init(smem_u32(&c.k_empty[s]), 1);
-        }
-        for (int s = 0; s < kV2Stages; ++s) {
-            mbar_init(smem_u32(&c.v_full[s]), 2);
-            mbar_init(smem_u32(&c.v_empty[s]), 1);
-        }
-        for (int x = 0; x < 2; ++x) {
-            mbar_init(smem_u32(&c.s_full[x]), 1);
-            mbar_init(smem_u32(&c.p_full[x]), 8);  // 4 softmax warps of each CTA
-            mbar_init(smem_u32(&c.o_done[x]), 1);
-            mbar_init(smem_u32(&c.d_full[x]), 1);
-        }
-        fence_mbar_init();
-    }
-    if (warp == 0) {
-        tmem_alloc_2cta(smem_u32(&c.tmem_base), kTmemCols);
-        tmem_relinquish_2cta();
-    }
-    tc_fence_before();
-    cluster_sync();
-    tc_fence_after();
-    const uint32_t tbase = c.tmem_base;
-    const int64_t total = g.z * g.hq * p.pairs_per_head;  // quads
-    const int64_t clusters = gridDim.x / 2;
-    const int64_t cid = blockIdx.x / 2;
-    const int64_t rowu = g.d;
-
-    if (warp >= kMmaWarp) setmaxnreg_dec<kOtherRegs>();
-    if (warp >= kKWarp0) {
-        // ============================== loaders (both CTAs) ==============================
-        const bool kgrp = warp < kVWarp0;
-        const int lt = (warp - (kgrp ? kKWarp0 : kVWarp0)) * 32 + lane;
-        const int wl = lt & 31, wi = lt >> 5;
-        // gather4 ops per block: K: 32 (16 row groups x 2 halves of this CTA's 64 keys) on
-        // lanes 0-7 of the 4 K warps; V: 32 (32 row groups of this CTA's 64 dims) on lanes
-        // 0-10 of the 3 V warps. Q (K group): 64 per tile of this CTA, one per lane.
-        const int op = kgrp ? (wl < 8 ? wi * 8 + wl : -1) : (wl < 11 && wi * 11 + wl < 32 ? wi * 11 + wl : -1);
-        const int nst = kgrp ? kK2Stages : kV2Stages;
-        const int lag = nst;
-        uint64_t* xfull = kgrp ? c.k_full : c.v_full;
-        uint64_t* xempty = kgrp ? c.k_empty : c.v_empty;
-        const uint32_t stage_bytes = kgrp ? kKStage2 : kVStage2;
-        const uint32_t xbase = kgrp ? sK : sV;
-        const CUtensorMap* xmap = kgrp ? &kmap : &vmap;
-        uint32_t gx = 0, qcount = 0;
-        for (int64_t it = cid; it < total; it += clusters) {
-            const QuadInfo Q = quad_info(p, it, rank);
-            if (Q.nb == 0) continue;
-            const int32_t* kv = (Q.np > 0) ? a.kv_seg(Q.zh, Q.n) : nullptr;
-            if (kgrp) {
-                // ---- Q: this CTA's tile of each slot
-                mbar_wait(smem_u32(&c.q_empty), (qcount & 1) ^ 1, 1101);
-                const int64_t qb = g.q_base(Q.zh) / rowu, qs = g.qs[2] / rowu;
-                const bool q_tile = p.q_contig && !((a.mode & kStateIn) && a.q_reorder);
-                uint32_t qbytes = 0;
-                for (int x = 0; x < 2; ++x) qbytes += Q.has[x] ? kTileBytes : 0;
-                if (lt == 0) mbar_expect_tx_cluster(lead(&c.q_full), qbytes);
-                named_bar_sync(3, kKThreads);
-                for (int x = 0; x < 2; ++x) {
-                    if (!Q.has[x]) continue;
-                    const uint32_t qdst = sQ + x * kTileBytes;
-                    if (q_tile && Q.tn[x] == kBM) {
-                        if (lt < 2)
-                            tma_load2d_2cta(qdst + lt * kHalf, &qtile, lt * 64, (int32_t)(qb + (Q.sb + Q.t0[x]) * qs),
-                                            lead(&c.q_full));
-                    } else if (lt < 64) {
-                        const int grp = lt >> 1, h = lt & 1;
-                        int32_t rows[4];
-                        for (int i = 0; i < 4; ++i) rows[i] = (int32_t)(qb + q_row2(a, Q, x, grp * 4 + i) * qs);
-                        tma_gather4_2cta(qdst + h * kHalf + grp * 512, &qmap, h * 64, rows[0], rows[1], rows[2],
-                                         rows[3], lead(&c.q_full));
-                    }
-                }
-                ++qcount;
-            }
-            const int64_t xb = (kgrp ? g.k_base(Q.zh) : g.v_base(Q.zh)) / rowu;
-            const int64_t xs = (kgrp ? g.ks[2] : g.vs[2]) / rowu;
-            const bool kv_contig = p.kv_contig;
-            // rows of this lane's op in block j (K: keys 64*rank + 4*(op>>1) + i; V: keys 4*op + i)
-            auto op_rows = [&](int j, int32_t (&rr)[4]) {
-                for (int i = 0; i < 4; ++i) {
-                    const int key = kgrp ? 64 * rank + 4 * (op >> 1) + i : 4 * op + i;
-                    rr[i] = (op >= 0 && j < Q.nb) ? (int32_t)(xb + key_token2(Q, kv, j, key) * xs) : 0;
-                }
-            };
-            int32_t cur[4], nxt[4];
-            const auto gathered = [&](int j) { return !(j < Q.ndmax && kv_contig); };
-            if (gathered(0)) op_rows(0, cur);
-            int stop_at[2] = {1 << 30, 1 << 30};
-            int known = -1;
-            int nx = 0;
-            for (int j = 0; j < Q.nb; ++j) {
-                const bool gat = gathered(j);
-                if (j + 1 < Q.nb && gathered(j + 1)) op_rows(j + 1, nxt);
-                const uint32_t gi = gx + j;
-                const int st = gi % nst;
-                mbar_wait(smem_u32(&xempty[st]), ((gi / nst) & 1) ^ 1, kgrp ? 1102 : 1103);
-                for (; known < j - lag;) {
-                    ++known;
-                    if (known >= Q.ndmax)
-                        for (int x = 0; x < 2; ++x)
-                            if (participates2(Q, x, known) && stop_at[x] > known && c.dec[x][known & 3] == 2)
-                                stop_at[x] = known;
-                }
-                bool need = false;
-                for (int x = 0; x < 2; ++x) need |= participates2(Q, x, j) && !(stop_at[x] <= j - lag);
-                if (!need) break;
-                const uint32_t dst = xbase + st * stage_bytes;
-                if (lt == 0) mbar_expect_tx_cluster(lead(&xfull[st]), stage_bytes);
-                if (lt == 0) tl2_mark(p, kgrp ? 9 : 10, gi);
-                named_bar_sync(kgrp ? 3 : 4, kgrp ? kKThreads : kVThreads);  // expect_tx before any bytes
-                if (!gat) {
-                    const int64_t tok0 = Q.sb + (int64_t)j * kBN;
-                    if (kgrp) {
-                        if (lt < 2)
-                            tma_load2d_2cta(dst + lt * kKHalf2, &ktile64, lt * 64, (int32_t)(xb + (tok0 + 64 * rank) * xs),
-                                            lead(&xfull[st]));
-                    } else if (lt == 0) {
-                        tma_load2d_2cta(dst, &vtile, 64 * rank, (int32_t)(xb + tok0 * xs), lead(&xfull[st]));
-                    }
-                } else if (op >= 0) {
-                    if (kgrp) {
-                        const int grp = op >> 1, h = op & 1;
-                        tma_gather4_2cta(dst + h * kKHalf2 + grp * 512, xmap, h * 64, cur[0], cur[1], cur[2], cur[3],
-                                         lead(&xfull[st]));
-                    } else {
-                        tma_gather4_2cta(dst + op * 512, xmap, 64 * rank, cur[0], cur[1], cur[2], cur[3],
-                                         lead(&xfull[st]));
-                    }
-                }
-                for (int i = 0; i < 4; ++i) cur[i] = nxt[i];
-                ++nx;
-            }
-            gx += nx;
-        }
-    } else if (warp == kMmaWarp) {
-        // ============================== MMA issuer (leader CTA) ==============================
-        if (rank == 0) {
-            const bool leader = elect_one();
-            const uint32_t idesc_s = umma_idesc_bf16(2 * kBM, kBN, false, false);
-            const uint32_t idesc_o = umma_idesc_bf16(2 * kBM, kD, false, true);
-            uint32_t gk = 0, gv = 0, qcount = 0;
-            uint32_t ns[2] = {0, 0};
-            const uint64_t dq0 = umma_desc_sw128(sQ, 16, 1024);
-            const uint64_t dk0 = umma_desc_sw128(sK, 16, 1024);
-            const uint64_t dv0 = umma_desc_sw128(sV, kHalf, 1024);
-            auto issue_s = [&](int x, int st) {
-                x = __shfl_sync(0xffffffffu, x, 0);
-                st = __shfl_sync(0xffffffffu, st, 0);
-                const uint64_t dq = dq0 + ((x * kTileBytes) >> 4);
-                const uint64_t dk = dk0 + ((st * kKStage2) >> 4);
-#pragma unroll
-                for (int kk = 0; kk < kD / 16; ++kk) {
-                    if (leader)
-                        umma_bf16_2cta(tbase + x * 256, dq + (((kk / 4) * kHalf + (kk % 4) * 32) >> 4),
-                                       dk + (((kk / 4) * kKHalf2 + (kk % 4) * 32) >> 4), idesc_s, kk > 0);
-                }
-                if (leader) umma_commit_2cta(smem_u32(&c.s_full[x]));
-            };
-            auto wait_k = [&](uint32_t gki) {
-                mbar_wait(smem_u32(&c.k_full[gki % kK2Stages]), (gki / kK2Stages) & 1, 2102);
-                tl2_mark(p, 8, gki);
-                tc_fence_after();
-            };
-            for (int64_t it = cid; it < total; it += clusters) {
-                const QuadInfo Q = quad_info(p, it, 0);
-                if (Q.nb == 0) continue;
-                mbar_wait(smem_u32(&c.q_full), qcount & 1, 2101);
-                ++qcount;
-                int stop_at[2] = {1 << 30, 1 << 30};
-                bool pv_any[2] = {false, false};
-                auto need = [&](int j, int lag) {
-                    bool n = false;
-                    for (int x = 0; x < 2; ++x) n |= participates2(Q, x, j) && !(stop_at[x] <= j - lag);
-                    return n;
-                };
-                wait_k(gk);
-                for (int x = 0; x < 2; ++x)
-                    if (participates2(Q, x, 0)) issue_s(x, gk % kK2Stages);
-                int nk = 0, nv = 0;
-                for (int j = 0;; ++j) {
-                    const uint32_t gki = gk + j, gvi = gv + j;
-                    const bool has_v = need(j, kV2Stages);
-                    const bool has_kn = (j + 1 < Q.nb) && need(j + 1, kK2Stages);
-                    bool v_ready = false, kn_ready = false;
-                    for (int x = 0; x < 2; ++x) {
-                        if (participates2(Q, x, j) && stop_at[x] > j - 1) {
-                            mbar_wait(smem_u32(&c.p_full[x]), ns[x] & 1, 2104);
-                            if (x == 0) tl2_mark(p, 5, ns[x]);
-                            ++ns[x];
-                            tc_fence_after();
-                            const bool diag = j < Q.ndmax;
-                            bool commit = true;
-                            if (!diag) {
-                                const volatile uint32_t* rv = c.red[x][j & 1];
-                                uint32_t any = 0;
-                                for (int w = 0; w < 8; ++w) any |= rv[w];
-                                commit = any != 0u;
-                                commit = __shfl_sync(0xffffffffu, commit, 0);
-                            }
-                            __syncwarp();
-                            if (leader && !diag) {
-                                // publish the slot decision to both CTAs (the release arrives order
-                                // the dec stores; the loaders read dec >= 3 blocks later)
-                                c.dec[x][j & 3] = commit ? 1 : 2;
-                                st_cluster_u8(peer(&c.dec[x][j & 3]), commit ? 1u : 2u);
-                                mbar_arrive(smem_u32(&c.d_full[x]));
-                                mbar_arrive_cluster(peer(&c.d_full[x]));
-                            }
-                            __syncwarp();
-                            if (commit) {
-                                if (!v_ready) {
-                                    mbar_wait(smem_u32(&c.v_full[gvi % kV2Stages]), (gvi / kV2Stages) & 1, 2105);
-                                    tc_fence_after();
-                                    v_ready = true;
-                                }
-                                const int vst = __shfl_sync(0xffffffffu, (int)(gvi % kV2Stages), 0);
-                                const int xu = __shfl_sync(0xffffffffu, x, 0);
-                                const uint64_t dv = dv0 + ((vst * kVStage2) >> 4);
-#pragma unroll
-                                for (int kk = 0; kk < kBN / 16; ++kk)
-                                    if (leader)
-                                        umma_bf16_ts_2cta(tbase + xu * 256 + 128, tbase + xu * 256 + kk * 8,
-                                                          dv + ((kk * 16 * 128) >> 4), idesc_o,
-                                                          (kk > 0 || pv_any[x]) ? 1 : 0);
-                                pv_any[x] = true;
-                                if (x == 0) tl2_mark(p, 6, ns[x] - 1);
-                                if (leader && j == last_block2(Q, x)) umma_commit_2cta(smem_u32(&c.o_done[x]));
-                            } else {
-                                stop_at[x] = j;
-                                if (leader) umma_commit_2cta(smem_u32(&c.o_done[x]));
-                            }
-                        }
-                        if (has_kn && participates2(Q, x, j + 1) && stop_at[x] > j) {
-                            if (!kn_ready) {
-                                wait_k(gki + 1);
-                                kn_ready = true;
-                            }
-                            issue_s(x, (gki + 1) % kK2Stages);
-                            if (x == 0) tl2_mark(p, 7, ns[x]);
-                        }
-                    }
-                    if (has_v && !v_ready) mbar_wait(smem_u32(&c.v_full[gvi % kV2Stages]), (gvi / kV2Stages) & 1, 2106);
-                    if (leader) {
-                        umma_commit_2cta(smem_u32(&c.k_empty[gki % kK2Stages]));
-                        if (has_v) umma_commit_2cta(smem_u32(&c.v_empty[gvi % kV2Stages]));
-                    }
-                    ++nk;
-                    nv += has_v ? 1 : 0;
-                    if (!has_kn) break;
-                    if (!kn_ready) wait_k(gki + 1);
-                }
-                if (leader) umma_commit_2cta(smem_u32(&c.q_empty));
-                gk += nk;
-                gv += nv;
-            }
-        }
-        __syncwarp();
-    } else {
-        // ============================== softmax / epilogue (both CTAs, slot x) ==============================
-        setmaxnreg_inc<kSoftmaxRegs>();
-        const int x = warp / 4;
-        const int w4 = warp % 4;
-        const int r = threadIdx.x % 128;
-        const uint32_t lane_off = (uint32_t)(w4 * 32) << 16;
-        const uint32_t tS = tbase + lane_off + x * 256;
-        const uint32_t tO = tS + 128;
-        const uint32_t bar_id = 1 + x;
-        const float sc = p.scale_log2;
-        const uint32_t pfull_lead = lead(&c.p_full[x]);
-        uint32_t ns = 0, no = 0, nd_ph = 0;
-        auto zero_p = [&]() {
-            uint32_t z[16];
-#pragma unroll
-            for (int i = 0; i < 16; ++i) z[i] = 0u;
-#pragma unroll
-            for (int c0 = 0; c0 < kBN; c0 += 32) tmem_st16(tS + c0 / 2, z);
-        };
-        for (int64_t it = cid; it < total; it += clusters) {
-            float m2 = -INFINITY, ell = 0.0f;
-            float sacc = 1.0f;
-            bool pv_any = false;
-            int committed = 0, pairs = 0;
-            bool any = false;
-            {
-            const QuadInfo Q = quad_info(p, it, rank);
-            if (!Q.slot_has[x]) continue;
-            const int ndt_x = Q.ndt[x], ndmax = Q.ndmax, nb = Q.nb;
-            const int t0x = (int)Q.t0[x], segr = (int)Q.seg_rows, avail = (int)Q.avail;
-            const bool has = Q.has[x];
-            const bool valid = has && r < Q.tn[x];
-            bool stopped = !has;  // a missing tile rides along with P = 0
-            if (has) {
-                const int64_t slot = Q.zh * g.l + q_row2(a, Q, x, r);
-                if (a.mode & kStateIn) {
-                    m2 = a.m_in[slot] * 1.4426950408889634f;
-                    ell = a.ell_in[slot];
-                    const char* arow = reinterpret_cast<const char*>(a.acc_in + slot * kD);
-#pragma unroll
-                    for (int i = 0; i < 4; ++i) asm volatile("prefetch.global.L2 [%0];" ::"l"(arow + 128 * i));
-                }
-            }
-            for (int j = 0; j < nb; ++j) {
-                if (!participates2(Q, x, j)) continue;
-                any = true;
-                mbar_wait(smem_u32(&c.s_full[x]), ns & 1, 3101);
-                if (x == 0 && r == 0) tl2_mark(p, 1, ns);
-                ++ns;
-                tc_fence_after();
-                const bool is_diag = j < ndmax;
-                const bool zmode = stopped || (is_diag && j >= ndt_x);
-                float m_use = m2, alpha = 1.0f, rowsum = 0.0f;
-                bool rescale = false;
-                if (!zmode) {
-                    uint32_t sv[kBN];
-#pragma unroll
-                    for (int c0 = 0; c0 < kBN; c0 += 32) tmem_ld32(tS + c0, *reinterpret_cast<uint32_t(*)[32]>(&sv[c0]));
-                    tmem_ld_wait();
-                    int lim;
-                    if (is_diag) {
-                        const int k0 = j * kBN;
-                        const int kn = min(kBN, segr - k0);
-                        const int vis = (k0 + kn - 1 <= t0x) ? kn : min(kn, t0x + r - k0 + 1);
-                        lim = max(0, vis);
-                    } else {
-                        lim = min(kBN, avail - (j - ndmax) * kBN);
-                    }
-                    const bool full = __all_sync(0xffffffffu, lim >= kBN);
-                    float rs[4] = {0.0f, 0.0f, 0.0f, 0.0f};
-                    float mxa[8];
-#pragma unroll
-                    for (int i = 0; i < 8; ++i) mxa[i] = -INFINITY;
-                    // three-input max (FMNMX3): 64 instructions for the 128 scores
-                    if (full) {
-#pragma unroll
-                        for (int i = 0; i < kBN; i += 2)
-                            mxa[(i >> 1) & 7] = fmax3(mxa[(i >> 1) & 7], __uint_as_float(sv[i]), __uint_as_float(sv[i + 1]));
-                    } else {
-#pragma unroll
-                        for (int i = 0; i < kBN; i += 2)
-                            mxa[(i >> 1) & 7] = fmax3(mxa[(i >> 1) & 7], i < lim ? __uint_as_float(sv[i]) : -INFINITY,
-                                                      i + 1 < lim ? __uint_as_float(sv[i + 1]) : -INFINITY);
-                    }
-                    const float mx = fmax3(fmax3(mxa[0], mxa[1], mxa[2]), fmax3(mxa[3], mxa[4], mxa[5]),
-                                           fmaxf(mxa[6], mxa[7])) * sc;
-                    const float m_new = fmaxf(m2, mx);
-                    rescale = (m_new > m2 + kRescaleThresh) || (m2 == -INFINITY);
-                    m_use = rescale ? m_new : m2;
-                    const float neg_ref = (m_use == -INFINITY) ? 0.0f : -m_use;
-                    alpha = (m2 == -INFINITY) ? 0.0f : ex2(m2 + neg_ref);
-                    if (full) {
-#pragma unroll
-                        for (int c0 = 0; c0 < kBN; c0 += 32) {
-                            uint32_t pk[16];
-#pragma unroll
-                            for (int i = 0; i < 32; i += 2) {
-                                const float e0 = ex2(fmaf(__uint_as_float(sv[c0 + i]), sc, neg_ref));
-                                const float e1 = ex2(fmaf(__uint_as_float(sv[c0 + i + 1]), sc, neg_ref));
-                                rs[(i >> 1) & 3] += e0 + e1;
-                                pk[i >> 1] = pack_bf16(e0, e1);
-                            }
-                            tmem_st16(tS + c0 / 2, pk);
-                        }
-                    } else {
-#pragma unroll
-                        for (int c0 = 0; c0 < kBN; c0 += 32) {
-                            uint32_t pk[16];
-#pragma unroll
-                            for (int i = 0; i < 32; i += 2) {
-                                const float e0 = c0 + i < lim ? ex2(fmaf(__uint_as_float(sv[c0 + i]), sc, neg_ref)) : 0.0f;
-                                const float e1 = c0 + i + 1 < lim ? ex2(fmaf(__uint_as_float(sv[c0 + i + 1]), sc, neg_ref)) : 0.0f;
-                                rs[(i >> 1) & 3] += e0 + e1;
-                                pk[i >> 1] = pack_bf16(e0, e1);
-                            }
-                            tmem_st16(tS + c0 / 2, pk);
-                        }
-                    }
-                    rowsum = (rs[0] + rs[1]) + (rs[2] + rs[3]);
-                    if (rescale) sacc *= alpha;
-                    if (__any_sync(0xffffffffu, pv_any && rescale && m2 != -INFINITY)) {
-#pragma unroll
-                        for (int c0 = 0; c0 < kD; c0 += 32) {
-                            uint32_t v[32];
-                            tmem_ld32(tO + c0, v);
-                            tmem_ld_wait();
-#pragma unroll
-                            for (int i = 0; i < 32; ++i) v[i] = __float_as_uint(__uint_as_float(v[i]) * alpha);
-                            tmem_st32(tO + c0, v);
-                        }
-                    }
-                } else {
-                    zero_p();
-                }
-                if (x == 0 && r == 0) tl2_mark(p, 2, ns - 1);
-                bool tile_commit = !zmode;
-                if (!is_diag) {
-                    // this tile's decision from its 4 warps' votes (CTA-local), before P is final:
-                    // a stopping tile zeroes its P so the slot's P V leaves its O unchanged
-                    const bool cont = !zmode && valid && (rowsum >= (float)a.tau * (ell * alpha));
-                    const uint32_t vote = __ballot_sync(0xffffffffu, cont) != 0u;
-                    if (lane == 0) {
-                        c.red[x][j & 1][4 * rank + w4] = vote;
-                        if (rank != 0) st_cluster_u32(lead(&c.red[x][j & 1][4 * rank + w4]), vote);
-                    }
-                    named_bar_sync(bar_id, 128);
-                    const volatile uint32_t* rv = &c.red[x][j & 1][4 * rank];
-                    tile_commit = !zmode && ((rv[0] | rv[1] | rv[2] | rv[3]) != 0u);
-                    if (!zmode && !tile_commit) zero_p();
-                }
-                tmem_st_wait();
-                tc_fence_before();
-                __syncwarp();
-                if (lane == 0) {
-                    if (rank == 0) mbar_arrive(smem_u32(&c.p_full[x]));
-                    else mbar_arrive_cluster(pfull_lead);
-                }
-                if (x == 0 && r == 0) tl2_mark(p, 3, ns - 1);
-                if (!zmode) {
-                    ell = tile_commit ? ell * alpha + rowsum : ell * alpha;
-                    m2 = m_use;
-                    pv_any |= tile_commit;
-                    if (tile_commit && !is_diag) {
-                        ++committed;
-                        pairs += min(kBN, avail - (j - ndmax) * kBN);
-                    }
-                    if (!tile_commit) stopped = true;
-                }
-                if (!is_diag) {
-                    mbar_wait_cluster(smem_u32(&c.d_full[x]), nd_ph & 1, 3102);
-                    if (x == 0 && r == 0) tl2_mark(p, 4, ns - 1);
-                    ++nd_ph;
-                    if (c.dec[x][j & 3] != 1) break;  // the slot (both tiles) stopped
-                }
-            }
-            }  // block loop scope
-            const QuadInfo Q = quad_info(p, it, rank);
-            if (any) {
-                mbar_wait(smem_u32(&c.o_done[x]), no & 1, 3104);
-                ++no;
-                tc_fence_after();
-            }
-            if (Q.has[x]) {
-                const bool valid = r < Q.tn[x];
-                const int64_t grow = q_row2(a, Q, x, r);
-                const int64_t slot = Q.zh * g.l + grow;
-                uint32_t ov[kD];
-#pragma unroll
-                for (int c0 = 0; c0 < kD; c0 += 32) tmem_ld32(tO + c0, *reinterpret_cast<uint32_t(*)[32]>(&ov[c0]));
-                tmem_ld_wait();
-                if (!pv_any) {
-#pragma unroll
-                    for (int i = 0; i < kD; ++i) ov[i] = 0u;
-                }
-                if (a.mode & kStateIn) {
-                    const float4* src = reinterpret_cast<const float4*>(a.acc_in + slot * kD);
-#pragma unroll
-                    for (int i = 0; i < kD / 4; ++i) {
-                        const float4 y = src[i];
-                        ov[4 * i] = __float_as_uint(fmaf(y.x, sacc, __uint_as_float(ov[4 * i])));
-                        ov[4 * i + 1] = __float_as_uint(fmaf(y.y, sacc, __uint_as_float(ov[4 * i + 1])));
-                        ov[4 * i + 2] = __float_as_uint(fmaf(y.z, sacc, __uint_as_float(ov[4 * i + 2])));
-                        ov[4 * i + 3] = __float_as_uint(fmaf(y.w, sacc, __uint_as_float(ov[4 * i + 3])));
-                    }
-                }
-                const float inv = 1.0f / ell;
-                const bool overflow = (a.mode & kPrefix) && Q.np > 0 && committed == Q.np && a.truncated(Q.n);
-                const bool resume_later = overflow && a.acc_out != nullptr;
-                const bool save_state = (a.mode & kStateOut) || resume_later;
-                if (valid && save_state) {
-                    float4* dst = reinterpret_cast<float4*>(a.acc_out + slot * kD);
-#pragma unroll
-                    for (int i = 0; i < kD / 4; ++i)
-                        dst[i] = make_float4(__uint_as_float(ov[4 * i]), __uint_as_float(ov[4 * i + 1]),
-                                             __uint_as_float(ov[4 * i + 2]), __uint_as_float(ov[4 * i + 3]));
-                }
-                if (valid && (a.mode & kFinal) && !resume_later) {
-                    const int64_t ooff = g.o_base(Q.zh) + grow * g.os[2];
-                    if (g.out_bf16) {
-                        uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(a.o) + ooff);
-#pragma unroll
-                        for (int i = 0; i < kD / 8; ++i) {
-                            uint4 w;
-                            w.x = pack_bf16(__uint_as_float(ov[8 * i]) * inv, __uint_as_float(ov[8 * i + 1]) * inv);
-                            w.y = pack_bf16(__uint_as_float(ov[8 * i + 2]) * inv, __uint_as_float(ov[8 * i + 3]) * inv);
-                            w.z = pack_bf16(__uint_as_float(ov[8 * i + 4]) * inv, __uint_as_float(ov[8 * i + 5]) * inv);
-                            w.w = pack_bf16(__uint_as_float(ov[8 * i + 6]) * inv, __uint_as_float(ov[8 * i + 7]) * inv);
-                            dst[i] = w;
-                        }
-                    } else {
-                        float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(a.o) + ooff);
-#pragma unroll
-                        for (int i = 0; i < kD / 4; ++i)
-                            dst[i] = make_float4(__uint_as_float(ov[4 * i]) * inv, __uint_as_float(ov[4 * i + 1]) * inv,
-                                                 __uint_as_float(ov[4 * i + 2]) * inv, __uint_as_float(ov[4 * i + 3]) * inv);
-                    }
-                }
-                if (valid && save_state) {
-                    a.m_out[slot] = (m2 == -INFINITY) ? -INFINITY : m2 * 0.6931471805599453f;
-                    a.ell_out[slot] = ell;
-                }
-                if (valid && (a.mode & kFinal) && !resume_later && ell == 0.0f) atomicExch(a.err_flag, 2);
-                if ((a.mode & kPrefix) && r == 0) {
-                    const int64_t tile = Q.zh * a.tiles_per_head + Q.n * a.T + Q.ti[x];
-                    if (overflow) {
-                        const int s2 = atomicAdd(a.ovf_count, 1);
-                        a.ovf_tiles[s2] = (int32_t)tile;
-                        if (a.ovf_base) a.ovf_base[s2] = committed;
-                    } else {
-                        a.processed[(Q.zh * g.N + Q.n) * a.T + Q.ti[x]] = committed;
-                    }
-                    if (pairs && (!overflow || resume_later))
-                        atomicAdd((unsigned long long*)&a.pass2_pairs[Q.zh], (unsigned long long)pairs * Q.tn[x]);
-                }
-            }
-            tc_fence_before();
-            named_bar_sync(bar_id, 128);
-        }
-    }
-    tc_fence_before();
-    cluster_sync();
-    if (warp == 0) tmem_dealloc_2cta(tbase, kTmemCols);
-}
-
 // ---------------------------------------------------------------- host side
 PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
     static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -2185,36 +1585,44 @@ cudaError_t launch_tc_pass(const PassArgs& a, cudaStream_t st) {
         tc_diag_kernel<<<grid, kDThreads, kDSmemBytes, st>>>(pd, qtile, ktile, vtile);
         return cudaGetLastError();
     }
-    for (const void* f : {(const void*)tc_pass_kernel<false>, (const void*)tc_pass_kernel<true>})
+    for (const void* f : {(const void*)tc_pass_kernel<false, 1>, (const void*)tc_pass_kernel<true, 1>,
+                          (const void*)tc_pass_kernel<true, 2>})
         if (cudaError_t e = smem_attr(f, kSmemBytes)) return e;
-    // CTA-pair variant (cta_group::2, quads of tiles) only on request (S2O_TC_CTAS=2): it halves
-    // the gathered bytes per SM but its per-block cross-SM handshakes (4 remote p_full arrivals,
-    // remote decision publication) cost more than they save at C3 (pass-2 8.9 vs 7.4 ms,
-    // profiles/r01_summary.md), so the single-CTA kernel is the default.
-    static const bool pair_on = [] {
-        const char* e = std::getenv("S2O_TC_CTAS");
-        return e && std::strcmp(e, "2") == 0;
+    // Prefix passes over whole segments (pass-2, fused) run on 2-CTA clusters with multicast K/V
+    // (quads of tiles); tile-list reruns of plan levels and diagonal-only passes on single CTAs.
+    // S2O_CLUSTER=0 selects the single-CTA pair kernel (A/B aid).
+    static const bool cluster_on = [] {
+        const char* e = std::getenv("S2O_CLUSTER");
+        return !(e && std::strcmp(e, "0") == 0);
     }();
-    if (!a.tile_list && pair_on && sms >= 2) {
-        CUtensorMap ktile64;
-        if (!make_row_map(&ktile64, a.k, krows, 64)) return cudaErrorInvalidValue;
+    if ((a.mode & kPrefix) && !a.tile_list && cluster_on && sms >= 2) {
         TcParams p2 = p;
         p2.pairs_full = (a.T + 3) / 4;  // quads per full segment
         p2.pairs_per_head = (g.N - 1) * p2.pairs_full + (t_last + 3) / 4;
-        if (cudaError_t e = smem_attr((const void*)tc_pass2cta_kernel, k2SmemBytes)) return e;
         const int64_t work2 = g.z * g.hq * p2.pairs_per_head;
         if (work2 == 0) return cudaSuccess;
         const int clusters = (int)std::max<int64_t>(1, std::min<int64_t>(work2, sms / 2));
-        tc_pass2cta_kernel<<<2 * clusters, kThreads, k2SmemBytes, st>>>(p2, qmap, kmap, vmap, qtile, ktile64, vtile);
-        return cudaGetLastError();
+        cudaLaunchConfig_t lc = {};
+        lc.gridDim = dim3(2 * clusters);
+        lc.blockDim = dim3(kThreads);
+        lc.dynamicSmemBytes = kSmemBytes;
+        lc.stream = st;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = 2;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        lc.attrs = at;
+        lc.numAttrs = 1;
+        return cudaLaunchKernelEx(&lc, tc_pass_kernel<true, 2>, p2, qmap, kmap, vmap, qtile, ktile, vtile);
     }
     const int64_t work = a.tile_list ? a.tile_count : g.z * g.hq * p.pairs_per_head;
     if (work == 0) return cudaSuccess;
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(work, sms));
     if (a.mode & kPrefix)
-        tc_pass_kernel<true><<<grid, kThreads, kSmemBytes, st>>>(p, qmap, kmap, vmap, qtile, ktile, vtile);
+        tc_pass_kernel<true, 1><<<grid, kThreads, kSmemBytes, st>>>(p, qmap, kmap, vmap, qtile, ktile, vtile);
     else
-        tc_pass_kernel<false><<<grid, kThreads, kSmemBytes, st>>>(p, qmap, kmap, vmap, qtile, ktile, vtile);
+        tc_pass_kernel<false, 1><<<grid, kThreads, kSmemBytes, st>>>(p, qmap, kmap, vmap, qtile, ktile, vtile);
     return cudaGetLastError();
 }
 

@@ -417,59 +417,37 @@ __device__ __forceinline__ void st_cluster_u32(uint32_t cl_addr, uint32_t v) {
 __device__ __forceinline__ void st_cluster_u8(uint32_t cl_addr, uint32_t v) {
     asm volatile("st.shared::cluster.u8 [%0], %1;" ::"r"(cl_addr), "r"(v) : "memory");
 }
-// TMA into this CTA's smem, completion counted on the pair leader's mbarrier (cl_bar)
-__device__ __forceinline__ void tma_gather4_2cta(uint32_t sdst, const CUtensorMap* map, int32_t col, int32_t r0,
-                                                 int32_t r1, int32_t r2, int32_t r3, uint32_t cl_bar) {
+// Cluster multicast (2-CTA clusters of the pass kernel): the same smem offset (data and
+// mbarrier) in every CTA of `mask` receives the bytes; complete_tx lands on each destination's
+// barrier. sdst / bar are this CTA's shared::cta addresses (valid shared::cluster addresses).
+__device__ __forceinline__ void tma_gather4_mc(uint32_t sdst, const CUtensorMap* map, int32_t col, int32_t r0,
+                                               int32_t r1, int32_t r2, int32_t r3, uint32_t bar, uint16_t mask) {
     asm volatile(
-        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes "
-        "[%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(sdst),
-        "l"(reinterpret_cast<uint64_t>(map)), "r"(col), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(cl_bar)
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes.multicast::cluster "
+        "[%0], [%1, {%2, %3, %4, %5, %6}], [%7], %8;" ::"r"(sdst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(col), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(bar), "h"(mask)
         : "memory");
 }
-__device__ __forceinline__ void tma_load2d_2cta(uint32_t sdst, const CUtensorMap* map, int32_t col, int32_t row,
-                                                uint32_t cl_bar) {
+__device__ __forceinline__ void tma_load2d_mc(uint32_t sdst, const CUtensorMap* map, int32_t col, int32_t row,
+                                              uint32_t bar, uint16_t mask) {
     asm volatile(
-        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes "
-        "[%0], [%1, {%2, %3}], [%4];" ::"r"(sdst),
-        "l"(reinterpret_cast<uint64_t>(map)), "r"(col), "r"(row), "r"(cl_bar)
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster "
+        "[%0], [%1, {%2, %3}], [%4], %5;" ::"r"(sdst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(col), "r"(row), "r"(bar), "h"(mask)
         : "memory");
 }
-__device__ __forceinline__ void tmem_alloc_2cta(uint32_t smem_dst, uint32_t ncols) {
-    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_dst), "r"(ncols)
-                 : "memory");
-}
-__device__ __forceinline__ void tmem_relinquish_2cta() {
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
-}
-__device__ __forceinline__ void tmem_dealloc_2cta(uint32_t taddr, uint32_t ncols) {
-    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols) : "memory");
-}
-// D[tmem] (+)= A[smem] * B[smem] across the CTA pair (M = 256: A rows 0-127 in CTA 0, 128-255 in
-// CTA 1; B split by N across the pair). Issued by one thread of the leader CTA.
-__device__ __forceinline__ void umma_bf16_2cta(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
-                                               uint32_t accumulate) {
+// Arrive on the same-offset mbarrier of every CTA in `mask` once all earlier MMAs of this thread
+// completed.
+__device__ __forceinline__ void umma_commit_mc(uint32_t bar, uint16_t mask) {
     asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "setp.ne.b32 p, %4, 0;\n\t"
-        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
-        "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+        "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(bar),
+        "h"(mask)
         : "memory");
 }
-__device__ __forceinline__ void umma_bf16_ts_2cta(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
-                                                  uint32_t accumulate) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "setp.ne.b32 p, %4, 0;\n\t"
-        "tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
-        "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
-        : "memory");
-}
-// Arrive on the same-offset mbarrier of both CTAs when all earlier pair MMAs complete.
-__device__ __forceinline__ void umma_commit_2cta(uint32_t bar) {
-    asm volatile(
-        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(bar),
-        "h"((unsigned short)3)
-        : "memory");
+__device__ __forceinline__ uint32_t ld_volatile_u32(uint32_t saddr) {
+    uint32_t v;
+    asm volatile("ld.volatile.shared::cta.u32 %0, [%1];" : "=r"(v) : "r"(saddr) : "memory");
+    return v;
 }
 
 }  // namespace sm100
