@@ -1,7 +1,7 @@
 """The single-CTA pair kernel (tc_pass_kernel<.., 1>) for prefix passes, selected with
 S2O_CLUSTER=0 (read once per process, so the cases run in a subprocess; the default is the
 2-CTA multicast cluster kernel, covered by every other tcgen05 test): traces equal to the exact
-generic path (threshold ties aside: at most one tile and one chunk on these inputs), outputs
+generic path up to threshold ties (|gain - tau| / tau <= 1e-4 in the reference arithmetic), outputs
 within the tcgen05 tolerance (bf16 operands, fp32 accumulation): max |dO| <= 2.5e-2,
 mean <= 2e-3 against the generic fp64 path."""
 from __future__ import annotations
@@ -20,6 +20,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 SCRIPT = r"""
 import json, sys
 sys.path.insert(0, sys.argv[1])
+import numpy as np
 import torch
 import paper_2602_22575_b200 as s2o
 out = []
@@ -36,7 +37,19 @@ for (hq, hkv, l, s, reorder, fused, tau) in json.loads(sys.argv[2]):
         res[path] = r
     a, b = res[s2o.PATH_TCGEN05], res[s2o.PATH_GENERIC]
     d = (a.out.float() - b.out.float()).abs()
+    # differing tiles must be threshold ties in the reference arithmetic
+    from oracle.oracle import Port, trace_ties
+    rep = hq // hkv
+    qf, kf, vf = (t.float().cpu().numpy() for t in (qd, kd, vd))
+    cfg = s2o.KernelConfig(seg_len=s, tau=tau, q_reorder=reorder, fused=fused)
+    plan, _ = s2o.build_plan(qd, kd, s)
+    n_seg = plan.seg.seg_count
+    ties = trace_ties(Port(), qf, np.repeat(kf, rep, 1), np.repeat(vf, rep, 1), cfg,
+                      plan.q_perm.reshape(hq, n_seg, -1).cpu().numpy(), plan.kv_perm.reshape(hq, -1).cpu().numpy(),
+                      a.trace.processed.reshape(hq, n_seg, -1).cpu().numpy(),
+                      b.trace.processed.reshape(hq, n_seg, -1).cpu().numpy())
     out.append({"trace_diff": int((a.trace.processed != b.trace.processed).sum().item()),
+                "all_ties": all(t["tie"] for t in ties),
                 "tiles": int(a.trace.processed.numel()),
                 "max": d.max().item(), "mean": d.mean().item(),
                 "p2": [int(a.trace.pass2_pairs.sum().item()), int(b.trace.pass2_pairs.sum().item())]})
@@ -55,7 +68,7 @@ def test_pair_kernel_matches_exact_path():
     assert r.returncode == 0, r.stderr[-2000:]
     rows = json.loads(r.stdout.strip().splitlines()[-1])
     for case, row in zip(CASES, rows):
-        assert row["trace_diff"] <= max(1, row["tiles"] // 100), (case, row)
+        assert row["all_ties"], (case, row)
         assert row["max"] <= 2.5e-2 and row["mean"] <= 2e-3, (case, row)
         if row["trace_diff"] == 0:
             assert row["p2"][0] == row["p2"][1], (case, row)
