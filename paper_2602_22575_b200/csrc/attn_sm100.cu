@@ -1588,12 +1588,15 @@ cudaError_t launch_tc_pass(const PassArgs& a, cudaStream_t st) {
     for (const void* f : {(const void*)tc_pass_kernel<false, 1>, (const void*)tc_pass_kernel<true, 1>,
                           (const void*)tc_pass_kernel<true, 2>})
         if (cudaError_t e = smem_attr(f, kSmemBytes)) return e;
-    // Prefix passes over whole segments (pass-2, fused) run on 2-CTA clusters with multicast K/V
-    // (quads of tiles); tile-list reruns of plan levels and diagonal-only passes on single CTAs.
-    // S2O_CLUSTER=0 selects the single-CTA pair kernel (A/B aid).
+    // Opt-in (S2O_CLUSTER=1): prefix passes over whole segments on 2-CTA clusters with multicast
+    // K/V (quads of tiles). It halves the TMA gather ops and L2 reads per SM, but the two CTAs'
+    // pipelines are coupled stage by stage (a stage is free only when both MMA warps released
+    // it; a quad's stream runs until all four tiles stopped) and that coupling costs more than
+    // the loads save: pass-2 at C3 7.20 ms vs 6.05 ms for the single-CTA pair kernel (same box,
+    // round 2), so the pair kernel stays the default.
     static const bool cluster_on = [] {
         const char* e = std::getenv("S2O_CLUSTER");
-        return !(e && std::strcmp(e, "0") == 0);
+        return e && std::strcmp(e, "1") == 0;
     }();
     if ((a.mode & kPrefix) && !a.tile_list && cluster_on && sms >= 2) {
         TcParams p2 = p;

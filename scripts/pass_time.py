@@ -25,7 +25,7 @@ cfg = s2o.KernelConfig(seg_len=2048, tau=0.005)
 plan, _ = s2o.build_plan(qd, kd, 2048)
 t1 = timeit(lambda: s2o.pass1_dense_init(qd, kd, vd, cfg))
 bufs = s2o.pass1_dense_init(qd, kd, vd, cfg)
-t2 = timeit(lambda: s2o.pass2_sparse(qd, kd, vd, bufs, plan, cfg))
+t2 = timeit(lambda: s2o.pass2_sparse(qd, kd, vd, bufs, plan, cfg, check=False))
 o, tr = s2o.pass2_sparse(qd, kd, vd, bufs, plan, cfg)
 torch.cuda.synchronize()
 pairs = int(tr.pass2_pairs.sum().item())

@@ -1,6 +1,6 @@
-"""The single-CTA pair kernel (tc_pass_kernel<.., 1>) for prefix passes, selected with
-S2O_CLUSTER=0 (read once per process, so the cases run in a subprocess; the default is the
-2-CTA multicast cluster kernel, covered by every other tcgen05 test): traces equal to the exact
+"""The opt-in 2-CTA multicast cluster kernel (tc_pass_kernel<.., 2>) for prefix passes, selected
+with S2O_CLUSTER=1 (read once per process, so the cases run in a subprocess; the default single-CTA
+pair kernel is covered by every other tcgen05 test): traces equal to the exact
 generic path up to threshold ties (|gain - tau| / tau <= 1e-4 in the reference arithmetic), outputs
 within the tcgen05 tolerance (bf16 operands, fp32 accumulation): max |dO| <= 2.5e-2,
 mean <= 2e-3 against the generic fp64 path."""
@@ -61,8 +61,8 @@ CASES = [(4, 2, 4096, 512, True, False, 0.005), (8, 2, 8192, 2048, True, False, 
          (2, 1, 4096, 1024, True, False, 0.0)]
 
 
-def test_pair_kernel_matches_exact_path():
-    env = dict(os.environ, S2O_CLUSTER="0")
+def test_cluster_kernel_matches_exact_path():
+    env = dict(os.environ, S2O_CLUSTER="1")
     r = subprocess.run([sys.executable, "-c", SCRIPT, ROOT, json.dumps(CASES)], env=env, capture_output=True,
                        text=True, timeout=600)
     assert r.returncode == 0, r.stderr[-2000:]
