@@ -8,8 +8,10 @@
  * s2o::KernelConfig 1:1, and a CUDA stream passed as void*. No torch types.
  *
  * Conventions
- *  - Device entry points are stream-ordered and asynchronous; they never allocate, never
- *    synchronise, and are thread-safe for distinct streams/workspaces.
+ *  - Device entry points are stream-ordered and asynchronous; they never allocate device
+ *    buffers, never synchronise, and are thread-safe for distinct streams/workspaces. They may be
+ *    captured into a CUDA graph (s2o_attention_fwd's data-dependent plan levels are a graph
+ *    WHILE node: added to the capturing graph, or launched as a cached graph otherwise).
  *  - Q is [Z, Hq, L, D]; K and V are [Z, Hkv, L, D] (GQA: q head h reads kv head
  *    h / (Hq/Hkv)). Element strides (batch, head, token) are given per tensor; the channel
  *    stride is 1. So both the reference [Z,H,L,D] layout and [Z,L,H,D] are accepted.

@@ -248,7 +248,7 @@ size_t generic_scratch_bytes(const PassArgs& a) {
 }
 
 cudaError_t launch_generic_pass(const PassArgs& a, void* scratch, cudaStream_t st) {
-    const int64_t tiles = a.num_tiles();
+    const int64_t tiles = a.max_tiles();
     if (tiles == 0) return cudaSuccess;
     const int grid = std::min(grid_for(tiles), 256 * 8);
     generic_pass_kernel<<<grid, kThreads, 0, st>>>(a, reinterpret_cast<double*>(scratch));

@@ -308,6 +308,7 @@ tc_pass_kernel(const TcParams p, const __grid_constant__ CUtensorMap qmap,
                const __grid_constant__ CUtensorMap vtile) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char* smem = smem_raw;
+    if (p.a.tile_list && p.a.num_tiles() == 0) return;  // a stream-ordered level with nothing to redo
     if ((smem_u32(smem) & 1023u) != 0) __trap();  // SWIZZLE_128B tiles need a 1024-B aligned base
     Ctrl& c = *reinterpret_cast<Ctrl*>(smem + kOffCtrl);
     const PassArgs& a = p.a;
@@ -353,7 +354,7 @@ tc_pass_kernel(const TcParams p, const __grid_constant__ CUtensorMap qmap,
     tc_fence_after();
     const uint32_t tbase = c.tmem_base;
     if (threadIdx.x == 0) tl_cta(p, 0);
-    const int64_t total = a.tile_list ? a.tile_count : g.z * g.hq * p.pairs_per_head;
+    const int64_t total = a.tile_list ? a.num_tiles() : g.z * g.hq * p.pairs_per_head;
     const uint32_t rank = kCl == 2 ? cluster_rank() : 0u;
     const uint32_t peer = rank ^ 1u;
     // kCl = 2: clusters take quads statically (cluster c: c, c + #clusters, ...); every warp of
@@ -1619,7 +1620,7 @@ cudaError_t launch_tc_pass(const PassArgs& a, cudaStream_t st) {
         lc.numAttrs = 1;
         return cudaLaunchKernelEx(&lc, tc_pass_kernel<true, 2>, p2, qmap, kmap, vmap, qtile, ktile, vtile);
     }
-    const int64_t work = a.tile_list ? a.tile_count : g.z * g.hq * p.pairs_per_head;
+    const int64_t work = a.tile_list ? a.max_tiles() : g.z * g.hq * p.pairs_per_head;
     if (work == 0) return cudaSuccess;
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(work, sms));
     if (a.mode & kPrefix)

@@ -8,6 +8,8 @@
 #include <string>
 #include <vector>
 
+#include <cub/block/block_scan.cuh>
+
 #include "internal.h"
 
 namespace s2o {
@@ -33,6 +35,9 @@ s2o_status cuda_fail(cudaError_t e, const char* where) {
 size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
 constexpr int64_t kMaxPlanDepth = 6144;  // 3/4 of select_topk_kernel smem capacity (kSelCap = 8192)
+// Level control words at the head of the overflow area: [0] overflow tiles, [1] selection flag,
+// [2] segments of the next level, [3] tiles to rerun, [4..5] level base (int64).
+constexpr int kCtlWords = 16;
 
 // Geometry + generic argument checks shared by every entry point.
 s2o_status make_geo(const s2o_problem* p, int64_t seg_len, Geo* g) {
@@ -166,6 +171,224 @@ s2o_status bt_setup(const s2o_problem* p, int64_t rows, int64_t cols, int64_t to
     L->p2 = take(sizeof(int64_t) * zh);
     L->pass = take(pass_ws_bytes(*a));
     L->total = off + 256;
+    return S2O_OK;
+}
+
+// ------------------------------------------------------------------ stream-ordered plan levels
+// A tile that walks its whole truncated kv list without stopping resumes on the next plan level
+// (the following topt entries of the same order). Whether that happens is known only on the
+// device, so the level loop is a CUDA graph WHILE node: the body holds two levels (lists A -> B,
+// then B -> A), each a prep kernel (reads the overflow count; builds the sorted segment list of
+// the overflow tiles; sets the loop condition), the level selection (segment count from device
+// memory) and the pass rerun (tile list length from device memory); kernels of an empty level
+// exit at once. An IF node after the loop runs the full-plan fallback when a selection could not
+// be certified. The nodes go into the caller's graph when `stream` is being captured, else into a
+// cached executable graph launched on `stream`: either way nothing synchronises the host.
+struct LevelLoop {
+    Geo g;
+    PassArgs a, a2;
+    int32_t path, fused;
+    int64_t topt;
+    const void *q, *k;
+    int32_t *qp, *kvp;
+    int64_t* p1;
+    int32_t* ctl;
+    uint8_t* marks;
+    int32_t* seglist;
+    int32_t *lists[2], *tiles[2], *bases[2];
+    float *acc, *ell, *m;
+    char *plan_ws, *pass_ws;
+    size_t pass_bytes;
+};
+
+__global__ void __launch_bounds__(1024)
+level_prep_kernel(int32_t* __restrict__ ctl, const int32_t* __restrict__ tiles_in, int32_t* __restrict__ seglist,
+                  uint8_t* __restrict__ marks, int64_t tiles_per_head, int64_t T, int64_t N, int64_t nsegs,
+                  int64_t topt, cudaGraphConditionalHandle h_loop, cudaGraphConditionalHandle h_fallback) {
+    using Scan = cub::BlockScan<int, 1024>;
+    __shared__ typename Scan::TempStorage tmp;
+    __shared__ int s_base;
+    const int tid = threadIdx.x;
+    const int cnt = ctl[0], flag = ctl[1];
+    if (cnt == 0 || flag != 0) {  // no level needed, or a selection failed: leave the loop
+        if (tid == 0) {
+            ctl[2] = 0;
+            ctl[3] = 0;
+            cudaGraphSetConditional(h_loop, 0);
+            cudaGraphSetConditional(h_fallback, flag != 0 ? 1u : 0u);
+        }
+        return;
+    }
+    const int64_t full = (N - 1) * T;
+    for (int i = tid; i < cnt; i += blockDim.x) {
+        const int64_t t = tiles_in[i], zh = t / tiles_per_head, r = t % tiles_per_head;
+        marks[zh * N + (r < full ? r / T : N - 1)] = 1;
+    }
+    if (tid == 0) s_base = 0;
+    __syncthreads();
+    for (int64_t c0 = 0; c0 < nsegs; c0 += blockDim.x) {  // segment codes in increasing order
+        const int64_t c = c0 + tid;
+        const int mk = c < nsegs ? marks[c] : 0;
+        int pos, tot;
+        Scan(tmp).ExclusiveSum(mk, pos, tot);
+        if (mk) {
+            seglist[s_base + pos] = (int32_t)c;
+            marks[c] = 0;
+        }
+        __syncthreads();
+        if (tid == 0) s_base += tot;
+        __syncthreads();
+    }
+    if (tid == 0) {
+        ctl[2] = s_base;
+        ctl[3] = cnt;
+        ctl[0] = 0;
+        *reinterpret_cast<int64_t*>(ctl + 4) += topt;
+        cudaGraphSetConditional(h_loop, 1);
+    }
+}
+
+// The loop body (two levels) and the fallback body, enqueued on `st` (being captured).
+s2o_status level_body(const LevelLoop& L, cudaStream_t st, cudaGraphConditionalHandle hl,
+                      cudaGraphConditionalHandle hf) {
+    const Geo& g = L.g;
+    const int64_t nsegs = g.z * g.hq * g.N;
+    for (int cur = 0; cur < 2; ++cur) {
+        level_prep_kernel<<<1, 1024, 0, st>>>(L.ctl, L.tiles[cur], L.seglist, L.marks, L.a.tiles_per_head, L.a.T,
+                                              g.N, nsegs, L.topt, hl, hf);
+        S2O_CUDA_TRY(cudaGetLastError(), "level prep");
+        S2O_CUDA_TRY(launch_plan_level_dev(g, L.seglist, L.ctl + 2, L.lists[cur],
+                                           reinterpret_cast<const int64_t*>(L.ctl + 4), L.lists[cur ^ 1], L.topt,
+                                           L.ctl + 1, L.plan_ws, st), "plan level");
+        PassArgs a3 = L.a2;
+        if (L.fused) {  // the diagonal part is done: resume the saved state, prefix only
+            a3.mode = kStateIn | kPrefix | kFinal;
+            a3.acc_in = L.acc; a3.ell_in = L.ell; a3.m_in = L.m;
+        }
+        a3.kv_perm = L.lists[cur ^ 1];
+        a3.lvl_base = 0;
+        a3.lvl_base_dev = reinterpret_cast<const int64_t*>(L.ctl + 4);
+        a3.tile_list = L.tiles[cur];
+        a3.tile_base = L.bases[cur];
+        a3.tile_count = 0;
+        a3.tile_count_dev = L.ctl + 3;
+        a3.ovf_tiles = L.tiles[cur ^ 1];
+        a3.ovf_base = L.bases[cur ^ 1];
+        if (s2o_status e = run_pass(a3, L.path, L.pass_ws, L.pass_bytes, st, false)) return e;
+    }
+    return S2O_OK;
+}
+
+s2o_status fallback_body(const LevelLoop& L, cudaStream_t st) {
+    // a selection could not be certified: full plan, recompute everything
+    S2O_CUDA_TRY(launch_plan_build(L.g, L.q, L.k, L.qp, L.kvp, L.plan_ws, st), "plan build");
+    PassArgs a3 = L.a2;
+    a3.kv_perm = L.kvp;
+    a3.kv_top = 0;
+    a3.lvl_base = 0;
+    a3.acc_out = a3.ell_out = a3.m_out = nullptr;
+    S2O_CUDA_TRY(launch_trace_init(L.a, L.p1, st), "trace init");
+    if (!L.fused) {  // pass-1 state was overwritten by saved levels: redo pass-1
+        PassArgs a1 = L.a;
+        a1.mode = kDiag | kStateOut;
+        a1.q_reorder = 0;
+        a1.acc_out = L.acc; a1.ell_out = L.ell; a1.m_out = L.m;
+        if (s2o_status e = run_pass(a1, L.path, L.pass_ws, L.pass_bytes, st)) return e;
+    }
+    return run_pass(a3, L.path, L.pass_ws, L.pass_bytes, st);
+}
+
+// Capture `fn` (enqueues work on a stream) into the body graph of a conditional node.
+template <typename F>
+s2o_status capture_into(cudaGraph_t body, cudaStream_t side, F&& fn) {
+    S2O_CUDA_TRY(cudaStreamBeginCaptureToGraph(side, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed),
+                 "begin capture");
+    s2o_status e = fn(side);
+    cudaGraph_t out = nullptr;
+    cudaError_t ce = cudaStreamEndCapture(side, &out);
+    if (e) return e;
+    if (ce != cudaSuccess) return cuda_fail(ce, "end capture");
+    return S2O_OK;
+}
+
+// Add WHILE(level loop) -> IF(fallback) to `graph` after `deps`; *last = the IF node.
+s2o_status add_level_nodes(const LevelLoop& L, cudaGraph_t graph, const cudaGraphNode_t* deps, size_t ndeps,
+                           cudaStream_t side, cudaGraphNode_t* last) {
+    cudaGraphConditionalHandle hl, hf;
+    S2O_CUDA_TRY(cudaGraphConditionalHandleCreate(&hl, graph, 1, cudaGraphCondAssignDefault), "cond handle");
+    S2O_CUDA_TRY(cudaGraphConditionalHandleCreate(&hf, graph, 0, cudaGraphCondAssignDefault), "cond handle");
+    cudaGraphNodeParams wp = {};
+    wp.type = cudaGraphNodeTypeConditional;
+    wp.conditional.handle = hl;
+    wp.conditional.type = cudaGraphCondTypeWhile;
+    wp.conditional.size = 1;
+    cudaGraphNode_t wnode;
+    S2O_CUDA_TRY(cudaGraphAddNode(&wnode, graph, deps, ndeps, &wp), "while node");
+    if (s2o_status e = capture_into(wp.conditional.phGraph_out[0], side,
+                                    [&](cudaStream_t t) { return level_body(L, t, hl, hf); }))
+        return e;
+    cudaGraphNodeParams fp = {};
+    fp.type = cudaGraphNodeTypeConditional;
+    fp.conditional.handle = hf;
+    fp.conditional.type = cudaGraphCondTypeIf;
+    fp.conditional.size = 1;
+    S2O_CUDA_TRY(cudaGraphAddNode(last, graph, &wnode, 1, &fp), "if node");
+    return capture_into(fp.conditional.phGraph_out[0], side, [&](cudaStream_t t) { return fallback_body(L, t); });
+}
+
+struct LoopCache {
+    std::mutex mu;
+    std::vector<std::pair<std::string, cudaGraphExec_t>> execs;  // (key bytes incl. device, exec)
+    std::vector<std::pair<int, cudaStream_t>> side;               // per device capture stream
+} g_loops;
+
+s2o_status enqueue_level_loop(const LevelLoop& L, cudaStream_t s) {
+    int dev = 0;
+    S2O_CUDA_TRY(cudaGetDevice(&dev), "device");
+    std::lock_guard<std::mutex> lock(g_loops.mu);
+    cudaStream_t side = nullptr;
+    for (auto& e : g_loops.side)
+        if (e.first == dev) side = e.second;
+    if (!side) {
+        S2O_CUDA_TRY(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking), "stream");
+        g_loops.side.emplace_back(dev, side);
+    }
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    S2O_CUDA_TRY(cudaStreamIsCapturing(s, &cs), "capture status");
+    if (cs == cudaStreamCaptureStatusActive) {  // into the caller's graph
+        cudaGraph_t graph;
+        const cudaGraphNode_t* deps = nullptr;
+        size_t ndeps = 0;
+        S2O_CUDA_TRY(cudaStreamGetCaptureInfo(s, &cs, nullptr, &graph, &deps, &ndeps), "capture info");
+        cudaGraphNode_t last;
+        if (s2o_status e = add_level_nodes(L, graph, deps, ndeps, side, &last)) return e;
+        S2O_CUDA_TRY(cudaStreamUpdateCaptureDependencies(s, &last, 1, cudaStreamSetCaptureDependencies),
+                     "capture dependencies");
+        return S2O_OK;
+    }
+    std::string key(reinterpret_cast<const char*>(&L), sizeof L);
+    key.append(reinterpret_cast<const char*>(&dev), sizeof dev);
+    cudaGraphExec_t exec = nullptr;
+    for (auto& e : g_loops.execs)
+        if (e.first == key) exec = e.second;
+    if (!exec) {
+        cudaGraph_t graph;
+        S2O_CUDA_TRY(cudaGraphCreate(&graph, 0), "graph");
+        cudaGraphNode_t last;
+        s2o_status e = add_level_nodes(L, graph, nullptr, 0, side, &last);
+        if (!e) {
+            cudaError_t ce = cudaGraphInstantiate(&exec, graph, 0);
+            if (ce != cudaSuccess) e = cuda_fail(ce, "graph instantiate");
+        }
+        cudaGraphDestroy(graph);
+        if (e) return e;
+        if (g_loops.execs.size() >= 16) {  // bounded cache: drop the oldest
+            cudaGraphExecDestroy(g_loops.execs.front().second);
+            g_loops.execs.erase(g_loops.execs.begin());
+        }
+        g_loops.execs.emplace_back(std::move(key), exec);
+    }
+    S2O_CUDA_TRY(cudaGraphLaunch(exec, s), "graph launch");
     return S2O_OK;
 }
 
@@ -461,7 +684,9 @@ static OpLayout op_layout(const Geo& g, const PassArgs& a, int fused, const s2o_
     L.kvperm = take(sizeof(int32_t) * std::max<int64_t>(1, zh * g.kv_per_head()));
     L.kvtop = take(2 * sizeof(int32_t) * std::max<int64_t>(1, zh * g.N * L.topt));  // level lists A, B
     // [0] overflow count, [1] selection flag, then tiles A/B, bases A/B, segment list
-    L.ovf = take(sizeof(int32_t) * (4 + 5 * zh * a.tiles_per_head));
+    // level control (kCtlWords int32: overflow count, selection flag, segment count, tile count,
+    // level base (int64)), tiles A/B, bases A/B, segment list, then one mark byte per segment
+    L.ovf = take(sizeof(int32_t) * (kCtlWords + 5 * zh * a.tiles_per_head) + zh * g.N);
     // pass state: pass-1 -> pass-2, and (also fused) the saved state of tiles that resume at the
     // next plan level of a truncated plan
     const bool state = !fused || L.topt > 0;
@@ -521,20 +746,21 @@ s2o_status s2o_attention_fwd(const s2o_problem* p, const void* q, const void* k,
     int64_t* p2 = pass2_pairs ? pass2_pairs : reinterpret_cast<int64_t*>(base + L.p2);
     // Truncated plan unless the caller asked for the full kv_perm (or no segment is long enough)
     const int64_t topt = kv_perm ? 0 : L.topt;
-    int32_t* ovf = reinterpret_cast<int32_t*>(base + L.ovf);  // [0] overflow count, [1] selection flag
+    int32_t* ovf = reinterpret_cast<int32_t*>(base + L.ovf);  // level control words, see kCtlWords
+    const int64_t ntiles = g.z * g.hq * a.tiles_per_head;
     if (topt > 0) {
-        S2O_CUDA_TRY(cudaMemsetAsync(ovf, 0, 4 * sizeof(int32_t), s), "memset");
+        S2O_CUDA_TRY(cudaMemsetAsync(ovf, 0, kCtlWords * sizeof(int32_t), s), "memset");
+        S2O_CUDA_TRY(cudaMemsetAsync(reinterpret_cast<char*>(ovf + kCtlWords + 5 * ntiles), 0, g.z * g.hq * g.N, s),
+                     "memset");
         S2O_CUDA_TRY(launch_plan_topk(g, q, k, qp, reinterpret_cast<int32_t*>(base + L.kvtop), topt, ovf + 1,
                                       base + L.plan, s), "plan top-k");
     } else {
         S2O_CUDA_TRY(launch_plan_build(g, q, k, qp, kvp, base + L.plan, s), "plan build");
     }
-    const int64_t ntiles = g.z * g.hq * a.tiles_per_head;
     int32_t* lists[2] = {reinterpret_cast<int32_t*>(base + L.kvtop),
                          reinterpret_cast<int32_t*>(base + L.kvtop) + std::max<int64_t>(1, g.z * g.hq * g.N * L.topt)};
-    int32_t* tiles[2] = {ovf + 4, ovf + 4 + ntiles};
-    int32_t* bases[2] = {ovf + 4 + 2 * ntiles, ovf + 4 + 3 * ntiles};
-    int32_t* seglist = ovf + 4 + 4 * ntiles;
+    int32_t* tiles[2] = {ovf + kCtlWords, ovf + kCtlWords + ntiles};
+    int32_t* bases[2] = {ovf + kCtlWords + 2 * ntiles, ovf + kCtlWords + 3 * ntiles};
     a.q = q; a.k = k; a.v = v; a.o = o;
     a.kv_perm = topt > 0 ? lists[0] : kvp;
     a.kv_top = topt;
@@ -567,88 +793,25 @@ s2o_status s2o_attention_fwd(const s2o_problem* p, const void* q, const void* k,
     }
     if ((st = run_pass(a2, cfg->path, base + L.pass, pass_ws_bytes(a), s))) return st;
     if (topt > 0) {
-        int32_t host[2] = {0, 0};
-        int cur = 0;
-        int64_t lvl_base = 0;
-        for (;;) {
-            S2O_CUDA_TRY(cudaMemcpyAsync(host, ovf, sizeof host, cudaMemcpyDeviceToHost, s), "d2h overflow");
-            S2O_CUDA_TRY(cudaStreamSynchronize(s), "sync");
-            if (host[0] == 0 || host[1] != 0) break;
-            // next plan level for the segments of the overflow tiles
-            std::vector<int32_t> ht(host[0]);
-            S2O_CUDA_TRY(cudaMemcpyAsync(ht.data(), tiles[cur], sizeof(int32_t) * host[0], cudaMemcpyDeviceToHost, s),
-                         "d2h tiles");
-            S2O_CUDA_TRY(cudaStreamSynchronize(s), "sync");
-            std::vector<int32_t> segs;
-            segs.reserve(ht.size());
-            for (int32_t t : ht) {
-                const int64_t zh = t / a.tiles_per_head, r = t % a.tiles_per_head;
-                const int64_t full = (g.N - 1) * a.T;
-                const int64_t n = r < full ? r / a.T : g.N - 1;
-                segs.push_back((int32_t)(zh * g.N + n));
-            }
-            std::sort(segs.begin(), segs.end());
-            segs.erase(std::unique(segs.begin(), segs.end()), segs.end());
-            S2O_CUDA_TRY(cudaMemcpyAsync(seglist, segs.data(), sizeof(int32_t) * segs.size(), cudaMemcpyHostToDevice, s),
-                         "h2d segments");
-            lvl_base += topt;
-            if (std::getenv("S2O_LEVEL_LOG"))
-                std::fprintf(stderr, "s2o plan level %lld: %d overflow tiles in %zu segments\n",
-                             (long long)(lvl_base / topt), host[0], segs.size());
-            const bool lvl_log = std::getenv("S2O_LEVEL_LOG") != nullptr;
-            cudaEvent_t lev[3];
-            if (lvl_log)
-                for (auto& e : lev) { cudaEventCreate(&e); }
-            if (lvl_log) cudaEventRecord(lev[0], s);
-            S2O_CUDA_TRY(launch_plan_level(g, seglist, (int64_t)segs.size(), lists[cur], lvl_base, lists[cur ^ 1], topt,
-                                           ovf + 1, base + L.plan, s), "plan level");
-            if (lvl_log) cudaEventRecord(lev[1], s);
-            S2O_CUDA_TRY(cudaMemsetAsync(ovf, 0, sizeof(int32_t), s), "memset");
-            PassArgs a3 = a2;
-            if (cfg->fused) {  // the diagonal part is done: resume the saved state, prefix only
-                a3.mode = kStateIn | kPrefix | kFinal;
-                a3.acc_in = acc; a3.ell_in = ell; a3.m_in = m;
-            }
-            a3.kv_perm = lists[cur ^ 1];
-            a3.lvl_base = lvl_base;
-            a3.tile_list = tiles[cur];
-            a3.tile_base = bases[cur];
-            a3.tile_count = host[0];
-            a3.ovf_tiles = tiles[cur ^ 1];
-            a3.ovf_base = bases[cur ^ 1];
-            if ((st = run_pass(a3, cfg->path, base + L.pass, pass_ws_bytes(a), s, false))) return st;
-            if (lvl_log) {
-                cudaEventRecord(lev[2], s);
-                cudaEventSynchronize(lev[2]);
-                float t01 = 0.f, t12 = 0.f;
-                cudaEventElapsedTime(&t01, lev[0], lev[1]);
-                cudaEventElapsedTime(&t12, lev[1], lev[2]);
-                std::fprintf(stderr, "   level selection %.3f ms, tile rerun %.3f ms\n", t01, t12);
-                for (auto& e : lev) cudaEventDestroy(e);
-            }
-            cur ^= 1;
-        }
-        if (host[1] != 0 && std::getenv("S2O_LEVEL_LOG"))
-            std::fprintf(stderr, "s2o plan: a selection was not certified at level %lld -> full plan\n",
-                         (long long)(lvl_base / topt));
-        if (host[1] != 0) {
-            // A selection could not be certified: full plan, recompute everything.
-            S2O_CUDA_TRY(launch_plan_build(g, q, k, qp, kvp, base + L.plan, s), "plan build");
-            PassArgs a3 = a2;
-            a3.kv_perm = kvp;
-            a3.kv_top = 0;
-            a3.lvl_base = 0;
-            a3.acc_out = a3.ell_out = a3.m_out = nullptr;
-            S2O_CUDA_TRY(launch_trace_init(a, p1, s), "trace init");
-            if (!cfg->fused) {  // pass-1 state was overwritten by saved levels: redo pass-1
-                PassArgs a1 = a;
-                a1.mode = kDiag | kStateOut;
-                a1.q_reorder = 0;
-                a1.acc_out = acc; a1.ell_out = ell; a1.m_out = m;
-                if ((st = run_pass(a1, cfg->path, base + L.pass, pass_ws_bytes(a), s))) return st;
-            }
-            if ((st = run_pass(a3, cfg->path, base + L.pass, pass_ws_bytes(a), s))) return st;
-        }
+        LevelLoop lp;
+        std::memset(&lp, 0, sizeof lp);  // the struct's bytes key the graph cache
+        lp.g = g;
+        lp.a = a;
+        lp.a2 = a2;
+        lp.path = cfg->path;
+        lp.fused = cfg->fused;
+        lp.topt = topt;
+        lp.q = q; lp.k = k;
+        lp.qp = qp; lp.kvp = kvp; lp.p1 = p1;
+        lp.ctl = ovf;
+        lp.marks = reinterpret_cast<uint8_t*>(ovf + kCtlWords + 5 * ntiles);
+        lp.seglist = ovf + kCtlWords + 4 * ntiles;
+        for (int i = 0; i < 2; ++i) { lp.lists[i] = lists[i]; lp.tiles[i] = tiles[i]; lp.bases[i] = bases[i]; }
+        lp.acc = acc; lp.ell = ell; lp.m = m;
+        lp.plan_ws = base + L.plan;
+        lp.pass_ws = base + L.pass;
+        lp.pass_bytes = pass_ws_bytes(a);
+        if ((st = enqueue_level_loop(lp, s))) return st;
     }
     g_err.clear();
     return S2O_OK;

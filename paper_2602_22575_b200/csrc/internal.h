@@ -54,20 +54,37 @@ struct PassArgs {
     int64_t lvl_base;       // kv_perm entries of a segment consumed by earlier plan levels
     int no_overflow;        // a short kv list is the whole list (block top-k baseline), no next level
     int32_t* work_ctr;      // pass scratch: dynamic work counter of the tcgen05 pass kernel (zeroed per pass)
+    // device-resident level state (stream-ordered plan levels, capi.cu): when set, the kernels
+    // read the tile-list length and the level base from device memory instead of tile_count /
+    // lvl_base (a launch whose list is empty exits at once)
+    const int32_t* tile_count_dev;
+    const int64_t* lvl_base_dev;
 
+    __host__ __device__ int64_t lvl() const {
+#ifdef __CUDA_ARCH__
+        return lvl_base_dev ? *lvl_base_dev : lvl_base;
+#else
+        return lvl_base;
+#endif
+    }
     // entries of segment n's (current level) kv list
     __host__ __device__ int64_t avail(int64_t n) const {
-        const int64_t rem = n * g.S - lvl_base;
+        const int64_t rem = n * g.S - lvl();
         return (kv_top > 0 && kv_top < rem) ? kv_top : rem;
     }
     // the level's list ran out before the segment's prefix did
-    __host__ __device__ bool truncated(int64_t n) const { return !no_overflow && lvl_base + avail(n) < n * g.S; }
+    __host__ __device__ bool truncated(int64_t n) const { return !no_overflow && lvl() + avail(n) < n * g.S; }
     __host__ __device__ const int32_t* kv_seg(int64_t zh, int64_t n) const {
         return kv_top > 0 ? kv_perm + (zh * g.N + n) * kv_top : kv_perm + zh * g.kv_per_head() + g.kv_off(n);
     }
     __host__ __device__ int64_t num_tiles() const {
+#ifdef __CUDA_ARCH__
+        if (tile_list && tile_count_dev) return *tile_count_dev;
+#endif
         return tile_list ? tile_count : g.z * g.hq * tiles_per_head;
     }
+    // host: the largest tile count a launch can see (device-resident lists: every tile)
+    int64_t max_tiles() const { return (tile_list && !tile_count_dev) ? tile_count : g.z * g.hq * tiles_per_head; }
     __device__ int64_t tile_at(int64_t i) const { return tile_list ? (int64_t)tile_list[i] : i; }
 };
 
@@ -81,6 +98,11 @@ cudaError_t launch_plan_topk(const Geo& g, const void* q, const void* k, int32_t
 cudaError_t launch_plan_level(const Geo& g, const int32_t* seg_list, int64_t nseg, const int32_t* prev,
                               int64_t lvl_base, int32_t* kvtop, int64_t topt, int32_t* flags, void* workspace,
                               cudaStream_t st);
+// The same with the segment count and level base in device memory: the grid covers every
+// segment and CTAs beyond *nseg_dev exit (stream-ordered plan levels).
+cudaError_t launch_plan_level_dev(const Geo& g, const int32_t* seg_list, const int32_t* nseg_dev,
+                                  const int32_t* prev, const int64_t* lvl_base_dev, int32_t* kvtop, int64_t topt,
+                                  int32_t* flags, void* workspace, cudaStream_t st);
 cudaError_t launch_segment_means(const Geo& g, const void* x, int which_kv, int64_t nseg_out,
                                  float* out, cudaStream_t st);
 

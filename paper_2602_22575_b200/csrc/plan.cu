@@ -762,7 +762,10 @@ __device__ __forceinline__ SelSeg sel_seg(const Geo& g, const int32_t* seg_list,
 __global__ void __launch_bounds__(kScanThreads, 3)
 sel_scan_kernel(Geo g, const uint64_t* __restrict__ kvkey, int64_t topt, uint64_t* __restrict__ ckey,
                 uint32_t* __restrict__ cidx, int32_t* __restrict__ ccount, int32_t* __restrict__ flags,
-                const int32_t* __restrict__ seg_list, const int32_t* __restrict__ prev, int64_t lvl_base) {
+                const int32_t* __restrict__ seg_list, const int32_t* __restrict__ prev, int64_t lvl_base,
+                const int32_t* __restrict__ nseg_dev, const int64_t* __restrict__ lvl_base_dev) {
+    if (nseg_dev && (int64_t)blockIdx.x >= *nseg_dev) return;  // device-sized level: CTA not used
+    if (lvl_base_dev) lvl_base = *lvl_base_dev;
     __shared__ typename SampSort::TempStorage samp;
     __shared__ int s_wsum[kScanThreads / 32];
     __shared__ int s_count;
@@ -952,7 +955,10 @@ struct SelSortSmem {  // ~170 KB: 1 CTA / SM
 __global__ void __launch_bounds__(kSelThreads)
 sel_sort_kernel(Geo g, const uint64_t* __restrict__ kvkey, const uint64_t* __restrict__ ckey,
                 const uint32_t* __restrict__ cidx, const int32_t* __restrict__ ccount, int64_t topt,
-                int32_t* __restrict__ kvtop, const int32_t* __restrict__ seg_list, int level0, int64_t lvl_base) {
+                int32_t* __restrict__ kvtop, const int32_t* __restrict__ seg_list, int level0, int64_t lvl_base,
+                const int32_t* __restrict__ nseg_dev, const int64_t* __restrict__ lvl_base_dev) {
+    if (nseg_dev && (int64_t)blockIdx.x >= *nseg_dev) return;
+    if (lvl_base_dev) lvl_base = *lvl_base_dev;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     SelSortSmem& sm = *reinterpret_cast<SelSortSmem*>(smem_raw);
     __shared__ unsigned long long s_or;
@@ -1144,13 +1150,14 @@ namespace {
 // Top-T selection of `nseg` segments (all of them, or seg_list) over the keys in ws.key0.
 cudaError_t launch_select(const Geo& g, const PlanWs& ws, int64_t nseg, const int32_t* seg_list,
                           const int32_t* prev, int64_t lvl_base, int32_t* kvtop, int64_t topt, int32_t* flags,
-                          cudaStream_t st) {
+                          cudaStream_t st, const int32_t* nseg_dev = nullptr, const int64_t* lvl_base_dev = nullptr) {
     sel_scan_kernel<<<(unsigned)nseg, kScanThreads, 0, st>>>(g, ws.key0, topt, ws.key1, ws.idx1, ws.ccount, flags,
-                                                             seg_list, prev, lvl_base);
+                                                             seg_list, prev, lvl_base, nseg_dev, lvl_base_dev);
     const size_t ssm = sizeof(SelSortSmem);
     cudaFuncSetAttribute(sel_sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssm);
     sel_sort_kernel<<<(unsigned)nseg, kSelThreads, ssm, st>>>(g, ws.key0, ws.key1, ws.idx1, ws.ccount, topt, kvtop,
-                                                              seg_list, prev == nullptr ? 1 : 0, lvl_base);
+                                                              seg_list, prev == nullptr ? 1 : 0, lvl_base, nseg_dev,
+                                                              lvl_base_dev);
     return cudaGetLastError();
 }
 }  // namespace
@@ -1189,6 +1196,17 @@ cudaError_t launch_plan_level(const Geo& g, const int32_t* seg_list, int64_t nse
     char* base = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(workspace) + 255) & ~uintptr_t(255));
     plan_ws_layout(g, base, &ws);  // the kv keys of the level-0 build are still in key0
     return launch_select(g, ws, nseg, seg_list, prev, lvl_base, kvtop, topt, flags, st);
+}
+
+cudaError_t launch_plan_level_dev(const Geo& g, const int32_t* seg_list, const int32_t* nseg_dev,
+                                  const int32_t* prev, const int64_t* lvl_base_dev, int32_t* kvtop, int64_t topt,
+                                  int32_t* flags, void* workspace, cudaStream_t st) {
+    const int64_t nmax = g.z * g.hq * (g.N - 1);
+    if (nmax <= 0) return cudaSuccess;
+    PlanWs ws;
+    char* base = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(workspace) + 255) & ~uintptr_t(255));
+    plan_ws_layout(g, base, &ws);
+    return launch_select(g, ws, nmax, seg_list, prev, 0, kvtop, topt, flags, st, nseg_dev, lvl_base_dev);
 }
 
 cudaError_t launch_segment_means(const Geo& g, const void* x, int which_kv, int64_t nseg_out,

@@ -298,3 +298,37 @@ def test_tc_pass1_states_short_tiles(cuda, port):
     mg = bufs.m.cpu().numpy().astype(np.float64)
     assert (mg <= m + 1e-3).all() and (mg >= m - 8.0 * np.log(2.0) - 1e-3).all()
     np.testing.assert_allclose(bufs.ell.cpu().numpy() * np.exp(mg - m), ell, rtol=2e-3)
+
+
+@pytest.mark.parametrize("depth", [0, 128])
+def test_cuda_graph_capture_and_replay(cuda, depth):
+    """s2o_attention_fwd is stream-ordered (no host synchronisation, the plan-level loop is a graph
+    WHILE node): captured into a CUDA graph and replayed it reproduces the eager call bit for bit,
+    also when tiles overflow a tiny truncated plan (depth 128 -> several device-side levels)."""
+    import paper_2602_22575_b200 as s2o
+    torch = cuda
+    q, k, v = inputs(s2o, 4, 2, 4096, seed=5)
+    qd, kd, vd = dev_bf16(torch, q), dev_bf16(torch, k), dev_bf16(torch, v)
+    cfg = s2o.KernelConfig(seg_len=512, tau=0.005, plan_depth=depth)
+    eager = s2o.s2o_attention(qd, kd, vd, cfg, want_plan=False)
+    torch.cuda.synchronize()
+    out = torch.empty_like(qd)
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(side):
+        s2o.s2o_attention(qd, kd, vd, cfg, out=out, want_plan=False, check=False)  # warm-up (workspace)
+    torch.cuda.current_stream().wait_stream(side)
+    torch.cuda.synchronize()
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph):
+        res = s2o.s2o_attention(qd, kd, vd, cfg, out=out, want_plan=False, check=False)
+    out.zero_()
+    graph.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(out, eager.out)
+    assert torch.equal(res.trace.processed, eager.trace.processed)
+    assert torch.equal(res.trace.pass2_pairs, eager.trace.pass2_pairs)
+    out.zero_()
+    graph.replay()  # replays are repeatable (level state re-initialised inside the graph)
+    torch.cuda.synchronize()
+    assert torch.equal(out, eager.out)
