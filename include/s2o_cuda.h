@@ -131,6 +131,18 @@ s2o_status s2o_segment_representatives(const s2o_problem* p, const void* q, cons
                                        int64_t seg_len, float* q_mean, float* k_mean,
                                        void* stream);
 
+/* rank_queries (plan.hpp:104-106, plan.cpp:69-101) with a caller-given guide, fp32 [Z, Hq, D] on the
+ * device (one vector per q head): s_Q = fp64 sequential dot(Q row, guide), per-segment stable
+ * descending argsort -> q_perm int32 [Z, Hq, N, S] (segment-local). Plan workspace. */
+s2o_status s2o_rank_queries(const s2o_problem* p, const void* q, const float* guide, int64_t seg_len,
+                            int32_t* q_perm, void* workspace, size_t workspace_bytes, void* stream);
+
+/* rank_prefix_keys (plan.hpp:108-111, plan.cpp:103-138) with caller-given segment representatives
+ * q_mean fp32 [Z, Hq, N, D] on the device: s_K[n, t] = fp64 sequential dot(q_mean[n], K[t]) for
+ * t < nS, stable descending argsort -> kv_perm (packed as for s2o_plan_build). Plan workspace. */
+s2o_status s2o_rank_prefix_keys(const s2o_problem* p, const void* k, const float* q_mean, int64_t seg_len,
+                                int32_t* kv_perm, void* workspace, size_t workspace_bytes, void* stream);
+
 /* build_plan (plan.hpp:115-116, plan.cpp:140-162): guide = k_mean[segment 0], q_perm
  * (rank_queries plan.cpp:69-101), kv_perm (rank_prefix_keys plan.cpp:103-138). Uses
  * cfg->seg_len and cfg->score_mode. cost2 (host, optional) receives RankingCost

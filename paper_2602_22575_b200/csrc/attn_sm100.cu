@@ -67,7 +67,7 @@ constexpr uint32_t kOffQ = 0;               // slot X at X * kTileBytes
 constexpr uint32_t kOffK = 2 * kTileBytes;
 constexpr uint32_t kOffV = kOffK + kKStages * kTileBytes;
 constexpr uint32_t kOffCtrl = kOffV + kVStages * kTileBytes;
-constexpr uint32_t kOffTok = kOffCtrl + 512;  // token rings: K group int32 [2][128], V group [2][144]
+constexpr uint32_t kOffTok = kOffCtrl + 512;  // token rings: K group int32 [2][128], V group [2][128]
 constexpr uint32_t kSmemBytes = kOffTok + 2304;  // 226.75 KB (base must be 1024-B aligned)
 constexpr uint32_t kTmemCols = 512;
 constexpr int kSoftmaxRegs = 192;   // setmaxnreg: softmax warpgroups (0, 1)
@@ -93,10 +93,6 @@ struct Ctrl {
     // (work_ctr) and every warp of the CTA takes them in order (item k in slot k & 3)
     uint64_t w_full[4], w_empty[4];
     int64_t wq[4];
-    // 2-CTA clusters: the PEER's stop decisions, written by the peer's MMA warp into this CTA
-    // (st.shared::cluster), indexed [pair sequence & 1][peer slot]: bits 31-17 sequence, bit 16
-    // stopped, bits 15-0 the stop block (stopped) or the number of blocks decided so far.
-    uint32_t pdec[2][2];
 };
 
 constexpr int kWarps = kThreads / 32;
@@ -140,15 +136,6 @@ __device__ __forceinline__ void tl_cta(const TcParams& p, int ev) {
 #endif
 }
 
-// Token rings: the loader thread owning rows r0, r0 + STEP, ... reads its tokens as int4 vectors,
-// so a ring stores row `row` at (row % STEP) * rows_per_thread + row / STEP.
-template <int STEP>
-struct TokRing {
-    static constexpr int kRpt = ((kBM + STEP - 1) / STEP + 3) / 4 * 4;  // rows per thread, padded
-    static constexpr int kSize = STEP * kRpt;                           // ints per block
-    __device__ static int pos(int row) { return (row % STEP) * kRpt + row / STEP; }
-};
-
 // Early-stop decision from the four per-warp votes (early_stop_check kernel.cpp:220-234: stop iff
 // max gain < tau, strictly, NaN gains dropped <=> continue iff some row has gain >= tau).
 __device__ __forceinline__ bool chunk_commit(const uint32_t* red) {
@@ -156,88 +143,60 @@ __device__ __forceinline__ bool chunk_commit(const uint32_t* red) {
     return (rv[0] | rv[1] | rv[2] | rv[3]) != 0u;
 }
 
+// 32-bit fields (L < 2^31, checked by make_geo): the loader and MMA warps hold this for a whole
+// pair at 64 registers.
 struct PairInfo {
-    int64_t zh, n, sb, seg_rows, avail;
-    int64_t ti[2], t0[2], tn[2];
+    int32_t zh, n, sb, seg_rows, avail;
+    int32_t ti[2], t0[2], tn[2];
     int has[2];
     int nd[2], ndmax, np, nb;
-    int phas[2], pnd[2];  // the peer CTA's two tiles (2-CTA clusters; phas = 0 otherwise)
 };
 
-// Work item `idx`: a pair of tiles (kCl = 1), or a quad of 4 tiles on a 2-CTA cluster (kCl = 2:
-// CTA `rank` owns tiles 4q + 2 rank + {0, 1}, the peer the other two; the K/V block stream is
-// the quad's).
-template <int kCl>
-__device__ __forceinline__ PairInfo pair_info(const TcParams& p, int64_t idx, uint32_t rank) {
+__device__ __forceinline__ PairInfo pair_info(const TcParams& p, int64_t idx) {
     const PassArgs& a = p.a;
     const Geo& g = a.g;
     PairInfo P;
-    P.phas[0] = P.phas[1] = 0;
-    P.pnd[0] = P.pnd[1] = 0;
-    int64_t pti[2] = {-1, -1};
-    if (kCl == 2) {
-        const int64_t G = g.group;
-        const int64_t zg = idx / (p.pairs_per_head * G);
-        const int64_t rem = idx % (p.pairs_per_head * G);
-        P.zh = zg * G + rem % G;
-        const int64_t r = rem / G;
-        const int64_t full = (g.N - 1) * p.pairs_full;
-        int64_t qi, tcount;
-        if (r < full) { P.n = r / p.pairs_full; qi = r % p.pairs_full; tcount = a.T; }
-        else { P.n = g.N - 1; qi = r - full; tcount = (g.last_len + kBM - 1) / kBM; }
-        for (int x = 0; x < 2; ++x) {
-            const int64_t mine = 4 * qi + 2 * rank + x, peer = 4 * qi + 2 * (1 - rank) + x;
-            P.ti[x] = mine < tcount ? mine : -1;
-            pti[x] = peer < tcount ? peer : -1;
-        }
-    } else if (a.tile_list) {
+    int64_t ti0, ti1, n;
+    if (a.tile_list) {
         const int64_t tile = a.tile_list[idx];
-        P.zh = tile / a.tiles_per_head;
+        P.zh = (int32_t)(tile / a.tiles_per_head);
         const int64_t r = tile % a.tiles_per_head;
         const int64_t full = (g.N - 1) * a.T;
-        if (r < full) { P.n = r / a.T; P.ti[0] = r % a.T; }
-        else { P.n = g.N - 1; P.ti[0] = r - full; }
-        P.ti[1] = -1;
+        if (r < full) { n = r / a.T; ti0 = r % a.T; }
+        else { n = g.N - 1; ti0 = r - full; }
+        ti1 = -1;
     } else {
         // The q heads of a GQA group share K/V: interleave them (head fastest) so the group's
         // CTAs walk the same segment's K/V rows at the same time and hit L2 together.
         const int64_t G = g.group;
         const int64_t zg = idx / (p.pairs_per_head * G);
         const int64_t rem = idx % (p.pairs_per_head * G);
-        P.zh = zg * G + rem % G;
+        P.zh = (int32_t)(zg * G + rem % G);
         const int64_t r = rem / G;
         const int64_t full = (g.N - 1) * p.pairs_full;
         int64_t pi, tcount;
-        if (r < full) { P.n = r / p.pairs_full; pi = r % p.pairs_full; tcount = a.T; }
-        else { P.n = g.N - 1; pi = r - full; tcount = (g.last_len + kBM - 1) / kBM; }
-        P.ti[0] = 2 * pi;
-        P.ti[1] = (2 * pi + 1 < tcount) ? 2 * pi + 1 : -1;
+        if (r < full) { n = r / p.pairs_full; pi = r % p.pairs_full; tcount = a.T; }
+        else { n = g.N - 1; pi = r - full; tcount = (g.last_len + kBM - 1) / kBM; }
+        ti0 = 2 * pi;
+        ti1 = (2 * pi + 1 < tcount) ? 2 * pi + 1 : -1;
     }
-    P.sb = P.n * g.S;
-    P.seg_rows = g.seg_rows(P.n);
-    P.avail = a.avail(P.n);
+    P.n = (int32_t)n;
+    P.ti[0] = (int32_t)ti0;
+    P.ti[1] = (int32_t)ti1;
+    P.sb = (int32_t)(n * g.S);
+    P.seg_rows = (int32_t)g.seg_rows(n);
+    P.avail = (int32_t)a.avail(n);
     P.ndmax = 0;
     for (int x = 0; x < 2; ++x) {
         P.has[x] = P.ti[x] >= 0;
         P.t0[x] = P.has[x] ? P.ti[x] * kBM : 0;
-        P.tn[x] = P.has[x] ? min((int64_t)kBM, P.seg_rows - P.t0[x]) : 0;
-        P.nd[x] = (P.has[x] && (a.mode & kDiag)) ? (int)((P.t0[x] + P.tn[x] - 1) / kBN + 1) : 0;
+        P.tn[x] = P.has[x] ? min(kBM, P.seg_rows - P.t0[x]) : 0;
+        P.nd[x] = (P.has[x] && (a.mode & kDiag)) ? (P.t0[x] + P.tn[x] - 1) / kBN + 1 : 0;
         P.ndmax = max(P.ndmax, P.nd[x]);
     }
-    for (int x = 0; x < 2; ++x) {  // peer tiles (kCl = 2): participation in the shared stream
-        P.phas[x] = pti[x] >= 0;
-        if (P.phas[x] && (a.mode & kDiag)) {
-            const int64_t t0 = pti[x] * kBM, tn = min((int64_t)kBM, P.seg_rows - t0);
-            P.pnd[x] = (int)((t0 + tn - 1) / kBN + 1);
-            P.ndmax = max(P.ndmax, P.pnd[x]);
-        }
-    }
-    P.np = ((a.mode & kPrefix) && P.n > 0) ? (int)((P.avail + kBN - 1) / kBN) : 0;
+    P.np = ((a.mode & kPrefix) && P.n > 0) ? (P.avail + kBN - 1) / kBN : 0;
     P.nb = P.ndmax + P.np;
     return P;
-}
-__device__ __forceinline__ bool peer_participates(const PairInfo& P, int x, int j) {
-    return P.phas[x] && (j < P.ndmax ? j < P.pnd[x] : true);
 }
 
 __device__ __forceinline__ bool participates(const PairInfo& P, int x, int j) {
@@ -268,39 +227,7 @@ __device__ __forceinline__ int64_t key_token(const PairInfo& P, const int32_t* k
     return (int64_t)kv[c0 + (i < cn ? i : 0)];
 }
 
-// Peer decision word (Ctrl::pdec) for one slot after block j of pair `seq` (kCl = 2).
-__device__ __forceinline__ uint32_t dec_word(uint32_t seq, bool stopped, int v) {
-    return ((seq & 0x7fffu) << 17) | (stopped ? 0x10000u : 0u) | ((uint32_t)v & 0xffffu);
-}
-// Has the peer's slot x stopped at a block <= b? Spins until the peer's MMA warp has published
-// decisions through block b (it publishes after every block; it is never more than a few blocks
-// behind, since both CTAs consume the same multicast K/V stages).
-__device__ __forceinline__ bool peer_stopped_by(const Ctrl& c, const PairInfo& P, uint32_t seq, int x, int b) {
-    if (b < P.ndmax) return false;  // diagonal blocks always commit
-    const uint32_t addr = smem_u32(&c.pdec[seq & 1][x]);
-    uint32_t spins = 0;
-    for (;;) {
-        const uint32_t w = ld_volatile_u32(addr);
-        if ((w >> 17) == (seq & 0x7fffu)) {
-            const int v = (int)(w & 0xffffu);
-            if (w & 0x10000u) return v <= b;
-            if (v > b) return false;
-        }
-        if (++spins == (1u << 26)) {
-            printf("s2o watchdog: block %d thread %d peer decision seq %u slot %d block %d word %08x\n",
-                   (int)blockIdx.x, (int)threadIdx.x, seq, x, b, w);
-            __trap();
-        }
-    }
-}
-
-// kCl = 1: one CTA per pair of tiles. kCl = 2: 2-CTA clusters, one CTA per half of a quad of tiles
-// of the same (head, segment); each CTA gathers one 64-column half of every K/V block and
-// multicasts it to both, so every gathered block is fetched once for four tiles (half the TMA
-// ops and L2 reads per SM of kCl = 1). A stage is released when BOTH MMA warps are done with it
-// (multicast commits, empty barriers of count 2); the block stream runs while any of the four
-// tiles needs it, so each MMA warp publishes its slots' stop decisions into the peer (pdec).
-template <bool kPackedExp, int kCl>
+template <bool kPackedExp>
 __global__ void __launch_bounds__(kThreads, 1)
 tc_pass_kernel(const TcParams p, const __grid_constant__ CUtensorMap qmap,
                const __grid_constant__ CUtensorMap kmap, const __grid_constant__ CUtensorMap vmap,
@@ -326,13 +253,12 @@ tc_pass_kernel(const TcParams p, const __grid_constant__ CUtensorMap qmap,
         mbar_init(smem_u32(&c.q_empty), 1);
         for (int s = 0; s < kKStages; ++s) {
             mbar_init(smem_u32(&c.k_full[s]), kKThreads);
-            mbar_init(smem_u32(&c.k_empty[s]), kCl);  // one release per CTA of the cluster
+            mbar_init(smem_u32(&c.k_empty[s]), 1);
         }
         for (int s = 0; s < kVStages; ++s) {
             mbar_init(smem_u32(&c.v_full[s]), kVThreads);
-            mbar_init(smem_u32(&c.v_empty[s]), kCl);
+            mbar_init(smem_u32(&c.v_empty[s]), 1);
         }
-        for (int i = 0; i < 4; ++i) (&c.pdec[0][0])[i] = 0xffffffffu;
         for (int x = 0; x < 2; ++x) {
             mbar_init(smem_u32(&c.s_full[x]), 1);
             mbar_init(smem_u32(&c.p_full[x]), 4);
@@ -350,23 +276,10 @@ tc_pass_kernel(const TcParams p, const __grid_constant__ CUtensorMap qmap,
     }
     tc_fence_before();
     __syncthreads();
-    if (kCl == 2) cluster_sync();  // the peer's barriers are initialised before any multicast
     tc_fence_after();
     const uint32_t tbase = c.tmem_base;
     if (threadIdx.x == 0) tl_cta(p, 0);
     const int64_t total = a.tile_list ? a.num_tiles() : g.z * g.hq * p.pairs_per_head;
-    const uint32_t rank = kCl == 2 ? cluster_rank() : 0u;
-    const uint32_t peer = rank ^ 1u;
-    // kCl = 2: clusters take quads statically (cluster c: c, c + #clusters, ...); every warp of
-    // both CTAs walks the same sequence
-    const int64_t ncl = gridDim.x / kCl, cid = blockIdx.x / kCl;
-    auto next_item = [&](uint32_t wk) -> int64_t {
-        if (kCl == 2) {
-            const int64_t it = cid + (int64_t)wk * ncl;
-            return it < total ? it : -1;
-        }
-        return ring_get(c, wk, lane);
-    };
     const int64_t rowu = g.d;  // row unit of the tensor maps = D elements
 
     if (warp >= kMmaWarp) setmaxnreg_dec<kOtherRegs>();  // warpgroups 2-3
@@ -381,10 +294,8 @@ tc_pass_kernel(const TcParams p, const __grid_constant__ CUtensorMap qmap,
         const int nthr = kgrp ? kKThreads : kVThreads;
         const int lt = (warp - (kgrp ? kKWarp0 : kVWarp0)) * 32 + lane;
         const uint32_t gbar = kgrp ? 3 : 4;
-        constexpr int kKStep = kKThreads / 16, kVStep = kVThreads / 16;
-        const int ring_sz = kgrp ? TokRing<kKStep>::kSize : TokRing<kVStep>::kSize;
-        int32_t* ring0 = reinterpret_cast<int32_t*>(smem + kOffTok) + (kgrp ? 0 : 2 * TokRing<kKStep>::kSize);
-        auto ring_pos = [&](int row) { return kgrp ? TokRing<kKStep>::pos(row) : TokRing<kVStep>::pos(row); };
+        // token ring of the group: int32 [2 blocks][128 rows], row r of block j at ring0[(j & 1) * 128 + r]
+        int32_t* ring0 = reinterpret_cast<int32_t*>(smem + kOffTok) + (kgrp ? 0 : 2 * kBN);
         const CUtensorMap* xtile = kgrp ? &ktile : &vtile;
         const uint32_t xbase = kgrp ? sK : sV;
         const int nst = kgrp ? kKStages : kVStages;
@@ -393,15 +304,15 @@ tc_pass_kernel(const TcParams p, const __grid_constant__ CUtensorMap qmap,
         uint64_t* xempty = kgrp ? c.k_empty : c.v_empty;
         uint32_t gx = 0, qcount = 0;
         for (uint32_t wk = 0;; ++wk) {
-            if (kCl == 1 && kgrp && lt == 0) {  // producer: the next pair index (or -1) into ring slot wk & 3
+            if (kgrp && lt == 0) {  // producer: the next pair index (or -1) into ring slot wk & 3
                 mbar_wait(smem_u32(&c.w_empty[wk & 3]), ((wk >> 2) & 1) ^ 1, 5002);
                 const int64_t v = (int64_t)atomicAdd(a.work_ctr, 1);
                 *reinterpret_cast<volatile int64_t*>(&c.wq[wk & 3]) = v < total ? v : -1;
                 mbar_arrive(smem_u32(&c.w_full[wk & 3]));
             }
-            const int64_t it = next_item(wk);
+            const int64_t it = ring_get(c, wk, lane);
             if (it < 0) break;
-            const PairInfo P = pair_info<kCl>(p, it, rank);
+            const PairInfo P = pair_info(p, it);
             if (P.nb == 0) continue;
             const int32_t* kv = (P.np > 0) ? a.kv_seg(P.zh, P.n) : nullptr;
             named_bar_sync(gbar, nthr);  // every thread of the group is done with its ring
@@ -427,14 +338,19 @@ tc_pass_kernel(const TcParams p, const __grid_constant__ CUtensorMap qmap,
                                     tma_load2d(sQ + x * kTileBytes + h * kHalf, &qtile, h * 64,
                                                (int32_t)(qb + (P.sb + P.t0[x]) * qs), smem_u32(&c.q_full));
                 } else {
-                    // permuted Q rows: one TMA gather4 op per lane, (slot, row group, column half)
+                    // permuted Q rows: TMA gather4, 128 ops (slot, row group, column half), 32 per
+                    // warp with warp-uniform operands and one elected lane issuing (as for K/V)
                     // (A/B against 16-B cp.async: pass-2 6.03 -> 5.90 ms)
-                    const int x = lt >> 6, grp = (lt >> 1) & 31, h = lt & 1;
-                    if (P.has[x]) {
+                    const bool el = elect_one();
+                    const int wi = lt >> 5;
+                    for (int o = wi * 32; o < wi * 32 + 32; ++o) {
+                        const int x = o >> 6, grp = (o >> 1) & 31, h = o & 1;
+                        if (!P.has[x]) continue;
                         int32_t rr[4];
-                        for (int i = 0; i < 4; ++i) rr[i] = (int32_t)(qb + q_row(a, P, x, grp * 4 + i) * qs);
-                        tma_gather4(sQ + x * kTileBytes + h * kHalf + grp * 512, &qmap, h * 64, rr[0], rr[1], rr[2],
-                                    rr[3], smem_u32(&c.q_full));
+                        for (int i = 0; i < 4; ++i)
+                            rr[i] = __shfl_sync(0xffffffffu, (int32_t)(qb + q_row(a, P, x, grp * 4 + i) * qs), 0);
+                        if (el) tma_gather4(sQ + x * kTileBytes + h * kHalf + grp * 512, &qmap, h * 64, rr[0], rr[1],
+                                            rr[2], rr[3], smem_u32(&c.q_full));
                     }
                 }
                 if (lt == 0) tl_mark(p, 29, qcount);
@@ -457,10 +373,10 @@ tc_pass_kernel(const TcParams p, const __grid_constant__ CUtensorMap qmap,
             int nx = 0;
             for (int j = 0; j < P.nb; ++j) {
                 const bool gat = gathered(j);
-                int32_t* ring = ring0 + (j & 1) * ring_sz;
+                int32_t* ring = ring0 + (j & 1) * kBN;
                 if (gat)
                     for (int u = 0; u < 2; ++u)
-                        if (lt + u * nthr < kBN) ring[ring_pos(lt + u * nthr)] = tk[u];
+                        if (lt + u * nthr < kBN) ring[lt + u * nthr] = tk[u];
                 fetch_tok(j + 1, tk);  // prefetch (latency overlaps the stage wait)
                 if (gat) named_bar_sync(gbar, nthr);
                 const uint32_t gi = gx + j;
@@ -477,33 +393,11 @@ tc_pass_kernel(const TcParams p, const __grid_constant__ CUtensorMap qmap,
                 }
                 bool need = false;
                 for (int x = 0; x < 2; ++x) need |= participates(P, x, j) && !(stop_at[x] <= j - lag);
-                if (kCl == 2)  // the quad's stream: the peer's tiles count too (same answer in both CTAs)
-                    for (int x = 0; x < 2 && !need; ++x)
-                        need |= peer_participates(P, x, j) && !peer_stopped_by(c, P, wk, x, j - lag);
                 if (!need) break;
                 const uint32_t dst = xbase + st * kTileBytes;
                 if (lt == 0) mbar_expect_tx(smem_u32(&xfull[st]), kTileBytes);
                 else mbar_arrive(smem_u32(&xfull[st]));
-                if (kCl == 2) {
-                    // this CTA's 64-column half of the block, multicast to both CTAs
-                    const int h = (int)rank;
-                    if (!gat) {
-                        if (lt == 0)
-                            tma_load2d_mc(dst + h * kHalf, xtile, h * 64,
-                                          (int32_t)(xb + (P.sb + (int64_t)j * kBN) * xs), smem_u32(&xfull[st]), 3);
-                    } else {
-                        // 32 gather4 ops (row groups) on lanes 0-7 (K) / 0-10 (V) of the group's warps
-                        const int wl = lt & 31, wi = lt >> 5;
-                        const int per = kgrp ? 8 : 11;
-                        const int grp = wl < per ? wi * per + wl : 32;
-                        if (grp < 32) {
-                            int32_t rr[4];
-                            for (int i = 0; i < 4; ++i) rr[i] = (int32_t)(xb + (int64_t)ring[ring_pos(4 * grp + i)] * xs);
-                            tma_gather4_mc(dst + h * kHalf + grp * 512, kgrp ? &kmap : &vmap, h * 64, rr[0], rr[1], rr[2],
-                                           rr[3], smem_u32(&xfull[st]), 3);
-                        }
-                    }
-                } else if (!gat) {
+                if (!gat) {
                     if (lt == 0) {
                         const int64_t tok = P.sb + (int64_t)j * kBN;
                         for (int h = 0; h < 2; ++h)
@@ -512,16 +406,23 @@ tc_pass_kernel(const TcParams p, const __grid_constant__ CUtensorMap qmap,
                 } else {
                     // TMA tile::gather4 (A/B: 9 % faster pass-2 than 16-B cp.async, which competes with
                     // the tensor core for the LSU/shared-memory path): 64 ops (32 row groups x 2 column
-                    // halves) on lanes 0-15 (K) / 0-21 (V) of the group's warps
-                    const int wl = lt & 31, wi = lt >> 5;
+                    // halves), 16 per K warp / 22 per V warp. Each warp walks its ops with warp-uniform
+                    // operands (the 4 tokens of a row group are one broadcast 16-B shared load,
+                    // shuffled from lane 0 so they live in uniform registers) and one elected lane
+                    // issues: no per-lane operand waterfall, no per-lane row registers.
+                    const int wi = lt >> 5;
                     const int per = kgrp ? 16 : 22;
-                    const int opi = wl < per ? wi * per + wl : 64;
-                    if (opi < 64) {
-                        const int grp = opi >> 1, h = opi & 1;
-                        int32_t rr[4];
-                        for (int i = 0; i < 4; ++i) rr[i] = (int32_t)(xb + (int64_t)ring[ring_pos(4 * grp + i)] * xs);
-                        tma_gather4(dst + h * kHalf + grp * 512, kgrp ? &kmap : &vmap, h * 64, rr[0], rr[1], rr[2],
-                                    rr[3], smem_u32(&xfull[st]));
+                    const int o_end = min(64, (wi + 1) * per);
+                    const CUtensorMap* xmap = kgrp ? &kmap : &vmap;
+                    const bool el = elect_one();
+                    for (int o = wi * per; o < o_end; ++o) {
+                        const int grp = o >> 1, h = o & 1;
+                        const int4 t4 = *reinterpret_cast<const int4*>(ring + 4 * grp);
+                        const int32_t r0 = __shfl_sync(0xffffffffu, (int32_t)(xb + (int64_t)t4.x * xs), 0);
+                        const int32_t r1 = __shfl_sync(0xffffffffu, (int32_t)(xb + (int64_t)t4.y * xs), 0);
+                        const int32_t r2 = __shfl_sync(0xffffffffu, (int32_t)(xb + (int64_t)t4.z * xs), 0);
+                        const int32_t r3 = __shfl_sync(0xffffffffu, (int32_t)(xb + (int64_t)t4.w * xs), 0);
+                        if (el) tma_gather4(dst + h * kHalf + grp * 512, xmap, h * 64, r0, r1, r2, r3, smem_u32(&xfull[st]));
                     }
                 }
                 if (lt == 0) tl_mark(p, kgrp ? 10 : 2, gi);
@@ -562,14 +463,12 @@ tc_pass_kernel(const TcParams p, const __grid_constant__ CUtensorMap qmap,
             auto wait_k = [&](uint32_t gki) {
                 mbar_wait(smem_u32(&c.k_full[gki % kKStages]), (gki / kKStages) & 1, 2002);
                 tl_mark(p, 5, gki);
-                fence_proxy_async_smem();  // cp.async (generic proxy) writes -> UMMA reads
                 tc_fence_after();
             };
-            const uint32_t pdec_peer = kCl == 2 ? mapa(smem_u32(&c.pdec[0][0]), peer) : 0u;
             for (uint32_t wk = 0;; ++wk) {
-                const int64_t it = next_item(wk);
+                const int64_t it = ring_get(c, wk, lane);
                 if (it < 0) break;
-                const PairInfo P = pair_info<kCl>(p, it, rank);
+                const PairInfo P = pair_info(p, it);
                 if (P.nb == 0) continue;
                 mbar_wait(smem_u32(&c.q_full), qcount & 1, 2001);
                 tl_mark(p, 26, qcount);
@@ -580,9 +479,6 @@ tc_pass_kernel(const TcParams p, const __grid_constant__ CUtensorMap qmap,
                 auto need = [&](int j, int lag) {
                     bool n = false;
                     for (int x = 0; x < 2; ++x) n |= participates(P, x, j) && !(stop_at[x] <= j - lag);
-                    if (kCl == 2)  // the quad's stream (the loaders evaluate the same union)
-                        for (int x = 0; x < 2 && !n; ++x)
-                            n |= peer_participates(P, x, j) && !peer_stopped_by(c, P, wk, x, j - lag);
                     return n;
                 };
                 wait_k(gk);
@@ -608,7 +504,6 @@ tc_pass_kernel(const TcParams p, const __grid_constant__ CUtensorMap qmap,
                                 if (!v_ready) {
                                     mbar_wait(smem_u32(&c.v_full[gvi % kVStages]), (gvi / kVStages) & 1, 2005);
                                     tl_mark(p, 28, gki);
-                                    fence_proxy_async_smem();
                                     tc_fence_after();
                                     v_ready = true;
                                 }
@@ -637,20 +532,10 @@ tc_pass_kernel(const TcParams p, const __grid_constant__ CUtensorMap qmap,
                         }
                     }
                     if (has_v && !v_ready) mbar_wait(smem_u32(&c.v_full[gvi % kVStages]), (gvi / kVStages) & 1, 2006);
-                    if (kCl == 2 && leader)  // this CTA's decisions through block j, into the peer
-                        for (int x = 0; x < 2; ++x)
-                            st_cluster_u32(pdec_peer + (uint32_t)(((wk & 1) * 2 + x) * 4),
-                                           stop_at[x] <= j ? dec_word(wk, true, stop_at[x]) : dec_word(wk, false, j + 1));
                     // both slots' decisions on block j are read: the loader may reuse its stages
-                    // (kCl = 2: in both CTAs -- each stage holds halves loaded by both)
                     if (leader) {
-                        if (kCl == 2) {
-                            umma_commit_mc(smem_u32(&c.k_empty[gki % kKStages]), 3);
-                            if (has_v) umma_commit_mc(smem_u32(&c.v_empty[gvi % kVStages]), 3);
-                        } else {
-                            umma_commit(smem_u32(&c.k_empty[gki % kKStages]));
-                            if (has_v) umma_commit(smem_u32(&c.v_empty[gvi % kVStages]));
-                        }
+                        umma_commit(smem_u32(&c.k_empty[gki % kKStages]));
+                        if (has_v) umma_commit(smem_u32(&c.v_empty[gvi % kVStages]));
                     }
                     tl_mark(p, 8, gki);
                     ++nk;
@@ -676,7 +561,7 @@ tc_pass_kernel(const TcParams p, const __grid_constant__ CUtensorMap qmap,
         const float sc = p.scale_log2;
         uint32_t ns = 0, no = 0, npf = 0;
         for (uint32_t wk = 0;; ++wk) {
-            const int64_t it = next_item(wk);
+            const int64_t it = ring_get(c, wk, lane);
             if (it < 0) break;
             float m2, ell;
             float sacc = 1.0f;    // scale of the resumed accumulator (kStateIn)
@@ -686,7 +571,7 @@ tc_pass_kernel(const TcParams p, const __grid_constant__ CUtensorMap qmap,
             const bool tl_on = r == 0;
             {
             // 32-bit copies of what the block loop needs (keeps the 128 scores in registers)
-            const PairInfo P = pair_info<kCl>(p, it, rank);
+            const PairInfo P = pair_info(p, it);
             if (!P.has[x]) continue;
             if (tl_on) tl_mark(p, 11 + 4 * x, no);
             const int nd_x = P.nd[x], ndmax = P.ndmax, nb = P.nb;
@@ -875,7 +760,7 @@ tc_pass_kernel(const TcParams p, const __grid_constant__ CUtensorMap qmap,
                 if (!commit) break;
             }
             }  // block loop scope
-            const PairInfo P = pair_info<kCl>(p, it, rank);
+            const PairInfo P = pair_info(p, it);
             const bool valid = r < P.tn[x];
             const int64_t grow = q_row(a, P, x, r);
             const int64_t slot = P.zh * g.l + grow;
@@ -997,7 +882,6 @@ tc_pass_kernel(const TcParams p, const __grid_constant__ CUtensorMap qmap,
     }
     tc_fence_before();
     __syncthreads();
-    if (kCl == 2) cluster_sync();  // no CTA leaves while its peer may still multicast into it
     if (threadIdx.x == 0) tl_cta(p, 3);
     if (warp == 0) tmem_dealloc(tbase, kTmemCols);
 }
@@ -1586,47 +1470,15 @@ cudaError_t launch_tc_pass(const PassArgs& a, cudaStream_t st) {
         tc_diag_kernel<<<grid, kDThreads, kDSmemBytes, st>>>(pd, qtile, ktile, vtile);
         return cudaGetLastError();
     }
-    for (const void* f : {(const void*)tc_pass_kernel<false, 1>, (const void*)tc_pass_kernel<true, 1>,
-                          (const void*)tc_pass_kernel<true, 2>})
+    for (const void* f : {(const void*)tc_pass_kernel<false>, (const void*)tc_pass_kernel<true>})
         if (cudaError_t e = smem_attr(f, kSmemBytes)) return e;
-    // Opt-in (S2O_CLUSTER=1): prefix passes over whole segments on 2-CTA clusters with multicast
-    // K/V (quads of tiles). It halves the TMA gather ops and L2 reads per SM, but the two CTAs'
-    // pipelines are coupled stage by stage (a stage is free only when both MMA warps released
-    // it; a quad's stream runs until all four tiles stopped) and that coupling costs more than
-    // the loads save: pass-2 at C3 7.20 ms vs 6.05 ms for the single-CTA pair kernel (same box,
-    // round 2), so the pair kernel stays the default.
-    static const bool cluster_on = [] {
-        const char* e = std::getenv("S2O_CLUSTER");
-        return e && std::strcmp(e, "1") == 0;
-    }();
-    if ((a.mode & kPrefix) && !a.tile_list && cluster_on && sms >= 2) {
-        TcParams p2 = p;
-        p2.pairs_full = (a.T + 3) / 4;  // quads per full segment
-        p2.pairs_per_head = (g.N - 1) * p2.pairs_full + (t_last + 3) / 4;
-        const int64_t work2 = g.z * g.hq * p2.pairs_per_head;
-        if (work2 == 0) return cudaSuccess;
-        const int clusters = (int)std::max<int64_t>(1, std::min<int64_t>(work2, sms / 2));
-        cudaLaunchConfig_t lc = {};
-        lc.gridDim = dim3(2 * clusters);
-        lc.blockDim = dim3(kThreads);
-        lc.dynamicSmemBytes = kSmemBytes;
-        lc.stream = st;
-        cudaLaunchAttribute at[1];
-        at[0].id = cudaLaunchAttributeClusterDimension;
-        at[0].val.clusterDim.x = 2;
-        at[0].val.clusterDim.y = 1;
-        at[0].val.clusterDim.z = 1;
-        lc.attrs = at;
-        lc.numAttrs = 1;
-        return cudaLaunchKernelEx(&lc, tc_pass_kernel<true, 2>, p2, qmap, kmap, vmap, qtile, ktile, vtile);
-    }
     const int64_t work = a.tile_list ? a.max_tiles() : g.z * g.hq * p.pairs_per_head;
     if (work == 0) return cudaSuccess;
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(work, sms));
     if (a.mode & kPrefix)
-        tc_pass_kernel<true, 1><<<grid, kThreads, kSmemBytes, st>>>(p, qmap, kmap, vmap, qtile, ktile, vtile);
+        tc_pass_kernel<true><<<grid, kThreads, kSmemBytes, st>>>(p, qmap, kmap, vmap, qtile, ktile, vtile);
     else
-        tc_pass_kernel<false, 1><<<grid, kThreads, kSmemBytes, st>>>(p, qmap, kmap, vmap, qtile, ktile, vtile);
+        tc_pass_kernel<false><<<grid, kThreads, kSmemBytes, st>>>(p, qmap, kmap, vmap, qtile, ktile, vtile);
     return cudaGetLastError();
 }
 

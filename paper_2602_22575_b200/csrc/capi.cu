@@ -506,6 +506,32 @@ s2o_status s2o_segment_representatives(const s2o_problem* p, const void* q, cons
     return S2O_OK;
 }
 
+s2o_status s2o_rank_queries(const s2o_problem* p, const void* q, const float* guide, int64_t seg_len,
+                            int32_t* q_perm, void* workspace, size_t workspace_bytes, void* stream) {
+    Geo g;
+    s2o_status st = make_geo(p, seg_len, &g);
+    if (st) return st;
+    if (!q || !guide || !q_perm) return fail(S2O_ERR_INVALID_ARG, "null pointer");
+    if (!workspace || workspace_bytes < plan_workspace_bytes(g)) return fail(S2O_ERR_WORKSPACE, "workspace too small");
+    S2O_CUDA_TRY(launch_rank_queries(g, q, guide, q_perm, workspace, reinterpret_cast<cudaStream_t>(stream)),
+                 "rank queries");
+    g_err.clear();
+    return S2O_OK;
+}
+
+s2o_status s2o_rank_prefix_keys(const s2o_problem* p, const void* k, const float* q_mean, int64_t seg_len,
+                                int32_t* kv_perm, void* workspace, size_t workspace_bytes, void* stream) {
+    Geo g;
+    s2o_status st = make_geo(p, seg_len, &g);
+    if (st) return st;
+    if (!k || !q_mean || (g.N > 1 && !kv_perm)) return fail(S2O_ERR_INVALID_ARG, "null pointer");
+    if (!workspace || workspace_bytes < plan_workspace_bytes(g)) return fail(S2O_ERR_WORKSPACE, "workspace too small");
+    S2O_CUDA_TRY(launch_rank_prefix_keys(g, k, q_mean, kv_perm, workspace, reinterpret_cast<cudaStream_t>(stream)),
+                 "rank prefix keys");
+    g_err.clear();
+    return S2O_OK;
+}
+
 s2o_status s2o_plan_build(const s2o_problem* p, const void* q, const void* k,
                           const s2o_kernel_config* cfg, int32_t* q_perm, int32_t* kv_perm,
                           int64_t* cost2, void* workspace, size_t workspace_bytes, void* stream) {

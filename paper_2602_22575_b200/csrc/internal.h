@@ -105,6 +105,10 @@ cudaError_t launch_plan_level_dev(const Geo& g, const int32_t* seg_list, const i
                                   int32_t* flags, void* workspace, cudaStream_t st);
 cudaError_t launch_segment_means(const Geo& g, const void* x, int which_kv, int64_t nseg_out,
                                  float* out, cudaStream_t st);
+cudaError_t launch_rank_queries(const Geo& g, const void* q, const float* guide, int32_t* q_perm, void* workspace,
+                                cudaStream_t st);
+cudaError_t launch_rank_prefix_keys(const Geo& g, const void* k, const float* q_mean, int32_t* kv_perm,
+                                    void* workspace, cudaStream_t st);
 
 // generic SIMT fp64 path
 size_t generic_scratch_bytes(const PassArgs& a);

@@ -1230,6 +1230,34 @@ cudaError_t launch_segment_means(const Geo& g, const void* x, int which_kv, int6
     return cudaGetLastError();
 }
 
+// rank_queries (plan.cpp:69-101) with a caller-given guide per (z, q head) [Z, Hq, D] fp32: the q
+// ranking kernels index the guide per kv head, so run them on a view with one kv head per q head.
+cudaError_t launch_rank_queries(const Geo& g, const void* q, const float* guide, int32_t* q_perm, void* workspace,
+                                cudaStream_t st) {
+    PlanWs ws;
+    char* base = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(workspace) + 255) & ~uintptr_t(255));
+    plan_ws_layout(g, base, &ws);
+    Geo gq = g;
+    gq.hkv = g.hq;
+    gq.group = 1;
+    cudaError_t err;
+    if ((err = launch_q_rank(gq, q, guide, ws.q_mean, ws.key0, q_perm, st)) != cudaSuccess) return err;
+    if (g.S > kRun && (err = sort_family(0, gq, ws, q_perm, st)) != cudaSuccess) return err;
+    return cudaSuccess;
+}
+
+// rank_prefix_keys (plan.cpp:103-138) with caller-given segment representatives q_mean [Z, Hq, N, D].
+cudaError_t launch_rank_prefix_keys(const Geo& g, const void* k, const float* q_mean, int32_t* kv_perm,
+                                    void* workspace, cudaStream_t st) {
+    if (g.N < 2) return cudaSuccess;
+    PlanWs ws;
+    char* base = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(workspace) + 255) & ~uintptr_t(255));
+    plan_ws_layout(g, base, &ws);
+    cudaError_t err;
+    if ((err = launch_kv_score(g, k, q_mean, ws.key0, st)) != cudaSuccess) return err;
+    return sort_family(1, g, ws, kv_perm, st);
+}
+
 cudaError_t launch_plan_build(const Geo& g, const void* q, const void* k, int32_t* q_perm,
                               int32_t* kv_perm, void* workspace, cudaStream_t st) {
     PlanWs ws;

@@ -93,31 +93,7 @@ __device__ __forceinline__ bool elect_one() {
     return pred != 0;
 }
 
-// Wait with cluster-scope acquire (the phase was completed by an arrive from the peer CTA).
-__device__ __forceinline__ void mbar_wait_cluster(uint32_t bar, uint32_t parity, int tag = 0) {
-    uint32_t spins = 0;
-    for (;;) {
-        uint32_t ok;
-        asm volatile(
-            "{\n\t.reg .pred p;\n\t"
-            "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
-            "selp.u32 %0, 1, 0, p;\n\t}"
-            : "=r"(ok)
-            : "r"(bar), "r"(parity)
-            : "memory");
-        if (ok) return;
-        if (tag != 0 && ++spins == (1u << 24)) {
-            printf("s2o watchdog: block %d thread %d tag %d parity %u\n", (int)blockIdx.x, (int)threadIdx.x,
-                   tag, parity);
-            __trap();
-        }
-    }
-}
 
-// ------------------------------------------------------------------ fences / barriers
-__device__ __forceinline__ void fence_proxy_async_smem() {
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-}
 __device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t count) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
 }
@@ -244,16 +220,6 @@ __device__ __forceinline__ void umma_commit(uint32_t bar) {
                  : "memory");
 }
 
-// ------------------------------------------------------------------ copies
-// 16-byte cp.async; bytes < 16 zero-fills the tail (0 -> all zeros).
-__device__ __forceinline__ void cp_async16(uint32_t sdst, const void* gsrc, uint32_t src_bytes) {
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(sdst), "l"(gsrc), "r"(src_bytes)
-                 : "memory");
-}
-// Arrive (counted, no increment) on `bar` once this thread's prior cp.asyncs land.
-__device__ __forceinline__ void cp_async_arrive_noinc(uint32_t bar) {
-    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(bar) : "memory");
-}
 
 // TMA: gather 4 rows (row indices r0..r3) of a 2-D tensor map starting at column col.
 __device__ __forceinline__ void tma_gather4(uint32_t sdst, const CUtensorMap* map, int32_t col, int32_t r0,
@@ -385,69 +351,6 @@ __device__ __forceinline__ float ex2(float x) {
     float y;
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
     return y;
-}
-
-// ------------------------------------------------------------------ CTA pair (cta_group::2)
-__device__ __forceinline__ uint32_t cluster_rank() {
-    uint32_t r;
-    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
-    return r;
-}
-// shared::cluster address of the same-offset object in CTA `rank` of the cluster
-__device__ __forceinline__ uint32_t mapa(uint32_t smem_addr, uint32_t rank) {
-    uint32_t r;
-    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_addr), "r"(rank));
-    return r;
-}
-__device__ __forceinline__ void cluster_sync() {
-    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-}
-__device__ __forceinline__ void fence_acq_rel_cluster() { asm volatile("fence.acq_rel.cluster;" ::: "memory"); }
-__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cl_addr) {
-    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cl_addr) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx_cluster(uint32_t cl_addr, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.release.cluster.shared::cluster.b64 _, [%0], %1;" ::"r"(cl_addr),
-                 "r"(bytes)
-                 : "memory");
-}
-__device__ __forceinline__ void st_cluster_u32(uint32_t cl_addr, uint32_t v) {
-    asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(cl_addr), "r"(v) : "memory");
-}
-__device__ __forceinline__ void st_cluster_u8(uint32_t cl_addr, uint32_t v) {
-    asm volatile("st.shared::cluster.u8 [%0], %1;" ::"r"(cl_addr), "r"(v) : "memory");
-}
-// Cluster multicast (2-CTA clusters of the pass kernel): the same smem offset (data and
-// mbarrier) in every CTA of `mask` receives the bytes; complete_tx lands on each destination's
-// barrier. sdst / bar are this CTA's shared::cta addresses (valid shared::cluster addresses).
-__device__ __forceinline__ void tma_gather4_mc(uint32_t sdst, const CUtensorMap* map, int32_t col, int32_t r0,
-                                               int32_t r1, int32_t r2, int32_t r3, uint32_t bar, uint16_t mask) {
-    asm volatile(
-        "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes.multicast::cluster "
-        "[%0], [%1, {%2, %3, %4, %5, %6}], [%7], %8;" ::"r"(sdst),
-        "l"(reinterpret_cast<uint64_t>(map)), "r"(col), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(bar), "h"(mask)
-        : "memory");
-}
-__device__ __forceinline__ void tma_load2d_mc(uint32_t sdst, const CUtensorMap* map, int32_t col, int32_t row,
-                                              uint32_t bar, uint16_t mask) {
-    asm volatile(
-        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster "
-        "[%0], [%1, {%2, %3}], [%4], %5;" ::"r"(sdst),
-        "l"(reinterpret_cast<uint64_t>(map)), "r"(col), "r"(row), "r"(bar), "h"(mask)
-        : "memory");
-}
-// Arrive on the same-offset mbarrier of every CTA in `mask` once all earlier MMAs of this thread
-// completed.
-__device__ __forceinline__ void umma_commit_mc(uint32_t bar, uint16_t mask) {
-    asm volatile(
-        "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(bar),
-        "h"(mask)
-        : "memory");
-}
-__device__ __forceinline__ uint32_t ld_volatile_u32(uint32_t saddr) {
-    uint32_t v;
-    asm volatile("ld.volatile.shared::cta.u32 %0, [%1];" : "=r"(v) : "r"(saddr) : "memory");
-    return v;
 }
 
 }  // namespace sm100
