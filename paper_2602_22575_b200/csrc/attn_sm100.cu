@@ -338,19 +338,14 @@ tc_pass_kernel(const TcParams p, const __grid_constant__ CUtensorMap qmap,
                                     tma_load2d(sQ + x * kTileBytes + h * kHalf, &qtile, h * 64,
                                                (int32_t)(qb + (P.sb + P.t0[x]) * qs), smem_u32(&c.q_full));
                 } else {
-                    // permuted Q rows: TMA gather4, 128 ops (slot, row group, column half), 32 per
-                    // warp with warp-uniform operands and one elected lane issuing (as for K/V)
+                    // permuted Q rows: one TMA gather4 op per lane, (slot, row group, column half)
                     // (A/B against 16-B cp.async: pass-2 6.03 -> 5.90 ms)
-                    const bool el = elect_one();
-                    const int wi = lt >> 5;
-                    for (int o = wi * 32; o < wi * 32 + 32; ++o) {
-                        const int x = o >> 6, grp = (o >> 1) & 31, h = o & 1;
-                        if (!P.has[x]) continue;
+                    const int x = lt >> 6, grp = (lt >> 1) & 31, h = lt & 1;
+                    if (P.has[x]) {
                         int32_t rr[4];
-                        for (int i = 0; i < 4; ++i)
-                            rr[i] = __shfl_sync(0xffffffffu, (int32_t)(qb + q_row(a, P, x, grp * 4 + i) * qs), 0);
-                        if (el) tma_gather4(sQ + x * kTileBytes + h * kHalf + grp * 512, &qmap, h * 64, rr[0], rr[1],
-                                            rr[2], rr[3], smem_u32(&c.q_full));
+                        for (int i = 0; i < 4; ++i) rr[i] = (int32_t)(qb + q_row(a, P, x, grp * 4 + i) * qs);
+                        tma_gather4(sQ + x * kTileBytes + h * kHalf + grp * 512, &qmap, h * 64, rr[0], rr[1], rr[2],
+                                    rr[3], smem_u32(&c.q_full));
                     }
                 }
                 if (lt == 0) tl_mark(p, 29, qcount);
@@ -360,10 +355,11 @@ tc_pass_kernel(const TcParams p, const __grid_constant__ CUtensorMap qmap,
             const int64_t xs = (kgrp ? g.ks[2] : g.vs[2]) / rowu;
             const auto gathered = [&](int j) { return !(j < P.ndmax && p.kv_contig); };
             // tokens of block j: entries lt and lt + nthr (< 128) in registers, one block ahead
+            // (stored as tensor-map row coordinates xb + token * xs, ready for the gather ops)
             auto fetch_tok = [&](int j, int32_t (&tk)[2]) {
                 for (int u = 0; u < 2; ++u) {
                     const int i = lt + u * nthr;
-                    tk[u] = (i < kBN && j < P.nb && gathered(j)) ? (int32_t)key_token(P, kv, j, i) : 0;
+                    tk[u] = (i < kBN && j < P.nb && gathered(j)) ? (int32_t)(xb + key_token(P, kv, j, i) * xs) : 0;
                 }
             };
             int32_t tk[2];
@@ -406,23 +402,18 @@ tc_pass_kernel(const TcParams p, const __grid_constant__ CUtensorMap qmap,
                 } else {
                     // TMA tile::gather4 (A/B: 9 % faster pass-2 than 16-B cp.async, which competes with
                     // the tensor core for the LSU/shared-memory path): 64 ops (32 row groups x 2 column
-                    // halves), 16 per K warp / 22 per V warp. Each warp walks its ops with warp-uniform
-                    // operands (the 4 tokens of a row group are one broadcast 16-B shared load,
-                    // shuffled from lane 0 so they live in uniform registers) and one elected lane
-                    // issues: no per-lane operand waterfall, no per-lane row registers.
-                    const int wi = lt >> 5;
+                    // halves) on lanes 0-15 (K) / 0-21 (V) of the group's warps. Per-lane operands (the
+                    // compiler issues them lane by lane); an elected-lane loop over warp-uniform operands
+                    // measured slower (pass-2 6.05 -> 7.09 ms at C3: the serial per-op shuffle and load
+                    // latencies outweigh the waterfall).
+                    const int wl = lt & 31, wi = lt >> 5;
                     const int per = kgrp ? 16 : 22;
-                    const int o_end = min(64, (wi + 1) * per);
-                    const CUtensorMap* xmap = kgrp ? &kmap : &vmap;
-                    const bool el = elect_one();
-                    for (int o = wi * per; o < o_end; ++o) {
-                        const int grp = o >> 1, h = o & 1;
+                    const int opi = wl < per ? wi * per + wl : 64;
+                    if (opi < 64) {
+                        const int grp = opi >> 1, h = opi & 1;
                         const int4 t4 = *reinterpret_cast<const int4*>(ring + 4 * grp);
-                        const int32_t r0 = __shfl_sync(0xffffffffu, (int32_t)(xb + (int64_t)t4.x * xs), 0);
-                        const int32_t r1 = __shfl_sync(0xffffffffu, (int32_t)(xb + (int64_t)t4.y * xs), 0);
-                        const int32_t r2 = __shfl_sync(0xffffffffu, (int32_t)(xb + (int64_t)t4.z * xs), 0);
-                        const int32_t r3 = __shfl_sync(0xffffffffu, (int32_t)(xb + (int64_t)t4.w * xs), 0);
-                        if (el) tma_gather4(dst + h * kHalf + grp * 512, xmap, h * 64, r0, r1, r2, r3, smem_u32(&xfull[st]));
+                        tma_gather4(dst + h * kHalf + grp * 512, kgrp ? &kmap : &vmap, h * 64, t4.x, t4.y, t4.z, t4.w,
+                                    smem_u32(&xfull[st]));
                     }
                 }
                 if (lt == 0) tl_mark(p, kgrp ? 10 : 2, gi);
