@@ -77,9 +77,6 @@ constexpr int kLaunchRegs = 65536 / kThreads / 8 * 8;  // 128: what __launch_bou
 static_assert(kSoftmaxRegs - kLaunchRegs <= kLaunchRegs - kOtherRegs, "register pool overcommitted");
 static_assert(sizeof(uint64_t) * 31 + 4 + 64 + 8 <= 512, "Ctrl exceeds its 512 B");
 constexpr float kRescaleThresh = 8.0f;
-#ifndef S2O_POLY_MOD
-#define S2O_POLY_MOD 0  // pass-2 softmax: every n-th exponential pair on the FMA pipe (0 = all MUFU)
-#endif
   // lazy max update, log2 units (factor 256)
 
 struct Ctrl {
@@ -655,14 +652,7 @@ tc_pass_kernel(const TcParams p, const __grid_constant__ CUtensorMap qmap,
                                 for (int i = 0; i < 32; i += 2) {
                                     const float2 arg = ffma2(make_float2(__uint_as_float(sv[c0 + i]), __uint_as_float(sv[c0 + i + 1])),
                                                              sc2, nr2);
-#if S2O_POLY_MOD > 0
-                                    // every S2O_POLY_MOD-th pair on the FMA pipe (MUFU offload)
-                                    const float2 e = ((i >> 1) % S2O_POLY_MOD == S2O_POLY_MOD - 1)
-                                                         ? ex2_poly4x2(arg)
-                                                         : make_float2(ex2(arg.x), ex2(arg.y));
-#else
                                     const float2 e = make_float2(ex2(arg.x), ex2(arg.y));
-#endif
                                     rs2[(i >> 1) & 1] = fadd2(rs2[(i >> 1) & 1], e);
                                     pk[i >> 1] = pack_bf16(e.x, e.y);
                                 }
@@ -899,11 +889,6 @@ tc_pass_kernel(const TcParams p, const __grid_constant__ CUtensorMap qmap,
 // tensor pipe executes in order, so the new S overwrites P(j) only after P V(j) read it).
 // pv_done[b] completes once per P V on buffer b: a softmax that must rescale O at block gb (lazy
 // max update, rare) first waits for P V(gb-1), i.e. all earlier P V of the tile.
-#ifdef S2O_DIAG_NOEXP  // dev timing aid: exponentials replaced by a multiply (results are garbage)
-#define DX2(x) ((x) * 0.5f)
-#else
-#define DX2(x) ex2(x)
-#endif
 #ifndef S2O_DIAG_POLY
 #define S2O_DIAG_POLY 8  // diagonal kernel: every n-th exponential pair on the FMA pipe (0 = all MUFU; A/B: 8 -3 %, 4 even)
 #endif
@@ -1047,10 +1032,6 @@ tc_diag_kernel(const TcParams p, const __grid_constant__ CUtensorMap qtile,
             for (int j = 0; j < t.nd; ++j, ++gi) {
                 const int st = gi % nst;
                 mbar_wait(smem_u32(&xempty[st]), ((gi / nst) & 1) ^ 1, kl ? 4002 : 4003);
-#ifdef S2O_DIAG_NOLOAD  // dev timing aid: no K/V data movement (results are garbage)
-                mbar_arrive(smem_u32(&xfull[st]));
-                continue;
-#endif
                 mbar_expect_tx(smem_u32(&xfull[st]), kTileBytes);
                 const uint32_t dst = xbase + st * kTileBytes;
                 for (int h = 0; h < 2; ++h)
@@ -1110,7 +1091,7 @@ tc_diag_kernel(const TcParams p, const __grid_constant__ CUtensorMap qtile,
 #pragma unroll
                 for (int kk = 0; kk < kBN / 16; ++kk)
                     if (leader)
-                        umma_bf16_ts(tbase + (kDSBuf + ob) * 128, tbase + (blk % kDSBuf) * 128 + kk * 8,
+                        umma_bf16_ts(tbase + (kDSBuf + ob) * 128, tbase + (blk % kDSBuf) * 128 + kk * 8 + (kk >= 4 ? 32 : 0),
                                      dv + ((kk * 16 * 128) >> 4), idesc_o, (kk > 0 || j > 0) ? 1 : 0);
                 if (leader) {
                     umma_commit(smem_u32(&c.pv_done[blk % kDSBuf]));
@@ -1177,59 +1158,73 @@ tc_diag_kernel(const TcParams p, const __grid_constant__ CUtensorMap qtile,
                         mxa[(i >> 1) & 7] = fmax3(mxa[(i >> 1) & 7], i < lim ? __uint_as_float(sv[i]) : -INFINITY,
                                                   i + 1 < lim ? __uint_as_float(sv[i + 1]) : -INFINITY);
                 }
-                float mx = fmax3(fmax3(mxa[0], mxa[1], mxa[2]), fmax3(mxa[3], mxa[4], mxa[5]), fmaxf(mxa[6], mxa[7]));
-                // exchange with the other half (double-buffered by block parity): after this barrier
-                // both halves have also finished reading S, so P may overwrite it
+                const float mx_h = fmax3(fmax3(mxa[0], mxa[1], mxa[2]), fmax3(mxa[3], mxa[4], mxa[5]),
+                                         fmaxf(mxa[6], mxa[7])) * sc;
+                // P = exp2(s * scale - m_use) in bf16 into this half's own S columns [64h, 64h + 32)
+                // (so neither half waits for the other to finish reading S), rowsum in fp32
+                float rs[4];
+                auto exps = [&](float m_use) {
+                    const float neg_ref = (m_use == -INFINITY) ? 0.0f : -m_use;
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) rs[i] = 0.0f;
+                    if (full) {
+#pragma unroll
+                        for (int c0 = 0; c0 < 64; c0 += 32) {
+                            uint32_t pk[16];
+#pragma unroll
+                            for (int i = 0; i < 32; i += 2) {
+                                float e0, e1;
+#if S2O_DIAG_POLY > 0
+                                if ((i >> 1) % S2O_DIAG_POLY == S2O_DIAG_POLY - 1) {  // FMA-pipe exp2 (MUFU offload)
+                                    const float2 e = ex2_poly4x2(make_float2(fmaf(__uint_as_float(sv[c0 + i]), sc, neg_ref),
+                                                                             fmaf(__uint_as_float(sv[c0 + i + 1]), sc, neg_ref)));
+                                    e0 = e.x;
+                                    e1 = e.y;
+                                } else
+#endif
+                                {
+                                    e0 = ex2(fmaf(__uint_as_float(sv[c0 + i]), sc, neg_ref));
+                                    e1 = ex2(fmaf(__uint_as_float(sv[c0 + i + 1]), sc, neg_ref));
+                                }
+                                rs[(i >> 1) & 3] += e0 + e1;
+                                pk[i >> 1] = pack_bf16(e0, e1);
+                            }
+                            tmem_st16(tS + h * 64 + c0 / 2, pk);
+                        }
+                    } else {
+#pragma unroll
+                        for (int c0 = 0; c0 < 64; c0 += 32) {
+                            uint32_t pk[16];
+#pragma unroll
+                            for (int i = 0; i < 32; i += 2) {
+                                const float e0 = c0 + i < lim ? ex2(fmaf(__uint_as_float(sv[c0 + i]), sc, neg_ref)) : 0.0f;
+                                const float e1 =
+                                    c0 + i + 1 < lim ? ex2(fmaf(__uint_as_float(sv[c0 + i + 1]), sc, neg_ref)) : 0.0f;
+                                rs[(i >> 1) & 3] += e0 + e1;
+                                pk[i >> 1] = pack_bf16(e0, e1);
+                            }
+                            tmem_st16(tS + h * 64 + c0 / 2, pk);
+                        }
+                    }
+                };
+                // Row max across the two halves (smem, double-buffered by block parity, one named
+                // barrier per warp pair and block). Lazy rescaling keeps the reference m2 unless the
+                // block max exceeds it by kRescaleThresh, so when this half stays below that the
+                // exponentials start at once with m2 (speculation) and the exchange comes after;
+                // only if the other half's max forces a rescale are this half's P recomputed.
                 float* xb = xch + (gb & 1) * 256;
-                xb[h * 128 + r] = mx;
+                xb[h * 128 + r] = mx_h;
+                const bool spec = __all_sync(0xffffffffu, m2 != -INFINITY && mx_h <= m2 + kRescaleThresh);
+                float m_use = m2;
+                if (spec) exps(m2);
                 named_bar_sync(1 + q, 64);
-                mx = fmaxf(mx, xb[(1 - h) * 128 + r]) * sc;
+                const float mx = fmaxf(mx_h, xb[(1 - h) * 128 + r]);
                 if (threadIdx.x == 0) tl_mark(p, 25, gb);
                 const float m_new = fmaxf(m2, mx);
                 const bool rescale = (m_new > m2 + kRescaleThresh) || (m2 == -INFINITY);
-                const float m_use = rescale ? m_new : m2;
-                const float neg_ref = (m_use == -INFINITY) ? 0.0f : -m_use;
-                const float alpha = (m2 == -INFINITY) ? 0.0f : ex2(m2 + neg_ref);
-                float rs[4] = {0.0f, 0.0f, 0.0f, 0.0f};
-                if (full) {
-#pragma unroll
-                    for (int c0 = 0; c0 < 64; c0 += 32) {
-                        uint32_t pk[16];
-#pragma unroll
-                        for (int i = 0; i < 32; i += 2) {
-                            float e0, e1;
-#if S2O_DIAG_POLY > 0
-                            if ((i >> 1) % S2O_DIAG_POLY == S2O_DIAG_POLY - 1) {  // FMA-pipe exp2 (MUFU offload)
-                                const float2 e = ex2_poly4x2(make_float2(fmaf(__uint_as_float(sv[c0 + i]), sc, neg_ref),
-                                                                         fmaf(__uint_as_float(sv[c0 + i + 1]), sc, neg_ref)));
-                                e0 = e.x;
-                                e1 = e.y;
-                            } else
-#endif
-                            {
-                                e0 = DX2(fmaf(__uint_as_float(sv[c0 + i]), sc, neg_ref));
-                                e1 = DX2(fmaf(__uint_as_float(sv[c0 + i + 1]), sc, neg_ref));
-                            }
-                            rs[(i >> 1) & 3] += e0 + e1;
-                            pk[i >> 1] = pack_bf16(e0, e1);
-                        }
-                        tmem_st16(tS + h * 32 + c0 / 2, pk);
-                    }
-                } else {
-#pragma unroll
-                    for (int c0 = 0; c0 < 64; c0 += 32) {
-                        uint32_t pk[16];
-#pragma unroll
-                        for (int i = 0; i < 32; i += 2) {
-                            const float e0 = c0 + i < lim ? DX2(fmaf(__uint_as_float(sv[c0 + i]), sc, neg_ref)) : 0.0f;
-                            const float e1 =
-                                c0 + i + 1 < lim ? DX2(fmaf(__uint_as_float(sv[c0 + i + 1]), sc, neg_ref)) : 0.0f;
-                            rs[(i >> 1) & 3] += e0 + e1;
-                            pk[i >> 1] = pack_bf16(e0, e1);
-                        }
-                        tmem_st16(tS + h * 32 + c0 / 2, pk);
-                    }
-                }
+                if (rescale) m_use = m_new;
+                if (!spec || __any_sync(0xffffffffu, rescale)) exps(m_use);  // rows without a rescale: same values
+                const float alpha = (m2 == -INFINITY) ? 0.0f : ex2(m2 - m_use);
                 const float rowsum = (rs[0] + rs[1]) + (rs[2] + rs[3]);
                 // O rescale (lazy, rare; this half's 64 columns): all earlier P V of the tile done
                 if (__any_sync(0xffffffffu, j > 0 && rescale && m2 != -INFINITY)) {

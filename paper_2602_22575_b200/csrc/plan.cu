@@ -544,161 +544,6 @@ kv_score128_kernel(const __nv_bfloat16* __restrict__ k, Geo g, const float* __re
     }
 }
 
-// kv scoring v2 for the product shape (bf16 K, D = 128, S % 512 == 0): the same register-tiled
-// fp64 GEMM S[pairs x keys] = q_mean . K^T (8 x 8 accumulators per thread, each output summed over
-// d = 0..127 in order from 0.0 with DFMA: exactly dot_f's sequence, plan.cpp:14-20), but K is staged
-// in shared memory already converted to fp64 -- the bf16 -> fp64 conversions (F2F, 1 per 8 DFMA in
-// kv_score128_kernel) leave the inner loop, which is then 64 DFMA + 8 conflict-free LDS.128 per
-// lane per d. One CTA per SM (256 threads, 8 warps of 32 pairs x 64 keys); K goes through shared
-// memory in d-chunks, double-buffered: the next chunk's bf16 rows are fetched into registers while
-// the current chunk is consumed. Tile: 64 pairs x 256 keys; a remainder of <= 32 pairs of a key
-// block runs as one 32 x 512 tile over two key blocks of the same segment (WIDE).
-template <bool WIDE>
-struct KsCfg {
-    static constexpr int NP = WIDE ? 32 : 64;     // pairs per tile
-    static constexpr int NK = WIDE ? 512 : 256;   // keys per tile
-    static constexpr int DC = WIDE ? 16 : 32;     // d per staged chunk (DC * NK * 8 B = 64 KB)
-    static constexpr int NCH = 128 / DC;
-    static constexpr int PIECES = DC / 8;         // 16-B bf16 pieces per key row and chunk
-    static constexpr int LOADS = NK * PIECES / 256;  // uint4 per thread per chunk (4)
-    static constexpr size_t kSmem = sizeof(double) * (128 * NP + 2 * DC * NK);
-};
-constexpr int kKS2_Threads = 256;
-constexpr int kKS2_Keys = 256;  // key block (grid unit) = the narrow tile's keys
-
-template <bool WIDE>
-__device__ __forceinline__ void ks2_tile(const __nv_bfloat16* __restrict__ kbase, int64_t kstride, const Geo& g,
-                                         const float* __restrict__ q_mean, uint64_t* __restrict__ kvkey,
-                                         int64_t z, int64_t kvh, int64_t t0, int64_t n_lo, int64_t nsegs,
-                                         int64_t p0, int64_t pairs, unsigned char* smem) {
-    using C = KsCfg<WIDE>;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    double* Qd = reinterpret_cast<double*>(smem);  // [128 d][NP]
-    double* Kd = Qd + 128 * C::NP;                 // [2][DC][NK]
-    // q_mean rows of the tile's pairs -> fp64, transposed
-    for (int e = tid; e < C::NP * 32; e += kKS2_Threads) {
-        const int qp = e / 32, c4 = e % 32;
-        const int64_t pq = p0 + qp;
-        float4 x = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (pq < pairs) {
-            const int64_t h = kvh * g.group + pq / nsegs, n = n_lo + pq % nsegs;
-            x = reinterpret_cast<const float4*>(q_mean + ((z * g.hq + h) * g.N + n) * 128)[c4];
-        }
-        Qd[(4 * c4 + 0) * C::NP + qp] = (double)x.x;
-        Qd[(4 * c4 + 1) * C::NP + qp] = (double)x.y;
-        Qd[(4 * c4 + 2) * C::NP + qp] = (double)x.z;
-        Qd[(4 * c4 + 3) * C::NP + qp] = (double)x.w;
-    }
-    // K chunk fetch: thread -> (key = e % NK, piece = e / NK) for e = tid + 256 i
-    uint4 kr[C::LOADS];
-    auto fetch = [&](int ch) {
-#pragma unroll
-        for (int i = 0; i < C::LOADS; ++i) {
-            const int e = tid + i * kKS2_Threads, key = e % C::NK, pc = e / C::NK;
-            const int64_t t = t0 + key;
-            kr[i] = t < g.l ? *reinterpret_cast<const uint4*>(kbase + t * kstride + ch * C::DC + pc * 8)
-                            : make_uint4(0u, 0u, 0u, 0u);
-        }
-    };
-    auto stash = [&](double* dst) {  // dst: [DC][NK]
-#pragma unroll
-        for (int i = 0; i < C::LOADS; ++i) {
-            const int e = tid + i * kKS2_Threads, key = e % C::NK, pc = e / C::NK;
-            const uint32_t w[4] = {kr[i].x, kr[i].y, kr[i].z, kr[i].w};
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                dst[(pc * 8 + 2 * u) * C::NK + key] = (double)__uint_as_float(w[u] << 16);
-                dst[(pc * 8 + 2 * u + 1) * C::NK + key] = (double)__uint_as_float(w[u] & 0xffff0000u);
-            }
-        }
-    };
-    fetch(0);
-    stash(Kd);
-    // warp tile: 32 pairs (wp) x 64 keys (wk); lane: pairs wp*32 + pg*8 + [0, 8), keys
-    // wk*64 + 16 r + 2 kg + {0, 1}, r = 0..3
-    const int wp = WIDE ? 0 : (warp & 1), wk = WIDE ? warp : (warp >> 1);
-    const int pg = lane >> 3, kg = lane & 7;
-    double acc[8][8];
-#pragma unroll
-    for (int i = 0; i < 8; ++i)
-#pragma unroll
-        for (int r = 0; r < 8; ++r) acc[i][r] = 0.0;
-    const double* qcol = Qd + wp * 32 + pg * 8;
-    __syncthreads();
-#pragma unroll 1
-    for (int ch = 0; ch < C::NCH; ++ch) {
-        if (ch + 1 < C::NCH) fetch(ch + 1);
-        const double* kb = Kd + (ch & 1) * C::DC * C::NK + wk * 64 + 2 * kg;
-        const double* qb = qcol + ch * C::DC * C::NP;
-#pragma unroll 2
-        for (int dd = 0; dd < C::DC; ++dd) {
-            double qv[8], kv[8];
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                const double2 x = *reinterpret_cast<const double2*>(qb + dd * C::NP + 2 * i);
-                qv[2 * i] = x.x;
-                qv[2 * i + 1] = x.y;
-                const double2 y = *reinterpret_cast<const double2*>(kb + dd * C::NK + 16 * i);
-                kv[2 * i] = y.x;
-                kv[2 * i + 1] = y.y;
-            }
-#pragma unroll
-            for (int i = 0; i < 8; ++i)
-#pragma unroll
-                for (int r = 0; r < 8; ++r) acc[i][r] = fma(qv[i], kv[r], acc[i][r]);
-        }
-        if (ch + 1 < C::NCH) stash(Kd + ((ch + 1) & 1) * C::DC * C::NK);
-        __syncthreads();
-    }
-    const int64_t kvp = g.kv_per_head();
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-        const int64_t p = p0 + wp * 32 + pg * 8 + i;
-        if (p >= pairs) continue;
-        const int64_t h = kvh * g.group + p / nsegs, n = n_lo + p % nsegs;
-        uint64_t* dst = kvkey + (z * g.hq + h) * kvp + g.kv_off(n);
-#pragma unroll
-        for (int r = 0; r < 4; ++r) {
-            const int64_t t = t0 + wk * 64 + 16 * r + 2 * kg;  // t < n_lo * S <= n * S
-            if (t + 1 < g.l) {
-                *reinterpret_cast<ulonglong2*>(dst + t) =
-                    make_ulonglong2(desc_key(acc[i][2 * r]), desc_key(acc[i][2 * r + 1]));
-            } else if (t < g.l) {
-                dst[t] = desc_key(acc[i][2 * r]);
-            }
-        }
-    }
-}
-
-__global__ void __launch_bounds__(kKS2_Threads, 1)
-kv_score2_kernel(const __nv_bfloat16* __restrict__ k, Geo g, const float* __restrict__ q_mean,
-                 uint64_t* __restrict__ kvkey, int max_batches) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    const int64_t kb = blockIdx.x / max_batches;  // 256-key block
-    const int batch = blockIdx.x % max_batches;
-    const int64_t zg = blockIdx.y;
-    const int64_t z = zg / g.hkv, kvh = zg % g.hkv;
-    const int64_t t0 = kb * kKS2_Keys;
-    const int64_t n_lo = t0 / g.S + 1;
-    const int64_t nsegs = (n_lo < g.N) ? g.N - n_lo : 0;
-    const int64_t pairs = g.group * nsegs;
-    const int64_t p0 = (int64_t)batch * KsCfg<false>::NP;
-    if (p0 >= pairs) return;
-    const bool wide = pairs - p0 <= KsCfg<true>::NP;  // the even block's wide tile covers kb, kb + 1
-    const __nv_bfloat16* kbase = k + z * g.ks[0] + kvh * g.ks[1];
-    if (wide) {
-        if (kb & 1) return;
-        ks2_tile<true>(kbase, g.ks[2], g, q_mean, kvkey, z, kvh, t0, n_lo, nsegs, p0, pairs, smem_raw);
-    } else {
-        ks2_tile<false>(kbase, g.ks[2], g, q_mean, kvkey, z, kvh, t0, n_lo, nsegs, p0, pairs, smem_raw);
-    }
-}
-
-bool kv_score2_ok(const Geo& g, const void* k) {
-    return g.in_bf16 && g.d == 128 && g.ks[0] % 8 == 0 && g.ks[1] % 8 == 0 && g.ks[2] % 8 == 0 &&
-           (reinterpret_cast<uintptr_t>(k) & 15) == 0 && g.S % 512 == 0;
-}
-
 bool kv_score128_ok(const Geo& g, const void* k) {
     return g.in_bf16 && g.d == 128 && g.ks[0] % 8 == 0 && g.ks[1] % 8 == 0 && g.ks[2] % 8 == 0 &&
            (reinterpret_cast<uintptr_t>(k) & 15) == 0 && g.S % 2 == 0;
@@ -707,20 +552,6 @@ bool kv_score128_ok(const Geo& g, const void* k) {
 cudaError_t launch_kv_score(const Geo& g, const void* k, const float* q_mean, uint64_t* kvkey, cudaStream_t st) {
     const int64_t keys = (g.N - 1) * g.S;  // tokens that appear in some prefix
     const int64_t blocks = (keys + kSK - 1) / kSK;
-    static const bool v2 = [] {
-        const char* e = std::getenv("S2O_KV_SCORE");
-        return !(e && std::strcmp(e, "1") == 0);
-    }();
-    if (v2 && kv_score2_ok(g, k)) {
-        const int64_t kblocks = (keys + kKS2_Keys - 1) / kKS2_Keys;
-        const int max_batches = (int)((g.group * (g.N - 1) + KsCfg<false>::NP - 1) / KsCfg<false>::NP);
-        const size_t smem = std::max(KsCfg<false>::kSmem, KsCfg<true>::kSmem);
-        dim3 grid((unsigned)(kblocks * max_batches), (unsigned)(g.z * g.hkv));
-        cudaFuncSetAttribute(kv_score2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        kv_score2_kernel<<<grid, kKS2_Threads, smem, st>>>(reinterpret_cast<const __nv_bfloat16*>(k), g, q_mean, kvkey,
-                                                           max_batches);
-        return cudaGetLastError();
-    }
     if (kv_score128_ok(g, k)) {
         const int max_batches = (int)((g.group * (g.N - 1) + kKS_Pairs - 1) / kKS_Pairs);
         dim3 grid((unsigned)(blocks * max_batches), (unsigned)(g.z * g.hkv));
