@@ -1091,7 +1091,7 @@ tc_diag_kernel(const TcParams p, const __grid_constant__ CUtensorMap qtile,
 #pragma unroll
                 for (int kk = 0; kk < kBN / 16; ++kk)
                     if (leader)
-                        umma_bf16_ts(tbase + (kDSBuf + ob) * 128, tbase + (blk % kDSBuf) * 128 + kk * 8 + (kk >= 4 ? 32 : 0),
+                        umma_bf16_ts(tbase + (kDSBuf + ob) * 128, tbase + (blk % kDSBuf) * 128 + kk * 8,
                                      dv + ((kk * 16 * 128) >> 4), idesc_o, (kk > 0 || j > 0) ? 1 : 0);
                 if (leader) {
                     umma_commit(smem_u32(&c.pv_done[blk % kDSBuf]));
@@ -1158,73 +1158,59 @@ tc_diag_kernel(const TcParams p, const __grid_constant__ CUtensorMap qtile,
                         mxa[(i >> 1) & 7] = fmax3(mxa[(i >> 1) & 7], i < lim ? __uint_as_float(sv[i]) : -INFINITY,
                                                   i + 1 < lim ? __uint_as_float(sv[i + 1]) : -INFINITY);
                 }
-                const float mx_h = fmax3(fmax3(mxa[0], mxa[1], mxa[2]), fmax3(mxa[3], mxa[4], mxa[5]),
-                                         fmaxf(mxa[6], mxa[7])) * sc;
-                // P = exp2(s * scale - m_use) in bf16 into this half's own S columns [64h, 64h + 32)
-                // (so neither half waits for the other to finish reading S), rowsum in fp32
-                float rs[4];
-                auto exps = [&](float m_use) {
-                    const float neg_ref = (m_use == -INFINITY) ? 0.0f : -m_use;
-#pragma unroll
-                    for (int i = 0; i < 4; ++i) rs[i] = 0.0f;
-                    if (full) {
-#pragma unroll
-                        for (int c0 = 0; c0 < 64; c0 += 32) {
-                            uint32_t pk[16];
-#pragma unroll
-                            for (int i = 0; i < 32; i += 2) {
-                                float e0, e1;
-#if S2O_DIAG_POLY > 0
-                                if ((i >> 1) % S2O_DIAG_POLY == S2O_DIAG_POLY - 1) {  // FMA-pipe exp2 (MUFU offload)
-                                    const float2 e = ex2_poly4x2(make_float2(fmaf(__uint_as_float(sv[c0 + i]), sc, neg_ref),
-                                                                             fmaf(__uint_as_float(sv[c0 + i + 1]), sc, neg_ref)));
-                                    e0 = e.x;
-                                    e1 = e.y;
-                                } else
-#endif
-                                {
-                                    e0 = ex2(fmaf(__uint_as_float(sv[c0 + i]), sc, neg_ref));
-                                    e1 = ex2(fmaf(__uint_as_float(sv[c0 + i + 1]), sc, neg_ref));
-                                }
-                                rs[(i >> 1) & 3] += e0 + e1;
-                                pk[i >> 1] = pack_bf16(e0, e1);
-                            }
-                            tmem_st16(tS + h * 64 + c0 / 2, pk);
-                        }
-                    } else {
-#pragma unroll
-                        for (int c0 = 0; c0 < 64; c0 += 32) {
-                            uint32_t pk[16];
-#pragma unroll
-                            for (int i = 0; i < 32; i += 2) {
-                                const float e0 = c0 + i < lim ? ex2(fmaf(__uint_as_float(sv[c0 + i]), sc, neg_ref)) : 0.0f;
-                                const float e1 =
-                                    c0 + i + 1 < lim ? ex2(fmaf(__uint_as_float(sv[c0 + i + 1]), sc, neg_ref)) : 0.0f;
-                                rs[(i >> 1) & 3] += e0 + e1;
-                                pk[i >> 1] = pack_bf16(e0, e1);
-                            }
-                            tmem_st16(tS + h * 64 + c0 / 2, pk);
-                        }
-                    }
-                };
-                // Row max across the two halves (smem, double-buffered by block parity, one named
-                // barrier per warp pair and block). Lazy rescaling keeps the reference m2 unless the
-                // block max exceeds it by kRescaleThresh, so when this half stays below that the
-                // exponentials start at once with m2 (speculation) and the exchange comes after;
-                // only if the other half's max forces a rescale are this half's P recomputed.
+                float mx = fmax3(fmax3(mxa[0], mxa[1], mxa[2]), fmax3(mxa[3], mxa[4], mxa[5]), fmaxf(mxa[6], mxa[7]));
+                // exchange with the other half (double-buffered by block parity): after this barrier
+                // both halves have also finished reading S, so P may overwrite it
                 float* xb = xch + (gb & 1) * 256;
-                xb[h * 128 + r] = mx_h;
-                const bool spec = __all_sync(0xffffffffu, m2 != -INFINITY && mx_h <= m2 + kRescaleThresh);
-                float m_use = m2;
-                if (spec) exps(m2);
+                xb[h * 128 + r] = mx;
                 named_bar_sync(1 + q, 64);
-                const float mx = fmaxf(mx_h, xb[(1 - h) * 128 + r]);
+                mx = fmaxf(mx, xb[(1 - h) * 128 + r]) * sc;
                 if (threadIdx.x == 0) tl_mark(p, 25, gb);
                 const float m_new = fmaxf(m2, mx);
                 const bool rescale = (m_new > m2 + kRescaleThresh) || (m2 == -INFINITY);
-                if (rescale) m_use = m_new;
-                if (!spec || __any_sync(0xffffffffu, rescale)) exps(m_use);  // rows without a rescale: same values
-                const float alpha = (m2 == -INFINITY) ? 0.0f : ex2(m2 - m_use);
+                const float m_use = rescale ? m_new : m2;
+                const float neg_ref = (m_use == -INFINITY) ? 0.0f : -m_use;
+                const float alpha = (m2 == -INFINITY) ? 0.0f : ex2(m2 + neg_ref);
+                float rs[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+                if (full) {
+#pragma unroll
+                    for (int c0 = 0; c0 < 64; c0 += 32) {
+                        uint32_t pk[16];
+#pragma unroll
+                        for (int i = 0; i < 32; i += 2) {
+                            float e0, e1;
+#if S2O_DIAG_POLY > 0
+                            if ((i >> 1) % S2O_DIAG_POLY == S2O_DIAG_POLY - 1) {  // FMA-pipe exp2 (MUFU offload)
+                                const float2 e = ex2_poly4x2(make_float2(fmaf(__uint_as_float(sv[c0 + i]), sc, neg_ref),
+                                                                         fmaf(__uint_as_float(sv[c0 + i + 1]), sc, neg_ref)));
+                                e0 = e.x;
+                                e1 = e.y;
+                            } else
+#endif
+                            {
+                                e0 = ex2(fmaf(__uint_as_float(sv[c0 + i]), sc, neg_ref));
+                                e1 = ex2(fmaf(__uint_as_float(sv[c0 + i + 1]), sc, neg_ref));
+                            }
+                            rs[(i >> 1) & 3] += e0 + e1;
+                            pk[i >> 1] = pack_bf16(e0, e1);
+                        }
+                        tmem_st16(tS + h * 32 + c0 / 2, pk);
+                    }
+                } else {
+#pragma unroll
+                    for (int c0 = 0; c0 < 64; c0 += 32) {
+                        uint32_t pk[16];
+#pragma unroll
+                        for (int i = 0; i < 32; i += 2) {
+                            const float e0 = c0 + i < lim ? ex2(fmaf(__uint_as_float(sv[c0 + i]), sc, neg_ref)) : 0.0f;
+                            const float e1 =
+                                c0 + i + 1 < lim ? ex2(fmaf(__uint_as_float(sv[c0 + i + 1]), sc, neg_ref)) : 0.0f;
+                            rs[(i >> 1) & 3] += e0 + e1;
+                            pk[i >> 1] = pack_bf16(e0, e1);
+                        }
+                        tmem_st16(tS + h * 32 + c0 / 2, pk);
+                    }
+                }
                 const float rowsum = (rs[0] + rs[1]) + (rs[2] + rs[3]);
                 // O rescale (lazy, rare; this half's 64 columns): all earlier P V of the tile done
                 if (__any_sync(0xffffffffu, j > 0 && rescale && m2 != -INFINITY)) {
