@@ -887,8 +887,8 @@ tc_pass_kernel(const TcParams p, const __grid_constant__ CUtensorMap qmap,
 // tile). Blocks are numbered globally per CTA (gb); block gb uses S buffer gb % kDSBuf. MMA
 // order: S(0..kDSBuf-1), then per block j: P V(j), S(j+kDSBuf) (into the buffer P(j) held; the
 // tensor pipe executes in order, so the new S overwrites P(j) only after P V(j) read it).
-// pv_done[b] completes once per P V on buffer b: a softmax that must rescale O at block gb (lazy
-// max update, rare) first waits for P V(gb-1), i.e. all earlier P V of the tile.
+// A softmax that must rescale O at block gb (lazy max update, rare) first waits for P V(gb-1),
+// i.e. all earlier P V of the tile, on the V stage barrier that P V commits (v_empty).
 #ifndef S2O_DIAG_POLY
 #define S2O_DIAG_POLY 8  // diagonal kernel: every n-th exponential pair on the FMA pipe (0 = all MUFU; A/B: 8 -3 %, 4 even)
 #endif
@@ -914,7 +914,7 @@ constexpr uint32_t kDSmemBytes = kDOffX + 2 * 2 * 128 * 4;  // 197.25 KB
 struct CtrlD {
     uint64_t q_full[kDQBuf], q_empty[kDQBuf];
     uint64_t k_full[kDKStages], k_empty[kDKStages], v_full[kDVStages], v_empty[kDVStages];
-    uint64_t s_full[kDSBuf], p_full[kDSBuf], pv_done[kDSBuf];  // per S buffer
+    uint64_t s_full[kDSBuf], p_full[kDSBuf];                    // per S buffer
     uint64_t o_done[kDOBuf], o_free[kDOBuf];                    // per O buffer
     uint64_t ml_full[2], ml_free[2];                            // (m, ell) hand-off slots (tile parity)
     uint32_t tmem_base;
@@ -980,15 +980,15 @@ tc_diag_kernel(const TcParams p, const __grid_constant__ CUtensorMap qtile,
         for (int b = 0; b < kDSBuf; ++b) {
             mbar_init(smem_u32(&c.s_full[b]), 1);
             mbar_init(smem_u32(&c.p_full[b]), kDSoftWarps);  // both row halves
-            mbar_init(smem_u32(&c.pv_done[b]), 1);
         }
         for (int b = 0; b < kDOBuf; ++b) {
             mbar_init(smem_u32(&c.o_done[b]), 1);
             mbar_init(smem_u32(&c.o_free[b]), 4);   // epilogue warps
         }
         for (int b = 0; b < 2; ++b) {
-            mbar_init(smem_u32(&c.ml_full[b]), kDSoftWarps);
-            mbar_init(smem_u32(&c.ml_free[b]), 4);  // epilogue warps
+            // per-thread arrivals: every writer / reader of the slot releases its own accesses
+            mbar_init(smem_u32(&c.ml_full[b]), kDSoftWarps * 32);
+            mbar_init(smem_u32(&c.ml_free[b]), 4 * 32);  // epilogue threads
         }
         fence_mbar_init();
     }
@@ -1094,7 +1094,6 @@ tc_diag_kernel(const TcParams p, const __grid_constant__ CUtensorMap qtile,
                         umma_bf16_ts(tbase + (kDSBuf + ob) * 128, tbase + (blk % kDSBuf) * 128 + kk * 8,
                                      dv + ((kk * 16 * 128) >> 4), idesc_o, (kk > 0 || j > 0) ? 1 : 0);
                 if (leader) {
-                    umma_commit(smem_u32(&c.pv_done[blk % kDSBuf]));
                     umma_commit(smem_u32(&c.v_empty[vst]));
                     if (j == t.nd - 1) umma_commit(smem_u32(&c.o_done[ob]));
                 }
@@ -1214,9 +1213,10 @@ tc_diag_kernel(const TcParams p, const __grid_constant__ CUtensorMap qtile,
                 const float rowsum = (rs[0] + rs[1]) + (rs[2] + rs[3]);
                 // O rescale (lazy, rare; this half's 64 columns): all earlier P V of the tile done
                 if (__any_sync(0xffffffffu, j > 0 && rescale && m2 != -INFINITY)) {
-                    // P V(gb-1) done (then all earlier ones are): its buffer's barrier is at most one
-                    // phase behind, since S(gb) completing implies P V(gb - kDSBuf) completed
-                    mbar_wait(smem_u32(&c.pv_done[(gb - 1) % kDSBuf]), ((gb - 1) / kDSBuf) & 1, 4202);
+                    // P V(gb-1) done (then all earlier ones are): P V commits the V stage barrier
+                    // v_empty[(gb-1) % kDVStages], whose next phase needs P V(gb+1), i.e. P(gb+1)
+                    // from this very warp, so the parity wait is exact
+                    mbar_wait(smem_u32(&c.v_empty[(gb - 1) % kDVStages]), ((gb - 1) / kDVStages) & 1, 4202);
                     tc_fence_after();
 #pragma unroll
                     for (int c0 = 0; c0 < 64; c0 += 32) {
@@ -1244,8 +1244,7 @@ tc_diag_kernel(const TcParams p, const __grid_constant__ CUtensorMap qtile,
                 float* mlb = ml + (tk & 1) * 384;
                 if (h == 0) mlb[r] = m2;
                 mlb[128 + h * 128 + r] = ell;
-                __syncwarp();
-                if (lane == 0) mbar_arrive(smem_u32(&c.ml_full[tk & 1]));
+                mbar_arrive(smem_u32(&c.ml_full[tk & 1]));
             }
         }
     } else if (warp < kDEpiWarp0 + 4) {
@@ -1270,10 +1269,8 @@ tc_diag_kernel(const TcParams p, const __grid_constant__ CUtensorMap qtile,
             const float m2 = ml[mb * 384 + r], ell = ml[mb * 384 + 128 + r] + ml[mb * 384 + 256 + r];
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) {
-                mbar_arrive(smem_u32(&c.o_free[ob]));   // O buffer reusable
-                mbar_arrive(smem_u32(&c.ml_free[mb]));  // (m, ell) slot reusable
-            }
+            if (lane == 0) mbar_arrive(smem_u32(&c.o_free[ob]));  // O buffer reusable
+            mbar_arrive(smem_u32(&c.ml_free[mb]));                // (m, ell) slot reusable
             const int64_t grow = t.sb + t.t0 + rr;
             const int64_t slot = t.zh * g.l + grow;
             if (valid && (a.mode & kStateOut)) {
