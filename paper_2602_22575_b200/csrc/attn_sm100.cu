@@ -1384,6 +1384,12 @@ cudaError_t smem_attr(const void* fn, uint32_t bytes) {
 
 }  // namespace
 
+bool make_bf16_row_map(void* map, const void* base, int64_t rows, uint32_t box_rows) {
+    return make_row_map(reinterpret_cast<CUtensorMap*>(map), base, rows, box_rows);
+}
+int64_t bf16_row_span(const int64_t* st, int64_t z, int64_t h, int64_t l) { return span_rows(st, z, h, l); }
+cudaError_t set_max_dyn_smem(const void* fn, uint32_t bytes) { return smem_attr(fn, bytes); }
+
 bool tc_supported(const PassArgs& a) {
     const Geo& g = a.g;
     if (!g.in_bf16 || g.d != kD || a.bm != kBM || a.bn != kBN) return false;

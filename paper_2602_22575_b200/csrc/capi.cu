@@ -257,7 +257,7 @@ s2o_status level_body(const LevelLoop& L, cudaStream_t st, cudaGraphConditionalH
         level_prep_kernel<<<1, 1024, 0, st>>>(L.ctl, L.tiles[cur], L.seglist, L.marks, L.a.tiles_per_head, L.a.T,
                                               g.N, nsegs, L.topt, hl, hf);
         S2O_CUDA_TRY(cudaGetLastError(), "level prep");
-        S2O_CUDA_TRY(launch_plan_level_dev(g, L.seglist, L.ctl + 2, L.lists[cur],
+        S2O_CUDA_TRY(launch_plan_level_dev(g, L.k, L.seglist, L.ctl + 2, L.lists[cur],
                                            reinterpret_cast<const int64_t*>(L.ctl + 4), L.lists[cur ^ 1], L.topt,
                                            L.ctl + 1, L.plan_ws, st), "plan level");
         PassArgs a3 = L.a2;

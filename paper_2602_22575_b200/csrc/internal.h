@@ -93,14 +93,12 @@ cudaError_t launch_plan_build(const Geo& g, const void* q, const void* k, int32_
                               int32_t* kv_perm, void* workspace, cudaStream_t st);
 cudaError_t launch_plan_topk(const Geo& g, const void* q, const void* k, int32_t* q_perm, int32_t* kvtop,
                              int64_t topt, int32_t* flags, void* workspace, cudaStream_t st);
-// Next plan level: for the listed segments (codes zh * N + n), the topt entries of kv_perm that
-// follow the last entry of `prev` (entries [lvl_base, lvl_base + topt) of the full order).
-cudaError_t launch_plan_level(const Geo& g, const int32_t* seg_list, int64_t nseg, const int32_t* prev,
-                              int64_t lvl_base, int32_t* kvtop, int64_t topt, int32_t* flags, void* workspace,
-                              cudaStream_t st);
-// The same with the segment count and level base in device memory: the grid covers every
-// segment and CTAs beyond *nseg_dev exit (stream-ordered plan levels).
-cudaError_t launch_plan_level_dev(const Geo& g, const int32_t* seg_list, const int32_t* nseg_dev,
+// Next plan level: for the segments listed in seg_list (codes zh * N + n, count *nseg_dev), the
+// topt entries of kv_perm that follow the last entry of `prev` (entries [lvl_base, lvl_base + topt)
+// of the full order, *lvl_base_dev). The grid covers every segment and CTAs beyond *nseg_dev exit
+// (stream-ordered plan levels). The first level after a candidate-pruned level 0 scores every
+// prefix key once (K is needed for that).
+cudaError_t launch_plan_level_dev(const Geo& g, const void* k, const int32_t* seg_list, const int32_t* nseg_dev,
                                   const int32_t* prev, const int64_t* lvl_base_dev, int32_t* kvtop, int64_t topt,
                                   int32_t* flags, void* workspace, cudaStream_t st);
 cudaError_t launch_segment_means(const Geo& g, const void* x, int which_kv, int64_t nseg_out,
@@ -114,7 +112,13 @@ cudaError_t launch_rank_prefix_keys(const Geo& g, const void* k, const float* q_
 size_t generic_scratch_bytes(const PassArgs& a);
 cudaError_t launch_generic_pass(const PassArgs& a, void* scratch, cudaStream_t st);
 
-// tcgen05 path (bf16, D = 128, b_m = 128, b_n in {64, 128})
+// 2-D TMA view of a [.., 128] bf16 tensor as rows of 128 elements (box: box_rows x 64 columns,
+// SWIZZLE_128B); `map` is a CUtensorMap. Row span of a strided [z, h, l, 128] tensor in rows.
+bool make_bf16_row_map(void* map, const void* base, int64_t rows, uint32_t box_rows);
+int64_t bf16_row_span(const int64_t* st, int64_t z, int64_t h, int64_t l);
+cudaError_t set_max_dyn_smem(const void* fn, uint32_t bytes);  // once per (kernel, device)
+
+// tcgen05 path (bf16, D = 128, b_m = 128, b_n = 128)
 bool tc_supported(const PassArgs& a);
 cudaError_t launch_tc_pass(const PassArgs& a, cudaStream_t st);
 

@@ -25,6 +25,7 @@
 
 #include "common.cuh"
 #include "internal.h"
+#include "sm100.cuh"
 #include "sort.cuh"
 
 #include <cub/block/block_radix_sort.cuh>
@@ -432,7 +433,10 @@ __device__ __forceinline__ double bf16_hi_to_f64(uint32_t w) { return (double)__
 
 __global__ void __launch_bounds__(kKS_Threads, 2)
 kv_score128_kernel(const __nv_bfloat16* __restrict__ k, Geo g, const float* __restrict__ q_mean,
-                   uint64_t* __restrict__ kvkey, int max_batches) {
+                   uint64_t* __restrict__ kvkey, int max_batches, int64_t n_hi, const int32_t* __restrict__ skip_if,
+                   const int32_t* __restrict__ need) {
+    // plan levels: the keys are already there, or no segment needs a level
+    if ((skip_if && *skip_if) || (need && *need == 0)) return;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int64_t kb = blockIdx.x / max_batches;
@@ -441,7 +445,8 @@ kv_score128_kernel(const __nv_bfloat16* __restrict__ k, Geo g, const float* __re
     const int64_t z = zg / g.hkv, kvh = zg % g.hkv;
     const int64_t t0 = kb * kSK;
     const int64_t n_lo = t0 / g.S + 1;
-    const int64_t nsegs = (n_lo < g.N) ? g.N - n_lo : 0;
+    const int64_t n_end = n_hi < g.N ? n_hi : g.N;  // segments [n_lo, n_end) only
+    const int64_t nsegs = (n_lo < n_end) ? n_end - n_lo : 0;
     const int64_t pairs = g.group * nsegs;
     const int64_t p0 = (int64_t)batch * kKS_Pairs;
     if (p0 >= pairs) return;
@@ -549,17 +554,23 @@ bool kv_score128_ok(const Geo& g, const void* k) {
            (reinterpret_cast<uintptr_t>(k) & 15) == 0 && g.S % 2 == 0;
 }
 
-cudaError_t launch_kv_score(const Geo& g, const void* k, const float* q_mean, uint64_t* kvkey, cudaStream_t st) {
-    const int64_t keys = (g.N - 1) * g.S;  // tokens that appear in some prefix
+// Exact scores of segments [1, n_hi) (n_hi >= N: all); skip_if (device flag, optional): a launch that
+// finds it set exits at once.
+cudaError_t launch_kv_score(const Geo& g, const void* k, const float* q_mean, uint64_t* kvkey, cudaStream_t st,
+                            int64_t n_hi = INT64_MAX, const int32_t* skip_if = nullptr, const int32_t* need = nullptr) {
+    const int64_t n_end = std::min<int64_t>(n_hi, g.N);
+    if (n_end < 2) return cudaSuccess;
+    const int64_t keys = (n_end - 1) * g.S;  // tokens that appear in some prefix
     const int64_t blocks = (keys + kSK - 1) / kSK;
     if (kv_score128_ok(g, k)) {
-        const int max_batches = (int)((g.group * (g.N - 1) + kKS_Pairs - 1) / kKS_Pairs);
+        const int max_batches = (int)((g.group * (n_end - 1) + kKS_Pairs - 1) / kKS_Pairs);
         dim3 grid((unsigned)(blocks * max_batches), (unsigned)(g.z * g.hkv));
         cudaFuncSetAttribute(kv_score128_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kKS_Smem);
         kv_score128_kernel<<<grid, kKS_Threads, kKS_Smem, st>>>(reinterpret_cast<const __nv_bfloat16*>(k), g, q_mean,
-                                                         kvkey, max_batches);
+                                                         kvkey, max_batches, n_hi, skip_if, need);
         return cudaGetLastError();
     }
+    if (n_end < g.N || skip_if) return cudaErrorInvalidValue;  // generic scoring: whole plans only
     const size_t smem = sizeof(double) * g.d * kSPairs + sizeof(float) * g.d * kSK;
     cudaFuncSetAttribute(kv_score_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     dim3 grid((unsigned)blocks, (unsigned)(g.z * g.hkv));
@@ -766,7 +777,7 @@ __global__ void __launch_bounds__(kScanThreads, 3)
 sel_scan_kernel(Geo g, const uint64_t* __restrict__ kvkey, int64_t topt, uint64_t* __restrict__ ckey,
                 uint32_t* __restrict__ cidx, int32_t* __restrict__ ccount, int32_t* __restrict__ flags,
                 const int32_t* __restrict__ seg_list, const int32_t* __restrict__ prev, int64_t lvl_base,
-                const int32_t* __restrict__ nseg_dev, const int64_t* __restrict__ lvl_base_dev) {
+                const int32_t* __restrict__ nseg_dev, const int64_t* __restrict__ lvl_base_dev, int64_t n_max) {
     if (nseg_dev && (int64_t)blockIdx.x >= *nseg_dev) return;  // device-sized level: CTA not used
     if (lvl_base_dev) lvl_base = *lvl_base_dev;
     __shared__ typename SampSort::TempStorage samp;
@@ -777,6 +788,7 @@ sel_scan_kernel(Geo g, const uint64_t* __restrict__ kvkey, int64_t topt, uint64_
     const SelSeg sg = sel_seg(g, seg_list, topt, lvl_base);
     const int64_t len = sg.len, tt = sg.tt;
     if (len <= kSelCap && !prev) return;  // every key is a candidate (sel_sort_kernel reads them)
+    if (sg.n >= n_max) return;            // selected by the candidate path (plan_tc.cuh)
     const uint64_t* keys = kvkey + sg.off;
     uint64_t* ck = ckey + sg.off;  // candidates <= min(cap, len) fit the segment's own slot
     uint32_t* ci = cidx + sg.off;
@@ -1063,6 +1075,8 @@ sel_sort_kernel(Geo g, const uint64_t* __restrict__ kvkey, const uint64_t* __res
     }
 }
 
+#include "plan_tc.cuh"
+
 struct PlanWs {
     float* guide;      // [Z*Hkv*D]
     float* q_mean;     // [Z*Hq*N*D]
@@ -1073,7 +1087,15 @@ struct PlanWs {
     uint32_t* idx0;
     uint32_t* idx1;
     int32_t* ccount;   // [Z*Hq*N] top-T candidate counts (candidates live in key1 / idx1)
+    // candidate-pruned selection (plan_tc.cuh)
+    float* thr;        // [Z*Hq*N]
+    float* ec;         // [Z*Hq*N]
+    uint64_t* kth;     // [Z*Hq*N]
+    int32_t* ccnt;     // [Z*Hq*N][nch]
+    int32_t* full;     // 1: key0 holds every exact prefix-key score (plan levels need them)
 };
+
+int64_t cand_chunks(const Geo& g) { return std::max<int64_t>(1, ((g.N - 1) * g.S + kCR - 1) / kCR); }
 
 size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
 
@@ -1096,6 +1118,11 @@ size_t plan_ws_layout(const Geo& g, char* base, PlanWs* out) {
     ws.idx0 = reinterpret_cast<uint32_t*>(take(sizeof(uint32_t) * total));
     ws.idx1 = reinterpret_cast<uint32_t*>(take(sizeof(uint32_t) * total));
     ws.ccount = reinterpret_cast<int32_t*>(take(sizeof(int32_t) * zhq * g.N));
+    ws.thr = reinterpret_cast<float*>(take(sizeof(float) * zhq * g.N));
+    ws.ec = reinterpret_cast<float*>(take(sizeof(float) * zhq * g.N));
+    ws.kth = reinterpret_cast<uint64_t*>(take(sizeof(uint64_t) * zhq * g.N));
+    ws.ccnt = reinterpret_cast<int32_t*>(take(sizeof(int32_t) * zhq * g.N * cand_chunks(g)));
+    ws.full = reinterpret_cast<int32_t*>(take(sizeof(int32_t)));
     if (out) *out = ws;
     return off;
 }
@@ -1153,9 +1180,10 @@ namespace {
 // Top-T selection of `nseg` segments (all of them, or seg_list) over the keys in ws.key0.
 cudaError_t launch_select(const Geo& g, const PlanWs& ws, int64_t nseg, const int32_t* seg_list,
                           const int32_t* prev, int64_t lvl_base, int32_t* kvtop, int64_t topt, int32_t* flags,
-                          cudaStream_t st, const int32_t* nseg_dev = nullptr, const int64_t* lvl_base_dev = nullptr) {
+                          cudaStream_t st, const int32_t* nseg_dev = nullptr, const int64_t* lvl_base_dev = nullptr,
+                          int64_t n_max = INT64_MAX) {
     sel_scan_kernel<<<(unsigned)nseg, kScanThreads, 0, st>>>(g, ws.key0, topt, ws.key1, ws.idx1, ws.ccount, flags,
-                                                             seg_list, prev, lvl_base, nseg_dev, lvl_base_dev);
+                                                             seg_list, prev, lvl_base, nseg_dev, lvl_base_dev, n_max);
     const size_t ssm = sizeof(SelSortSmem);
     cudaFuncSetAttribute(sel_sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssm);
     sel_sort_kernel<<<(unsigned)nseg, kSelThreads, ssm, st>>>(g, ws.key0, ws.key1, ws.idx1, ws.ccount, topt, kvtop,
@@ -1166,6 +1194,86 @@ cudaError_t launch_select(const Geo& g, const PlanWs& ws, int64_t nseg, const in
 }  // namespace
 
 
+
+// The candidate-pruned selection (plan_tc.cuh) serves bf16, D = 128 plans with 128-row-aligned,
+// contiguous K rows and S % 128 == 0; S2O_PLAN_TC=0 forces the dense-scoring selection.
+bool select_tc_ok(const Geo& g, const void* k, int64_t topt) {
+    static const bool on = [] {
+        const char* e = std::getenv("S2O_PLAN_TC");
+        return !(e && std::strcmp(e, "0") == 0);
+    }();
+    return on && kv_score128_ok(g, k) && g.ks[2] == 128 && g.ks[1] % 128 == 0 && g.ks[0] % 128 == 0 &&
+           g.S % 128 == 0 && g.N >= 2 && topt <= kSelCap && bf16_row_span(g.ks, g.z, g.hkv, g.l) < (int64_t(1) << 31);
+}
+
+cudaError_t launch_select_tc(const Geo& g, const void* k, const PlanWs& ws, int32_t* kvtop, int64_t topt,
+                             int32_t* flags, cudaStream_t st) {
+    cudaError_t err;
+    const int64_t zhq = g.z * g.hq;
+    // segments n < n_cand: dense exact scores (most of their keys would be candidates anyway);
+    // n < n_direct of them (at most kSelCap keys) are sorted whole, the others selected by sel_scan
+    const int64_t n_direct = std::min<int64_t>(g.N, kSelCap / g.S + 1);
+    const int64_t n_cand = std::min<int64_t>(g.N, std::max<int64_t>(n_direct, (kCandDensity * topt + g.S - 1) / g.S));
+    if ((err = cudaMemsetAsync(ws.full, 0, sizeof(int32_t), st)) != cudaSuccess) return err;
+    if (n_cand >= 2 && (err = launch_kv_score(g, k, ws.q_mean, ws.key0, st, n_cand)) != cudaSuccess) return err;
+    if (n_cand < g.N) {
+        // step 1: exact scores of every 16th key (a strided view of K), into key1
+        Geo gv = g;
+        gv.S = g.S / kSampStride;
+        gv.l = (g.N - 1) * gv.S;
+        gv.ks[2] = g.ks[2] * kSampStride;
+        const void* kview = reinterpret_cast<const __nv_bfloat16*>(k) + kSampPhase * g.ks[2];
+        if ((err = launch_kv_score(gv, kview, ws.q_mean, ws.key1, st)) != cudaSuccess) return err;
+        const unsigned rows = (unsigned)(zhq * (g.N - 1));
+        cand_thresh_kernel<<<rows, kThrThreads, 0, st>>>(g, ws.key1, gv.S, ws.q_mean, topt, n_cand, ws.thr, ws.ec, ws.kth);
+        if ((err = cudaGetLastError()) != cudaSuccess) return err;
+        // step 2: tensor-core candidates + exact rescoring, into the key0 / idx0 row regions
+        CUtensorMap kmap;
+        if (!make_bf16_row_map(&kmap, k, bf16_row_span(g.ks, g.z, g.hkv, g.l), 128)) return cudaErrorInvalidValue;
+        CandArgs ca;
+        ca.g = g;
+        ca.q_mean = ws.q_mean;
+        ca.thr = ws.thr;
+        ca.ec = ws.ec;
+        ca.ckey = ws.key0;
+        ca.cidx = ws.idx0;
+        ca.ccnt = ws.ccnt;
+        ca.nch = cand_chunks(g);
+        ca.n_cand = n_cand;
+        ca.rows = g.group * (g.N - n_cand);
+        if ((err = set_max_dyn_smem((const void*)kv_cand_kernel, kCSmem)) != cudaSuccess) return err;
+        dim3 grid((unsigned)ca.nch, (unsigned)((ca.rows + 127) / 128), (unsigned)(g.z * g.hkv));
+        kv_cand_kernel<<<grid, kCThreads, kCSmem, st>>>(ca, kmap);
+        if ((err = cudaGetLastError()) != cudaSuccess) return err;
+        // step 3: certification + exact first-T compaction, into key1 / idx1 at the row offsets
+        cand_pack_kernel<false><<<rows, kPackThreads, 0, st>>>(g, ws.key0, ws.idx0, ws.ccnt, ca.nch, ws.kth, topt,
+                                                                n_cand, ws.key1, ws.idx1, ws.ccount, flags);
+        if ((err = set_max_dyn_smem((const void*)cand_pack_kernel<true>, sizeof(PackSmem))) != cudaSuccess) return err;
+        cand_pack_kernel<true><<<rows, kPackThreads, sizeof(PackSmem), st>>>(g, ws.key0, ws.idx0, ws.ccnt, ca.nch,
+                                                                             ws.kth, topt, n_cand, ws.key1, ws.idx1,
+                                                                             ws.ccount, flags);
+        if ((err = cudaGetLastError()) != cudaSuccess) return err;
+    }
+    if (n_cand > n_direct)  // the densely scored segments too long to sort whole
+        sel_scan_kernel<<<(unsigned)(zhq * (g.N - 1)), kScanThreads, 0, st>>>(
+            g, ws.key0, topt, ws.key1, ws.idx1, ws.ccount, flags, nullptr, nullptr, 0, nullptr, nullptr, n_cand);
+    // step 4: stable sort of each row's T candidates (or every key of a short segment)
+    const size_t ssm = sizeof(SelSortSmem);
+    if ((err = set_max_dyn_smem((const void*)sel_sort_kernel, (uint32_t)ssm)) != cudaSuccess) return err;
+    sel_sort_kernel<<<(unsigned)(zhq * (g.N - 1)), kSelThreads, ssm, st>>>(g, ws.key0, ws.key1, ws.idx1, ws.ccount, topt,
+                                                                          kvtop, nullptr, 1, 0, nullptr, nullptr);
+    return cudaGetLastError();
+}
+
+// Plan levels read every exact score from key0: after a candidate-pruned level 0 they are scored
+// once, by the first level that needs them (device flag, so this stays stream-ordered).
+cudaError_t ensure_full_keys(const Geo& g, const void* k, const PlanWs& ws, const int32_t* need, cudaStream_t st) {
+    if (!kv_score128_ok(g, k)) return cudaSuccess;  // the generic selection always scores everything
+    cudaError_t err = launch_kv_score(g, k, ws.q_mean, ws.key0, st, INT64_MAX, ws.full, need);
+    if (err != cudaSuccess) return err;
+    set_flag_kernel<<<1, 1, 0, st>>>(ws.full, 1, need);
+    return cudaGetLastError();
+}
 
 // Plan for the fused operator: q_perm in full, kv_perm truncated to its top `topt` entries
 // per segment, laid out [Z*Hq][N][topt] (segment 0 unused). flags[0] is set if a selection
@@ -1182,7 +1290,9 @@ cudaError_t launch_plan_topk(const Geo& g, const void* q, const void* k, int32_t
         if (g.S > kRun && (err = sort_family(0, g, ws, q_perm, st)) != cudaSuccess) return err;
     }
     if (g.N > 1) {
+        if (select_tc_ok(g, k, topt)) return launch_select_tc(g, k, ws, kvtop, topt, flags, st);
         if ((err = launch_kv_score(g, k, ws.q_mean, ws.key0, st)) != cudaSuccess) return err;
+        if (kv_score128_ok(g, k)) set_flag_kernel<<<1, 1, 0, st>>>(ws.full, 1, nullptr);
         if ((err = launch_select(g, ws, g.z * g.hq * (g.N - 1), nullptr, nullptr, 0, kvtop, topt, flags, st)) !=
             cudaSuccess)
             return err;
@@ -1191,17 +1301,7 @@ cudaError_t launch_plan_topk(const Geo& g, const void* q, const void* k, int32_t
 }
 
 
-cudaError_t launch_plan_level(const Geo& g, const int32_t* seg_list, int64_t nseg, const int32_t* prev,
-                              int64_t lvl_base, int32_t* kvtop, int64_t topt, int32_t* flags, void* workspace,
-                              cudaStream_t st) {
-    if (nseg == 0) return cudaSuccess;
-    PlanWs ws;
-    char* base = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(workspace) + 255) & ~uintptr_t(255));
-    plan_ws_layout(g, base, &ws);  // the kv keys of the level-0 build are still in key0
-    return launch_select(g, ws, nseg, seg_list, prev, lvl_base, kvtop, topt, flags, st);
-}
-
-cudaError_t launch_plan_level_dev(const Geo& g, const int32_t* seg_list, const int32_t* nseg_dev,
+cudaError_t launch_plan_level_dev(const Geo& g, const void* k, const int32_t* seg_list, const int32_t* nseg_dev,
                                   const int32_t* prev, const int64_t* lvl_base_dev, int32_t* kvtop, int64_t topt,
                                   int32_t* flags, void* workspace, cudaStream_t st) {
     const int64_t nmax = g.z * g.hq * (g.N - 1);
@@ -1209,6 +1309,8 @@ cudaError_t launch_plan_level_dev(const Geo& g, const int32_t* seg_list, const i
     PlanWs ws;
     char* base = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(workspace) + 255) & ~uintptr_t(255));
     plan_ws_layout(g, base, &ws);
+    cudaError_t err = ensure_full_keys(g, k, ws, nseg_dev, st);
+    if (err != cudaSuccess) return err;
     return launch_select(g, ws, nmax, seg_list, prev, 0, kvtop, topt, flags, st, nseg_dev, lvl_base_dev);
 }
 

@@ -61,7 +61,8 @@ def lib() -> C.CDLL:
     """Load (building if needed) libs2o_cuda.so. Raises if it cannot be loaded."""
     global _LIB
     if _LIB is None:
-        path = _build.build()  # no-op when the in-tree .so matches its sources
+        # S2O_LIB_PATH: a prebuilt variant of the library (dev A/B builds); else the in-tree build
+        path = os.environ.get("S2O_LIB_PATH") or _build.build()  # no-op when the .so matches its sources
         _LIB = C.CDLL(path)
         _LIB.s2o_last_error.restype = C.c_char_p
         _LIB.s2o_status_string.restype = C.c_char_p
