@@ -630,8 +630,10 @@ tc_pass_kernel(const TcParams p, const __grid_constant__ CUtensorMap qmap,
                     const float m_new = fmaxf(m2, mx);
                     // early_stop_check's "uninitialized state" (kernel.cpp:228): the reference's
                     // fp64 prev = ell * e^(m - m') is <= 0 iff ell <= 0 or e^(m - m') underflows
-                    // fp64 (a max jump beyond 1075 log2 units)
-                    if (!is_diag && valid && (ell <= 0.0f || m_new - m2 > 1075.0f)) atomicExch(a.err_flag, 1);
+                    // fp64 (a max jump beyond 1075 log2 units) -- unless ell is NaN or infinite
+                    // (a poisoned row: prev is NaN, which the reference does not reject)
+                    if (!is_diag && valid && fabsf(ell) <= 3.402823466e38f && (ell <= 0.0f || m_new - m2 > 1075.0f))
+                        atomicExch(a.err_flag, 1);
                     rescale = (m_new > m2 + kRescaleThresh) || (m2 == -INFINITY);
                     m_use = rescale ? m_new : m2;
                     const float neg_ref = (m_use == -INFINITY) ? 0.0f : -m_use;
@@ -880,7 +882,8 @@ tc_pass_kernel(const TcParams p, const __grid_constant__ CUtensorMap qmap,
 //   warps 8-11  epilogue: read O of a finished tile from TMEM, persist state / write O, so the
 //               softmax warps go straight on to the next tile
 //   warp 12     MMA issuer (one elected lane)
-//   warp 13     Q + K loader (lane 0, 2-D TMA tiles), warp 14 V loader (lane 0), warp 15 idle
+//   warp 13     Q + K loader (lane 0, 2-D TMA tiles), warp 14 V loader (lane 0), warp 15 reads
+//               each tile's diagonal V block for non-finite values (masked-key poison, exact rerun)
 //
 // TMEM: S buffers at columns [0, 128), [128, 256), [256, 384) (P in bf16 over the first 64
 // columns of its buffer), O at [384, 512) (kDSBuf = 2: two S buffers, O double-buffered by
@@ -1007,8 +1010,37 @@ tc_diag_kernel(const TcParams p, const __grid_constant__ CUtensorMap qtile,
     // (setmaxnreg inside each role branch, so the softmax code is dominated by its increase)
     if (warp == kDKWarp || warp == kDVWarp || warp > kDVWarp) {
         setmaxnreg_dec<kDOtherRegs>();
+        if (warp > kDVWarp) {
+            // ============================== poison check ==============================
+            // Masked keys are skipped by the reference (attention.cpp:55-57) but the tensor core
+            // multiplies them: 0 * NaN / 0 * Inf in P V would poison earlier rows. Only a tile's
+            // last (diagonal) block has masked keys, so this warp reads that V block (from L2: the
+            // V loader has just fetched it) for non-finite bf16 values, off the pipeline; a hit
+            // lists the tile for the exact rerun that run_pass launches after this kernel.
+            if (!a.poison_cnt) return;
+            const __nv_bfloat16* vbase = reinterpret_cast<const __nv_bfloat16*>(a.v);
+            for (int64_t it = blockIdx.x; it < total; it += gridDim.x) {
+                const TileInfo t = diag_tile(p, it);
+                const int64_t k0 = t.sb + (int64_t)(t.nd - 1) * kBN;  // first key of the diagonal block
+                const int64_t kn = min((int64_t)kBN, g.l - k0);
+                const uint4* vb = reinterpret_cast<const uint4*>(vbase + g.v_base(t.zh) + k0 * kD);
+                uint32_t bad = 0u;
+#pragma unroll 4
+                for (int64_t i = lane; i < kn * (kD / 8); i += 32) {
+                    const uint4 w = vb[i];
+                    for (const uint32_t x : {w.x, w.y, w.z, w.w})
+                        bad |= (((x & 0x7f80u) == 0x7f80u) | ((x & 0x7f800000u) == 0x7f800000u)) ? 1u : 0u;
+                }
+                if (__any_sync(0xffffffffu, bad != 0u) && lane == 0) {
+                    const int64_t T = a.T, full = (g.N - 1) * T, ti = t.t0 / kBM;
+                    const int64_t gt = t.zh * a.tiles_per_head + (t.n < g.N - 1 ? t.n * T + ti : full + ti);
+                    a.poison_list[atomicAdd(a.poison_cnt, 1)] = (int32_t)gt;
+                }
+            }
+            return;
+        }
         // ============================== loaders (one lane each) ==============================
-        if (lane != 0 || warp > kDVWarp) return;
+        if (lane != 0) return;
         const bool kl = warp == kDKWarp;
         const CUtensorMap* xtile = kl ? &ktile : &vtile;
         const uint32_t xbase = kl ? sK : sV;
@@ -1390,6 +1422,18 @@ bool make_bf16_row_map(void* map, const void* base, int64_t rows, uint32_t box_r
 int64_t bf16_row_span(const int64_t* st, int64_t z, int64_t h, int64_t l) { return span_rows(st, z, h, l); }
 cudaError_t set_max_dyn_smem(const void* fn, uint32_t bytes) { return smem_attr(fn, bytes); }
 
+// Diagonal-only passes (pass-1, the dense reference) on contiguous rows run on the single-tile
+// kernel with double-buffered S (S2O_DIAG_KERNEL=0 selects the pair kernel instead).
+bool tc_diag_used(const PassArgs& a) {
+    static const bool diag_on = [] {
+        const char* e = std::getenv("S2O_DIAG_KERNEL");
+        return !(e && std::strcmp(e, "0") == 0);
+    }();
+    const Geo& g = a.g;
+    return diag_on && (a.mode & kDiag) && !(a.mode & (kPrefix | kStateIn)) && !a.tile_list && g.qs[2] == kD &&
+           g.ks[2] == kD && g.vs[2] == kD;
+}
+
 bool tc_supported(const PassArgs& a) {
     const Geo& g = a.g;
     if (!g.in_bf16 || g.d != kD || a.bm != kBM || a.bn != kBN) return false;
@@ -1430,12 +1474,7 @@ cudaError_t launch_tc_pass(const PassArgs& a, cudaStream_t st) {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     // Diagonal-only passes (pass-1, the dense reference) on contiguous rows: the single-tile
     // kernel with double-buffered S (S2O_DIAG_KERNEL=0 selects the pair kernel instead).
-    static const bool diag_on = [] {
-        const char* e = std::getenv("S2O_DIAG_KERNEL");
-        return !(e && std::strcmp(e, "0") == 0);
-    }();
-    if (diag_on && (a.mode & kDiag) && !(a.mode & (kPrefix | kStateIn)) && !a.tile_list && p.q_contig &&
-        p.kv_contig) {
+    if (tc_diag_used(a)) {
         TcParams pd = p;
         pd.pairs_per_head = (g.N - 1) * a.T + t_last;  // tiles per head (diag_tile)
         if (cudaError_t e = smem_attr((const void*)tc_diag_kernel, kDSmemBytes)) return e;

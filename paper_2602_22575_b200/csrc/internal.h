@@ -59,6 +59,10 @@ struct PassArgs {
     // lvl_base (a launch whose list is empty exits at once)
     const int32_t* tile_count_dev;
     const int64_t* lvl_base_dev;
+    // pass-1 on the diagonal tcgen05 kernel: tiles whose diagonal V block holds a non-finite value
+    // (a masked future key would leak 0 * NaN through P V) are appended here and rerun exactly
+    int32_t* poison_cnt;
+    int32_t* poison_list;
 
     __host__ __device__ int64_t lvl() const {
 #ifdef __CUDA_ARCH__
@@ -120,6 +124,7 @@ cudaError_t set_max_dyn_smem(const void* fn, uint32_t bytes);  // once per (kern
 
 // tcgen05 path (bf16, D = 128, b_m = 128, b_n = 128)
 bool tc_supported(const PassArgs& a);
+bool tc_diag_used(const PassArgs& a);  // launch_tc_pass takes the diagonal (pass-1) kernel
 cudaError_t launch_tc_pass(const PassArgs& a, cudaStream_t st);
 
 // block top-k baseline selection (baseline.cu): row stats, block masses, kv token lists

@@ -279,3 +279,32 @@ def test_truncated_plan_is_prefix_of_full_plan(cuda):
             t = min(n * 1024, depth)
             off = plan.seg.kv_offset(n)
             assert torch.equal(kvt[:, :, n, :t], plan.kv_perm[:, :, off: off + t]), (depth, n)
+
+
+def test_nan_poisoned_future_keys_tensor_core_path(cuda):
+    """Acceptance C4 on the tcgen05 path: pass-1's diagonal kernel multiplies masked keys by
+    P = 0, so a non-finite V row among them would give 0 * NaN = NaN; the kernel lists such tiles
+    and run_pass recomputes them exactly (masked keys skipped, attention.cpp:55-57). Rows before
+    the poison stay finite and agree with the clean run; rows after it are NaN as in the
+    reference."""
+    import paper_2602_22575_b200 as s2o
+    torch = cuda
+    l, seg = 4096, 1024
+    q, k, v = s2o.generate_synthetic("mixed", l // 64, 8.0, 5, 1, 2, l, 128)
+    qd, kd, vd = (torch.from_numpy(np.ascontiguousarray(x)).cuda().to(torch.bfloat16) for x in (q, k[:, :1], v[:, :1]))
+    cfg = s2o.KernelConfig(seg_len=seg, tau=0.005, path=s2o.PATH_TCGEN05)
+    exact = s2o.KernelConfig(seg_len=seg, tau=0.005, path=s2o.PATH_GENERIC)
+    for cut in (1030, 2100, 3500):  # inside the diagonal block of a tile (not on a block edge)
+        kp, vp = kd.clone(), vd.clone()
+        kp[0, 0, cut + 1:] = float("nan")
+        vp[0, 0, cut + 1:] = float("nan")
+        got = s2o.s2o_attention(qd, kp, vp, cfg, want_plan=False)
+        want = s2o.s2o_attention(qd, kp, vp, exact, want_plan=False)
+        torch.cuda.synchronize()
+        before = got.out.float()[0, :, : cut + 1]
+        assert torch.isfinite(before).all(), f"cut {cut}: NaN leaked into earlier rows"
+        d = (before - want.out.float()[0, :, : cut + 1]).abs()
+        # the tensor-core bar of test_gpu_tc.py (bf16 P, fp32 state); rows whose stop decision
+        # sits on a threshold tie may differ by a chunk, so the max is looser than the mean
+        assert d.mean().item() < 2e-3 and d.max().item() < 5e-2, (cut, d.max().item(), d.mean().item())
+        assert torch.isnan(got.out.float()[0, :, cut + 1:]).all()
