@@ -151,7 +151,7 @@ struct HostArena {
     std::mutex mu;
     cudaStream_t stream = nullptr;           // compute
     cudaStream_t s_in = nullptr, s_out = nullptr;  // host->device / device->host copies
-    cudaEvent_t ev_h2d[2] = {}, ev_comp[2] = {}, ev_d2h[2] = {};
+    cudaEvent_t ev_h2d[2] = {}, ev_comp[2] = {}, ev_d2h[2] = {}, ev_kv[2] = {};
     void* dev = nullptr;
     size_t bytes = 0;
     int32_t* flags = nullptr;  // pinned, one per chunk
@@ -974,7 +974,8 @@ static s2o_status attention_host_pipelined(const s2o_problem* p, const Geo& g, c
     const size_t off_qp = off_o + align256(ob), off_kvp = off_qp + align256(qpb);
     const size_t off_pr = off_kvp + align256(kvpb), off_p1 = off_pr + align256(prb), off_p2 = off_p1 + align256(pairb);
     const size_t set_bytes = off_p2 + align256(pairb);
-    const size_t need = 2 * set_bytes + SL.total + 256 + 2 * align256(kb);  // + K/V of the split group
+    const size_t kvset = 2 * align256(kb);                         // K + V of one GQA group
+    const size_t need = 2 * set_bytes + SL.total + 256 + 2 * kvset;  // + K/V of two groups in flight
     std::lock_guard<std::mutex> lock(g_host.mu);
     if (!g_host.stream) S2O_CUDA_TRY(cudaStreamCreateWithFlags(&g_host.stream, cudaStreamNonBlocking), "stream");
     if (!g_host.s_in) {
@@ -984,6 +985,7 @@ static s2o_status attention_host_pipelined(const s2o_problem* p, const Geo& g, c
             S2O_CUDA_TRY(cudaEventCreateWithFlags(&g_host.ev_h2d[b], cudaEventDisableTiming), "event");
             S2O_CUDA_TRY(cudaEventCreateWithFlags(&g_host.ev_comp[b], cudaEventDisableTiming), "event");
             S2O_CUDA_TRY(cudaEventCreateWithFlags(&g_host.ev_d2h[b], cudaEventDisableTiming), "event");
+            S2O_CUDA_TRY(cudaEventCreateWithFlags(&g_host.ev_kv[b], cudaEventDisableTiming), "event");
         }
     }
     if (g_host.bytes < need) {
@@ -993,7 +995,7 @@ static s2o_status attention_host_pipelined(const s2o_problem* p, const Geo& g, c
         S2O_CUDA_TRY(cudaMalloc(&g_host.dev, need), "arena alloc");
         g_host.bytes = need;
     }
-    const int64_t max_chunks = nchunks + grp;
+    const int64_t max_chunks = nchunks * grp;  // at most one part per q head
     if (g_host.nflags < max_chunks) {
         if (g_host.flags) cudaFreeHost(g_host.flags);
         g_host.flags = nullptr;
@@ -1003,19 +1005,24 @@ static s2o_status attention_host_pipelined(const s2o_problem* p, const Geo& g, c
     }
     char* set[2] = {reinterpret_cast<char*>(g_host.dev), reinterpret_cast<char*>(g_host.dev) + set_bytes};
     char* ws = reinterpret_cast<char*>(g_host.dev) + 2 * set_bytes;
-    char* kvlast = ws + SL.total + 256;  // K/V of the last group when it is split per q head
+    char* kvbuf[2] = {ws + SL.total + 256, ws + SL.total + 256 + kvset};  // K/V of group zg in kvbuf[zg & 1]
     cudaStream_t sc = g_host.stream, si = g_host.s_in, so = g_host.s_out;
-    // Chunks: whole GQA groups, except the last group, which goes half a group at a time (its K/V
-    // once, into kvlast) so the pipeline tail -- last compute + last D2H -- is shorter.
-    struct Chunk { int64_t zg, q0, nq; bool shared_kv; };
+    // Chunks: a GQA group goes in parts of `step` q heads with its K/V copied once, with the first
+    // part, into a per-group-parity buffer. Whole groups, except the last, which goes in halves so
+    // the pipeline's drain (the last compute + D2H run alone) is shorter. Measured at C3 (e2e ms,
+    // S2O_HOST_PART_HEADS = parts for every group): 4 -> 36.8, 2 -> 37.3, 1 -> 44.6 (a 1-head part
+    // computes slower than its copy; more parts add per-call overhead).
+    static const int64_t split_env = [] {
+        const char* e = std::getenv("S2O_HOST_PART_HEADS");
+        return e ? std::atoll(e) : 0ll;
+    }();
+    struct Chunk { int64_t zg, q0, nq; bool first, last; };
     std::vector<Chunk> chunks;
     for (int64_t zg = 0; zg < nchunks; ++zg) {
-        if (zg + 1 < nchunks || grp == 1) {
-            chunks.push_back({zg, 0, grp, false});
-        } else {  // halves: a 1-head problem computes slower than its copy, a half-group does not
-            const int64_t step = std::max<int64_t>(1, grp / 2);
-            for (int64_t h = 0; h < grp; h += step) chunks.push_back({zg, h, std::min(step, grp - h), true});
-        }
+        const int64_t want = split_env > 0 ? split_env : (zg + 1 == nchunks ? grp / 2 : grp);
+        const int64_t step = std::min<int64_t>(grp, std::max<int64_t>(1, want));
+        for (int64_t h = 0; h < grp; h += step)
+            chunks.push_back({zg, h, std::min(step, grp - h), h == 0, h + step >= grp});
     }
     const int64_t ncs = (int64_t)chunks.size();
     auto h0_of = [&](const Chunk& ch) { return (ch.zg / p->hkv) * p->hq + (ch.zg % p->hkv) * grp + ch.q0; };
@@ -1027,12 +1034,11 @@ static s2o_status attention_host_pipelined(const s2o_problem* p, const Geo& g, c
         const char* hk = reinterpret_cast<const char*>(k) + esz_in * row * ch.zg;
         const char* hv = reinterpret_cast<const char*>(v) + esz_in * row * ch.zg;
         S2O_CUDA_TRY(cudaMemcpyAsync(set[b] + off_q, hq, esz_in * row * ch.nq, cudaMemcpyHostToDevice, si), "h2d q");
-        if (!ch.shared_kv) {
-            S2O_CUDA_TRY(cudaMemcpyAsync(set[b] + off_k, hk, kb, cudaMemcpyHostToDevice, si), "h2d k");
-            S2O_CUDA_TRY(cudaMemcpyAsync(set[b] + off_v, hv, kb, cudaMemcpyHostToDevice, si), "h2d v");
-        } else if (ch.q0 == 0) {  // stream order: later sub-chunks' events follow this copy
-            S2O_CUDA_TRY(cudaMemcpyAsync(kvlast, hk, kb, cudaMemcpyHostToDevice, si), "h2d k");
-            S2O_CUDA_TRY(cudaMemcpyAsync(kvlast + align256(kb), hv, kb, cudaMemcpyHostToDevice, si), "h2d v");
+        if (ch.first) {  // the group's K/V (its buffer was last read by group zg - 2's last part)
+            char* kvd = kvbuf[ch.zg & 1];
+            if (ch.zg >= 2) S2O_CUDA_TRY(cudaStreamWaitEvent(si, g_host.ev_kv[ch.zg & 1], 0), "wait");
+            S2O_CUDA_TRY(cudaMemcpyAsync(kvd, hk, kb, cudaMemcpyHostToDevice, si), "h2d k");
+            S2O_CUDA_TRY(cudaMemcpyAsync(kvd + align256(kb), hv, kb, cudaMemcpyHostToDevice, si), "h2d v");
         }
         S2O_CUDA_TRY(cudaEventRecord(g_host.ev_h2d[b], si), "record");
         return S2O_OK;
@@ -1056,8 +1062,8 @@ static s2o_status attention_host_pipelined(const s2o_problem* p, const Geo& g, c
         if ((st = make_geo(&cp, cfg->seg_len, &cg))) { drain(); return st; }
         const PassArgs ca = base_args(cg, cfg);
         const OpLayout CL = op_layout(cg, ca, cfg->fused, cfg);
-        const char* dk = ch.shared_kv ? kvlast : cs + off_k;
-        const char* dv = ch.shared_kv ? kvlast + align256(kb) : cs + off_v;
+        const char* dk = kvbuf[ch.zg & 1];
+        const char* dv = kvbuf[ch.zg & 1] + align256(kb);
         st = s2o_attention_fwd(&cp, cs + off_q, dk, dv, cfg, cs + off_o,
                                reinterpret_cast<int32_t*>(cs + off_qp),
                                kvpb ? reinterpret_cast<int32_t*>(cs + off_kvp) : nullptr,
@@ -1068,6 +1074,7 @@ static s2o_status attention_host_pipelined(const s2o_problem* p, const Geo& g, c
         const int32_t* dflag = reinterpret_cast<const int32_t*>(cwb + CL.pass + align256(generic_scratch_bytes(ca)));
         S2O_CUDA_TRY(cudaMemcpyAsync(&g_host.flags[c], dflag, sizeof(int32_t), cudaMemcpyDeviceToHost, sc), "d2h flag");
         S2O_CUDA_TRY(cudaEventRecord(g_host.ev_comp[b], sc), "record");
+        if (ch.last) S2O_CUDA_TRY(cudaEventRecord(g_host.ev_kv[ch.zg & 1], sc), "record");  // K/V buffer free
         S2O_CUDA_TRY(cudaStreamWaitEvent(so, g_host.ev_comp[b], 0), "wait");
         const int64_t h0 = h0_of(ch), nq = ch.nq;
         S2O_CUDA_TRY(cudaMemcpyAsync(reinterpret_cast<char*>(o) + esz_out * row * h0, cs + off_o, esz_out * row * nq,
@@ -1187,7 +1194,7 @@ void s2o_host_release(void) {
         *s = nullptr;
     }
     for (int b = 0; b < 2; ++b)
-        for (cudaEvent_t* e : {&g_host.ev_h2d[b], &g_host.ev_comp[b], &g_host.ev_d2h[b]}) {
+        for (cudaEvent_t* e : {&g_host.ev_h2d[b], &g_host.ev_comp[b], &g_host.ev_d2h[b], &g_host.ev_kv[b]}) {
             if (*e) cudaEventDestroy(*e);
             *e = nullptr;
         }
