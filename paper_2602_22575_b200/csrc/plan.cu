@@ -433,10 +433,8 @@ __device__ __forceinline__ double bf16_hi_to_f64(uint32_t w) { return (double)__
 
 __global__ void __launch_bounds__(kKS_Threads, 2)
 kv_score128_kernel(const __nv_bfloat16* __restrict__ k, Geo g, const float* __restrict__ q_mean,
-                   uint64_t* __restrict__ kvkey, int max_batches, int64_t n_hi, const int32_t* __restrict__ skip_if,
-                   const int32_t* __restrict__ need) {
-    // plan levels: the keys are already there, or no segment needs a level
-    if ((skip_if && *skip_if) || (need && *need == 0)) return;
+                   uint64_t* __restrict__ kvkey, int max_batches, int64_t n_hi, const int32_t* __restrict__ skip) {
+    if (skip && *skip) return;  // device-side gate (plan levels)
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int64_t kb = blockIdx.x / max_batches;
@@ -448,6 +446,10 @@ kv_score128_kernel(const __nv_bfloat16* __restrict__ k, Geo g, const float* __re
     const int64_t n_end = n_hi < g.N ? n_hi : g.N;  // segments [n_lo, n_end) only
     const int64_t nsegs = (n_lo < n_end) ? n_end - n_lo : 0;
     const int64_t pairs = g.group * nsegs;
+    auto pair_hn = [&](int64_t p, int64_t& h, int64_t& n) {  // pair p of this key block -> (q head, segment)
+        h = kvh * g.group + p / nsegs;
+        n = n_lo + p % nsegs;
+    };
     const int64_t p0 = (int64_t)batch * kKS_Pairs;
     if (p0 >= pairs) return;
     const int64_t rem = pairs - p0;  // pairs from p0 on
@@ -481,8 +483,8 @@ kv_score128_kernel(const __nv_bfloat16* __restrict__ k, Geo g, const float* __re
         const int64_t pq = p0 + qp;
         const float* qsrc = nullptr;
         if (pq < pairs) {
-            const int64_t h = kvh * g.group + pq / nsegs;
-            const int64_t n = n_lo + pq % nsegs;
+            int64_t h, n;
+            pair_hn(pq, h, n);
             qsrc = q_mean + ((z * g.hq + h) * g.N + n) * 128 + qh * dlen;
         }
 #pragma unroll 4
@@ -537,8 +539,8 @@ kv_score128_kernel(const __nv_bfloat16* __restrict__ k, Geo g, const float* __re
     for (int i = 0; i < 8; ++i) {
         const int64_t p = p0 + 32 * wpair + 8 * (i >> 1) + 2 * pg + (i & 1);
         if (p >= pairs) continue;
-        const int64_t h = kvh * g.group + p / nsegs;
-        const int64_t n = n_lo + p % nsegs;
+        int64_t h, n;
+        pair_hn(p, h, n);
         uint64_t* dst = kvkey + (z * g.hq + h) * kvp + g.kv_off(n);
         const int64_t lim = n * g.S;
 #pragma unroll
@@ -554,10 +556,10 @@ bool kv_score128_ok(const Geo& g, const void* k) {
            (reinterpret_cast<uintptr_t>(k) & 15) == 0 && g.S % 2 == 0;
 }
 
-// Exact scores of segments [1, n_hi) (n_hi >= N: all); skip_if (device flag, optional): a launch that
-// finds it set exits at once.
+// Exact scores of segments [1, n_hi) (n_hi >= N: all); skip (device, optional): the launch exits
+// at once when *skip != 0.
 cudaError_t launch_kv_score(const Geo& g, const void* k, const float* q_mean, uint64_t* kvkey, cudaStream_t st,
-                            int64_t n_hi = INT64_MAX, const int32_t* skip_if = nullptr, const int32_t* need = nullptr) {
+                            int64_t n_hi = INT64_MAX, const int32_t* skip = nullptr) {
     const int64_t n_end = std::min<int64_t>(n_hi, g.N);
     if (n_end < 2) return cudaSuccess;
     const int64_t keys = (n_end - 1) * g.S;  // tokens that appear in some prefix
@@ -567,10 +569,10 @@ cudaError_t launch_kv_score(const Geo& g, const void* k, const float* q_mean, ui
         dim3 grid((unsigned)(blocks * max_batches), (unsigned)(g.z * g.hkv));
         cudaFuncSetAttribute(kv_score128_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kKS_Smem);
         kv_score128_kernel<<<grid, kKS_Threads, kKS_Smem, st>>>(reinterpret_cast<const __nv_bfloat16*>(k), g, q_mean,
-                                                         kvkey, max_batches, n_hi, skip_if, need);
+                                                         kvkey, max_batches, n_hi, skip);
         return cudaGetLastError();
     }
-    if (n_end < g.N || skip_if) return cudaErrorInvalidValue;  // generic scoring: whole plans only
+    if (n_end < g.N || skip) return cudaErrorInvalidValue;  // generic scoring: whole plans only
     const size_t smem = sizeof(double) * g.d * kSPairs + sizeof(float) * g.d * kSK;
     cudaFuncSetAttribute(kv_score_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     dim3 grid((unsigned)blocks, (unsigned)(g.z * g.hkv));
@@ -1093,6 +1095,7 @@ struct PlanWs {
     uint64_t* kth;     // [Z*Hq*N]
     int32_t* ccnt;     // [Z*Hq*N][nch]
     int32_t* full;     // 1: key0 holds every exact prefix-key score (plan levels need them)
+    uint8_t* scored;   // [Z*Hq*N] 1: key0 holds every exact prefix-key score of that segment
 };
 
 int64_t cand_chunks(const Geo& g) { return std::max<int64_t>(1, ((g.N - 1) * g.S + kCR - 1) / kCR); }
@@ -1122,7 +1125,8 @@ size_t plan_ws_layout(const Geo& g, char* base, PlanWs* out) {
     ws.ec = reinterpret_cast<float*>(take(sizeof(float) * zhq * g.N));
     ws.kth = reinterpret_cast<uint64_t*>(take(sizeof(uint64_t) * zhq * g.N));
     ws.ccnt = reinterpret_cast<int32_t*>(take(sizeof(int32_t) * zhq * g.N * cand_chunks(g)));
-    ws.full = reinterpret_cast<int32_t*>(take(sizeof(int32_t)));
+    ws.full = reinterpret_cast<int32_t*>(take(2 * sizeof(int32_t)));  // full, dense-gate scratch
+    ws.scored = reinterpret_cast<uint8_t*>(take(zhq * g.N));
     if (out) *out = ws;
     return off;
 }
@@ -1215,6 +1219,7 @@ cudaError_t launch_select_tc(const Geo& g, const void* k, const PlanWs& ws, int3
     const int64_t n_direct = std::min<int64_t>(g.N, kSelCap / g.S + 1);
     const int64_t n_cand = std::min<int64_t>(g.N, std::max<int64_t>(n_direct, (kCandDensity * topt + g.S - 1) / g.S));
     if ((err = cudaMemsetAsync(ws.full, 0, sizeof(int32_t), st)) != cudaSuccess) return err;
+    if ((err = cudaMemsetAsync(ws.scored, 0, zhq * g.N, st)) != cudaSuccess) return err;
     if (n_cand >= 2 && (err = launch_kv_score(g, k, ws.q_mean, ws.key0, st, n_cand)) != cudaSuccess) return err;
     if (n_cand < g.N) {
         // step 1: exact scores of every 16th key (a strided view of K), into key1
@@ -1265,13 +1270,80 @@ cudaError_t launch_select_tc(const Geo& g, const void* k, const PlanWs& ws, int3
     return cudaGetLastError();
 }
 
-// Plan levels read every exact score from key0: after a candidate-pruned level 0 they are scored
-// once, by the first level that needs them (device flag, so this stays stream-ordered).
-cudaError_t ensure_full_keys(const Geo& g, const void* k, const PlanWs& ws, const int32_t* need, cudaStream_t st) {
+// Plan levels read every exact prefix-key score of the segments they serve from key0. After a
+// candidate-pruned level 0 those are scored here, stream-ordered (counts in device memory) and only
+// when a level is needed:
+//  * few listed segments (< kLevelDense): kv_score_rows_kernel, a persistent loop over (segment,
+//    256-key block) items of the segments not scored before (~5 us per segment at C3);
+//  * many (low tau): kv_score128_kernel over every key once (1.8 ms at C3), then `full` is set and
+//    later levels skip both kernels.
+constexpr int kLSKeys = 256, kLSThreads = 128, kLevelDense = 320;
+__global__ void __launch_bounds__(kLSThreads)
+kv_score_rows_kernel(Geo g, const __nv_bfloat16* __restrict__ k, const float* __restrict__ q_mean,
+                     uint64_t* __restrict__ kvkey, const int32_t* __restrict__ seg_list,
+                     const int32_t* __restrict__ nseg_dev, const uint8_t* __restrict__ scored,
+                     const int32_t* __restrict__ full) {
+    __shared__ double qs[128];
+    if (*full || *nseg_dev >= kLevelDense) return;
+    const int64_t nseg = *nseg_dev;
+    const int64_t blocks = ((g.N - 1) * g.S + kLSKeys - 1) / kLSKeys;  // of the longest prefix
+    for (int64_t w = blockIdx.x; w < nseg * blocks; w += gridDim.x) {
+        const int64_t code = seg_list[w / blocks], kb = w % blocks;
+        const int64_t zh = code / g.N, n = code % g.N;
+        const int64_t t0 = kb * kLSKeys, len = n * g.S;
+        if (scored[code] || t0 >= len) continue;  // uniform across the CTA
+        __syncthreads();  // previous item's qs readers are done
+        if (threadIdx.x < 128) qs[threadIdx.x] = (double)q_mean[code * 128 + threadIdx.x];
+        __syncthreads();
+        const __nv_bfloat16* kb0 = k + (zh / g.hq) * g.ks[0] + g.kvh(zh) * g.ks[1];
+        uint64_t* dst = kvkey + zh * g.kv_per_head() + g.kv_off(n);
+        for (int64_t t = t0 + threadIdx.x; t < min(len, t0 + kLSKeys); t += kLSThreads) {
+            const uint4* kr = reinterpret_cast<const uint4*>(kb0 + t * g.ks[2]);
+            double acc = 0.0;  // dot_f order: d = 0..127 from 0.0 (plan.cpp:14-20)
+#pragma unroll 4
+            for (int c = 0; c < 16; ++c) {
+                const uint4 w4 = kr[c];
+                const uint32_t wv[4] = {w4.x, w4.y, w4.z, w4.w};
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    acc = fma(qs[8 * c + 2 * e], (double)__uint_as_float(wv[e] << 16), acc);
+                    acc = fma(qs[8 * c + 2 * e + 1], (double)__uint_as_float(wv[e] & 0xffff0000u), acc);
+                }
+            }
+            dst[t] = desc_key(acc);
+        }
+    }
+}
+
+__global__ void level_keys_done_kernel(const int32_t* __restrict__ seg_list, const int32_t* __restrict__ nseg_dev,
+                                       uint8_t* __restrict__ scored, int32_t* __restrict__ full) {
+    const int64_t nseg = *nseg_dev;
+    if (nseg >= kLevelDense) {
+        if (blockIdx.x == 0 && threadIdx.x == 0) *full = 1;
+        return;
+    }
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nseg; i += (int64_t)gridDim.x * blockDim.x)
+        scored[seg_list[i]] = 1;
+}
+
+__global__ void dense_gate_kernel(const int32_t* __restrict__ nseg_dev, const int32_t* __restrict__ full,
+                                  int32_t* __restrict__ skip) {
+    *skip = (*full || *nseg_dev < kLevelDense) ? 1 : 0;
+}
+
+cudaError_t ensure_level_keys(const Geo& g, const void* k, const PlanWs& ws, const int32_t* seg_list,
+                              const int32_t* nseg_dev, cudaStream_t st) {
     if (!kv_score128_ok(g, k)) return cudaSuccess;  // the generic selection always scores everything
-    cudaError_t err = launch_kv_score(g, k, ws.q_mean, ws.key0, st, INT64_MAX, ws.full, need);
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    int32_t* skip = ws.full + 1;  // same 256-B slot
+    dense_gate_kernel<<<1, 1, 0, st>>>(nseg_dev, ws.full, skip);
+    cudaError_t err = launch_kv_score(g, k, ws.q_mean, ws.key0, st, INT64_MAX, skip);
     if (err != cudaSuccess) return err;
-    set_flag_kernel<<<1, 1, 0, st>>>(ws.full, 1, need);
+    kv_score_rows_kernel<<<sms * 8, kLSThreads, 0, st>>>(g, reinterpret_cast<const __nv_bfloat16*>(k), ws.q_mean,
+                                                          ws.key0, seg_list, nseg_dev, ws.scored, ws.full);
+    level_keys_done_kernel<<<8, 256, 0, st>>>(seg_list, nseg_dev, ws.scored, ws.full);
     return cudaGetLastError();
 }
 
@@ -1292,7 +1364,7 @@ cudaError_t launch_plan_topk(const Geo& g, const void* q, const void* k, int32_t
     if (g.N > 1) {
         if (select_tc_ok(g, k, topt)) return launch_select_tc(g, k, ws, kvtop, topt, flags, st);
         if ((err = launch_kv_score(g, k, ws.q_mean, ws.key0, st)) != cudaSuccess) return err;
-        if (kv_score128_ok(g, k)) set_flag_kernel<<<1, 1, 0, st>>>(ws.full, 1, nullptr);
+        if (kv_score128_ok(g, k)) set_flag_kernel<<<1, 1, 0, st>>>(ws.full, 1);
         if ((err = launch_select(g, ws, g.z * g.hq * (g.N - 1), nullptr, nullptr, 0, kvtop, topt, flags, st)) !=
             cudaSuccess)
             return err;
@@ -1309,7 +1381,7 @@ cudaError_t launch_plan_level_dev(const Geo& g, const void* k, const int32_t* se
     PlanWs ws;
     char* base = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(workspace) + 255) & ~uintptr_t(255));
     plan_ws_layout(g, base, &ws);
-    cudaError_t err = ensure_full_keys(g, k, ws, nseg_dev, st);
+    cudaError_t err = ensure_level_keys(g, k, ws, seg_list, nseg_dev, st);
     if (err != cudaSuccess) return err;
     return launch_select(g, ws, nmax, seg_list, prev, 0, kvtop, topt, flags, st, nseg_dev, lvl_base_dev);
 }

@@ -483,7 +483,7 @@ __device__ __forceinline__ double desc_key_value(uint64_t key) {  // inverse of 
 }
 
 // Step 1: per row (zh, n >= n_cand): theta from the exact scores of the sampled keys, e_q.
-constexpr int kThrThreads = 512;
+constexpr int kThrThreads = 1024;
 __global__ void __launch_bounds__(kThrThreads)
 cand_thresh_kernel(Geo g, const uint64_t* __restrict__ samp, int64_t s2, const float* __restrict__ q_mean,
                    int64_t topt, int64_t n_cand, float* __restrict__ thr, float* __restrict__ ec,
@@ -500,7 +500,7 @@ cand_thresh_kernel(Geo g, const uint64_t* __restrict__ samp, int64_t s2, const f
     // between T and the count above theta, so certification fails ~1e-9 per row
     const double x = (double)tt * (double)m / (double)len;
     const int64_t rank = min(m, max((int64_t)1, (int64_t)ceil(x + 6.0 * sqrt(x) + 18.0)));
-    constexpr int kPer = 32;  // keys per thread held in registers (m <= 16384), else re-read
+    constexpr int kPer = 16;  // keys per thread held in registers (m <= 16384), else re-read
     uint64_t kr[kPer];
     const bool in_regs = m <= kThrThreads * kPer;
     if (in_regs) {
@@ -703,6 +703,4 @@ cand_pack_kernel(Geo g, const uint64_t* __restrict__ ckey_in, const uint32_t* __
     if (tid == 0) *outc = n_less + need_eq;
 }
 
-__global__ void set_flag_kernel(int32_t* f, int32_t v, const int32_t* need) {
-    if (!need || *need != 0) *f = v;
-}
+__global__ void set_flag_kernel(int32_t* f, int32_t v) { *f = v; }

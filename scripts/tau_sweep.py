@@ -33,6 +33,9 @@ def main():
     ap.add_argument("--seg", type=int, default=2048)
     ap.add_argument("--ref-segments", type=int, default=4)
     ap.add_argument("--ref-heads", type=int, default=2)
+    ap.add_argument("--full-ref-heads", type=int, default=1,
+                    help="q heads compared with the compiled reference over the FULL sequence at every tau "
+                         "(one CPU process per tau, in parallel); 0: off")
     ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "tau_sweep.json"))
     args = ap.parse_args()
 
@@ -111,6 +114,44 @@ def main():
         rows.append(row)
         print(json.dumps(row), flush=True)
         del res, diff
+    # ---- full-depth parity: the first `full_ref_heads` q heads over all L tokens, every tau, against
+    # the compiled reference (one process per tau; traces must agree up to threshold ties)
+    if args.full_ref_heads > 0:
+        import multiprocessing as mp
+        from oracle.oracle import trace_ties
+        hf = list(range(args.full_ref_heads))
+        qf = q[:, hf].float().cpu().numpy()
+        kf = k[:, [h // (HQ // HKV) for h in hf]].float().cpu().numpy()
+        vf = v[:, [h // (HQ // HKV) for h in hf]].float().cpu().numpy()
+        devs = {}
+        for tau in TAUS:
+            cfg = s2o.KernelConfig(seg_len=S, tau=tau, tiles=s2o.TileSpec(128, 128))
+            res = s2o.s2o_attention(q, k, v, cfg, want_plan=False)
+            torch.cuda.synchronize()
+            devs[tau] = (res.trace.processed.reshape(HQ, L // S, -1).cpu().numpy()[hf],
+                         res.out[:, hf].float().cpu().numpy(), res.trace.pass2_pairs[0, hf].cpu().numpy())
+            del res
+        t0 = time.perf_counter()
+        with mp.get_context("spawn").Pool(len(TAUS)) as pool:
+            refs = pool.starmap(_ref_full, [(qf, kf, vf, S, tau) for tau in TAUS])
+        wall = time.perf_counter() - t0
+        for row, tau, (ro, rt, rq, rkv, rp2, secs) in zip(rows, TAUS, refs):
+            got_t, go, gp2 = devs[tau]
+            class Cfg:
+                pass
+            c = Cfg()
+            c.seg_len, c.tau, c.b_m, c.b_n, c.q_reorder, c.fused, c.local_window = S, tau, 128, 128, True, False, -1
+            want_t = rt.reshape(got_t.shape)
+            ties = trace_ties(Ref(), qf, kf, vf, c, rq, rkv, got_t, want_t) if (got_t != want_t).any() else []
+            row["ref_full_depth"] = {
+                "heads": len(hf), "tokens": L, "tiles": int(want_t.size),
+                "trace_tiles_differing": int((got_t != want_t).sum()),
+                "differences_all_threshold_ties": all(t["tie"] for t in ties), "ties": ties[:8],
+                "pass2_pairs": {"device": gp2.tolist(), "reference": rp2.tolist()},
+                "max_abs_out_diff": float(np.abs(go - ro).max()), "mean_abs_out_diff": float(np.abs(go - ro).mean()),
+                "cpu_s": round(secs, 1)}
+            print(json.dumps({"tau": tau, "ref_full_depth": row["ref_full_depth"]}), flush=True)
+        print(f"full-depth reference: {len(TAUS)} processes, {wall:.0f} s wall", flush=True)
     doc = {"config": {"workload": "C5: C3 layer (32q/8kv, d=128, bf16, L=%d, S=%d, 128x128) tau sweep" % (L, S),
                       "data": "synthetic mixed stripes (L/64, gain 8, seed 0)",
                       "dense": "torch SDPA bf16 causal GQA on the same GPU (fp32 difference)",
@@ -119,6 +160,19 @@ def main():
     os.makedirs(os.path.dirname(args.out), exist_ok=True)
     with open(args.out, "w") as f:
         json.dump(doc, f, indent=1)
+
+
+def _ref_full(qf, kf, vf, S, tau):
+    """Worker: the compiled reference's s2o_attention on the given heads (full length)."""
+    import time as _t
+    from oracle.oracle import Ref
+    class Cfg:
+        pass
+    c = Cfg()
+    c.seg_len, c.tau, c.b_m, c.b_n, c.q_reorder, c.fused, c.local_window = S, tau, 128, 128, True, False, -1
+    t0 = _t.perf_counter()
+    ro, rt, rp = Ref().attention(qf, kf, vf, c)
+    return ro, rt.processed, rp.q_perm, rp.kv_perm, rt.pass2_pairs, _t.perf_counter() - t0
 
 
 if __name__ == "__main__":
