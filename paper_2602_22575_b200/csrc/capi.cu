@@ -1007,11 +1007,12 @@ static s2o_status attention_host_pipelined(const s2o_problem* p, const Geo& g, c
     char* ws = reinterpret_cast<char*>(g_host.dev) + 2 * set_bytes;
     char* kvbuf[2] = {ws + SL.total + 256, ws + SL.total + 256 + kvset};  // K/V of group zg in kvbuf[zg & 1]
     cudaStream_t sc = g_host.stream, si = g_host.s_in, so = g_host.s_out;
-    // Chunks: a GQA group goes in parts of `step` q heads with its K/V copied once, with the first
-    // part, into a per-group-parity buffer. Whole groups, except the last, which goes in halves so
-    // the pipeline's drain (the last compute + D2H run alone) is shorter. Measured at C3 (e2e ms,
-    // S2O_HOST_PART_HEADS = parts for every group): 4 -> 36.8, 2 -> 37.3, 1 -> 44.6 (a 1-head part
-    // computes slower than its copy; more parts add per-call overhead).
+    // Chunks: a GQA group goes in parts of q heads with its K/V copied once, with the first part,
+    // into a per-group-parity buffer. Whole groups, except the first, whose first part is one head
+    // (the pipeline's fill: that H2D runs alone), and the last, which goes in halves (the drain: the
+    // last compute + D2H run alone). Measured at C3 (e2e ms): this 35.3; whole groups + halved last
+    // 36.0; S2O_HOST_PART_HEADS = parts for every group: 4 -> 36.8, 2 -> 37.3, 1 -> 44.6 (a 1-head
+    // part computes slower than its copy; more parts add per-call overhead); a 1-head last part 35.5.
     static const int64_t split_env = [] {
         const char* e = std::getenv("S2O_HOST_PART_HEADS");
         return e ? std::atoll(e) : 0ll;
@@ -1019,6 +1020,12 @@ static s2o_status attention_host_pipelined(const s2o_problem* p, const Geo& g, c
     struct Chunk { int64_t zg, q0, nq; bool first, last; };
     std::vector<Chunk> chunks;
     for (int64_t zg = 0; zg < nchunks; ++zg) {
+        if (split_env <= 0 && zg == 0 && nchunks > 1 && grp >= 4) {
+            // the fill: the first part's H2D runs alone, so it is one q head (+ the group's K/V)
+            chunks.push_back({zg, 0, 1, true, false});
+            chunks.push_back({zg, 1, grp - 1, false, true});
+            continue;
+        }
         const int64_t want = split_env > 0 ? split_env : (zg + 1 == nchunks ? grp / 2 : grp);
         const int64_t step = std::min<int64_t>(grp, std::max<int64_t>(1, want));
         for (int64_t h = 0; h < grp; h += step)
