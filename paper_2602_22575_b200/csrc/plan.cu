@@ -1199,6 +1199,33 @@ cudaError_t launch_select(const Geo& g, const PlanWs& ws, int64_t nseg, const in
 
 
 
+// Row tiles of kv_cand_kernel: replicate the rows of short prefixes (their candidates per key tile
+// scale with 1 / n) so every lane carries a similar load: rep ~ (N - 1) / n, at most 4. False when
+// the geometry needs more tiles than CandArgs holds (the caller then uses the dense selection).
+bool cand_row_tiles(const Geo& g, int64_t n_cand, CandArgs* ca) {
+    ca->ntiles = 0;
+    if (g.group > 128) return false;
+    // (A/B at C3, kv_cand ms: n * rep <= N - 1, rep <= 4: 1.12; <= 2 (N - 1): 1.44; rep <= 8 with
+    // <= 2 (N - 1): 1.36; no replication: 1.21 -- more row tiles cost more K conversion and MMA)
+    for (int64_t n = n_cand; n < g.N;) {
+        int64_t rep = 4;
+        while (rep > 1 && (n * rep > g.N - 1 || g.group * rep > 128)) rep /= 2;
+        const int64_t nseg = std::min<int64_t>(std::max<int64_t>(1, 128 / rep / g.group), g.N - n);
+        if (ca->ntiles == kCMaxRowTiles) return false;
+        ca->tn0[ca->ntiles] = (int32_t)n;
+        ca->tnc[ca->ntiles] = (int32_t)nseg;
+        ca->trep[ca->ntiles] = (int32_t)rep;
+        ++ca->ntiles;
+        n += nseg;
+    }
+    return true;
+}
+
+int64_t cand_first_segment(const Geo& g, int64_t topt) {
+    const int64_t n_direct = std::min<int64_t>(g.N, kSelCap / g.S + 1);
+    return std::min<int64_t>(g.N, std::max<int64_t>(n_direct, (kCandDensity * topt + g.S - 1) / g.S));
+}
+
 // The candidate-pruned selection (plan_tc.cuh) serves bf16, D = 128 plans with 128-row-aligned,
 // contiguous K rows and S % 128 == 0; S2O_PLAN_TC=0 forces the dense-scoring selection.
 bool select_tc_ok(const Geo& g, const void* k, int64_t topt) {
@@ -1206,8 +1233,10 @@ bool select_tc_ok(const Geo& g, const void* k, int64_t topt) {
         const char* e = std::getenv("S2O_PLAN_TC");
         return !(e && std::strcmp(e, "0") == 0);
     }();
+    CandArgs ca;
     return on && kv_score128_ok(g, k) && g.ks[2] == 128 && g.ks[1] % 128 == 0 && g.ks[0] % 128 == 0 &&
-           g.S % 128 == 0 && g.N >= 2 && topt <= kSelCap && bf16_row_span(g.ks, g.z, g.hkv, g.l) < (int64_t(1) << 31);
+           g.S % 128 == 0 && g.N >= 2 && topt <= kSelCap && bf16_row_span(g.ks, g.z, g.hkv, g.l) < (int64_t(1) << 31) &&
+           cand_row_tiles(g, cand_first_segment(g, topt), &ca);
 }
 
 cudaError_t launch_select_tc(const Geo& g, const void* k, const PlanWs& ws, int32_t* kvtop, int64_t topt,
@@ -1217,7 +1246,7 @@ cudaError_t launch_select_tc(const Geo& g, const void* k, const PlanWs& ws, int3
     // segments n < n_cand: dense exact scores (most of their keys would be candidates anyway);
     // n < n_direct of them (at most kSelCap keys) are sorted whole, the others selected by sel_scan
     const int64_t n_direct = std::min<int64_t>(g.N, kSelCap / g.S + 1);
-    const int64_t n_cand = std::min<int64_t>(g.N, std::max<int64_t>(n_direct, (kCandDensity * topt + g.S - 1) / g.S));
+    const int64_t n_cand = cand_first_segment(g, topt);
     if ((err = cudaMemsetAsync(ws.full, 0, sizeof(int32_t), st)) != cudaSuccess) return err;
     if ((err = cudaMemsetAsync(ws.scored, 0, zhq * g.N, st)) != cudaSuccess) return err;
     if (n_cand >= 2 && (err = launch_kv_score(g, k, ws.q_mean, ws.key0, st, n_cand)) != cudaSuccess) return err;
@@ -1244,10 +1273,9 @@ cudaError_t launch_select_tc(const Geo& g, const void* k, const PlanWs& ws, int3
         ca.cidx = ws.idx0;
         ca.ccnt = ws.ccnt;
         ca.nch = cand_chunks(g);
-        ca.n_cand = n_cand;
-        ca.rows = g.group * (g.N - n_cand);
+        if (!cand_row_tiles(g, n_cand, &ca)) return cudaErrorInvalidValue;
         if ((err = set_max_dyn_smem((const void*)kv_cand_kernel, kCSmem)) != cudaSuccess) return err;
-        dim3 grid((unsigned)ca.nch, (unsigned)((ca.rows + 127) / 128), (unsigned)(g.z * g.hkv));
+        dim3 grid((unsigned)ca.nch, (unsigned)ca.ntiles, (unsigned)(g.z * g.hkv));
         kv_cand_kernel<<<grid, kCThreads, kCSmem, st>>>(ca, kmap);
         if ((err = cudaGetLastError()) != cudaSuccess) return err;
         // step 3: certification + exact first-T compaction, into key1 / idx1 at the row offsets

@@ -79,9 +79,15 @@ struct CandArgs {
     uint32_t* cidx;
     int32_t* ccnt;        // [Z*Hq*N][nch] candidates per (row, chunk)
     int64_t nch;          // chunks of the longest prefix
-    int64_t n_cand;       // first segment selected here (earlier ones are scored densely)
-    int64_t rows;         // rows per kv head: group * (N - n_cand), row = (n - n_cand) * group + h % group
+    // row tiles (the same for every kv head): tile y holds segments [tn0[y], tn0[y] + tnc[y]) of the
+    // kv head's q heads, row u = (n - tn0) * group + h % group, U = tnc * group <= 128 / trep rows,
+    // each replicated trep times over the 128 MMA rows / TMEM lanes (lane l holds row l % (128 /
+    // trep)): a short prefix concentrates a row's candidates in few key tiles, so those rows get
+    // more lanes (their candidates split by rank over the replicas)
+    int32_t tn0[64], tnc[64], trep[64];
+    int32_t ntiles;
 };
+constexpr int kCMaxRowTiles = 64;
 
 // bf16 (as the high half of a fp32 word, low 16 bits zero) -> high 32 bits of the equal double;
 // the low 32 bits are zero for every bf16 value. Zeros, infinities and NaN handled; a bf16
@@ -114,12 +120,13 @@ kv_cand_kernel(const CandArgs a, const __grid_constant__ CUtensorMap kmap) {
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     const int64_t chunk = blockIdx.x;
     const int64_t z = blockIdx.z / g.hkv, kvh = blockIdx.z % g.hkv;
-    const int64_t rho0 = (int64_t)blockIdx.y * 128;
-    const int64_t rho_end = min(rho0 + 128, a.rows);
-    const int64_t n_top = a.n_cand + (rho_end - 1) / g.group;  // rows are ordered by segment
+    const int ty = blockIdx.y;
+    const int64_t tn0 = a.tn0[ty], rep = a.trep[ty];
+    const int64_t n_top = tn0 + a.tnc[ty] - 1;  // longest prefix of the tile
+    const int64_t urows = (int64_t)a.tnc[ty] * g.group, uspan = 128 / rep;
     const int64_t key_end = n_top * g.S;
     const int64_t t_begin = chunk * kCR;
-    if (rho0 >= a.rows || t_begin >= key_end) return;  // nothing here
+    if (t_begin >= key_end) return;  // nothing here
     const int ntiles = (int)min((int64_t)kCTiles, (key_end - t_begin + 127) / 128);
     const uint32_t sK = smem_u32(smem + kCOffK);
     float* kn = reinterpret_cast<float*>(smem + kCOffKn);
@@ -141,10 +148,11 @@ kv_cand_kernel(const CandArgs a, const __grid_constant__ CUtensorMap kmap) {
     }
     // ---- the row of TMEM lane r (quadrant warp % 4) for row and converter warps
     const int r = (warp % 4) * 32 + lane;
-    const int64_t rho = rho0 + r;  // consecutive rows (similar prefix lengths) share a warp
-    const bool in = warp < kCTmaWarp && rho < rho_end;
-    const int64_t n = in ? a.n_cand + rho / g.group : 0;
-    const int64_t zh = z * g.hq + kvh * g.group + (in ? rho % g.group : 0);
+    const int64_t u = r % uspan;     // the lane's row (consecutive rows share a warp)
+    const int replica = (int)(r / uspan);
+    const bool in = warp < kCTmaWarp && u < urows;
+    const int64_t n = in ? tn0 + u / g.group : 0;
+    const int64_t zh = z * g.hq + kvh * g.group + (in ? u % g.group : 0);
     const int64_t rowcode = zh * g.N + n;
     const int64_t lim = in ? n * g.S : 0;
     tc_fence_before();
@@ -310,22 +318,39 @@ kv_cand_kernel(const CandArgs a, const __grid_constant__ CUtensorMap kmap) {
             const uint32_t m[4] = {mm.x, mm.y, mm.z, mm.w};
             const int pc0 = __popc(m[0]), pc1 = pc0 + __popc(m[1]), pc2 = pc1 + __popc(m[2]);
             const int total = pc2 + __popc(m[3]);
-            // this warp's share: every other candidate by rank (sub 0 even, sub 1 odd ranks): bit i of
-            // the prefix XOR x is the parity of the candidates at or below i
+            // this thread's share of the row's candidates: ranks = replica * kCSub + sub (mod
+            // trep * kCSub); for one replica, the parity of the rank (bit i of the prefix XOR x is
+            // the parity of the candidates at or below i)
             static_assert(kCSub == 2, "rank split by parity");
             uint32_t mine[4];
-            uint32_t carry = 0u;  // parity of the candidates in earlier words
+            if (rep == 1) {
+                uint32_t carry = 0u;  // parity of the candidates in earlier words
 #pragma unroll
-            for (int q4 = 0; q4 < 4; ++q4) {
-                uint32_t x = m[q4];
-                x ^= x << 1;
-                x ^= x << 2;
-                x ^= x << 4;
-                x ^= x << 8;
-                x ^= x << 16;
-                const uint32_t even = m[q4] & (carry ? ~x : x);  // global rank even
-                mine[q4] = sub == 0 ? even : (m[q4] & ~even);
-                carry ^= (uint32_t)__popc(m[q4]) & 1u;
+                for (int q4 = 0; q4 < 4; ++q4) {
+                    uint32_t x = m[q4];
+                    x ^= x << 1;
+                    x ^= x << 2;
+                    x ^= x << 4;
+                    x ^= x << 8;
+                    x ^= x << 16;
+                    const uint32_t even = m[q4] & (carry ? ~x : x);  // global rank even
+                    mine[q4] = sub == 0 ? even : (m[q4] & ~even);
+                    carry ^= (uint32_t)__popc(m[q4]) & 1u;
+                }
+            } else {
+                const int slots = (int)rep * kCSub, me = replica * kCSub + sub;
+                int rk = 0;
+#pragma unroll
+                for (int q4 = 0; q4 < 4; ++q4) {
+                    uint32_t w = m[q4], keep = 0u;
+                    while (w) {
+                        const uint32_t b = w & (0u - w);
+                        if (rk % slots == me) keep |= b;
+                        ++rk;
+                        w ^= b;
+                    }
+                    mine[q4] = keep;
+                }
             }
             // ---- exact fp64 rescoring, kCG candidates at a time (dot_f order: d = 0..127 from 0.0)
             constexpr int kCG = 4;
@@ -387,7 +412,7 @@ kv_cand_kernel(const CandArgs a, const __grid_constant__ CUtensorMap kmap) {
             run += total;
             mbar_arrive(smem_u32(&c.h_free[s]));
         }
-        if (sub == 0 && lim > t_begin) a.ccnt[rowcode * a.nch + chunk] = run;
+        if (sub == 0 && replica == 0 && lim > t_begin) a.ccnt[rowcode * a.nch + chunk] = run;
     }
     tc_fence_before();
     __syncthreads();
