@@ -1021,6 +1021,8 @@ tc_diag_kernel(const TcParams p, const __grid_constant__ CUtensorMap qtile,
             const __nv_bfloat16* vbase = reinterpret_cast<const __nv_bfloat16*>(a.v);
             for (int64_t it = blockIdx.x; it < total; it += gridDim.x) {
                 const TileInfo t = diag_tile(p, it);
+                // the q heads of a GQA group share the V rows: the group's first head checks for all
+                if ((t.zh % g.hq) % g.group != 0) continue;
                 const int64_t k0 = t.sb + (int64_t)(t.nd - 1) * kBN;  // first key of the diagonal block
                 const int64_t kn = min((int64_t)kBN, g.l - k0);
                 const uint4* vb = reinterpret_cast<const uint4*>(vbase + g.v_base(t.zh) + k0 * kD);
@@ -1033,8 +1035,9 @@ tc_diag_kernel(const TcParams p, const __grid_constant__ CUtensorMap qtile,
                 }
                 if (__any_sync(0xffffffffu, bad != 0u) && lane == 0) {
                     const int64_t T = a.T, full = (g.N - 1) * T, ti = t.t0 / kBM;
-                    const int64_t gt = t.zh * a.tiles_per_head + (t.n < g.N - 1 ? t.n * T + ti : full + ti);
-                    a.poison_list[atomicAdd(a.poison_cnt, 1)] = (int32_t)gt;
+                    const int64_t r = t.n < g.N - 1 ? t.n * T + ti : full + ti;
+                    const int pos = atomicAdd(a.poison_cnt, (int)g.group);
+                    for (int64_t u = 0; u < g.group; ++u) a.poison_list[pos + u] = (int32_t)((t.zh + u) * a.tiles_per_head + r);
                 }
             }
             return;
