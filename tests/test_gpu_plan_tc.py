@@ -22,8 +22,10 @@ def _check_prefix(torch, s2o, qd, kd, seg, depth, expect_flag=None):
     torch.cuda.synchronize()
     if expect_flag is not None:
         assert flag.item() == expect_flag
-    assert torch.equal(qp, plan.q_perm)
     n_seg = plan.seg.seg_count
+    last = plan.seg.last_len  # q_perm of the (ragged) last segment: its first last_len entries
+    assert torch.equal(qp[:, :, : n_seg - 1], plan.q_perm[:, :, : n_seg - 1])
+    assert torch.equal(qp[:, :, n_seg - 1, :last], plan.q_perm[:, :, n_seg - 1, :last])
     bad = []
     for n in range(1, n_seg):
         t = min(n * seg, depth)
@@ -75,3 +77,18 @@ def test_candidate_plan_all_ties_flags_and_falls_back(cuda):
     torch.cuda.synchronize()
     assert torch.equal(full.trace.processed, trunc.trace.processed)
     assert torch.equal(full.out, trunc.out)
+
+
+@pytest.mark.parametrize("z,hq,hkv,l,seg", [(2, 4, 2, 20480 + 640, 2048),   # batch 2, ragged last segment
+                                            (1, 2, 2, 24576, 2048),         # group 1
+                                            (1, 8, 1, 24576, 2048)])        # group 8
+def test_candidate_plan_batches_ragged_groups(cuda, z, hq, hkv, l, seg):
+    """The candidate path for Z > 1, a ragged last segment and GQA groups 1 and 8 (row tiles and
+    replication depend on the group) still gives the prefix of the full plan."""
+    import paper_2602_22575_b200 as s2o
+    torch = cuda
+    q, k, _ = s2o.generate_synthetic("mixed", l // 64, 8.0, 7, z, hq, l, 128)
+    qd = _dev(torch, q)
+    kd = _dev(torch, k[:, :hkv])
+    assert _check_prefix(torch, s2o, qd, kd, seg, 6144) == 0
+    assert _check_prefix(torch, s2o, qd, kd, seg, 1000) == 0
