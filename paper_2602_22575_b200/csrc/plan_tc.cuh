@@ -354,9 +354,6 @@ kv_cand_kernel(const CandArgs a, const __grid_constant__ CUtensorMap kmap) {
             }
             // ---- exact fp64 rescoring, kCG candidates at a time (dot_f order: d = 0..127 from 0.0)
             constexpr int kCG = 4;
-#ifdef S2O_CAND_NORESCORE  // timing aid: no exact rescoring
-            mine[0] = mine[1] = mine[2] = mine[3] = 0u;
-#endif
             while (__any_sync(0xffffffffu, (mine[0] | mine[1] | mine[2] | mine[3]) != 0u)) {
                 int jk[kCG];
 #pragma unroll
