@@ -883,7 +883,7 @@ tc_pass_kernel(const TcParams p, const __grid_constant__ CUtensorMap qmap,
 //               softmax warps go straight on to the next tile
 //   warp 12     MMA issuer (one elected lane)
 //   warp 13     Q + K loader (lane 0, 2-D TMA tiles), warp 14 V loader (lane 0), warp 15 reads
-//               each tile's diagonal V block for non-finite values (masked-key poison, exact rerun)
+//               (idle: the masked-key poison check is poison_scan_kernel)
 //
 // TMEM: S buffers at columns [0, 128), [128, 256), [256, 384) (P in bf16 over the first 64
 // columns of its buffer), O at [384, 512) (kDSBuf = 2: two S buffers, O double-buffered by
@@ -1010,38 +1010,7 @@ tc_diag_kernel(const TcParams p, const __grid_constant__ CUtensorMap qtile,
     // (setmaxnreg inside each role branch, so the softmax code is dominated by its increase)
     if (warp == kDKWarp || warp == kDVWarp || warp > kDVWarp) {
         setmaxnreg_dec<kDOtherRegs>();
-        if (warp > kDVWarp) {
-            // ============================== poison check ==============================
-            // Masked keys are skipped by the reference (attention.cpp:55-57) but the tensor core
-            // multiplies them: 0 * NaN / 0 * Inf in P V would poison earlier rows. Only a tile's
-            // last (diagonal) block has masked keys, so this warp reads that V block (from L2: the
-            // V loader has just fetched it) for non-finite bf16 values, off the pipeline; a hit
-            // lists the tile for the exact rerun that run_pass launches after this kernel.
-            if (!a.poison_cnt) return;
-            const __nv_bfloat16* vbase = reinterpret_cast<const __nv_bfloat16*>(a.v);
-            for (int64_t it = blockIdx.x; it < total; it += gridDim.x) {
-                const TileInfo t = diag_tile(p, it);
-                // the q heads of a GQA group share the V rows: the group's first head checks for all
-                if ((t.zh % g.hq) % g.group != 0) continue;
-                const int64_t k0 = t.sb + (int64_t)(t.nd - 1) * kBN;  // first key of the diagonal block
-                const int64_t kn = min((int64_t)kBN, g.l - k0);
-                const uint4* vb = reinterpret_cast<const uint4*>(vbase + g.v_base(t.zh) + k0 * kD);
-                uint32_t bad = 0u;
-#pragma unroll 4
-                for (int64_t i = lane; i < kn * (kD / 8); i += 32) {
-                    const uint4 w = vb[i];
-                    for (const uint32_t x : {w.x, w.y, w.z, w.w})
-                        bad |= (((x & 0x7f80u) == 0x7f80u) | ((x & 0x7f800000u) == 0x7f800000u)) ? 1u : 0u;
-                }
-                if (__any_sync(0xffffffffu, bad != 0u) && lane == 0) {
-                    const int64_t T = a.T, full = (g.N - 1) * T, ti = t.t0 / kBM;
-                    const int64_t r = t.n < g.N - 1 ? t.n * T + ti : full + ti;
-                    const int pos = atomicAdd(a.poison_cnt, (int)g.group);
-                    for (int64_t u = 0; u < g.group; ++u) a.poison_list[pos + u] = (int32_t)((t.zh + u) * a.tiles_per_head + r);
-                }
-            }
-            return;
-        }
+        if (warp > kDVWarp) return;  // (the masked-key poison check is poison_scan_kernel)
         // ============================== loaders (one lane each) ==============================
         if (lane != 0) return;
         const bool kl = warp == kDKWarp;
@@ -1366,6 +1335,693 @@ tc_diag_kernel(const TcParams p, const __grid_constant__ CUtensorMap qtile,
     }
 }
 
+// ============================================================== two-tile diagonal kernel
+// Pass-1 with TWO 128-row query tiles in flight per CTA (S2O_DIAG2=1 selects it; A/B against
+// tc_diag_kernel). The tiles of a work item read the same K/V rows: the two q heads 2i, 2i+1 of
+// a GQA group at the same (segment, tile) when the group is even, else two adjacent tiles of one
+// head (the longer first). Every K/V block is loaded once for both.
+//
+//   warps 0-3   softmax of tile 0 (thread = row = TMEM lane, all 128 key columns)
+//   warps 4-7   softmax of tile 1: the two warps an SMSP runs belong to different tiles, so one
+//               tile's S load / row max / P store overlaps the other's exponentials
+//   warps 8-11  epilogue (O of a finished tile -> state / output), warp 12 MMA issuer,
+//               warp 13 K loader, warp 14 V loader, warp 15 Q loader
+//
+// TMEM: S_x (P_x in bf16 over its first 64 columns) at [128x, 128x + 128), O_x at
+// [256 + 128x, ...). MMA order per block j: P V_0(j), S_0(j+1), P V_1(j), S_1(j+1); the tensor
+// pipe is in order, so S_x(j+1) overwrites P_x(j) only after P V_x(j) read it, and s_full_x(j+1)
+// (a commit after S_x(j+1)) also covers P V_x(j): a softmax that rescales O_x (lazy max) after
+// waiting for s_full_x needs no other barrier. Q has three 32 KB slots, so the next item's first
+// Q tile lands while this item runs.
+constexpr int kEThreads = 512;
+#ifdef S2O_D2_NOXITEM  // A/B: each item's first S issued at its start (not after the last P V)
+constexpr bool kNoXItem = true;
+#else
+constexpr bool kNoXItem = false;
+#endif
+#ifdef S2O_D2_NOMMA  // timing aid: barriers only, no tensor-core work
+constexpr bool kNoMma = true;
+#else
+constexpr bool kNoMma = false;
+#endif
+constexpr int kEEpiWarp0 = 8, kEMmaWarp = 12, kEKWarp = 13, kEVWarp = 14, kEQWarp = 15;
+#ifndef S2O_D2_MMAREGS
+#define S2O_D2_MMAREGS 64
+#endif
+constexpr int kESoftRegs = 184, kEEpiRegs = 80, kEMmaRegs = S2O_D2_MMAREGS, kELoadRegs = 64;
+static_assert(8 * (kESoftRegs - 128) <= 4 * (128 - kEEpiRegs) + (128 - kEMmaRegs) + 3 * (128 - kELoadRegs),
+              "register pool");
+#ifndef S2O_D2_QSLOTS
+#define S2O_D2_QSLOTS 3
+#endif
+#ifndef S2O_D2_KST
+#define S2O_D2_KST 2
+#endif
+#ifndef S2O_D2_VST
+#define S2O_D2_VST 2
+#endif
+constexpr int kEQSlots = S2O_D2_QSLOTS, kEKStages = S2O_D2_KST, kEVStages = S2O_D2_VST;
+constexpr uint32_t kEOffQ = 0;
+constexpr uint32_t kEOffK = kEQSlots * kTileBytes;
+constexpr uint32_t kEOffV = kEOffK + kEKStages * kTileBytes;
+constexpr uint32_t kEOffCtrl = kEOffV + kEVStages * kTileBytes;
+constexpr uint32_t kEOffML = kEOffCtrl + 256;               // float [2 tiles][m, ell][128 rows]
+constexpr uint32_t kESmemBytes = kEOffML + 2 * 2 * 128 * 4;  // 226.25 KB
+static_assert(kESmemBytes <= 232448, "shared memory");
+
+struct CtrlE {
+    uint64_t q_full[kEQSlots], q_empty[kEQSlots];
+    uint64_t k_full[kEKStages], k_empty[kEKStages], v_full[kEVStages], v_empty[kEVStages];
+    uint64_t s_full[2], p_full[2], o_done[2], o_free[2], ml_full[2], ml_free[2];  // per tile slot
+    uint32_t tmem_base;
+};
+static_assert(sizeof(CtrlE) <= 256, "CtrlE exceeds its 256 B");
+
+// Work items of the two-tile kernel (launcher: pairs_per_head = tiles per head).
+__device__ __forceinline__ int64_t diag2_items(const TcParams& p) {
+    const Geo& g = p.a.g;
+    if (g.group % 2 == 0) return g.z * g.hq / 2 * p.pairs_per_head;
+    const int64_t T = p.a.T, t_last = (g.last_len + kBM - 1) / kBM;
+    return g.z * g.hq * ((g.N - 1) * ((T + 1) / 2) + (t_last + 1) / 2);
+}
+
+// Tile x (0, 1) of work item idx; nd = 0 when the item has no second tile. Items are ordered
+// as diag_tile's (GQA group interleaved innermost, longest tiles first within a head).
+// Work-item cursor of the two-tile kernel. Every role walks items blockIdx.x, +gridDim.x, ...;
+// the index is kept in mixed radix (a: head pair / head in the group, (n, u): segment and tile
+// (pair) in longest-first order, zg: kv head) and advanced by carries, because integer division
+// needs MUFU.RCP, which the softmax warps keep saturated (a division-based decode at every item
+// boundary cost the MMA issuer ~2 k clk). Items are ordered as diag_tile's (GQA group innermost).
+struct D2Cur {
+    uint32_t a, n, u, zg;      // position
+    uint32_t sa, sn, su, sz;   // the stride gridDim.x in the same radix
+};
+struct D2Rad {
+    uint32_t A, U, Ul, N, T, tl, G;
+    __device__ __forceinline__ explicit D2Rad(const TcParams& p) {
+        const Geo& g = p.a.g;
+        G = (uint32_t)g.group;
+        T = (uint32_t)p.a.T;
+        N = (uint32_t)g.N;
+        tl = (uint32_t)((g.last_len + kBM - 1) / kBM);
+        const bool hp = G % 2 == 0;  // q heads 2i, 2i+1 of the group (else adjacent tiles of one head)
+        A = hp ? G / 2 : G;
+        U = hp ? T : (T + 1) / 2;
+        Ul = hp ? tl : (tl + 1) / 2;
+    }
+};
+
+__device__ __forceinline__ void d2_decode(const D2Rad& R, uint32_t v, uint32_t& a, uint32_t& n, uint32_t& u, uint32_t& zg) {
+    const uint32_t per = (R.N - 1) * R.U + R.Ul;  // units per kv head (or q head)
+    a = v % R.A;
+    const uint32_t q = v / R.A;
+    const uint32_t r = q % per;
+    zg = q / per;
+    n = r / R.U;
+    u = r % R.U;
+}
+
+__device__ __forceinline__ D2Cur d2_init(const D2Rad& R) {
+    D2Cur c;
+    d2_decode(R, blockIdx.x, c.a, c.n, c.u, c.zg);
+    d2_decode(R, gridDim.x, c.sa, c.sn, c.su, c.sz);
+    return c;
+}
+
+__device__ __forceinline__ void d2_next(const D2Rad& R, D2Cur& c) {
+    c.a += c.sa;
+    const uint32_t c1 = c.a >= R.A ? 1u : 0u;
+    c.a -= c1 * R.A;
+    c.u += c.su + c1;
+    if (c.u >= R.U) {
+        c.u -= R.U;
+        ++c.n;
+    }
+    c.n += c.sn;
+    if (c.n > R.N - 1 || (c.n == R.N - 1 && c.u >= R.Ul)) {  // past this kv head: subtract its units
+        if (c.u >= R.Ul) c.u -= R.Ul;
+        else {
+            c.u += R.U - R.Ul;
+            --c.n;
+        }
+        c.n -= R.N - 1;
+        ++c.zg;
+    }
+    c.zg += c.sz;
+}
+
+// Tile x (0, 1) of the cursor's item; nd = 0 when the item has no second tile.
+__device__ __forceinline__ TileInfo d2_tile(const TcParams& p, const D2Rad& R, const D2Cur& c, int x) {
+    const Geo& g = p.a.g;
+    const bool last = c.n == R.N - 1;
+    int32_t ti;
+    TileInfo t;
+    if (R.G % 2 == 0) {
+        t.zh = (int64_t)c.zg * R.G + 2 * c.a + x;
+        ti = (int32_t)((last ? R.tl : R.T) - 1 - c.u);
+    } else {
+        t.zh = (int64_t)c.zg * R.G + c.a;
+        ti = (int32_t)((last ? R.tl : R.T) - 1 - 2 * c.u) - x;
+    }
+    t.n = c.n;
+    t.sb = (int64_t)c.n * g.S;
+    t.segr = (int)g.seg_rows(c.n);
+    if (ti < 0) {
+        t.t0 = 0;
+        t.tn = 0;
+        t.nd = 0;
+        return t;
+    }
+    t.t0 = (int64_t)ti * kBM;
+    t.tn = min(kBM, t.segr - ti * kBM);
+    t.nd = (ti * kBM + t.tn - 1) / kBN + 1;
+    return t;
+}
+
+#ifndef S2O_D2_POLY0
+#define S2O_D2_POLY0 S2O_DIAG_POLY
+#endif
+#ifndef S2O_D2_POLY1
+#define S2O_D2_POLY1 S2O_DIAG_POLY
+#endif
+// P = exp2(s * scale - m) for a full row of 128 scores into the first 64 columns of S (bf16
+// pairs), with every P-th pair on the FMA-pipe polynomial (P = 0: all MUFU). Per tile slot, so
+// the two slots' softmax warps, which share an SMSP, can lean on different pipes.
+template <int P>
+__device__ __forceinline__ void d2_exps(const uint32_t (&sv)[128], float sc, float neg_ref, uint32_t tS, float (&rs)[4]) {
+#pragma unroll
+    for (int c0 = 0; c0 < 128; c0 += 32) {
+        uint32_t pk[16];
+#pragma unroll
+        for (int i = 0; i < 32; i += 2) {
+            float e0, e1;
+            if (P > 0 && (i >> 1) % (P > 0 ? P : 1) == P - 1) {
+                const float2 e = ex2_poly4x2(make_float2(fmaf(__uint_as_float(sv[c0 + i]), sc, neg_ref),
+                                                         fmaf(__uint_as_float(sv[c0 + i + 1]), sc, neg_ref)));
+                e0 = e.x;
+                e1 = e.y;
+            } else {
+#ifdef S2O_D2_NOEXP  // timing aid: exponentials replaced by a multiply
+                e0 = fmaf(__uint_as_float(sv[c0 + i]), sc, neg_ref) * 0.001f;
+                e1 = fmaf(__uint_as_float(sv[c0 + i + 1]), sc, neg_ref) * 0.001f;
+#else
+                e0 = ex2(fmaf(__uint_as_float(sv[c0 + i]), sc, neg_ref));
+                e1 = ex2(fmaf(__uint_as_float(sv[c0 + i + 1]), sc, neg_ref));
+#endif
+            }
+            rs[(i >> 1) & 3] += e0 + e1;
+            pk[i >> 1] = pack_bf16(e0, e1);
+        }
+        tmem_st16(tS + c0 / 2, pk);
+    }
+}
+
+__global__ void __launch_bounds__(kEThreads, 1)
+tc_diag2_kernel(const TcParams p, const __grid_constant__ CUtensorMap qtile,
+                const __grid_constant__ CUtensorMap ktile, const __grid_constant__ CUtensorMap vtile) {
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    unsigned char* smem = smem_raw;
+    if ((smem_u32(smem) & 1023u) != 0) __trap();
+    CtrlE& c = *reinterpret_cast<CtrlE*>(smem + kEOffCtrl);
+    const PassArgs& a = p.a;
+    const Geo& g = a.g;
+    const int warp = threadIdx.x / 32;
+    const int lane = threadIdx.x % 32;
+    const uint32_t sQ = smem_u32(smem + kEOffQ);
+    const uint32_t sK = smem_u32(smem + kEOffK);
+    const uint32_t sV = smem_u32(smem + kEOffV);
+    if (threadIdx.x == 0) {
+        for (int b = 0; b < kEQSlots; ++b) {
+            mbar_init(smem_u32(&c.q_full[b]), 1);
+            mbar_init(smem_u32(&c.q_empty[b]), 1);
+        }
+        for (int s = 0; s < kEKStages; ++s) {
+            mbar_init(smem_u32(&c.k_full[s]), 1);
+            mbar_init(smem_u32(&c.k_empty[s]), 1);
+        }
+        for (int s = 0; s < kEVStages; ++s) {
+            mbar_init(smem_u32(&c.v_full[s]), 1);
+            mbar_init(smem_u32(&c.v_empty[s]), 1);
+        }
+        for (int x = 0; x < 2; ++x) {
+            mbar_init(smem_u32(&c.s_full[x]), 1);
+            mbar_init(smem_u32(&c.p_full[x]), 4);    // the tile's softmax warps
+            mbar_init(smem_u32(&c.o_done[x]), 1);
+            mbar_init(smem_u32(&c.o_free[x]), 4);    // epilogue warps
+            mbar_init(smem_u32(&c.ml_full[x]), 128);  // per-thread: each releases its own write
+            mbar_init(smem_u32(&c.ml_free[x]), 128);
+        }
+        fence_mbar_init();
+    }
+    if (warp == 0) {
+        tmem_alloc(smem_u32(&c.tmem_base), kTmemCols);
+        tmem_relinquish();
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tbase = c.tmem_base;
+    const int64_t total = diag2_items(p);
+    const D2Rad R(p);
+    const int64_t rowu = g.d;
+    float* ml = reinterpret_cast<float*>(smem + kEOffML);
+    if (warp >= kEKWarp) {
+        // ============================== loaders (one lane each) ==============================
+        // warp 13: K blocks, warp 14: V blocks, warp 15: Q tiles (its own lane, so a Q slot that
+        // frees late never holds back the next item's first K block)
+        setmaxnreg_dec<kELoadRegs>();
+        if (lane != 0) return;
+        if (warp == kEQWarp) {
+            uint32_t qs = 0;
+            D2Cur cu = d2_init(R);
+            for (int64_t it = blockIdx.x; it < total; it += gridDim.x, d2_next(R, cu))
+                for (int x = 0; x < 2; ++x) {
+                    const TileInfo t = d2_tile(p, R, cu, x);
+                    if (t.nd == 0) continue;
+                    const uint32_t sl = qs % kEQSlots;
+                    mbar_wait(smem_u32(&c.q_empty[sl]), ((qs / kEQSlots) & 1) ^ 1, 4011);
+                    tl_mark(p, 24, qs);
+                    mbar_expect_tx(smem_u32(&c.q_full[sl]), kTileBytes);
+                    const int64_t qb = g.q_base(t.zh) / rowu;
+                    for (int h = 0; h < 2; ++h)
+                        tma_load2d(sQ + sl * kTileBytes + h * kHalf, &qtile, h * 64, (int32_t)(qb + t.sb + t.t0),
+                                   smem_u32(&c.q_full[sl]));
+                    ++qs;
+                    if (x == 0 && it + gridDim.x < total) {  // the next item's Q tiles into L2 (read from HBM once)
+                        D2Cur cn = cu;
+                        d2_next(R, cn);
+                        for (int y = 0; y < 2; ++y) {
+                            const TileInfo u = d2_tile(p, R, cn, y);
+                            if (u.nd == 0) continue;
+                            const int64_t ub = g.q_base(u.zh) / rowu;
+                            for (int h = 0; h < 2; ++h) tma_prefetch2d(&qtile, h * 64, (int32_t)(ub + u.sb + u.t0));
+                        }
+                    }
+                }
+            return;
+        }
+        const bool kl = warp == kEKWarp;
+        const CUtensorMap* xtile = kl ? &ktile : &vtile;
+        const uint32_t xbase = kl ? sK : sV;
+        const int nst = kl ? kEKStages : kEVStages;
+        uint64_t* xfull = kl ? c.k_full : c.v_full;
+        uint64_t* xempty = kl ? c.k_empty : c.v_empty;
+        uint32_t gi = 0;
+        D2Cur cu = d2_init(R);
+        for (int64_t it = blockIdx.x; it < total; it += gridDim.x, d2_next(R, cu)) {
+            const TileInfo t0 = d2_tile(p, R, cu, 0);
+            const int64_t xb = (kl ? g.k_base(t0.zh) : g.v_base(t0.zh)) / rowu;
+            for (int j = 0; j < t0.nd; ++j, ++gi) {  // tile 0 has the most blocks
+                const int st = gi % nst;
+                mbar_wait(smem_u32(&xempty[st]), ((gi / nst) & 1) ^ 1, kl ? 4012 : 4013);
+                tl_mark(p, kl ? 22 : 23, gi);
+#ifdef S2O_D2_NOLOAD  // timing aid: no K / V data movement
+                mbar_expect_tx(smem_u32(&xfull[st]), 0);
+                continue;
+#endif
+                mbar_expect_tx(smem_u32(&xfull[st]), kTileBytes);
+                const uint32_t dst = xbase + st * kTileBytes;
+                for (int h = 0; h < 2; ++h)
+                    tma_load2d(dst + h * kHalf, xtile, h * 64, (int32_t)(xb + t0.sb + (int64_t)j * kBN),
+                               smem_u32(&xfull[st]));
+            }
+        }
+        return;
+    }
+    if (warp == kEMmaWarp) {
+        // ============================== MMA issuer ==============================
+        // Per tile slot the S / P V stream runs on across work items: the first S of the next
+        // item's tile x is issued right after this item's last P V of slot x (and before the
+        // other slot's), so the tensor pipe has work while the epilogue drains O.
+        setmaxnreg_dec<kEMmaRegs>();
+        const bool leader = elect_one();
+        const uint32_t idesc_s = umma_idesc_bf16(kBM, kBN, false, false);
+        const uint32_t idesc_o = umma_idesc_bf16(kBM, kD, false, true);
+        const uint64_t dq0 = umma_desc_sw128(sQ, 16, 1024);
+        const uint64_t dk0 = umma_desc_sw128(sK, 16, 1024);
+        const uint64_t dv0 = umma_desc_sw128(sV, kHalf, 1024);
+        uint32_t kc = 0, vc = 0, qs = 0;
+        uint32_t bx[2] = {0u, 0u}, tx[2] = {0u, 0u};  // per tile slot: blocks, tiles so far
+        auto issue_s = [&](int x, uint32_t qsl, uint32_t kst) {
+            const uint64_t dq = dq0 + ((qsl * kTileBytes) >> 4);
+            const uint64_t dk = dk0 + ((kst * kTileBytes) >> 4);
+#pragma unroll
+            for (int kk = 0; kk < kD / 16; ++kk) {
+                const uint32_t off = ((kk / 4) * kHalf + (kk % 4) * 32) >> 4;
+                if (leader && !kNoMma) umma_bf16(tbase + x * 128, dq + off, dk + off, idesc_s, kk > 0);
+            }
+            if (leader) umma_commit(smem_u32(&c.s_full[x]));
+        };
+        // S_x(0) of an item's tile (Q slot assigned in load order); K(0) already waited for
+        auto first_s = [&](int x, int nd, uint32_t kst) -> uint32_t {
+            const uint32_t sl = qs % kEQSlots;
+            mbar_wait(smem_u32(&c.q_full[sl]), (qs / kEQSlots) & 1, 4112);
+            tl_mark(p, 25, qs);
+            ++qs;
+            tc_fence_after();
+            issue_s(x, sl, kst);
+            if (nd == 1 && leader) umma_commit(smem_u32(&c.q_empty[sl]));
+            return sl;
+        };
+        int64_t it = blockIdx.x;
+        int nd[2] = {0, 0};
+        uint32_t qsl[2] = {0u, 0u};
+        D2Cur cn = d2_init(R);  // the item after the current one (advanced at each item's start)
+        if (it < total) {
+            nd[0] = d2_tile(p, R, cn, 0).nd;
+            nd[1] = d2_tile(p, R, cn, 1).nd;
+        }
+        for (bool first = true; it < total; it += gridDim.x, first = false) {
+            if (first || kNoXItem) {
+                const uint32_t kst = kc % kEKStages;
+                mbar_wait(smem_u32(&c.k_full[kst]), (kc / kEKStages) & 1, 4111);
+                for (int x = 0; x < 2; ++x)
+                    if (nd[x]) qsl[x] = first_s(x, nd[x], kst);
+                if (leader) umma_commit(smem_u32(&c.k_empty[kst]));
+                ++kc;
+                __syncwarp();
+            }
+            const int64_t nit = it + gridDim.x;
+            // the next item's shape, decoded inside the first block (off the item boundary: the
+            // softmax warps sharing this SMSP leave the issuer few issue slots)
+            int nn[2] = {0, 0};
+            auto look = [&]() {
+                d2_next(R, cn);
+                if (nit < total) {
+                    nn[0] = d2_tile(p, R, cn, 0).nd;
+                    nn[1] = d2_tile(p, R, cn, 1).nd;
+                }
+            };
+            if (nd[0] == 1) look();
+            uint32_t nsl[2] = {0u, 0u};
+            tl_mark(p, 28, vc);
+            for (int j = 0; j < nd[0]; ++j) {
+                const uint32_t vst = vc % kEVStages;
+                const bool last = j + 1 == nd[0];
+                const bool knext = !last || (nn[0] > 0 && !kNoXItem);  // a K block follows (this item's or the next's)
+                const uint32_t kst = kc % kEKStages;
+                bool kwait = false;
+                tl_mark(p, 1, vc);
+                mbar_wait(smem_u32(&c.v_full[vst]), (vc / kEVStages) & 1, 4113);
+                const uint64_t dv = dv0 + ((vst * kTileBytes) >> 4);
+                for (int x = 0; x < 2; ++x) {
+                    if (j < nd[x]) {
+#ifndef S2O_D2_NOPWAIT
+                        mbar_wait(smem_u32(&c.p_full[x]), bx[x] & 1, 4114);
+#endif
+                        tl_mark(p, 2 + 3 * x, vc);
+                        ++bx[x];
+                        // the epilogue has read O_x of this slot's previous tile
+#ifndef S2O_D2_NOOWAIT
+                        if (j == 0) mbar_wait(smem_u32(&c.o_free[x]), (tx[x] & 1) ^ 1, 4115);
+#endif
+                        tc_fence_after();
+#pragma unroll
+                        for (int kk = 0; kk < kBN / 16; ++kk)
+                            if (leader && !kNoMma)
+                                umma_bf16_ts(tbase + (2 + x) * 128, tbase + x * 128 + kk * 8,
+                                             dv + ((kk * 16 * 128) >> 4), idesc_o, (kk > 0 || j > 0) ? 1 : 0);
+                        tl_mark(p, 4 + 3 * x, vc);
+                        if (j == nd[x] - 1) {
+                            if (leader) umma_commit(smem_u32(&c.o_done[x]));
+                            ++tx[x];
+                        }
+                    }
+                    if (j + 1 < nd[x]) {  // S_x(j+1)
+                        if (!kwait) {
+                            mbar_wait(smem_u32(&c.k_full[kst]), (kc / kEKStages) & 1, 4116);
+                            tc_fence_after();
+                            kwait = true;
+                        }
+                        issue_s(x, qsl[x], kst);
+                        tl_mark(p, 8 + x, vc);
+                        if (j + 2 == nd[x] && leader) umma_commit(smem_u32(&c.q_empty[qsl[x]]));
+                    } else if (last && nn[x] > 0 && !kNoXItem) {  // S_x(0) of the next item
+                        if (!kwait) {
+                            mbar_wait(smem_u32(&c.k_full[kst]), (kc / kEKStages) & 1, 4117);
+                            kwait = true;
+                        }
+                        nsl[x] = first_s(x, nn[x], kst);
+                        tl_mark(p, 26 + x, vc);
+                    }
+                    __syncwarp();
+                }
+                if (j == 0 && nd[0] > 1) look();
+                if (leader) umma_commit(smem_u32(&c.v_empty[vst]));
+                ++vc;
+                if (knext) {
+                    if (leader) umma_commit(smem_u32(&c.k_empty[kst]));
+                    ++kc;
+                }
+                __syncwarp();
+            }
+            tl_mark(p, 29, vc);
+            nd[0] = nn[0];
+            nd[1] = nn[1];
+            qsl[0] = nsl[0];
+            qsl[1] = nsl[1];
+        }
+        __syncwarp();
+    } else if (warp < kEEpiWarp0) {
+        // ============================== softmax ==============================
+        setmaxnreg_inc<kESoftRegs>();
+        const int x = warp >> 2, qd = warp & 3;
+        const int r = qd * 32 + lane;  // TMEM lane = row
+        const uint32_t lane_off = (uint32_t)(qd * 32) << 16;
+        const uint32_t tS = tbase + lane_off + x * 128;
+        const uint32_t tO = tbase + lane_off + (2 + x) * 128;
+        const float sc = p.scale_log2;
+        uint32_t bx = 0, tx = 0;
+        D2Cur cu = d2_init(R);
+        for (int64_t it = blockIdx.x; it < total; it += gridDim.x, d2_next(R, cu)) {
+            const TileInfo t = d2_tile(p, R, cu, x);
+            if (t.nd == 0) continue;
+            const bool valid = r < t.tn;
+            const int rr = valid ? r : 0;
+            const int t0x = (int)t.t0;
+            float m2 = -INFINITY, ell = 0.0f;
+            for (int j = 0; j < t.nd; ++j, ++bx) {
+                mbar_wait(smem_u32(&c.s_full[x]), bx & 1, 4211);
+                if (r == 0) tl_mark(p, 10 + 4 * x, bx);
+                tc_fence_after();
+#ifdef S2O_D2_NOSOFT  // timing aid: the MMA / load pipeline alone
+                __syncwarp();
+                if (lane == 0) mbar_arrive(smem_u32(&c.p_full[x]));
+                m2 = 0.0f;
+                ell = 1.0f;
+                continue;
+#endif
+                uint32_t sv[128];
+#pragma unroll
+                for (int c0 = 0; c0 < 128; c0 += 32) tmem_ld32(tS + c0, *reinterpret_cast<uint32_t(*)[32]>(&sv[c0]));
+                tmem_ld_wait();
+                if (r == 0) tl_mark(p, 11 + 4 * x, bx);
+                // visible keys of this row in block j (causal on segment positions, kernel.cpp:58-69)
+                const int k0 = j * kBN;
+                const int kn = min(kBN, t.segr - k0);
+                const int vis = (k0 + kn - 1 <= t0x) ? kn : min(kn, t0x + rr - k0 + 1);
+                const int lim = max(0, vis);
+                const bool full = __all_sync(0xffffffffu, lim >= 128);
+                float mxa[8];
+#pragma unroll
+                for (int i = 0; i < 8; ++i) mxa[i] = -INFINITY;
+                if (full) {
+#pragma unroll
+                    for (int i = 0; i < 128; i += 2)
+                        mxa[(i >> 1) & 7] = fmax3(mxa[(i >> 1) & 7], __uint_as_float(sv[i]), __uint_as_float(sv[i + 1]));
+                } else {
+#pragma unroll
+                    for (int i = 0; i < 128; i += 2)
+                        mxa[(i >> 1) & 7] = fmax3(mxa[(i >> 1) & 7], i < lim ? __uint_as_float(sv[i]) : -INFINITY,
+                                                  i + 1 < lim ? __uint_as_float(sv[i + 1]) : -INFINITY);
+                }
+                const float mx =
+                    fmax3(fmax3(mxa[0], mxa[1], mxa[2]), fmax3(mxa[3], mxa[4], mxa[5]), fmaxf(mxa[6], mxa[7])) * sc;
+                const float m_new = fmaxf(m2, mx);
+                const bool rescale = (m_new > m2 + kRescaleThresh) || (m2 == -INFINITY);
+                const float m_use = rescale ? m_new : m2;
+                const float neg_ref = (m_use == -INFINITY) ? 0.0f : -m_use;
+                const float alpha = (m2 == -INFINITY) ? 0.0f : ex2(m2 + neg_ref);
+                float rs[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+                if (full) {
+                    if (x == 0) d2_exps<S2O_D2_POLY0>(sv, sc, neg_ref, tS, rs);
+                    else d2_exps<S2O_D2_POLY1>(sv, sc, neg_ref, tS, rs);
+                } else {
+#pragma unroll
+                    for (int c0 = 0; c0 < 128; c0 += 32) {
+                        uint32_t pk[16];
+#pragma unroll
+                        for (int i = 0; i < 32; i += 2) {
+                            const float e0 = c0 + i < lim ? ex2(fmaf(__uint_as_float(sv[c0 + i]), sc, neg_ref)) : 0.0f;
+                            const float e1 =
+                                c0 + i + 1 < lim ? ex2(fmaf(__uint_as_float(sv[c0 + i + 1]), sc, neg_ref)) : 0.0f;
+                            rs[(i >> 1) & 3] += e0 + e1;
+                            pk[i >> 1] = pack_bf16(e0, e1);
+                        }
+                        tmem_st16(tS + c0 / 2, pk);
+                    }
+                }
+                if (r == 0) tl_mark(p, 12 + 4 * x, bx);
+                // O rescale (lazy, rare; after the exponentials, when S is no longer live): s_full_x(j)
+                // was committed after P V_x(j-1)
+                if (__any_sync(0xffffffffu, j > 0 && rescale && m2 != -INFINITY)) {
+#pragma unroll
+                    for (int c0 = 0; c0 < 128; c0 += 32) {
+                        uint32_t v[32];
+                        tmem_ld32(tO + c0, v);
+                        tmem_ld_wait();
+#pragma unroll
+                        for (int i = 0; i < 32; ++i) v[i] = __float_as_uint(__uint_as_float(v[i]) * alpha);
+                        tmem_st32(tO + c0, v);
+                    }
+                }
+                tmem_st_wait();
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(smem_u32(&c.p_full[x]));
+                if (r == 0) tl_mark(p, 13 + 4 * x, bx);
+                ell = ell * alpha + ((rs[0] + rs[1]) + (rs[2] + rs[3]));
+                m2 = m_use;
+            }
+            // (m, ell) to the epilogue; the slot's previous tile has been read
+            mbar_wait(smem_u32(&c.ml_free[x]), (tx & 1) ^ 1, 4212);
+            ml[x * 256 + r] = m2;
+            ml[x * 256 + 128 + r] = ell;
+            mbar_arrive(smem_u32(&c.ml_full[x]));
+            ++tx;
+        }
+    } else if (warp < kEEpiWarp0 + 4) {
+        // ============================== epilogue ==============================
+        setmaxnreg_dec<kEEpiRegs>();
+        const int r = (warp - kEEpiWarp0) * 32 + lane;  // TMEM lane quarter = warp % 4
+        const uint32_t lane_off = (uint32_t)((warp % 4) * 32) << 16;
+        uint32_t tx[2] = {0u, 0u};
+        D2Cur cu = d2_init(R);
+        for (int64_t it = blockIdx.x; it < total; it += gridDim.x, d2_next(R, cu)) {
+            for (int x = 0; x < 2; ++x) {
+                const TileInfo t = d2_tile(p, R, cu, x);
+                if (t.nd == 0) continue;
+                const bool valid = r < t.tn;
+                const int rr = valid ? r : 0;
+                mbar_wait(smem_u32(&c.ml_full[x]), tx[x] & 1, 4213);
+                const float m2 = ml[x * 256 + r], ell = ml[x * 256 + 128 + r];
+                mbar_arrive(smem_u32(&c.ml_free[x]));
+                mbar_wait(smem_u32(&c.o_done[x]), tx[x] & 1, 4214);
+                if (r == 0) tl_mark(p, 18 + 2 * x, tx[x]);
+                ++tx[x];
+                tc_fence_after();
+                const int64_t grow = t.sb + t.t0 + rr;
+                const int64_t slot = t.zh * g.l + grow;
+                const float inv = 1.0f / ell;
+                const int64_t ooff = g.o_base(t.zh) + grow * g.os[2];
+#pragma unroll
+                for (int c0 = 0; c0 < kD; c0 += 32) {
+                    uint32_t ov[32];
+                    tmem_ld32(tbase + lane_off + (2 + x) * 128 + c0, ov);
+                    tmem_ld_wait();
+                    if (c0 == kD - 32) {  // O_x fully read: the slot's next tile may accumulate
+                        tc_fence_before();
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive(smem_u32(&c.o_free[x]));
+                        if (r == 0) tl_mark(p, 19 + 2 * x, tx[x] - 1);
+                    }
+                    if (!valid) continue;
+#ifdef S2O_D2_NOSTORE
+                    if (ov[0] == 0x7fc00001u) a.acc_out[slot * kD + c0] = 1.0f;
+                    continue;
+#endif
+                    if (a.mode & kStateOut) {
+                        if (p.vec_acc) {
+                            float* dst = a.acc_out + slot * kD + c0;
+#pragma unroll
+                            for (int i = 0; i < 32; i += 8) stg256(dst + i, &ov[i]);
+                        } else {
+                            float4* dst = reinterpret_cast<float4*>(a.acc_out + slot * kD + c0);
+#pragma unroll
+                            for (int i = 0; i < 8; ++i)
+                                dst[i] = make_float4(__uint_as_float(ov[4 * i]), __uint_as_float(ov[4 * i + 1]),
+                                                     __uint_as_float(ov[4 * i + 2]), __uint_as_float(ov[4 * i + 3]));
+                        }
+                    }
+                    if (a.mode & kFinal) {
+                        if (g.out_bf16) {
+                            uint32_t w[16];
+#pragma unroll
+                            for (int e = 0; e < 16; ++e)
+                                w[e] = pack_bf16(__uint_as_float(ov[2 * e]) * inv, __uint_as_float(ov[2 * e + 1]) * inv);
+                            __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(a.o) + ooff + c0;
+                            if (p.vec_o) {
+                                stg256(dst, w);
+                                stg256(dst + 16, w + 8);
+                            } else {
+                                uint4* d4 = reinterpret_cast<uint4*>(dst);
+#pragma unroll
+                                for (int i = 0; i < 4; ++i) d4[i] = make_uint4(w[4 * i], w[4 * i + 1], w[4 * i + 2], w[4 * i + 3]);
+                            }
+                        } else {
+                            float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(a.o) + ooff + c0);
+#pragma unroll
+                            for (int i = 0; i < 8; ++i)
+                                dst[i] = make_float4(__uint_as_float(ov[4 * i]) * inv, __uint_as_float(ov[4 * i + 1]) * inv,
+                                                     __uint_as_float(ov[4 * i + 2]) * inv, __uint_as_float(ov[4 * i + 3]) * inv);
+                        }
+                    }
+                }
+                if (valid && (a.mode & kStateOut)) {
+                    a.m_out[slot] = (m2 == -INFINITY) ? -INFINITY : m2 * 0.6931471805599453f;
+                    a.ell_out[slot] = ell;
+                }
+                if (valid && (a.mode & kFinal) && ell == 0.0f) atomicExch(a.err_flag, 2);
+            }
+        }
+    }
+    tc_fence_before();
+    if (warp <= kEMmaWarp) named_bar_sync(5, 32 * (kEMmaWarp + 1));  // softmax, epilogue, MMA warps
+    if (warp == 0) {
+        tc_fence_after();
+        tmem_dealloc(tbase, kTmemCols);
+    }
+}
+
+// ============================================================== masked-key poison scan
+// Masked keys are skipped by the reference (attention.cpp:55-57), but the tensor core multiplies
+// them: 0 * NaN / 0 * Inf in P V would poison earlier rows of a diagonal tile. Only a tile's last
+// (diagonal) block has masked keys, and on the diagonal passes V block b of a segment is the
+// diagonal block of tile b. This kernel reads every V block once (one warp each; HBM-bound,
+// ~40 us at C3) and lists, for a block holding a non-finite bf16 value, the tiles of all q heads
+// of its group; run_pass recomputes the listed tiles on the exact path after the pass.
+__global__ void __launch_bounds__(256) poison_scan_kernel(const PassArgs a) {
+    const Geo& g = a.g;
+    const int64_t per = a.tiles_per_head, hkv = g.hq / g.group;
+    const int64_t total = g.z * hkv * per;
+    const int lane = threadIdx.x % 32;
+    const __nv_bfloat16* vbase = reinterpret_cast<const __nv_bfloat16*>(a.v);
+    for (int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / 32; w < total;
+         w += (int64_t)gridDim.x * blockDim.x / 32) {
+        const int64_t zk = w / per, r = w % per;
+        const int64_t zh0 = (zk / hkv) * g.hq + (zk % hkv) * g.group;  // first q head of the group
+        const int64_t full = (g.N - 1) * a.T;
+        const int64_t n = r < full ? r / a.T : g.N - 1;
+        const int64_t ti = r < full ? r % a.T : r - full;
+        const int64_t k0 = n * g.S + ti * kBN;
+        const int64_t kn = min((int64_t)kBN, g.seg_rows(n) - ti * kBN);
+        const uint4* vb = reinterpret_cast<const uint4*>(vbase + g.v_base(zh0) + k0 * g.vs[2]);
+        uint32_t bad = 0u;
+        const int64_t row4 = g.vs[2] / 8;  // row stride in uint4 (strides_ok: a multiple of 128)
+#pragma unroll 4
+        for (int64_t i = lane; i < kn * (kD / 8); i += 32) {
+            const uint4 x = vb[(i / (kD / 8)) * row4 + i % (kD / 8)];
+            for (const uint32_t v : {x.x, x.y, x.z, x.w})
+                bad |= (((v & 0x7f80u) == 0x7f80u) | ((v & 0x7f800000u) == 0x7f800000u)) ? 1u : 0u;
+        }
+        if (__any_sync(0xffffffffu, bad != 0u) && lane == 0) {
+            const int pos = atomicAdd(a.poison_cnt, (int)g.group);
+            for (int64_t u = 0; u < g.group; ++u) a.poison_list[pos + u] = (int32_t)((zh0 + u) * per + r);
+        }
+    }
+}
+
+
 // ---------------------------------------------------------------- host side
 PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
     static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -1448,6 +2104,17 @@ bool tc_supported(const PassArgs& a) {
     return get_encode() != nullptr;
 }
 
+cudaError_t launch_poison_scan(const PassArgs& a, cudaStream_t st) {
+    const int64_t warps = a.g.z * (a.g.hq / a.g.group) * a.tiles_per_head;
+    if (warps == 0) return cudaSuccess;
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((warps + 7) / 8, (int64_t)sms * 8));
+    poison_scan_kernel<<<grid, 256, 0, st>>>(a);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_tc_pass(const PassArgs& a, cudaStream_t st) {
     const Geo& g = a.g;
     CUtensorMap qmap, kmap, vmap, qtile, ktile, vtile;
@@ -1480,6 +2147,21 @@ cudaError_t launch_tc_pass(const PassArgs& a, cudaStream_t st) {
     if (tc_diag_used(a)) {
         TcParams pd = p;
         pd.pairs_per_head = (g.N - 1) * a.T + t_last;  // tiles per head (diag_tile)
+        static const bool two_tile = [] {
+            const char* e = std::getenv("S2O_DIAG2");
+            return e && std::strcmp(e, "1") == 0;
+        }();
+        if (two_tile) {  // tc_diag2_kernel: two tiles sharing K/V per work item
+            if (cudaError_t e = smem_attr((const void*)tc_diag2_kernel, kESmemBytes)) return e;
+            const int64_t work = g.group % 2 == 0
+                                     ? g.z * g.hq / 2 * pd.pairs_per_head
+                                     : g.z * g.hq * ((g.N - 1) * ((a.T + 1) / 2) + (t_last + 1) / 2);
+            if (work == 0) return cudaSuccess;
+            if (work >= (int64_t(1) << 31)) return cudaErrorInvalidValue;  // D2Cur: 32-bit item index
+            const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(work, sms));
+            tc_diag2_kernel<<<grid, kEThreads, kESmemBytes, st>>>(pd, qtile, ktile, vtile);
+            return cudaGetLastError();
+        }
         if (cudaError_t e = smem_attr((const void*)tc_diag_kernel, kDSmemBytes)) return e;
         const int64_t work = g.z * g.hq * pd.pairs_per_head;
         if (work == 0) return cudaSuccess;

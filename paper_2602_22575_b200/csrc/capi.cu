@@ -119,26 +119,28 @@ s2o_status run_pass(PassArgs a, int32_t path, void* ws, size_t ws_bytes, cudaStr
     if (path == S2O_PATH_TCGEN05 && !tc_supported(a))
         return fail(S2O_ERR_UNSUPPORTED, "tcgen05 path needs bf16 inputs, D=128, b_m=128, b_n=128");
     if (path_is_tc(a, path)) {
-        // pass-1 / dense on the diagonal kernel: tiles with a poisoned (non-finite) diagonal V block
-        // are listed by the kernel and recomputed by the exact path, which skips masked keys
+        // diagonal passes (pass-1, dense): tiles whose diagonal V block holds a non-finite value
+        // (masked keys the tensor core would multiply) are listed by poison_scan_kernel and
+        // recomputed by the exact path, which skips masked keys
         static const bool poison_on = [] {  // S2O_POISON_CHECK=0: off (A/B aid)
             const char* e = std::getenv("S2O_POISON_CHECK");
             return !(e && std::strcmp(e, "0") == 0);
         }();
         const bool diag_only = poison_on && (a.mode & kDiag) && !(a.mode & (kPrefix | kStateIn)) && !a.tile_list;
         if (diag_only) {
-            a.poison_cnt = a.err_flag + 5;
-            a.poison_list = reinterpret_cast<int32_t*>(base + align256(generic_scratch_bytes(a)) + 256);
-            if (!clear_flag) S2O_CUDA_TRY(cudaMemsetAsync(a.poison_cnt, 0, sizeof(int32_t), st), "memset");
-        }
-        S2O_CUDA_TRY(launch_tc_pass(a, st), "tcgen05 pass launch");
-        if (diag_only && tc_diag_used(a)) {
+            PassArgs s = a;
+            s.poison_cnt = a.err_flag + 5;
+            s.poison_list = reinterpret_cast<int32_t*>(base + align256(generic_scratch_bytes(a)) + 256);
+            if (!clear_flag) S2O_CUDA_TRY(cudaMemsetAsync(s.poison_cnt, 0, sizeof(int32_t), st), "memset");
+            S2O_CUDA_TRY(launch_poison_scan(s, st), "poison scan");
+            S2O_CUDA_TRY(launch_tc_pass(a, st), "tcgen05 pass launch");
             PassArgs r = a;
-            r.tile_list = a.poison_list;
+            r.tile_list = s.poison_list;
             r.tile_count = 0;
-            r.tile_count_dev = a.poison_cnt;
-            r.poison_cnt = r.poison_list = nullptr;
+            r.tile_count_dev = s.poison_cnt;
             S2O_CUDA_TRY(launch_generic_pass(r, base, st), "poison rerun");
+        } else {
+            S2O_CUDA_TRY(launch_tc_pass(a, st), "tcgen05 pass launch");
         }
     } else {
         S2O_CUDA_TRY(launch_generic_pass(a, base, st), "generic pass launch");

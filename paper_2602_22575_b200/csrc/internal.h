@@ -126,6 +126,7 @@ cudaError_t set_max_dyn_smem(const void* fn, uint32_t bytes);  // once per (kern
 bool tc_supported(const PassArgs& a);
 bool tc_diag_used(const PassArgs& a);  // launch_tc_pass takes the diagonal (pass-1) kernel
 cudaError_t launch_tc_pass(const PassArgs& a, cudaStream_t st);
+cudaError_t launch_poison_scan(const PassArgs& a, cudaStream_t st);  // lists tiles with a non-finite diagonal V block
 
 // block top-k baseline selection (baseline.cu): row stats, block masses, kv token lists
 cudaError_t launch_block_topk_select(const Geo& g, const void* q, const void* k, int64_t rows, int64_t cols,

@@ -232,6 +232,12 @@ __device__ __forceinline__ void tma_gather4(uint32_t sdst, const CUtensorMap* ma
 }
 
 // TMA: plain 2-D tile load (box from the tensor map) at (col, row).
+// L2 prefetch of a 2-D tensor tile (no shared memory, no barrier)
+__device__ __forceinline__ void tma_prefetch2d(const CUtensorMap* map, int32_t col, int32_t row) {
+    asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(reinterpret_cast<uint64_t>(map)),
+                 "r"(col), "r"(row)
+                 : "memory");
+}
 __device__ __forceinline__ void tma_load2d(uint32_t sdst, const CUtensorMap* map, int32_t col, int32_t row,
                                            uint32_t bar) {
     asm volatile(

@@ -10,6 +10,9 @@
 //   mode 7: mode 4 while warps 1-3 stream ld.shared over the operand tiles
 //   mode 8: TS (A = TMEM cols 0-63) -> SS writing cols 0-127 (the P-aliased-in-S hazard), back to back
 //   mode 9: mode 8 for two slots interleaved (slot x at cols 256x): PV0 S0 PV1 S1
+//   mode 10: mode 9 with a tcgen05.commit (no waiter) after every group
+//   mode 11: the two-tile diagonal kernel's layout (S_x at 128x, O_x at 256 + 128x) and commits
+//            (two after each S group, one after each P V group)
 // probe (after the modes): clocks from issuing 16 MMAs to (a) the last issue returning, (b) a
 // try_wait on an already-complete barrier returning, (c) the MMAs' commit completing
 // build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I paper_2602_22575_b200/csrc
@@ -25,19 +28,21 @@ __device__ volatile int g_stop;
 __global__ void __launch_bounds__(128, 1) bench(int mode, long long* out) {
     extern __shared__ __align__(1024) unsigned char sm_raw[];
     unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(sm_raw) + 1023) & ~uintptr_t(1023));
-    __shared__ uint64_t bar;
+    __shared__ uint64_t bar, bar2c, bar3c;
     __shared__ uint32_t tbase_s;
     const int warp = threadIdx.x / 32;
     for (int i = threadIdx.x; i < 3 * 32768 / 16; i += blockDim.x) reinterpret_cast<uint4*>(sm)[i] = make_uint4(0, 0, 0, 0);
     if (threadIdx.x == 0) {
         mbar_init(smem_u32(&bar), 1);
+        mbar_init(smem_u32(&bar2c), 1);
+        mbar_init(smem_u32(&bar3c), 1);
         fence_mbar_init();
     }
     if (warp == 0) {
         tmem_alloc(smem_u32(&tbase_s), 512);
         tmem_relinquish();
     }
-    fence_proxy_async_smem();
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -107,6 +112,21 @@ __global__ void __launch_bounds__(128, 1) bench(int mode, long long* out) {
                 case 9: {
                     const uint32_t x = (g >> 1) & 1;
                     if (g & 1) ss(tb + x * 256, id128); else ts(tb + x * 256 + 128, x * 256);
+                } break;
+                case 10: {
+                    const uint32_t x = (g >> 1) & 1;
+                    if (g & 1) ss(tb + x * 256, id128); else ts(tb + x * 256 + 128, x * 256);
+                    if (leader) umma_commit(smem_u32(&bar2c));
+                } break;
+                case 11: {
+                    const uint32_t x = (g >> 1) & 1;
+                    if (g & 1) {
+                        ss(tb + x * 128, id128);
+                        if (leader) { umma_commit(smem_u32(&bar2c)); umma_commit(smem_u32(&bar3c)); }
+                    } else {
+                        ts(tb + 256 + x * 128, x * 128);
+                        if (leader) umma_commit(smem_u32(&bar3c));
+                    }
                 } break;
             }
         }
@@ -181,8 +201,9 @@ int main() {
     cudaFuncSetAttribute(bench, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     const char* names[] = {"SS N128 latency/group", "SS N128 throughput", "TS N128 throughput", "SS N256 throughput",
                            "SS+TS N128 alternating", "SS N64 throughput", "SS+TS + TMEM ld/st traffic",
-                           "SS+TS + ld.shared traffic", "TS(P@S)->SS(S) hazard", "hazard, 2 slots"};
-    for (int mode = 0; mode < 10; ++mode) {
+                           "SS+TS + ld.shared traffic", "TS(P@S)->SS(S) hazard", "hazard, 2 slots", "2 slots + commit/group",
+                           "diag2 layout + commits"};
+    for (int mode = 0; mode < 12; ++mode) {
         for (int rep = 0; rep < 2; ++rep) bench<<<148, 128, smem>>>(mode, d);
         cudaError_t e = cudaDeviceSynchronize();
         if (e != cudaSuccess) { printf("error %s\n", cudaGetErrorString(e)); return 1; }

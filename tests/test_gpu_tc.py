@@ -239,32 +239,42 @@ _PASS1_SCRIPT = r"""
 import sys, numpy as np, torch
 sys.path.insert(0, sys.argv[1])
 import paper_2602_22575_b200 as s2o
-q, k, v = s2o.generate_synthetic("mixed", 3000 // 64, 8.0, 5, 1, 4, 3000, 128)
+hq, hkv, l, s = (int(x) for x in sys.argv[3:7])
+q, k, v = s2o.generate_synthetic("mixed", l // 64, 8.0, 5, 1, hq, l, 128)
 dev = lambda x: torch.from_numpy(np.ascontiguousarray(x)).cuda().to(torch.bfloat16)
-cfg = s2o.KernelConfig(seg_len=700, tau=0.005, tiles=s2o.TileSpec(128, 128), path=2)
-b = s2o.pass1_dense_init(dev(q), dev(k[:, :2]), dev(v[:, :2]), cfg)
+cfg = s2o.KernelConfig(seg_len=s, tau=0.005, tiles=s2o.TileSpec(128, 128), path=2)
+b = s2o.pass1_dense_init(dev(q), dev(k[:, :hkv]), dev(v[:, :hkv]), cfg)
 torch.cuda.synchronize()
 np.savez(sys.argv[2], acc=b.acc.cpu().numpy(), ell=b.ell.cpu().numpy(), m=b.m.cpu().numpy())
 """
 
 
-def test_diag_kernel_equals_pair_kernel(cuda, tmp_path):
-    """Pass-1 on the single-tile diagonal kernel (default) and on the pair kernel
-    (S2O_DIAG_KERNEL=0, read once per process, hence the subprocesses): the same state up to
-    fp32 summation order (ragged segments S=700, GQA 4/2)."""
+@pytest.mark.parametrize("var,hq,hkv,l,seg", [
+    ("S2O_DIAG_KERNEL=0", 4, 2, 3000, 700),  # the pair kernel
+    ("S2O_DIAG2=1", 4, 2, 3000, 700),        # two-tile kernel: q heads 2i, 2i+1 of a group
+    ("S2O_DIAG2=1", 8, 1, 5000, 2048),
+    ("S2O_DIAG2=1", 6, 2, 3000, 700),        # odd group: adjacent tiles of one head
+    ("S2O_DIAG2=1", 3, 3, 4200, 1000)])
+def test_diag_kernel_equals_variant(cuda, tmp_path, var, hq, hkv, l, seg):
+    """Pass-1 on the single-tile diagonal kernel (default) and on a variant kernel (env flag, read
+    once per process, hence the subprocesses): the same state up to fp32 summation order (ragged
+    segments, GQA groups even, odd and 1)."""
     import subprocess
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    name, val = var.split("=")
     out = {}
-    for flag in ("1", "0"):
-        f = str(tmp_path / f"p1_{flag}.npz")
-        env = dict(os.environ, S2O_DIAG_KERNEL=flag)
-        subprocess.run([sys.executable, "-c", _PASS1_SCRIPT, root, f], check=True, env=env, timeout=600)
-        out[flag] = np.load(f)
-    a, b = out["1"], out["0"]
+    for tag, extra in (("base", {}), ("var", {name: val})):
+        f = str(tmp_path / f"p1_{tag}.npz")
+        env = dict(os.environ, **extra)
+        subprocess.run([sys.executable, "-c", _PASS1_SCRIPT, root, f, str(hq), str(hkv), str(l), str(seg)],
+                       check=True, env=env, timeout=600)
+        out[tag] = np.load(f)
+    a, b = out["base"], out["var"]
     # invariant under the lazy reference: O = acc / ell and ell * e^m
     oa = a["acc"] / a["ell"][..., None]
     ob = b["acc"] / b["ell"][..., None]
+    assert np.isfinite(ob).all()
     assert np.abs(oa - ob).max() <= 2e-2 and np.abs(oa - ob).mean() <= 1e-3
     np.testing.assert_allclose(a["ell"] * np.exp(a["m"] - b["m"]), b["ell"], rtol=2e-3)
 
