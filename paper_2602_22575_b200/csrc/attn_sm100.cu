@@ -36,6 +36,8 @@
 
 #include <cmath>
 #include <cstdlib>
+#include <algorithm>
+#include <climits>
 #include <cstring>
 #include <mutex>
 #include <utility>
@@ -1336,7 +1338,7 @@ tc_diag_kernel(const TcParams p, const __grid_constant__ CUtensorMap qtile,
 }
 
 // ============================================================== two-tile diagonal kernel
-// Pass-1 with TWO 128-row query tiles in flight per CTA (S2O_DIAG2=1 selects it; A/B against
+// Pass-1 with TWO 128-row query tiles in flight per CTA (the default; S2O_DIAG2=0 selects
 // tc_diag_kernel). The tiles of a work item read the same K/V rows: the two q heads 2i, 2i+1 of
 // a GQA group at the same (segment, tile) when the group is even, else two adjacent tiles of one
 // head (the longer first). Every K/V block is loaded once for both.
@@ -1474,14 +1476,17 @@ __device__ __forceinline__ void d2_next(const D2Rad& R, D2Cur& c) {
 __device__ __forceinline__ TileInfo d2_tile(const TcParams& p, const D2Rad& R, const D2Cur& c, int x) {
     const Geo& g = p.a.g;
     const bool last = c.n == R.N - 1;
+    // longest tile (pair) first in even segments, shortest first in odd ones: a CTA's items
+    // (stride gridDim.x) then see every tile length, not a residue class of them
+    const uint32_t u = (c.n & 1u) ? (last ? R.Ul : R.U) - 1 - c.u : c.u;
     int32_t ti;
     TileInfo t;
     if (R.G % 2 == 0) {
         t.zh = (int64_t)c.zg * R.G + 2 * c.a + x;
-        ti = (int32_t)((last ? R.tl : R.T) - 1 - c.u);
+        ti = (int32_t)((last ? R.tl : R.T) - 1 - u);
     } else {
         t.zh = (int64_t)c.zg * R.G + c.a;
-        ti = (int32_t)((last ? R.tl : R.T) - 1 - 2 * c.u) - x;
+        ti = (int32_t)((last ? R.tl : R.T) - 1 - 2 * u) - x;
     }
     t.n = c.n;
     t.sb = (int64_t)c.n * g.S;
@@ -1543,6 +1548,7 @@ tc_diag2_kernel(const TcParams p, const __grid_constant__ CUtensorMap qtile,
     unsigned char* smem = smem_raw;
     if ((smem_u32(smem) & 1023u) != 0) __trap();
     CtrlE& c = *reinterpret_cast<CtrlE*>(smem + kEOffCtrl);
+    if (threadIdx.x == 0) tl_cta(p, 0);
     const PassArgs& a = p.a;
     const Geo& g = a.g;
     const int warp = threadIdx.x / 32;
@@ -1977,6 +1983,7 @@ tc_diag2_kernel(const TcParams p, const __grid_constant__ CUtensorMap qtile,
     }
     tc_fence_before();
     if (warp <= kEMmaWarp) named_bar_sync(5, 32 * (kEMmaWarp + 1));  // softmax, epilogue, MMA warps
+    if (threadIdx.x == 0) tl_cta(p, 3);
     if (warp == 0) {
         tc_fence_after();
         tmem_dealloc(tbase, kTmemCols);
@@ -2115,6 +2122,56 @@ cudaError_t launch_poison_scan(const PassArgs& a, cudaStream_t st) {
     return cudaGetLastError();
 }
 
+// Grid of the two-tile kernel. CTA b takes items b, b + grid, ...; in plain longest-first order
+// a CTA saw only every other tile length of a segment (148 / 2 = 74 = 10 mod 16 at C3: CTAs with
+// even b / 2 got 9 blocks per item on average, the others 8, and the kernel ran as long as the
+// busier half, measured CTA spans 2.16-2.60 ms). d2_tile alternates the order per segment; on
+// top, among grids of [sms - 12, sms] this picks the one whose busiest CTA has the fewest blocks
+// (host replica of the item order, computed once per shape).
+int diag2_grid(const Geo& g, int64_t T, int64_t work, int sms) {
+    if (work <= sms) return (int)std::max<int64_t>(1, work);
+    struct Key { int64_t G, T, N, tl, kh; int sms; int grid; };
+    static std::mutex mu;
+    static std::vector<Key> cache;
+    const int64_t G = g.group, N = g.N, tl = (g.last_len + kBM - 1) / kBM, kh = g.z * g.hq / g.group;
+    {
+        std::lock_guard<std::mutex> lock(mu);
+        for (const Key& k : cache)
+            if (k.G == G && k.T == T && k.N == N && k.tl == tl && k.kh == kh && k.sms == sms) return k.grid;
+    }
+    const bool hp = G % 2 == 0;
+    const int64_t A = hp ? G / 2 : G, U = hp ? T : (T + 1) / 2, Ul = hp ? tl : (tl + 1) / 2;
+    const int64_t R = (N - 1) * U + Ul;
+    std::vector<int64_t> blocks(work);  // blocks of item i (both tiles)
+    for (int64_t i = 0; i < work; ++i) {
+        const int64_t r = (i / A) % R;
+        const int64_t n = r < (N - 1) * U ? r / U : N - 1;
+        const int64_t u0 = r - n * U;
+        const int64_t u = (n & 1) ? (n == N - 1 ? Ul : U) - 1 - u0 : u0;  // d2_tile's snake order
+        const int64_t top = (n == N - 1 ? tl : T) - 1;
+        if (hp) blocks[i] = 2 * (top - u + 1);
+        else {
+            const int64_t t0 = top - 2 * u;
+            blocks[i] = (t0 + 1) + (t0 >= 1 ? t0 : 0);
+        }
+    }
+    int best = sms;
+    int64_t best_load = INT64_MAX;
+    std::vector<int64_t> load;
+    for (int grid = sms; grid >= std::max(1, sms - 12); --grid) {
+        load.assign(grid, 0);
+        for (int64_t i = 0; i < work; ++i) load[i % grid] += blocks[i];
+        const int64_t mx = *std::max_element(load.begin(), load.end());
+        if (mx < best_load) {
+            best_load = mx;
+            best = grid;
+        }
+    }
+    std::lock_guard<std::mutex> lock(mu);
+    cache.push_back({G, T, N, tl, kh, sms, best});
+    return best;
+}
+
 cudaError_t launch_tc_pass(const PassArgs& a, cudaStream_t st) {
     const Geo& g = a.g;
     CUtensorMap qmap, kmap, vmap, qtile, ktile, vtile;
@@ -2147,9 +2204,9 @@ cudaError_t launch_tc_pass(const PassArgs& a, cudaStream_t st) {
     if (tc_diag_used(a)) {
         TcParams pd = p;
         pd.pairs_per_head = (g.N - 1) * a.T + t_last;  // tiles per head (diag_tile)
-        static const bool two_tile = [] {
+        static const bool two_tile = [] {  // S2O_DIAG2=0: the single-tile kernel (A/B aid)
             const char* e = std::getenv("S2O_DIAG2");
-            return e && std::strcmp(e, "1") == 0;
+            return !(e && std::strcmp(e, "0") == 0);
         }();
         if (two_tile) {  // tc_diag2_kernel: two tiles sharing K/V per work item
             if (cudaError_t e = smem_attr((const void*)tc_diag2_kernel, kESmemBytes)) return e;
@@ -2158,7 +2215,7 @@ cudaError_t launch_tc_pass(const PassArgs& a, cudaStream_t st) {
                                      : g.z * g.hq * ((g.N - 1) * ((a.T + 1) / 2) + (t_last + 1) / 2);
             if (work == 0) return cudaSuccess;
             if (work >= (int64_t(1) << 31)) return cudaErrorInvalidValue;  // D2Cur: 32-bit item index
-            const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(work, sms));
+            const int grid = diag2_grid(g, a.T, work, sms);
             tc_diag2_kernel<<<grid, kEThreads, kESmemBytes, st>>>(pd, qtile, ktile, vtile);
             return cudaGetLastError();
         }

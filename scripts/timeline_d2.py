@@ -26,6 +26,14 @@ s2o.pass1_dense_init(qd, kd, vd, cfg)
 torch.cuda.synchronize()
 lib.s2o_debug_timeline(None)
 t = buf.cpu().numpy().reshape(32, CAP)
+st, en = t[0][:148], t[3][:148]
+if (st > 0).all() and (en > 0).all():  # per-CTA spans (global timer, ns)
+    d = (en - st) / 1e3
+    print(f"CTA spans us: min {d.min():.0f} median {np.median(d):.0f} max {d.max():.0f}; kernel "
+          f"{(en.max() - st.min()) / 1e3:.0f} us; end spread {(en.max() - en.min()) / 1e3:.0f} us")
+    np.save("gpurun_out/cta_spans_d2.npy", np.stack([st, en]))
+t[0] = 0
+t[3] = 0
 t0 = t[t > 0].min()
 rel = np.where(t > 0, t - t0, -1)
 np.save("gpurun_out/timeline_d2.npy", rel)

@@ -251,14 +251,14 @@ np.savez(sys.argv[2], acc=b.acc.cpu().numpy(), ell=b.ell.cpu().numpy(), m=b.m.cp
 
 @pytest.mark.parametrize("var,hq,hkv,l,seg", [
     ("S2O_DIAG_KERNEL=0", 4, 2, 3000, 700),  # the pair kernel
-    ("S2O_DIAG2=1", 4, 2, 3000, 700),        # two-tile kernel: q heads 2i, 2i+1 of a group
-    ("S2O_DIAG2=1", 8, 1, 5000, 2048),
-    ("S2O_DIAG2=1", 6, 2, 3000, 700),        # odd group: adjacent tiles of one head
-    ("S2O_DIAG2=1", 3, 3, 4200, 1000)])
+    ("S2O_DIAG2=0", 4, 2, 3000, 700),        # the single-tile kernel vs the two-tile default:
+    ("S2O_DIAG2=0", 8, 1, 5000, 2048),       #   q heads 2i, 2i+1 of a group,
+    ("S2O_DIAG2=0", 6, 2, 3000, 700),        #   odd group: adjacent tiles of one head
+    ("S2O_DIAG2=0", 3, 3, 4200, 1000)])
 def test_diag_kernel_equals_variant(cuda, tmp_path, var, hq, hkv, l, seg):
-    """Pass-1 on the single-tile diagonal kernel (default) and on a variant kernel (env flag, read
-    once per process, hence the subprocesses): the same state up to fp32 summation order (ragged
-    segments, GQA groups even, odd and 1)."""
+    """Pass-1 on the default diagonal kernel (two tiles per item) and on a variant kernel (env
+    flag, read once per process, hence the subprocesses): the same state up to fp32 summation
+    order (ragged segments, GQA groups even, odd and 1)."""
     import subprocess
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
