@@ -105,6 +105,20 @@ __device__ __forceinline__ int64_t ring_get(Ctrl& c, uint32_t k, int lane) {
     return it;
 }
 
+// Division by a launch constant without the integer-division sequence (its MUFU.RCP would queue
+// behind the softmax warps' exponentials on the same SMSP): q = (umulhi(n, mul) + n) >> shift,
+// exact for n < 2^31 (Granlund-Montgomery; mul, shift from the host).
+struct FastDiv {
+    uint32_t d, mul, shift;
+    FastDiv() = default;
+    explicit FastDiv(uint32_t div) : d(div) {
+        shift = 0;
+        while ((1ull << shift) < div) ++shift;
+        mul = (uint32_t)(((1ull << 32) * ((1ull << shift) - div)) / div + 1);
+    }
+    __device__ __forceinline__ uint32_t div(uint32_t n) const { return (__umulhi(n, mul) + n) >> shift; }
+};
+
 struct TcParams {
     PassArgs a;
     float scale_log2;  // (1/sqrt(D)) * log2(e)
@@ -112,6 +126,7 @@ struct TcParams {
     int vec_acc, vec_o;  // 256-bit epilogue accesses (32-B aligned state / output rows)
     int64_t pairs_per_head, pairs_full;  // pairs per head; pairs in a full segment
     unsigned long long* tl;              // optional timeline (CTA 0), see s2o_debug_timeline
+    FastDiv fd_pg, fd_g, fd_pf, fd_tph, fd_t;  // pairs_per_head * group, group, pairs_full, tiles_per_head, T
 };
 
 // Timeline events (profiling aid): tl[ev * kTlCap + seq] = clock64() in CTA 0.
@@ -156,26 +171,31 @@ __device__ __forceinline__ PairInfo pair_info(const TcParams& p, int64_t idx) {
     const Geo& g = a.g;
     PairInfo P;
     int64_t ti0, ti1, n;
+    // (32-bit FastDiv decode: item and tile indices < 2^31, checked by the launcher)
     if (a.tile_list) {
-        const int64_t tile = a.tile_list[idx];
-        P.zh = (int32_t)(tile / a.tiles_per_head);
-        const int64_t r = tile % a.tiles_per_head;
-        const int64_t full = (g.N - 1) * a.T;
-        if (r < full) { n = r / a.T; ti0 = r % a.T; }
+        const uint32_t tile = (uint32_t)a.tile_list[idx];
+        const uint32_t zh = p.fd_tph.div(tile);
+        P.zh = (int32_t)zh;
+        const uint32_t r = tile - zh * p.fd_tph.d;
+        const uint32_t full = (uint32_t)((g.N - 1) * a.T);
+        if (r < full) { n = p.fd_t.div(r); ti0 = r - (uint32_t)n * p.fd_t.d; }
         else { n = g.N - 1; ti0 = r - full; }
         ti1 = -1;
     } else {
         // The q heads of a GQA group share K/V: interleave them (head fastest) so the group's
         // CTAs walk the same segment's K/V rows at the same time and hit L2 together.
-        const int64_t G = g.group;
-        const int64_t zg = idx / (p.pairs_per_head * G);
-        const int64_t rem = idx % (p.pairs_per_head * G);
-        P.zh = (int32_t)(zg * G + rem % G);
-        const int64_t r = rem / G;
-        const int64_t full = (g.N - 1) * p.pairs_full;
+        const uint32_t G = p.fd_g.d, i32 = (uint32_t)idx;
+        const uint32_t zg = p.fd_pg.div(i32);
+        const uint32_t rem = i32 - zg * p.fd_pg.d;
+        const uint32_t r = p.fd_g.div(rem);
+        P.zh = (int32_t)(zg * G + (rem - r * G));
+        const uint32_t full = (uint32_t)((g.N - 1) * p.pairs_full);
         int64_t pi, tcount;
-        if (r < full) { n = r / p.pairs_full; pi = r % p.pairs_full; tcount = a.T; }
-        else { n = g.N - 1; pi = r - full; tcount = (g.last_len + kBM - 1) / kBM; }
+        if (r < full) {
+            n = p.fd_pf.div(r);
+            pi = r - (uint32_t)n * p.fd_pf.d;
+            tcount = a.T;
+        } else { n = g.N - 1; pi = r - full; tcount = (g.last_len + kBM - 1) / kBM; }
         ti0 = 2 * pi;
         ti1 = (2 * pi + 1 < tcount) ? 2 * pi + 1 : -1;
     }
@@ -2196,6 +2216,13 @@ cudaError_t launch_tc_pass(const PassArgs& a, cudaStream_t st) {
     p.tl = g_timeline;
     const int64_t t_last = (g.last_len + kBM - 1) / kBM;
     p.pairs_per_head = (g.N - 1) * p.pairs_full + (t_last + 1) / 2;
+    if (g.z * g.hq * std::max<int64_t>(p.pairs_per_head, a.tiles_per_head) >= (int64_t(1) << 31))
+        return cudaErrorInvalidValue;  // pair_info decodes 32-bit indices
+    p.fd_pg = FastDiv((uint32_t)(p.pairs_per_head * g.group));
+    p.fd_g = FastDiv((uint32_t)g.group);
+    p.fd_pf = FastDiv((uint32_t)std::max<int64_t>(1, p.pairs_full));
+    p.fd_tph = FastDiv((uint32_t)std::max<int64_t>(1, a.tiles_per_head));
+    p.fd_t = FastDiv((uint32_t)std::max<int64_t>(1, a.T));
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
