@@ -176,16 +176,19 @@ def plan_hbm(l: int, s: int, t_ms: float, pk: dict) -> dict:
 
 
 def launches_per_step(l: int, s: int) -> int:
-    """Our kernels per s2o_attention_fwd call with the truncated plan (no overflow rerun):
-    guide means, q ranking (+ q sort when S > 2048), kv scoring, top-T selection (scan + sort
-    kernels), trace init, pass-1 (tc_diag_kernel), pass-2 (tc_pass_kernel)."""
+    """Our kernels per s2o_attention_fwd call with the truncated plan (no overflow rerun), as the
+    ncu launch list of a bench run shows them: guide means and q ranking (+ the q sort when
+    S > 2048); for N > 1 segments the candidate top-T selection (dense kv scoring of the first
+    segments, sample scoring, threshold, kv_cand, two pack kernels, sel_scan, sel_sort); then trace
+    init, the masked-key poison scan, pass-1 (tc_diag2_kernel), the (empty) poison rerun and
+    pass-2 (tc_pass_kernel)."""
     n = -(-l // s)
     count = 2
     if s > 2048:
         count += 2 + plan_sort_passes(l, s)
     if n > 1:
-        count += 3
-    return count + 3
+        count += 8
+    return count + 5
 
 
 # ------------------------------------------------------------------ shared description
@@ -448,7 +451,7 @@ def run_ours(args, rank: int, world: int):
     if t_p2 >= t_p1:
         dom, f_dom, t_dom = "tc_pass_kernel (pass-2)", f_p2, t_p2
     else:
-        dom, f_dom, t_dom = "tc_diag_kernel (pass-1)", f_p1, t_p1
+        dom, f_dom, t_dom = "tc_diag2_kernel (pass-1)", f_p1, t_p1
     achieved = f_dom / (t_dom * 1e-3) / 1e12
     peak = float(pk.get("bf16_tflops", PEAKS_FALLBACK["bf16_tflops"]))
     traffic = None
