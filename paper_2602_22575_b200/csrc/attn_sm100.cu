@@ -1376,33 +1376,11 @@ tc_diag_kernel(const TcParams p, const __grid_constant__ CUtensorMap qtile,
 // waiting for s_full_x needs no other barrier. Q has three 32 KB slots, so the next item's first
 // Q tile lands while this item runs.
 constexpr int kEThreads = 512;
-#ifdef S2O_D2_NOXITEM  // A/B: each item's first S issued at its start (not after the last P V)
-constexpr bool kNoXItem = true;
-#else
-constexpr bool kNoXItem = false;
-#endif
-#ifdef S2O_D2_NOMMA  // timing aid: barriers only, no tensor-core work
-constexpr bool kNoMma = true;
-#else
-constexpr bool kNoMma = false;
-#endif
-constexpr int kEEpiWarp0 = 8, kEMmaWarp = 12, kEKWarp = 13, kEVWarp = 14, kEQWarp = 15;
-#ifndef S2O_D2_MMAREGS
-#define S2O_D2_MMAREGS 64
-#endif
-constexpr int kESoftRegs = 184, kEEpiRegs = 80, kEMmaRegs = S2O_D2_MMAREGS, kELoadRegs = 64;
+constexpr int kEEpiWarp0 = 8, kEMmaWarp = 12, kEKWarp = 13, kEQWarp = 15;  // warp 14: V loader
+constexpr int kESoftRegs = 184, kEEpiRegs = 80, kEMmaRegs = 64, kELoadRegs = 64;
 static_assert(8 * (kESoftRegs - 128) <= 4 * (128 - kEEpiRegs) + (128 - kEMmaRegs) + 3 * (128 - kELoadRegs),
               "register pool");
-#ifndef S2O_D2_QSLOTS
-#define S2O_D2_QSLOTS 3
-#endif
-#ifndef S2O_D2_KST
-#define S2O_D2_KST 2
-#endif
-#ifndef S2O_D2_VST
-#define S2O_D2_VST 2
-#endif
-constexpr int kEQSlots = S2O_D2_QSLOTS, kEKStages = S2O_D2_KST, kEVStages = S2O_D2_VST;
+constexpr int kEQSlots = 3, kEKStages = 2, kEVStages = 2;
 constexpr uint32_t kEOffQ = 0;
 constexpr uint32_t kEOffK = kEQSlots * kTileBytes;
 constexpr uint32_t kEOffV = kEOffK + kEKStages * kTileBytes;
@@ -1523,37 +1501,17 @@ __device__ __forceinline__ TileInfo d2_tile(const TcParams& p, const D2Rad& R, c
     return t;
 }
 
-#ifndef S2O_D2_POLY0
-#define S2O_D2_POLY0 S2O_DIAG_POLY
-#endif
-#ifndef S2O_D2_POLY1
-#define S2O_D2_POLY1 S2O_DIAG_POLY
-#endif
 // P = exp2(s * scale - m) for a full row of 128 scores into the first 64 columns of S (bf16
-// pairs), with every P-th pair on the FMA-pipe polynomial (P = 0: all MUFU). Per tile slot, so
-// the two slots' softmax warps, which share an SMSP, can lean on different pipes.
-template <int P>
+// pairs), all on MUFU: with the row in 128 registers the FMA-pipe polynomial's temporaries do not
+// fit, and every polynomial fraction measured slower (1/8 ... 1/2: +4 % ... +80 %).
 __device__ __forceinline__ void d2_exps(const uint32_t (&sv)[128], float sc, float neg_ref, uint32_t tS, float (&rs)[4]) {
 #pragma unroll
     for (int c0 = 0; c0 < 128; c0 += 32) {
         uint32_t pk[16];
 #pragma unroll
         for (int i = 0; i < 32; i += 2) {
-            float e0, e1;
-            if (P > 0 && (i >> 1) % (P > 0 ? P : 1) == P - 1) {
-                const float2 e = ex2_poly4x2(make_float2(fmaf(__uint_as_float(sv[c0 + i]), sc, neg_ref),
-                                                         fmaf(__uint_as_float(sv[c0 + i + 1]), sc, neg_ref)));
-                e0 = e.x;
-                e1 = e.y;
-            } else {
-#ifdef S2O_D2_NOEXP  // timing aid: exponentials replaced by a multiply
-                e0 = fmaf(__uint_as_float(sv[c0 + i]), sc, neg_ref) * 0.001f;
-                e1 = fmaf(__uint_as_float(sv[c0 + i + 1]), sc, neg_ref) * 0.001f;
-#else
-                e0 = ex2(fmaf(__uint_as_float(sv[c0 + i]), sc, neg_ref));
-                e1 = ex2(fmaf(__uint_as_float(sv[c0 + i + 1]), sc, neg_ref));
-#endif
-            }
+            const float e0 = ex2(fmaf(__uint_as_float(sv[c0 + i]), sc, neg_ref));
+            const float e1 = ex2(fmaf(__uint_as_float(sv[c0 + i + 1]), sc, neg_ref));
             rs[(i >> 1) & 3] += e0 + e1;
             pk[i >> 1] = pack_bf16(e0, e1);
         }
@@ -1661,10 +1619,6 @@ tc_diag2_kernel(const TcParams p, const __grid_constant__ CUtensorMap qtile,
                 const int st = gi % nst;
                 mbar_wait(smem_u32(&xempty[st]), ((gi / nst) & 1) ^ 1, kl ? 4012 : 4013);
                 tl_mark(p, kl ? 22 : 23, gi);
-#ifdef S2O_D2_NOLOAD  // timing aid: no K / V data movement
-                mbar_expect_tx(smem_u32(&xfull[st]), 0);
-                continue;
-#endif
                 mbar_expect_tx(smem_u32(&xfull[st]), kTileBytes);
                 const uint32_t dst = xbase + st * kTileBytes;
                 for (int h = 0; h < 2; ++h)
@@ -1694,7 +1648,7 @@ tc_diag2_kernel(const TcParams p, const __grid_constant__ CUtensorMap qtile,
 #pragma unroll
             for (int kk = 0; kk < kD / 16; ++kk) {
                 const uint32_t off = ((kk / 4) * kHalf + (kk % 4) * 32) >> 4;
-                if (leader && !kNoMma) umma_bf16(tbase + x * 128, dq + off, dk + off, idesc_s, kk > 0);
+                if (leader) umma_bf16(tbase + x * 128, dq + off, dk + off, idesc_s, kk > 0);
             }
             if (leader) umma_commit(smem_u32(&c.s_full[x]));
         };
@@ -1718,7 +1672,7 @@ tc_diag2_kernel(const TcParams p, const __grid_constant__ CUtensorMap qtile,
             nd[1] = d2_tile(p, R, cn, 1).nd;
         }
         for (bool first = true; it < total; it += gridDim.x, first = false) {
-            if (first || kNoXItem) {
+            if (first) {
                 const uint32_t kst = kc % kEKStages;
                 mbar_wait(smem_u32(&c.k_full[kst]), (kc / kEKStages) & 1, 4111);
                 for (int x = 0; x < 2; ++x)
@@ -1744,7 +1698,7 @@ tc_diag2_kernel(const TcParams p, const __grid_constant__ CUtensorMap qtile,
             for (int j = 0; j < nd[0]; ++j) {
                 const uint32_t vst = vc % kEVStages;
                 const bool last = j + 1 == nd[0];
-                const bool knext = !last || (nn[0] > 0 && !kNoXItem);  // a K block follows (this item's or the next's)
+                const bool knext = !last || nn[0] > 0;  // a K block follows (this item's or the next's)
                 const uint32_t kst = kc % kEKStages;
                 bool kwait = false;
                 tl_mark(p, 1, vc);
@@ -1752,19 +1706,15 @@ tc_diag2_kernel(const TcParams p, const __grid_constant__ CUtensorMap qtile,
                 const uint64_t dv = dv0 + ((vst * kTileBytes) >> 4);
                 for (int x = 0; x < 2; ++x) {
                     if (j < nd[x]) {
-#ifndef S2O_D2_NOPWAIT
                         mbar_wait(smem_u32(&c.p_full[x]), bx[x] & 1, 4114);
-#endif
                         tl_mark(p, 2 + 3 * x, vc);
                         ++bx[x];
                         // the epilogue has read O_x of this slot's previous tile
-#ifndef S2O_D2_NOOWAIT
                         if (j == 0) mbar_wait(smem_u32(&c.o_free[x]), (tx[x] & 1) ^ 1, 4115);
-#endif
                         tc_fence_after();
 #pragma unroll
                         for (int kk = 0; kk < kBN / 16; ++kk)
-                            if (leader && !kNoMma)
+                            if (leader)
                                 umma_bf16_ts(tbase + (2 + x) * 128, tbase + x * 128 + kk * 8,
                                              dv + ((kk * 16 * 128) >> 4), idesc_o, (kk > 0 || j > 0) ? 1 : 0);
                         tl_mark(p, 4 + 3 * x, vc);
@@ -1782,7 +1732,7 @@ tc_diag2_kernel(const TcParams p, const __grid_constant__ CUtensorMap qtile,
                         issue_s(x, qsl[x], kst);
                         tl_mark(p, 8 + x, vc);
                         if (j + 2 == nd[x] && leader) umma_commit(smem_u32(&c.q_empty[qsl[x]]));
-                    } else if (last && nn[x] > 0 && !kNoXItem) {  // S_x(0) of the next item
+                    } else if (last && nn[x] > 0) {  // S_x(0) of the next item
                         if (!kwait) {
                             mbar_wait(smem_u32(&c.k_full[kst]), (kc / kEKStages) & 1, 4117);
                             kwait = true;
@@ -1830,13 +1780,6 @@ tc_diag2_kernel(const TcParams p, const __grid_constant__ CUtensorMap qtile,
                 mbar_wait(smem_u32(&c.s_full[x]), bx & 1, 4211);
                 if (r == 0) tl_mark(p, 10 + 4 * x, bx);
                 tc_fence_after();
-#ifdef S2O_D2_NOSOFT  // timing aid: the MMA / load pipeline alone
-                __syncwarp();
-                if (lane == 0) mbar_arrive(smem_u32(&c.p_full[x]));
-                m2 = 0.0f;
-                ell = 1.0f;
-                continue;
-#endif
                 uint32_t sv[128];
 #pragma unroll
                 for (int c0 = 0; c0 < 128; c0 += 32) tmem_ld32(tS + c0, *reinterpret_cast<uint32_t(*)[32]>(&sv[c0]));
@@ -1870,8 +1813,7 @@ tc_diag2_kernel(const TcParams p, const __grid_constant__ CUtensorMap qtile,
                 const float alpha = (m2 == -INFINITY) ? 0.0f : ex2(m2 + neg_ref);
                 float rs[4] = {0.0f, 0.0f, 0.0f, 0.0f};
                 if (full) {
-                    if (x == 0) d2_exps<S2O_D2_POLY0>(sv, sc, neg_ref, tS, rs);
-                    else d2_exps<S2O_D2_POLY1>(sv, sc, neg_ref, tS, rs);
+                    d2_exps(sv, sc, neg_ref, tS, rs);
                 } else {
 #pragma unroll
                     for (int c0 = 0; c0 < 128; c0 += 32) {
@@ -1952,10 +1894,6 @@ tc_diag2_kernel(const TcParams p, const __grid_constant__ CUtensorMap qtile,
                         if (r == 0) tl_mark(p, 19 + 2 * x, tx[x] - 1);
                     }
                     if (!valid) continue;
-#ifdef S2O_D2_NOSTORE
-                    if (ov[0] == 0x7fc00001u) a.acc_out[slot * kD + c0] = 1.0f;
-                    continue;
-#endif
                     if (a.mode & kStateOut) {
                         if (p.vec_acc) {
                             float* dst = a.acc_out + slot * kD + c0;
