@@ -127,7 +127,34 @@ struct TcParams {
     int64_t pairs_per_head, pairs_full;  // pairs per head; pairs in a full segment
     unsigned long long* tl;              // optional timeline (CTA 0), see s2o_debug_timeline
     FastDiv fd_pg, fd_g, fd_pf, fd_tph, fd_t;  // pairs_per_head * group, group, pairs_full, tiles_per_head, T
+    FastDiv fd_hq;                             // q heads per batch
 };
+
+// Geo's q_base / k_base / v_base / o_base with FastDiv (the tc kernels call these per item)
+struct TcBase {
+    int64_t z, h, kvh;
+    __device__ __forceinline__ TcBase(const TcParams& p, int64_t zh) {
+        z = p.fd_hq.div((uint32_t)zh);
+        h = zh - z * (int64_t)p.fd_hq.d;
+        kvh = p.fd_g.div((uint32_t)h);
+    }
+};
+__device__ __forceinline__ int64_t tc_q_base(const TcParams& p, int64_t zh) {
+    const TcBase b(p, zh);
+    return b.z * p.a.g.qs[0] + b.h * p.a.g.qs[1];
+}
+__device__ __forceinline__ int64_t tc_o_base(const TcParams& p, int64_t zh) {
+    const TcBase b(p, zh);
+    return b.z * p.a.g.os[0] + b.h * p.a.g.os[1];
+}
+__device__ __forceinline__ int64_t tc_k_base(const TcParams& p, int64_t zh) {
+    const TcBase b(p, zh);
+    return b.z * p.a.g.ks[0] + b.kvh * p.a.g.ks[1];
+}
+__device__ __forceinline__ int64_t tc_v_base(const TcParams& p, int64_t zh) {
+    const TcBase b(p, zh);
+    return b.z * p.a.g.vs[0] + b.kvh * p.a.g.vs[1];
+}
 
 // Timeline events (profiling aid): tl[ev * kTlCap + seq] = clock64() in CTA 0.
 [[maybe_unused]] constexpr int kTlCap = 1024;
@@ -299,7 +326,7 @@ tc_pass_kernel(const TcParams p, const __grid_constant__ CUtensorMap qmap,
     const uint32_t tbase = c.tmem_base;
     if (threadIdx.x == 0) tl_cta(p, 0);
     const int64_t total = a.tile_list ? a.num_tiles() : g.z * g.hq * p.pairs_per_head;
-    const int64_t rowu = g.d;  // row unit of the tensor maps = D elements
+    constexpr int64_t rowu = kD;  // row unit of the tensor maps = D elements (tc path: d == 128)
 
     if (warp >= kMmaWarp) setmaxnreg_dec<kOtherRegs>();  // warpgroups 2-3
     if (warp >= kKWarp0) {
@@ -317,7 +344,6 @@ tc_pass_kernel(const TcParams p, const __grid_constant__ CUtensorMap qmap,
         int32_t* ring0 = reinterpret_cast<int32_t*>(smem + kOffTok) + (kgrp ? 0 : 2 * kBN);
         const CUtensorMap* xtile = kgrp ? &ktile : &vtile;
         const uint32_t xbase = kgrp ? sK : sV;
-        const int nst = kgrp ? kKStages : kVStages;
         const int lag = kgrp ? 3 : 2;  // decisions <= j-lag are final when stage j is acquired
         uint64_t* xfull = kgrp ? c.k_full : c.v_full;
         uint64_t* xempty = kgrp ? c.k_empty : c.v_empty;
@@ -339,7 +365,7 @@ tc_pass_kernel(const TcParams p, const __grid_constant__ CUtensorMap qmap,
             if (kgrp) {
                 // ---- Q (this CTA's slots; no multicast)
                 mbar_wait(smem_u32(&c.q_empty), (qcount & 1) ^ 1, 1001);
-                const int64_t qb = g.q_base(P.zh) / rowu, qs = g.qs[2] / rowu;
+                const int64_t qb = tc_q_base(p, P.zh) / rowu, qs = g.qs[2] / rowu;
                 const uint32_t qbytes = (uint32_t)(P.has[0] + P.has[1]) * kTileBytes;
                 const bool q_tile = p.q_contig && !((a.mode & kStateIn) && a.q_reorder) &&
                                     (!P.has[0] || P.tn[0] == kBM) && (!P.has[1] || P.tn[1] == kBM);
@@ -370,7 +396,7 @@ tc_pass_kernel(const TcParams p, const __grid_constant__ CUtensorMap qmap,
                 if (lt == 0) tl_mark(p, 29, qcount);
                 ++qcount;
             }
-            const int64_t xb = (kgrp ? g.k_base(P.zh) : g.v_base(P.zh)) / rowu;
+            const int64_t xb = (kgrp ? tc_k_base(p, P.zh) : tc_v_base(p, P.zh)) / rowu;
             const int64_t xs = (kgrp ? g.ks[2] : g.vs[2]) / rowu;
             const auto gathered = [&](int j) { return !(j < P.ndmax && p.kv_contig); };
             // tokens of block j: entries lt and lt + nthr (< 128) in registers, one block ahead
@@ -395,8 +421,11 @@ tc_pass_kernel(const TcParams p, const __grid_constant__ CUtensorMap qmap,
                 fetch_tok(j + 1, tk);  // prefetch (latency overlaps the stage wait)
                 if (gat) named_bar_sync(gbar, nthr);
                 const uint32_t gi = gx + j;
-                const int st = gi % nst;
-                mbar_wait(smem_u32(&xempty[st]), ((gi / nst) & 1) ^ 1, kgrp ? 1002 : 1003);
+                // stage / phase with compile-time divisors (a runtime divisor needs MUFU.RCP, which
+                // queues behind the softmax warps' exponentials)
+                const int st = kgrp ? (int)(gi % kKStages) : (int)(gi % kVStages);
+                const uint32_t sph = kgrp ? (gi / kKStages) & 1 : (gi / kVStages) & 1;
+                mbar_wait(smem_u32(&xempty[st]), sph ^ 1, kgrp ? 1002 : 1003);
                 if (lt == 0) tl_mark(p, kgrp ? 9 : 1, gi);
                 // stage reuse certifies both slots' decisions on blocks <= j - lag
                 for (; known < j - lag;) {
@@ -831,7 +860,7 @@ tc_pass_kernel(const TcParams p, const __grid_constant__ CUtensorMap qmap,
                 }
             }
             if (valid && (a.mode & kFinal) && !resume_later) {
-                const int64_t ooff = g.o_base(P.zh) + grow * g.os[2];
+                const int64_t ooff = tc_o_base(p, P.zh) + grow * g.os[2];
                 if (g.out_bf16 && p.vec_o) {
                     __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(a.o) + ooff;
 #pragma unroll
@@ -927,6 +956,7 @@ constexpr int kDThreads = 512;
 constexpr int kDSoftWarps = 8, kDEpiWarp0 = 8, kDMmaWarp = 12, kDKWarp = 13, kDVWarp = 14;
 constexpr int kDEpiRegs = 160, kDOtherRegs = 56;  // setmaxnreg (softmax warpgroups keep 128)
 constexpr int kDKStages = 2, kDVStages = 2;
+static_assert(kDKStages == kDVStages, "the diagonal loaders share one stage index");
 constexpr int kDQBuf = 2;  // Q double-buffered by tile parity: the next tile's Q lands during this one
 constexpr uint32_t kDOffQ = 0;
 constexpr uint32_t kDOffK = kDQBuf * kTileBytes;
@@ -1026,7 +1056,7 @@ tc_diag_kernel(const TcParams p, const __grid_constant__ CUtensorMap qtile,
     tc_fence_after();
     const uint32_t tbase = c.tmem_base;
     const int64_t total = g.z * g.hq * p.pairs_per_head;
-    const int64_t rowu = g.d;
+    constexpr int64_t rowu = kD;  // (tc path: d == 128)
     float* ml = reinterpret_cast<float*>(smem + kDOffML);
     float* xch = reinterpret_cast<float*>(smem + kDOffX);
     // (setmaxnreg inside each role branch, so the softmax code is dominated by its increase)
@@ -1038,7 +1068,6 @@ tc_diag_kernel(const TcParams p, const __grid_constant__ CUtensorMap qtile,
         const bool kl = warp == kDKWarp;
         const CUtensorMap* xtile = kl ? &ktile : &vtile;
         const uint32_t xbase = kl ? sK : sV;
-        const int nst = kl ? kDKStages : kDVStages;
         uint64_t* xfull = kl ? c.k_full : c.v_full;
         uint64_t* xempty = kl ? c.k_empty : c.v_empty;
         uint32_t gi = 0, qc = 0;
@@ -1048,16 +1077,16 @@ tc_diag_kernel(const TcParams p, const __grid_constant__ CUtensorMap qtile,
                 const uint32_t qb_i = qc % kDQBuf;
                 mbar_wait(smem_u32(&c.q_empty[qb_i]), ((qc / kDQBuf) & 1) ^ 1, 4001);
                 mbar_expect_tx(smem_u32(&c.q_full[qb_i]), kTileBytes);
-                const int64_t qb = g.q_base(t.zh) / rowu;
+                const int64_t qb = tc_q_base(p, t.zh) / rowu;
                 for (int h = 0; h < 2; ++h)
                     tma_load2d(sQ + qb_i * kTileBytes + h * kHalf, &qtile, h * 64, (int32_t)(qb + t.sb + t.t0),
                                smem_u32(&c.q_full[qb_i]));
                 ++qc;
             }
-            const int64_t xb = (kl ? g.k_base(t.zh) : g.v_base(t.zh)) / rowu;
+            const int64_t xb = (kl ? tc_k_base(p, t.zh) : tc_v_base(p, t.zh)) / rowu;
             for (int j = 0; j < t.nd; ++j, ++gi) {
-                const int st = gi % nst;
-                mbar_wait(smem_u32(&xempty[st]), ((gi / nst) & 1) ^ 1, kl ? 4002 : 4003);
+                const int st = (int)(gi % kDKStages);  // (kDKStages == kDVStages)
+                mbar_wait(smem_u32(&xempty[st]), ((gi / kDKStages) & 1) ^ 1, kl ? 4002 : 4003);
                 mbar_expect_tx(smem_u32(&xfull[st]), kTileBytes);
                 const uint32_t dst = xbase + st * kTileBytes;
                 for (int h = 0; h < 2; ++h)
@@ -1316,7 +1345,7 @@ tc_diag_kernel(const TcParams p, const __grid_constant__ CUtensorMap qtile,
             }
             if (valid && (a.mode & kFinal)) {
                 const float inv = 1.0f / ell;
-                const int64_t ooff = g.o_base(t.zh) + grow * g.os[2];
+                const int64_t ooff = tc_o_base(p, t.zh) + grow * g.os[2];
                 if (g.out_bf16 && p.vec_o) {
                     __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(a.o) + ooff;
 #pragma unroll
@@ -1381,6 +1410,7 @@ constexpr int kESoftRegs = 184, kEEpiRegs = 80, kEMmaRegs = 64, kELoadRegs = 64;
 static_assert(8 * (kESoftRegs - 128) <= 4 * (128 - kEEpiRegs) + (128 - kEMmaRegs) + 3 * (128 - kELoadRegs),
               "register pool");
 constexpr int kEQSlots = 3, kEKStages = 2, kEVStages = 2;
+static_assert(kEKStages == kEVStages, "the K and V loaders share one stage index");
 constexpr uint32_t kEOffQ = 0;
 constexpr uint32_t kEOffK = kEQSlots * kTileBytes;
 constexpr uint32_t kEOffV = kEOffK + kEKStages * kTileBytes;
@@ -1567,7 +1597,7 @@ tc_diag2_kernel(const TcParams p, const __grid_constant__ CUtensorMap qtile,
     const uint32_t tbase = c.tmem_base;
     const int64_t total = diag2_items(p);
     const D2Rad R(p);
-    const int64_t rowu = g.d;
+    constexpr int64_t rowu = kD;  // (tc path: d == 128)
     float* ml = reinterpret_cast<float*>(smem + kEOffML);
     if (warp >= kEKWarp) {
         // ============================== loaders (one lane each) ==============================
@@ -1586,7 +1616,7 @@ tc_diag2_kernel(const TcParams p, const __grid_constant__ CUtensorMap qtile,
                     mbar_wait(smem_u32(&c.q_empty[sl]), ((qs / kEQSlots) & 1) ^ 1, 4011);
                     tl_mark(p, 24, qs);
                     mbar_expect_tx(smem_u32(&c.q_full[sl]), kTileBytes);
-                    const int64_t qb = g.q_base(t.zh) / rowu;
+                    const int64_t qb = tc_q_base(p, t.zh) / rowu;
                     for (int h = 0; h < 2; ++h)
                         tma_load2d(sQ + sl * kTileBytes + h * kHalf, &qtile, h * 64, (int32_t)(qb + t.sb + t.t0),
                                    smem_u32(&c.q_full[sl]));
@@ -1597,7 +1627,7 @@ tc_diag2_kernel(const TcParams p, const __grid_constant__ CUtensorMap qtile,
                         for (int y = 0; y < 2; ++y) {
                             const TileInfo u = d2_tile(p, R, cn, y);
                             if (u.nd == 0) continue;
-                            const int64_t ub = g.q_base(u.zh) / rowu;
+                            const int64_t ub = tc_q_base(p, u.zh) / rowu;
                             for (int h = 0; h < 2; ++h) tma_prefetch2d(&qtile, h * 64, (int32_t)(ub + u.sb + u.t0));
                         }
                     }
@@ -1607,17 +1637,16 @@ tc_diag2_kernel(const TcParams p, const __grid_constant__ CUtensorMap qtile,
         const bool kl = warp == kEKWarp;
         const CUtensorMap* xtile = kl ? &ktile : &vtile;
         const uint32_t xbase = kl ? sK : sV;
-        const int nst = kl ? kEKStages : kEVStages;
         uint64_t* xfull = kl ? c.k_full : c.v_full;
         uint64_t* xempty = kl ? c.k_empty : c.v_empty;
         uint32_t gi = 0;
         D2Cur cu = d2_init(R);
         for (int64_t it = blockIdx.x; it < total; it += gridDim.x, d2_next(R, cu)) {
             const TileInfo t0 = d2_tile(p, R, cu, 0);
-            const int64_t xb = (kl ? g.k_base(t0.zh) : g.v_base(t0.zh)) / rowu;
+            const int64_t xb = (kl ? tc_k_base(p, t0.zh) : tc_v_base(p, t0.zh)) / rowu;
             for (int j = 0; j < t0.nd; ++j, ++gi) {  // tile 0 has the most blocks
-                const int st = gi % nst;
-                mbar_wait(smem_u32(&xempty[st]), ((gi / nst) & 1) ^ 1, kl ? 4012 : 4013);
+                const int st = (int)(gi % kEKStages);  // (kEKStages == kEVStages)
+                mbar_wait(smem_u32(&xempty[st]), ((gi / kEKStages) & 1) ^ 1, kl ? 4012 : 4013);
                 tl_mark(p, kl ? 22 : 23, gi);
                 mbar_expect_tx(smem_u32(&xfull[st]), kTileBytes);
                 const uint32_t dst = xbase + st * kTileBytes;
@@ -1881,7 +1910,7 @@ tc_diag2_kernel(const TcParams p, const __grid_constant__ CUtensorMap qtile,
                 const int64_t grow = t.sb + t.t0 + rr;
                 const int64_t slot = t.zh * g.l + grow;
                 const float inv = 1.0f / ell;
-                const int64_t ooff = g.o_base(t.zh) + grow * g.os[2];
+                const int64_t ooff = tc_o_base(p, t.zh) + grow * g.os[2];
 #pragma unroll
                 for (int c0 = 0; c0 < kD; c0 += 32) {
                     uint32_t ov[32];
@@ -2161,6 +2190,7 @@ cudaError_t launch_tc_pass(const PassArgs& a, cudaStream_t st) {
     p.fd_pf = FastDiv((uint32_t)std::max<int64_t>(1, p.pairs_full));
     p.fd_tph = FastDiv((uint32_t)std::max<int64_t>(1, a.tiles_per_head));
     p.fd_t = FastDiv((uint32_t)std::max<int64_t>(1, a.T));
+    p.fd_hq = FastDiv((uint32_t)g.hq);
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
