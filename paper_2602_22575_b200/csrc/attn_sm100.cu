@@ -77,12 +77,12 @@ constexpr int kOtherRegs = 64;      // MMA + loader warpgroups (2, 3)
 constexpr int kLaunchRegs = 65536 / kThreads / 8 * 8;  // 128: what __launch_bounds__(512, 1) allots
 // setmaxnreg.inc blocks until the pool has the registers: the decrements must cover it
 static_assert(kSoftmaxRegs - kLaunchRegs <= kLaunchRegs - kOtherRegs, "register pool overcommitted");
-static_assert(sizeof(uint64_t) * 31 + 4 + 64 + 8 <= 512, "Ctrl exceeds its 512 B");
+static_assert(sizeof(uint64_t) * 33 + 4 + 64 + 8 <= 512, "Ctrl exceeds its 512 B");
 constexpr float kRescaleThresh = 8.0f;
   // lazy max update, log2 units (factor 256)
 
 struct Ctrl {
-    uint64_t q_full, q_empty;
+    uint64_t q_full[2], q_empty[2];  // per slot: a slot's Q tile is released when its stream ends
     uint64_t k_full[kKStages], k_empty[kKStages], v_full[kVStages], v_empty[kVStages];
     uint64_t s_full[2], p_full[2], o_done[2];
     uint32_t tmem_base;
@@ -295,8 +295,10 @@ tc_pass_kernel(const TcParams p, const __grid_constant__ CUtensorMap qmap,
     if (threadIdx.x == 0) {
         // full barriers: every loader thread arrives once per phase (TMA expect_tx by one
         // thread + plain arrives, or cp.async.mbarrier.arrive.noinc by all)
-        mbar_init(smem_u32(&c.q_full), kKThreads);
-        mbar_init(smem_u32(&c.q_empty), 1);
+        for (int x = 0; x < 2; ++x) {
+            mbar_init(smem_u32(&c.q_full[x]), kKThreads);
+            mbar_init(smem_u32(&c.q_empty[x]), 1);
+        }
         for (int s = 0; s < kKStages; ++s) {
             mbar_init(smem_u32(&c.k_full[s]), kKThreads);
             mbar_init(smem_u32(&c.k_empty[s]), 1);
@@ -347,7 +349,7 @@ tc_pass_kernel(const TcParams p, const __grid_constant__ CUtensorMap qmap,
         const int lag = kgrp ? 3 : 2;  // decisions <= j-lag are final when stage j is acquired
         uint64_t* xfull = kgrp ? c.k_full : c.v_full;
         uint64_t* xempty = kgrp ? c.k_empty : c.v_empty;
-        uint32_t gx = 0, qcount = 0;
+        uint32_t gx = 0, qcount = 0, qslot[2] = {0u, 0u};
         for (uint32_t wk = 0;; ++wk) {
             if (kgrp && lt == 0) {  // producer: the next pair index (or -1) into ring slot wk & 3
                 mbar_wait(smem_u32(&c.w_empty[wk & 3]), ((wk >> 2) & 1) ^ 1, 5002);
@@ -363,34 +365,30 @@ tc_pass_kernel(const TcParams p, const __grid_constant__ CUtensorMap qmap,
             named_bar_sync(gbar, nthr);  // every thread of the group is done with its ring
             if (kgrp && lt == 0) tl_mark(p, 30, qcount);
             if (kgrp) {
-                // ---- Q (this CTA's slots; no multicast)
-                mbar_wait(smem_u32(&c.q_empty), (qcount & 1) ^ 1, 1001);
+                // ---- Q, per slot: slot x's tile loads as soon as slot x of the previous pair has
+                // issued its last S (its stream can end blocks before the other slot's)
                 const int64_t qb = tc_q_base(p, P.zh) / rowu, qs = g.qs[2] / rowu;
-                const uint32_t qbytes = (uint32_t)(P.has[0] + P.has[1]) * kTileBytes;
                 const bool q_tile = p.q_contig && !((a.mode & kStateIn) && a.q_reorder) &&
                                     (!P.has[0] || P.tn[0] == kBM) && (!P.has[1] || P.tn[1] == kBM);
-                if (lt == 0) {
-                    if (qbytes) mbar_expect_tx(smem_u32(&c.q_full), qbytes);
-                    else mbar_arrive(smem_u32(&c.q_full));
-                } else {
-                    mbar_arrive(smem_u32(&c.q_full));
-                }
-                if (q_tile) {
-                    if (lt == 0)
-                        for (int x = 0; x < 2; ++x)
-                            if (P.has[x])
-                                for (int h = 0; h < 2; ++h)
-                                    tma_load2d(sQ + x * kTileBytes + h * kHalf, &qtile, h * 64,
-                                               (int32_t)(qb + (P.sb + P.t0[x]) * qs), smem_u32(&c.q_full));
-                } else {
-                    // permuted Q rows: one TMA gather4 op per lane, (slot, row group, column half)
-                    // (A/B against 16-B cp.async: pass-2 6.03 -> 5.90 ms)
-                    const int x = lt >> 6, grp = (lt >> 1) & 31, h = lt & 1;
-                    if (P.has[x]) {
+                for (int x = 0; x < 2; ++x) {
+                    if (!P.has[x]) continue;
+                    mbar_wait(smem_u32(&c.q_empty[x]), (qslot[x] & 1) ^ 1, 1001);
+                    ++qslot[x];
+                    if (lt == 0) mbar_expect_tx(smem_u32(&c.q_full[x]), kTileBytes);
+                    else mbar_arrive(smem_u32(&c.q_full[x]));
+                    if (q_tile) {
+                        if (lt == 0)
+                            for (int h = 0; h < 2; ++h)
+                                tma_load2d(sQ + x * kTileBytes + h * kHalf, &qtile, h * 64,
+                                           (int32_t)(qb + (P.sb + P.t0[x]) * qs), smem_u32(&c.q_full[x]));
+                    } else if ((lt >> 6) == x) {
+                        // permuted Q rows: one TMA gather4 op per lane (row group, column half)
+                        // (A/B against 16-B cp.async: pass-2 6.03 -> 5.90 ms)
+                        const int grp = (lt >> 1) & 31, h = lt & 1;
                         int32_t rr[4];
                         for (int i = 0; i < 4; ++i) rr[i] = (int32_t)(qb + q_row(a, P, x, grp * 4 + i) * qs);
                         tma_gather4(sQ + x * kTileBytes + h * kHalf + grp * 512, &qmap, h * 64, rr[0], rr[1], rr[2],
-                                    rr[3], smem_u32(&c.q_full));
+                                    rr[3], smem_u32(&c.q_full[x]));
                     }
                 }
                 if (lt == 0) tl_mark(p, 29, qcount);
@@ -481,7 +479,7 @@ tc_pass_kernel(const TcParams p, const __grid_constant__ CUtensorMap qmap,
         {
             const uint32_t idesc_s = umma_idesc_bf16(kBM, kBN, false, false);
             const uint32_t idesc_o = umma_idesc_bf16(kBM, kD, false, true);
-            uint32_t gk = 0, gv = 0, qcount = 0;
+            uint32_t gk = 0, gv = 0, qcount = 0, qslot[2] = {0u, 0u};
             uint32_t ns[2] = {0, 0};  // p_full phases per slot
             // descriptor address field is addr >> 4 in the low bits: desc(a + off) = desc(a) + off/16
             const uint64_t dq0 = umma_desc_sw128(sQ, 16, 1024);
@@ -509,20 +507,29 @@ tc_pass_kernel(const TcParams p, const __grid_constant__ CUtensorMap qmap,
                 if (it < 0) break;
                 const PairInfo P = pair_info(p, it);
                 if (P.nb == 0) continue;
-                mbar_wait(smem_u32(&c.q_full), qcount & 1, 2001);
                 tl_mark(p, 26, qcount);
                 ++qcount;
                 int stop_at[2] = {1 << 30, 1 << 30};
                 bool pv_any[2] = {false, false};  // first P V of a slot overwrites O (accumulate = 0)
-                bool q_released = false;
+                bool qrel[2] = {!P.has[0], !P.has[1]};  // slot's Q released (after its last S)
+                auto release_q = [&](int x) {
+                    if (!qrel[x] && leader) umma_commit(smem_u32(&c.q_empty[x]));
+                    qrel[x] = true;
+                };
                 auto need = [&](int j, int lag) {
                     bool n = false;
                     for (int x = 0; x < 2; ++x) n |= participates(P, x, j) && !(stop_at[x] <= j - lag);
                     return n;
                 };
                 wait_k(gk);
-                for (int x = 0; x < 2; ++x)
+                for (int x = 0; x < 2; ++x) {
+                    if (!P.has[x]) continue;
+                    mbar_wait(smem_u32(&c.q_full[x]), qslot[x] & 1, 2001);
+                    ++qslot[x];
+                    tc_fence_after();
                     if (participates(P, x, 0)) issue_s(x, gk % kKStages);
+                    if (last_block(P, x) == 0) release_q(x);
+                }
                 tl_mark(p, 27, qcount - 1);
                 int nk = 0, nv = 0;
                 for (int j = 0;; ++j) {
@@ -558,6 +565,7 @@ tc_pass_kernel(const TcParams p, const __grid_constant__ CUtensorMap qmap,
                                 if (leader && j == last_block(P, x)) umma_commit(smem_u32(&c.o_done[x]));
                             } else {
                                 stop_at[x] = j;
+                                release_q(x);  // no further S of this slot
                                 if (leader) umma_commit(smem_u32(&c.o_done[x]));  // slot finished
                             }
                         }
@@ -567,6 +575,7 @@ tc_pass_kernel(const TcParams p, const __grid_constant__ CUtensorMap qmap,
                                 kn_ready = true;
                             }
                             issue_s(x, (gki + 1) % kKStages);
+                            if (j + 1 == last_block(P, x)) release_q(x);
                             if (x == 0) tl_mark(p, 31, gki);
                         }
                     }
@@ -582,7 +591,8 @@ tc_pass_kernel(const TcParams p, const __grid_constant__ CUtensorMap qmap,
                     if (!has_kn) break;
                     if (!kn_ready) wait_k(gki + 1);
                 }
-                if (leader && !q_released) umma_commit(smem_u32(&c.q_empty));
+                release_q(0);  // (slots whose stream ended without reaching their last block)
+                release_q(1);
                 gk += nk;
                 gv += nv;
             }
