@@ -55,7 +55,7 @@ namespace {
 constexpr int kD = 128;
 constexpr int kBM = 128;
 constexpr int kBN = 128;
-constexpr int kKStages = 3;  // K ring: block j may load once decisions <= j-3 are known
+constexpr int kKStages = 3;  // K ring: block j may load once decisions <= j-3 are known (A/B: 2 stages +9 %)
 constexpr int kVStages = 2;  // V ring: block j may load once decisions <= j-2 are known
 constexpr int kThreads = 512;
 constexpr int kMmaWarp = 8;
@@ -346,7 +346,7 @@ tc_pass_kernel(const TcParams p, const __grid_constant__ CUtensorMap qmap,
         int32_t* ring0 = reinterpret_cast<int32_t*>(smem + kOffTok) + (kgrp ? 0 : 2 * kBN);
         const CUtensorMap* xtile = kgrp ? &ktile : &vtile;
         const uint32_t xbase = kgrp ? sK : sV;
-        const int lag = kgrp ? 3 : 2;  // decisions <= j-lag are final when stage j is acquired
+        const int lag = kgrp ? kKStages : kVStages;  // decisions <= j-lag are final when stage j is acquired
         uint64_t* xfull = kgrp ? c.k_full : c.v_full;
         uint64_t* xempty = kgrp ? c.k_empty : c.v_empty;
         uint32_t gx = 0, qcount = 0, qslot[2] = {0u, 0u};
@@ -472,7 +472,7 @@ tc_pass_kernel(const TcParams p, const __grid_constant__ CUtensorMap qmap,
         // Ping-pong order (per block j, per slot x): wait P_x(j) -> O_x += P_x V(j) -> S_x(j+1)
         // = Q_x K(j+1)^T. The tensor pipe runs slot 1's PV/S while slot 0's softmax works and
         // vice versa. S_x(j+1) overwrites P_x(j) only after the in-order pipe consumed it.
-        // Blocks loaded (must match the loader): K(j) iff need(j, 3), V(j) iff need(j, 2).
+        // Blocks loaded (must match the loader): K(j) iff need(j, kKStages), V(j) iff need(j, kVStages).
         // The whole warp runs the control flow (warp-uniform values stay in uniform registers);
         // one elected lane issues each tcgen05 instruction.
         const bool leader = elect_one();
@@ -534,8 +534,8 @@ tc_pass_kernel(const TcParams p, const __grid_constant__ CUtensorMap qmap,
                 int nk = 0, nv = 0;
                 for (int j = 0;; ++j) {
                     const uint32_t gki = gk + j, gvi = gv + j;
-                    const bool has_v = need(j, 2);
-                    const bool has_kn = (j + 1 < P.nb) && need(j + 1, 3);
+                    const bool has_v = need(j, kVStages);
+                    const bool has_kn = (j + 1 < P.nb) && need(j + 1, kKStages);
                     bool v_ready = false, kn_ready = false;
                     for (int x = 0; x < 2; ++x) {
                         if (participates(P, x, j) && stop_at[x] > j - 1) {
