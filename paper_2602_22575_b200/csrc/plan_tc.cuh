@@ -338,14 +338,14 @@ kv_cand_kernel(const CandArgs a, const __grid_constant__ CUtensorMap kmap) {
                     carry ^= (uint32_t)__popc(m[q4]) & 1u;
                 }
             } else {
-                const int slots = (int)rep * kCSub, me = replica * kCSub + sub;
+                const int slots = (int)rep * kCSub, me = replica * kCSub + sub;  // slots: 2, 4 or 8
                 int rk = 0;
 #pragma unroll
                 for (int q4 = 0; q4 < 4; ++q4) {
                     uint32_t w = m[q4], keep = 0u;
                     while (w) {
                         const uint32_t b = w & (0u - w);
-                        if (rk % slots == me) keep |= b;
+                        if ((rk & (slots - 1)) == me) keep |= b;  // (power of two: no division)
                         ++rk;
                         w ^= b;
                     }
