@@ -72,8 +72,8 @@ constexpr uint32_t kOffCtrl = kOffV + kVStages * kTileBytes;
 constexpr uint32_t kOffTok = kOffCtrl + 512;  // token rings: K group int32 [2][128], V group [2][128]
 constexpr uint32_t kSmemBytes = kOffTok + 2304;  // 226.75 KB (base must be 1024-B aligned)
 constexpr uint32_t kTmemCols = 512;
-constexpr int kSoftmaxRegs = 184;   // setmaxnreg: softmax warpgroups (0, 1)
-constexpr int kOtherRegs = 72;      // MMA + loader warpgroups (2, 3)
+constexpr int kSoftmaxRegs = 176;   // setmaxnreg: softmax warpgroups (0, 1) (A/B: 192 5.69, 184 5.63, 176 5.59 ms)
+constexpr int kOtherRegs = 80;      // MMA + loader warpgroups (2, 3)
 constexpr int kLaunchRegs = 65536 / kThreads / 8 * 8;  // 128: what __launch_bounds__(512, 1) allots
 // setmaxnreg.inc blocks until the pool has the registers: the decrements must cover it
 static_assert(kSoftmaxRegs - kLaunchRegs <= kLaunchRegs - kOtherRegs, "register pool overcommitted");
