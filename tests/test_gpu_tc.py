@@ -122,6 +122,26 @@ def test_tc_pass1_states(cuda, port):
     np.testing.assert_allclose(lg, ell, rtol=2e-3)
 
 
+@pytest.mark.parametrize("hq,hkv", [(4, 2), (3, 1)])
+def test_tc_pass1_states_batched_gqa(cuda, port, hq, hkv):
+    """The two-tile pass-1 kernel against the oracle for Z = 2, an odd number of tiles per segment
+    (S = 384: 3 tiles) and a ragged last segment: q-head pairs (group 2) and adjacent-tile pairs
+    (group 3, whose last pair of a segment has one tile)."""
+    import paper_2602_22575_b200 as s2o
+    torch = cuda
+    parts = [inputs(s2o, hq, hkv, 1000, seed=s) for s in (11, 12)]
+    q, k, v = (np.concatenate([pp[i] for pp in parts], axis=0) for i in range(3))
+    c = Cfg(384, 0.005, 128, 128)
+    bufs = s2o.pass1_dense_init(dev_bf16(torch, q), dev_bf16(torch, k), dev_bf16(torch, v), kcfg(s2o, c, TC))
+    rep = hq // hkv
+    acc, ell, m = port.pass1(q, np.repeat(k, rep, 1), np.repeat(v, rep, 1), c)
+    got = (bufs.acc / bufs.ell[..., None]).cpu().numpy()
+    assert np.abs(got - acc / ell[..., None]).max() <= 2e-2
+    mg = bufs.m.cpu().numpy().astype(np.float64)
+    assert (mg <= m + 1e-3).all() and (mg >= m - 8.0 * np.log(2.0) - 1e-3).all()
+    np.testing.assert_allclose(bufs.ell.cpu().numpy() * np.exp(mg - m), ell, rtol=2e-3)
+
+
 def test_tc_dense_vs_sdpa(cuda):
     import paper_2602_22575_b200 as s2o
     torch = cuda
